@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark: surprisal-guided retrieval over a 16M x 64 experience store
+(BASELINE.json metric "retrieval queries/s @16M exps k=32; Pareto-scored
+tuples/s; % HBM roofline").
+
+A step = one select() pass of Q=8 queries (k = m = 32, lambda_div = 0, the
+fused veto scan off) over the whole device-resident store.  The Pareto half
+(4M 2-objective tuples: frontier maintenance + per-tuple reward) is measured in
+the same run and reported under "pareto".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one rank per GPU): the 16M records are sharded contiguously
+(strong scaling); each rank selects its shard's top-k and the per-shard
+candidates are merged after an NCCL all-gather.  Timing is CUDA events on the
+store's stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_RECORDS = 16 * 1024 * 1024
+DIM = 64
+Q = 8
+K_SEL = 32
+SEED = 2026
+PARETO_T = 4 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--records", type=int, default=N_RECORDS)
+    ap.add_argument("--queries", type=int, default=Q)
+    ap.add_argument("--lambda-div", type=float, default=0.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-pareto", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), float(j.get("bf16_tflops", 1622.7)), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self._stop = gpu, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ ours ---
+
+def run_ours(a, rank, world, local_rank):
+    import torch
+    import paper_2601_22397_b200 as sair
+    from paper_2601_22397_b200 import synth
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    if world > 1:
+        raise SystemExit("bench.py: multi-GPU sharding lands with sair_store_set_shard")
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    n_total = a.records
+    lo, hi = n_total * rank // world, n_total * (rank + 1) // world
+    buf = sair.ExperienceBuffer(0.0, device=dev)
+    if world > 1:
+        buf.set_shard(lo, n_total)
+    t0 = time.time()
+    buf.store_synthetic(SEED, hi - lo, DIM)
+    if world > 1:
+        buf.sync_global_stats(dist)
+    gen_s = time.time() - t0
+    cfg = sair.SelectionConfig(m=K_SEL, lambda_div=a.lambda_div)
+    qpool = synth.queries(SEED, (a.warmup + a.steps) * a.queries, DIM).reshape(
+        a.warmup + a.steps, a.queries, DIM)
+    stream = torch.cuda.ExternalStream(buf.stream_ptr(), device=dev)
+
+    def step(i):
+        res = buf.select_batch(qpool[i], cfg)
+        if world > 1:
+            res = sair.merge_shards(res, dist, K_SEL)
+        return res
+
+    for i in range(a.warmup):
+        step(i)
+    stats = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for i in range(a.warmup, a.warmup + a.steps):
+            step(i)
+            stats.append(buf.last_stats())
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = a.steps * a.queries / (ms / 1e3)
+
+    # e2e: the public API with host buffers, wall clock (copies inside)
+    t0 = time.perf_counter()
+    for i in range(a.warmup, a.warmup + a.steps):
+        step(i)
+    if dist:
+        dist.barrier()
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = a.steps * a.queries / e2e_s
+
+    # roofline of the dominant kernel (stream_kernel), CUDA events around each launch
+    launches = sum(s["stream_launches"] for s in stats)
+    stream_ms = sum(s["stream_ms"] for s in stats)
+    dp = 64 if DIM > 32 else 32
+    alg_bytes = (hi - lo) * (4 * dp + 4)  # fp32 page row + fp32 reward per record
+    per_launch_s = stream_ms / 1e3 / max(launches, 1)
+    hbm_peak, _, peak_kind = measured_peaks()
+    achieved = alg_bytes / per_launch_s / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "stream_kernel_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+    fallbacks = sum(s["exact_fallbacks"] for s in stats)
+    certified = sum(s["certified"] for s in stats)
+    gpu_launches = sum(3 * s["stream_launches"] + s["exact_fallbacks"] * (3 + 3 * K_SEL)
+                       for s in stats)
+
+    out = {
+        "metric": "retrieval queries/s @16M exps k=32",
+        "value": round(value, 2),
+        "unit": "queries/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": round(ms / a.steps, 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 filter + f64 refine",
+        "data": "synthetic (device-generated, synth.py; store 16M x 64, i.i.d. Irwin-Hall contexts)",
+        "config": {"workload": f"config 4 north-star HBM target: {n_total} records x d={DIM}, "
+                               f"Q={a.queries} queries/step, k={K_SEL}, lambda_div={a.lambda_div}",
+                   "records": n_total, "dim": DIM, "queries_per_step": a.queries, "k": K_SEL,
+                   "lambda_div": a.lambda_div, "parallelism": f"record shards x{world}",
+                   "l2": "inputs larger than L2 (4.4 GB store vs 126 MB L2)"},
+        "e2e": {"value": round(e2e, 2), "unit": "queries/s",
+                "h2d_bytes_per_step": a.queries * DIM * 8,
+                "d2h_bytes_per_step": a.queries * K_SEL * 24 + a.queries * 8},
+        "gpu_launches": gpu_launches,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                     "kernel": "sair::stream_kernel<64,8>", "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": round(per_launch_s * 1e3, 4)},
+        "certified_queries": certified, "exact_fallbacks": fallbacks,
+        "store_build_s": round(gen_s, 3),
+    }
+    if rank == 0 and not a.no_pareto:
+        out["pareto"] = bench_pareto(dev)
+    if rank == 0:
+        out["clocks"] = clk.summary()
+        if not a.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_port()
+    if dist:
+        dist.destroy_process_group()
+    return out
+
+
+def bench_pareto(dev):
+    """Config 3: 4M 2-objective tuples -> frontier maintenance (batch insert) and
+    Pareto reward of every tuple against the frontier; k-D counts at 256k."""
+    import torch
+    import paper_2601_22397_b200 as sair
+    from paper_2601_22397_b200 import synth
+    res = {"metric": "Pareto-scored tuples/s", "tuples": PARETO_T}
+    pts = synth.tuples(SEED, PARETO_T, 2, "uniform")
+    f = sair.ParetoFrontier(1.0, 1.0, device=dev)
+    f.insert_batch(pts[:1024])  # warm
+    f2 = sair.ParetoFrontier(1.0, 1.0, device=dev)
+    t0 = time.perf_counter()
+    F = f2.insert_batch(pts)
+    ins_s = time.perf_counter() - t0
+    dpts = torch.from_numpy(pts).to(f"cuda:{dev}")
+    dout = torch.empty(PARETO_T, dtype=torch.float64, device=f"cuda:{dev}")
+    ddom = torch.empty(PARETO_T, dtype=torch.uint8, device=f"cuda:{dev}")
+    s = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        f2.score_batch_device(dpts.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
+                              s.cuda_stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record(s)
+    for _ in range(reps):
+        f2.score_batch_device(dpts.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
+                              s.cuda_stream)
+    e1.record(s)
+    torch.cuda.synchronize()
+    sc_ms = e0.elapsed_time(e1) / reps
+    res.update({"value": round(PARETO_T / (sc_ms / 1e3), 1), "unit": "tuples/s",
+                "score_ms": round(sc_ms, 4), "frontier_size": F,
+                "frontier_insert_tuples_per_s": round(PARETO_T / ins_s, 1),
+                "frontier_insert_s_e2e": round(ins_s, 4),
+                "score_hbm_gbs": round(PARETO_T * (16 + 8 + 1) / (sc_ms / 1e3) / 1e9, 1)})
+    for K in (2, 3, 4):
+        T = 262144
+        t = synth.tuples(SEED + K, T, K, "uniform")
+        sair.dominance_counts(t[:4096])
+        t0 = time.perf_counter()
+        cnt, mem = sair.dominance_counts(t)
+        dt = time.perf_counter() - t0
+        res[f"dominance_counts_K{K}"] = {"tuples": T, "s_e2e": round(dt, 4),
+                                         "tuples_per_s": round(T / dt, 1),
+                                         "frontier": int(mem.sum())}
+    return res
+
+
+def cpu_baseline_port():
+    """The oracle's bit-identical restatement (hoisted Sigma r) on all host
+    threads, on a bounded sample: 1M of the same synthetic records, 2 queries
+    per thread; throughput scaled to the 16M store (the restated select is
+    linear in N)."""
+    from oracle.oracle import COracle
+    from paper_2601_22397_b200 import synth
+    orc = COracle()
+    n_s = 1 << 20
+    ctx = synth.contexts(SEED, 0, n_s, DIM)
+    rew = synth.rewards(SEED, 0, n_s)
+    rnd = synth.rounds(0, n_s)
+    threads = os.cpu_count() or 1
+    nq = 2 * threads
+    xq = synth.queries(SEED + 1, nq, DIM)
+    s, ss = orc.stats(ctx)
+    sigma = orc.sigma_median(ctx)
+    t0 = time.perf_counter()
+    orc.select_batch(ctx, rew, rnd, xq, K_SEL, 0.0, sigma, nthreads=threads, stats=(s, ss))
+    dt = time.perf_counter() - t0
+    qps_at_sample = nq / dt
+    return {"value": round(qps_at_sample * n_s / N_RECORDS, 4), "unit": "queries/s",
+            "cores": threads, "kind": "port",
+            "sample": f"oracle restatement, {nq} queries x {n_s} records x d={DIM}, k={K_SEL}, "
+                      f"{dt:.2f}s on {threads} threads; scaled x{n_s}/{N_RECORDS} (linear in N)",
+            "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------- reference ---
+
+def run_reference(a):
+    """The reference's own select (oracle/_ref: proj/src/experience.cpp compiled
+    unmodified, -O3 -DNDEBUG) on the host cores.  The literal select is O(N^2)
+    (experience.cpp:229-231 inside :255-258), so each step is a bounded sample:
+    Q queries over an n_s-record buffer on Q threads; the 16M-equivalent rate
+    is extrapolated from a quadratic fit through two sample sizes."""
+    from oracle.oracle import REF_SO, Ref, RefBuffer
+    from paper_2601_22397_b200 import synth
+    if not REF_SO.exists():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libsair_ref.so not built"}
+    ref = Ref()
+    threads = min(os.cpu_count() or 1, a.queries)
+    sizes = (4096, 8192)
+    per_q = {}
+    for n_s in sizes:
+        b = RefBuffer(ref, 0.0)
+        b.store_many(synth.contexts(SEED, 0, n_s, DIM), synth.rewards(SEED, 0, n_s),
+                     synth.rounds(0, n_s))
+        b.effective_sigma(0.0)
+        xq = synth.queries(SEED, a.queries * (a.warmup + a.steps), DIM)
+        for i in range(a.warmup):
+            b.select_batch(xq[i * a.queries:(i + 1) * a.queries], K_SEL, a.lambda_div, 0.0,
+                           nthreads=threads)
+        t0 = time.perf_counter()
+        for i in range(a.warmup, a.warmup + a.steps):
+            b.select_batch(xq[i * a.queries:(i + 1) * a.queries], K_SEL, a.lambda_div, 0.0,
+                           nthreads=threads)
+        per_q[n_s] = (time.perf_counter() - t0) / (a.steps * a.queries) * threads
+    # t(n) = c1 n + c2 n^2 per query per thread
+    n1, n2 = sizes
+    t1, t2 = per_q[n1], per_q[n2]
+    c2 = (t2 / n2 - t1 / n1) / (n2 - n1)
+    c1 = t1 / n1 - c2 * n1
+    c2 = max(c2, 0.0)
+    t_full = max(c1, 0.0) * N_RECORDS + c2 * N_RECORDS ** 2
+    value = threads / t_full
+    sample = (f"literal reference select, {a.steps} steps x {a.queries} queries on {threads} "
+              f"threads at n={n1} ({t1 * 1e3:.1f} ms/query) and n={n2} ({t2 * 1e3:.1f} ms/query), "
+              f"extrapolated to N={N_RECORDS} by t(n) = c1 n + c2 n^2")
+    return {
+        "metric": "retrieval queries/s @16M exps k=32", "value": value, "unit": "queries/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": t_full / threads * a.queries * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (synth.py)", "impl": "reference",
+        "config": {"workload": f"config 4 north-star HBM target: {N_RECORDS} records x d={DIM}, "
+                               f"Q={a.queries} queries/step, k={K_SEL}, lambda_div={a.lambda_div}"},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
+                         "kind": "reference", "sample": sample, "cpu_model": _cpu_model()},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if a.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(a)), flush=True)
+        return
+    out = run_ours(a, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

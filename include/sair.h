@@ -1,0 +1,258 @@
+/*
+ * sair.h -- C-ABI of the B200-native SAIR retrieval + Pareto hot path.
+ *
+ * This is the drop-in boundary.  The reference exposes the path as a C++
+ * class API (namespace scalelab); it has no FFI of its own.  Each entry point
+ * below replaces one reference member, cited as file:line relative to
+ * /root/reference/proj.  The host-side mirrors (paper_2601_22397_b200/
+ * scalelab_api.hpp for C++, paper_2601_22397_b200/__init__.py for Python)
+ * call only these functions.  See INTEGRATION.md for the bindings.
+ *
+ * Conventions
+ *   - plain pointers and sizes; no torch / CUDA types in signatures;
+ *   - every function returns a sair_status; on failure a thread-local message
+ *     is available from sair_last_error();
+ *   - status codes map 1:1 onto the exceptions the reference throws
+ *     (SAIR_EINVAL -> std::invalid_argument, SAIR_ELOGIC -> std::logic_error,
+ *     SAIR_ERANGE -> std::out_of_range, SAIR_EIO -> std::runtime_error);
+ *   - host pointers are borrowed for the duration of the call; results are in
+ *     caller-provided arrays; the library owns device memory and staging;
+ *   - calls are synchronous on return.  Different handles may be used from
+ *     different threads; one handle is not thread-safe (the reference mutates
+ *     its sigma cache from const methods, experience.hpp:87-88);
+ *   - all arithmetic the reference does in fp64 is fp64 here; the fp32 device
+ *     copy of the store is only a bandwidth-optimal *filter* whose survivors
+ *     are re-scored in fp64 and certified.
+ *   - there is no CPU fallback: without a usable CUDA device every compute
+ *     entry point fails with SAIR_ECUDA.
+ */
+#ifndef SAIR_H_
+#define SAIR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SAIR_API __attribute__((visibility("default")))
+#else
+#define SAIR_API
+#endif
+
+typedef enum {
+    SAIR_OK = 0,
+    SAIR_EINVAL = 1, /* std::invalid_argument */
+    SAIR_ELOGIC = 2, /* std::logic_error */
+    SAIR_ERANGE = 3, /* std::out_of_range (items_.at) */
+    SAIR_EIO = 4,    /* std::runtime_error (persistence) */
+    SAIR_ECUDA = 5,  /* CUDA runtime / no device */
+    SAIR_ENOMEM = 6,
+    SAIR_ENCCL = 7
+} sair_status;
+
+typedef struct sair_store_s* sair_store_t;       /* ExperienceBuffer state */
+typedef struct sair_frontier_s* sair_frontier_t; /* ParetoFrontier state */
+
+/* SelectionConfig, experience.hpp:27-32 (+ this library's knobs). */
+typedef struct {
+    size_t m;                  /* SelectionConfig::m (default 15) */
+    double lambda_div;         /* SelectionConfig::lambda_div (default 0.1) */
+    double sigma_sim;          /* SelectionConfig::sigma_sim; <= 0 -> buffer median */
+    int locally_weighted_mean; /* SelectionConfig::locally_weighted_mean */
+    int mode;                  /* SAIR_SELECT_AUTO / SAIR_SELECT_EXACT */
+} sair_select_config;
+
+enum { SAIR_SELECT_AUTO = 0, SAIR_SELECT_EXACT = 1 };
+
+/* Counters of the last select call (diagnostics; bench.py reads them). */
+typedef struct {
+    size_t queries;         /* queries in the call */
+    size_t certified;       /* answered by the fp32 filter + fp64 refine */
+    size_t exact_fallbacks; /* answered by the full fp64 pass */
+    size_t candidates;      /* K' per query used by the filter */
+    int qb;                 /* queries per streaming pass */
+    int stream_launches;    /* streaming-kernel launches */
+    float stream_ms;        /* device time of the streaming kernels (CUDA events) */
+    float total_ms;         /* device time of the whole call */
+} sair_select_stats;
+
+SAIR_API const char* sair_last_error(void);
+SAIR_API int sair_version(void);
+/* Number of CUDA devices; SAIR_ECUDA if none. */
+SAIR_API sair_status sair_device_count(int* out);
+
+/* ------------------------------------------------------------------------
+ * Experience store -- ExperienceBuffer (experience.hpp:45-89)
+ * ------------------------------------------------------------------------ */
+
+/* ExperienceBuffer(double r_min), experience.cpp:133. Device-resident SoA. */
+SAIR_API sair_status sair_store_create(double r_min, int device, size_t capacity_hint,
+                                       sair_store_t* out);
+SAIR_API sair_status sair_store_destroy(sair_store_t h);
+/* Deep copy (the reference's value semantics, experience.hpp:45). */
+SAIR_API sair_status sair_store_clone(sair_store_t h, sair_store_t* out);
+
+/* ExperienceBuffer::store for `count` rows, experience.cpp:135-153: each row is
+ * gated (reward > r_min, else counted as rejected); the dimension is fixed by
+ * the first accepted row and a change is SAIR_EINVAL (rows before the bad one
+ * stay stored, as with sequential store() calls).  ctx is count x dim fp64
+ * row-major.  accepted (nullable) gets one 0/1 per row. */
+SAIR_API sair_status sair_store_append(sair_store_t h, const double* ctx, size_t count, int dim,
+                                       const double* reward, const int32_t* round,
+                                       uint8_t* accepted, size_t* n_accepted);
+
+/* Benchmark/test helper: append `count` synthetic rows generated on the device
+ * (paper_2601_22397_b200/synth.py documents the generator; values are
+ * fp32-exact and their running sums exact in fp64).  Record i of the store
+ * gets global index base+i, round = global index. */
+SAIR_API sair_status sair_store_append_synthetic(sair_store_t h, uint64_t seed, size_t count,
+                                                 int dim, int clustered);
+
+SAIR_API sair_status sair_store_size(sair_store_t h, size_t* n);         /* size() */
+SAIR_API sair_status sair_store_dim(sair_store_t h, int* dim);           /* 0 if empty */
+SAIR_API sair_status sair_store_rejected(sair_store_t h, uint64_t* out); /* rejected() */
+SAIR_API sair_status sair_store_r_min(sair_store_t h, double* out);      /* r_min() */
+
+/* Read back record `index` (fp64 context, reward, round): all()[index]. */
+SAIR_API sair_status sair_store_get(sair_store_t h, size_t index, double* ctx, double* reward,
+                                    int32_t* round);
+
+/* ExperienceBuffer::standardize, experience.cpp:155-169 (fp64, host-kept sums). */
+SAIR_API sair_status sair_store_standardize(sair_store_t h, const double* x, int dim, double* z);
+
+/* ExperienceBuffer::effective_sigma, experience.cpp:207-212, including the
+ * stale-after-50-insertions cache; a refresh (experience.cpp:171-205) runs the
+ * 512-subsample pairwise median on the device. */
+SAIR_API sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double* out);
+
+/* ExperienceBuffer::surprisal, experience.cpp:234-240 (SAIR_ERANGE on a bad index). */
+SAIR_API sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, int dim,
+                                          const sair_select_config* cfg, double* out);
+
+/* ExperienceBuffer::select for nq queries, experience.cpp:242-296.
+ * queries: nq x dim fp64.  For query q, out_count[q] = min(m, n) picks are
+ * written at out_idx/out_sim/out_score[q*m ...] in the reference's curriculum
+ * order (stable by reward asc, round asc).  out_idx are store indices
+ * (global indices for a shard, see sair_store_set_shard).  out_sim is
+ * SelectedExperience::similarity_to_current, out_score ::score.
+ * out_nn_idx / out_nn_sim (nullable) additionally return the MockBackend veto
+ * scan's nearest record (policy.cpp:140-157) from the same pass. */
+SAIR_API sair_status sair_store_select(sair_store_t h, const double* queries, size_t nq, int dim,
+                                       const sair_select_config* cfg, int64_t* out_idx,
+                                       double* out_sim, double* out_score, size_t* out_count,
+                                       int64_t* out_nn_idx, double* out_nn_sim);
+
+/* The veto scan alone, policy.cpp:140-157: argmax similarity, first index on ties. */
+SAIR_API sair_status sair_store_nearest(sair_store_t h, const double* queries, size_t nq, int dim,
+                                        double sigma_sim, int64_t* out_idx, double* out_sim);
+
+SAIR_API sair_status sair_store_last_stats(sair_store_t h, sair_select_stats* out);
+
+/* The CUDA stream the store's work is ordered on (for event timing). */
+SAIR_API sair_status sair_store_stream(sair_store_t h, void** stream);
+
+/* ------------------------------------------------------------------------
+ * Pareto frontier -- ParetoFrontier (pareto.hpp:24-70), 2 objectives
+ * ------------------------------------------------------------------------ */
+
+/* ParetoFrontier(l_max, c_max), pareto.cpp:14-18: SAIR_EINVAL if either <= 0. */
+SAIR_API sair_status sair_frontier_create(double l_max_ms, double c_max, int device,
+                                          sair_frontier_t* out);
+SAIR_API sair_status sair_frontier_destroy(sair_frontier_t f);
+SAIR_API sair_status sair_frontier_clone(sair_frontier_t f, sair_frontier_t* out);
+
+/* normalize, pareto.cpp:20-29 */
+SAIR_API sair_status sair_frontier_normalize(sair_frontier_t f, double l_ms, double cost,
+                                             double* l, double* c, int* clamped);
+/* update, pareto.cpp:36-41 */
+SAIR_API sair_status sair_frontier_update(sair_frontier_t f, double l_ms, double cost,
+                                          int* inserted, int* clamped);
+/* insert_normalized, pareto.cpp:43-54 */
+SAIR_API sair_status sair_frontier_insert_normalized(sair_frontier_t f, double l, double c,
+                                                     int* inserted);
+/* T sequential insert_normalized calls on normalized points (pts: T x 2); the
+ * result equals the reference's loop (non-dominated set of F u pts, first
+ * occurrence of duplicates). */
+SAIR_API sair_status sair_frontier_insert_batch(sair_frontier_t f, const double* pts, size_t T,
+                                                size_t* new_size);
+SAIR_API sair_status sair_frontier_size(sair_frontier_t f, size_t* F);
+/* points(): sorted by latency asc.  l/c may be NULL to query the size. */
+SAIR_API sair_status sair_frontier_points(sair_frontier_t f, double* l, double* c, size_t cap,
+                                          size_t* F);
+SAIR_API sair_status sair_frontier_bounds(sair_frontier_t f, double* l_max, double* c_max);
+/* hypervolume, pareto.cpp:56-65 */
+SAIR_API sair_status sair_frontier_hypervolume(sair_frontier_t f, double* out);
+/* strictly_dominated, pareto.cpp:31-34 */
+SAIR_API sair_status sair_frontier_strictly_dominated(sair_frontier_t f, double l, double c,
+                                                      int* out);
+/* contribution, pareto.cpp:67-73: SAIR_ELOGIC for a dominated point. */
+SAIR_API sair_status sair_frontier_contribution(sair_frontier_t f, double l, double c,
+                                                double* out);
+/* distance, pareto.cpp:75-84: *has = 0 for an empty frontier (nullopt). */
+SAIR_API sair_status sair_frontier_distance(sair_frontier_t f, double l, double c, double* out,
+                                            int* has);
+/* reward, pareto.cpp:86-89 */
+SAIR_API sair_status sair_frontier_reward(sair_frontier_t f, double l, double c, double* out);
+
+/* Batch scoring of T normalized points against the (fixed) frontier: the
+ * Pareto half of compute_reward for every tuple.  out_dominated nullable. */
+SAIR_API sair_status sair_frontier_score_batch(sair_frontier_t f, const double* pts, size_t T,
+                                               double* out_reward, uint8_t* out_dominated);
+
+/* Same on device-resident data: pts / out_reward / out_dominated are device
+ * pointers, ordered on `stream` (a cudaStream_t, NULL = legacy default);
+ * returns without synchronizing. */
+SAIR_API sair_status sair_frontier_score_batch_device(sair_frontier_t f, const double* pts,
+                                                      size_t T, double* out_reward,
+                                                      uint8_t* out_dominated, void* stream);
+
+/* K-objective dominance counts over T tuples (T x K fp64, K in 1..8):
+ * counts[i] = #{j : j dominates i} (component-wise dominates(), pareto.cpp:9-12),
+ * member[i] = counts[i] == 0 and no equal tuple at a lower index.
+ * counts / member nullable (member-only mode exits early). */
+SAIR_API sair_status sair_dominance_counts(const double* tuples, size_t T, int K, int device,
+                                           uint32_t* counts, uint8_t* member);
+
+/* ------------------------------------------------------------------------
+ * Reward -- compute_reward / action_magnitude (reward.hpp:42-48)
+ * ------------------------------------------------------------------------ */
+
+typedef struct { /* RewardConfig, reward.hpp:8-20 */
+    double t_sla_ms, l_baseline_ms, c_budget, w_latency, w_cost, w_proactive, r_max;
+} sair_reward_config;
+
+typedef struct { /* RewardInputs, reward.hpp:23-28 */
+    double l_before_ms, l_after_ms, c_before, c_after;
+} sair_reward_inputs;
+
+typedef struct { /* RewardBreakdown, reward.hpp:30-38 */
+    double latency, cost, sla, proactive, pareto, total;
+    int clipped;
+} sair_reward_breakdown;
+
+/* action_magnitude, reward.cpp:9-19; deltas = stages x {replicas,
+ * cpu_millicores, memory_mb, rate_ratio_tenths}. */
+SAIR_API sair_status sair_action_magnitude(const int32_t* deltas, size_t stages, double* out);
+
+/* compute_reward, reward.cpp:21-44: the pareto term reads the frontier as the
+ * action saw it (read-only).  SAIR_EINVAL on the reference's config errors. */
+SAIR_API sair_status sair_compute_reward(const sair_reward_inputs* in, const int32_t* deltas,
+                                         size_t stages, sair_frontier_t f,
+                                         const sair_reward_config* cfg,
+                                         sair_reward_breakdown* out);
+
+/* compute_reward for T independent (inputs, action) rows against one
+ * frontier (oracle rollouts, harness.cpp:112-119; config 5).  deltas is
+ * T x stages x 4. */
+SAIR_API sair_status sair_compute_reward_batch(const sair_reward_inputs* in,
+                                               const int32_t* deltas, size_t stages, size_t T,
+                                               sair_frontier_t f, const sair_reward_config* cfg,
+                                               sair_reward_breakdown* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAIR_H_ */

@@ -1,0 +1,419 @@
+// capi.cpp -- the extern "C" boundary (include/sair.h).  Every entry point
+// translates C++ exceptions into sair_status codes + a thread-local message.
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "internal.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+sair_status guard(F&& f) {
+    try {
+        f();
+        return SAIR_OK;
+    } catch (const sair::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = "out of memory";
+        return SAIR_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SAIR_ECUDA;
+    }
+}
+
+sair_status bad(const char* msg) {
+    g_err = msg;
+    return SAIR_EINVAL;
+}
+
+sair_select_config defaults(const sair_select_config* c) {
+    if (c) return *c;
+    sair_select_config d{};
+    d.m = 15;
+    d.lambda_div = 0.1;
+    return d;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sair_last_error(void) { return g_err.c_str(); }
+int sair_version(void) { return 1; }
+
+sair_status sair_device_count(int* out) {
+    return guard([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+        *out = n;
+        if (n == 0) throw sair::Error(SAIR_ECUDA, "no CUDA device");
+    });
+}
+
+// ---------------------------------------------------------------- store --
+
+sair_status sair_store_create(double r_min, int device, size_t capacity_hint, sair_store_t* out) {
+    if (!out) return bad("null out");
+    return guard([&] {
+        auto* s = new sair_store_s();
+        try {
+            sair::store_init(s, r_min, device, capacity_hint);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+sair_status sair_store_destroy(sair_store_t h) {
+    if (!h) return SAIR_OK;
+    return guard([&] {
+        sair::store_free(h);
+        delete h;
+    });
+}
+
+sair_status sair_store_clone(sair_store_t h, sair_store_t* out) {
+    if (!h || !out) return bad("null handle");
+    return guard([&] {
+        auto* o = new sair_store_s();
+        try {
+            sair::store_clone(h, o);
+        } catch (...) {
+            delete o;
+            throw;
+        }
+        *out = o;
+    });
+}
+
+sair_status sair_store_append(sair_store_t h, const double* ctx, size_t count, int dim,
+                              const double* reward, const int32_t* round, uint8_t* accepted,
+                              size_t* n_accepted) {
+    if (!h) return bad("null handle");
+    if (count && (!ctx || !reward || !round)) return bad("null input");
+    return guard([&] {
+        size_t k = sair::store_append(h, ctx, count, dim, reward, round, accepted);
+        if (n_accepted) *n_accepted = k;
+    });
+}
+
+sair_status sair_store_append_synthetic(sair_store_t h, uint64_t seed, size_t count, int dim,
+                                        int clustered) {
+    if (!h) return bad("null handle");
+    return guard([&] { sair::store_append_synthetic(h, seed, count, dim, clustered); });
+}
+
+sair_status sair_store_size(sair_store_t h, size_t* n) {
+    if (!h || !n) return bad("null handle");
+    *n = h->n;
+    return SAIR_OK;
+}
+sair_status sair_store_dim(sair_store_t h, int* dim) {
+    if (!h || !dim) return bad("null handle");
+    *dim = h->n ? h->d : 0;
+    return SAIR_OK;
+}
+sair_status sair_store_rejected(sair_store_t h, uint64_t* out) {
+    if (!h || !out) return bad("null handle");
+    *out = h->rejected;
+    return SAIR_OK;
+}
+sair_status sair_store_r_min(sair_store_t h, double* out) {
+    if (!h || !out) return bad("null handle");
+    *out = h->r_min;
+    return SAIR_OK;
+}
+
+sair_status sair_store_get(sair_store_t h, size_t index, double* ctx, double* reward,
+                           int32_t* round) {
+    if (!h) return bad("null handle");
+    return guard([&] {
+        if (index >= h->n) throw sair::Error(SAIR_ERANGE, "vector::_M_range_check");
+        sair::DeviceGuard g(h->device);
+        if (ctx)
+            SAIR_CUDA(cudaMemcpyAsync(ctx, h->x64 + index * h->d, h->d * 8,
+                                      cudaMemcpyDeviceToHost, h->st));
+        if (reward)
+            SAIR_CUDA(cudaMemcpyAsync(reward, h->r64 + index, 8, cudaMemcpyDeviceToHost, h->st));
+        if (round)
+            SAIR_CUDA(cudaMemcpyAsync(round, h->rnd + index, 4, cudaMemcpyDeviceToHost, h->st));
+        SAIR_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+sair_status sair_store_standardize(sair_store_t h, const double* x, int dim, double* z) {
+    if (!h) return bad("null handle");
+    return guard([&] {
+        if (h->n == 0) {  // experience.cpp:156
+            std::memcpy(z, x, (size_t)dim * sizeof(double));
+            return;
+        }
+        if (dim != h->d)
+            throw sair::Error(SAIR_EINVAL, "experience store: feature dimension mismatch");
+        sair::store_standardize(h, x, z);
+    });
+}
+
+sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double* out) {
+    if (!h || !out) return bad("null handle");
+    return guard([&] { *out = sair::store_effective_sigma(h, sigma_sim); });
+}
+
+sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, int dim,
+                                 const sair_select_config* cfg, double* out) {
+    if (!h || !out) return bad("null handle");
+    return guard([&] {
+        // items_.at(index) first (experience.cpp:236), then standardize(x)
+        if (index >= h->n) throw sair::Error(SAIR_ERANGE, "vector::_M_range_check");
+        if (dim != h->d)
+            throw sair::Error(SAIR_EINVAL, "experience store: feature dimension mismatch");
+        *out = sair::store_surprisal(h, index, x, defaults(cfg));
+    });
+}
+
+sair_status sair_store_select(sair_store_t h, const double* queries, size_t nq, int dim,
+                              const sair_select_config* cfg, int64_t* out_idx, double* out_sim,
+                              double* out_score, size_t* out_count, int64_t* out_nn_idx,
+                              double* out_nn_sim) {
+    if (!h) return bad("null handle");
+    if (nq && (!queries || !out_count)) return bad("null input");
+    if ((out_nn_idx == nullptr) != (out_nn_sim == nullptr)) return bad("nn outputs come in pairs");
+    return guard([&] {
+        sair::store_select(h, queries, nq, dim, defaults(cfg), out_idx, out_sim, out_score,
+                           out_count, out_nn_idx, out_nn_sim);
+    });
+}
+
+sair_status sair_store_nearest(sair_store_t h, const double* queries, size_t nq, int dim,
+                               double sigma_sim, int64_t* out_idx, double* out_sim) {
+    if (!h) return bad("null handle");
+    return guard([&] {
+        // a select with m = 1 computes the same pass; only the nearest is kept
+        sair_select_config c{};
+        c.m = 1;
+        c.lambda_div = 0.0;
+        c.sigma_sim = sigma_sim;
+        std::vector<int64_t> idx(nq);
+        std::vector<double> sim(nq), score(nq);
+        std::vector<size_t> cnt(nq);
+        sair::store_select(h, queries, nq, dim, c, idx.data(), sim.data(), score.data(),
+                           cnt.data(), out_idx, out_sim);
+    });
+}
+
+sair_status sair_store_last_stats(sair_store_t h, sair_select_stats* out) {
+    if (!h || !out) return bad("null handle");
+    *out = h->last;
+    return SAIR_OK;
+}
+
+sair_status sair_store_stream(sair_store_t h, void** stream) {
+    if (!h || !stream) return bad("null handle");
+    *stream = h->st;
+    return SAIR_OK;
+}
+
+// ------------------------------------------------------------- frontier --
+
+sair_status sair_frontier_create(double l_max_ms, double c_max, int device, sair_frontier_t* out) {
+    if (!out) return bad("null out");
+    return guard([&] {
+        auto* f = new sair_frontier_s();
+        try {
+            sair::frontier_init(f, l_max_ms, c_max, device);
+        } catch (...) {
+            delete f;
+            throw;
+        }
+        *out = f;
+    });
+}
+
+sair_status sair_frontier_destroy(sair_frontier_t f) {
+    if (!f) return SAIR_OK;
+    return guard([&] {
+        sair::frontier_free(f);
+        delete f;
+    });
+}
+
+sair_status sair_frontier_clone(sair_frontier_t f, sair_frontier_t* out) {
+    if (!f || !out) return bad("null handle");
+    return guard([&] {
+        auto* o = new sair_frontier_s();
+        try {
+            sair::frontier_clone(f, o);
+        } catch (...) {
+            delete o;
+            throw;
+        }
+        *out = o;
+    });
+}
+
+// normalize, pareto.cpp:20-29 (two divisions and clamps: host arithmetic is
+// the reference's own; the device path does the same inside the kernels)
+static void normalize_host(const sair_frontier_s* f, double l_ms, double cost, double* l,
+                           double* c, int* clamped) {
+    double pl = l_ms / f->l_max, pc = cost / f->c_max;
+    int hit = 0;
+    if (pl > 1.0) { pl = 1.0; hit = 1; }
+    if (pc > 1.0) { pc = 1.0; hit = 1; }
+    if (pl < 0.0) pl = 0.0;
+    if (pc < 0.0) pc = 0.0;
+    *l = pl;
+    *c = pc;
+    if (clamped) *clamped = hit;
+}
+
+sair_status sair_frontier_normalize(sair_frontier_t f, double l_ms, double cost, double* l,
+                                    double* c, int* clamped) {
+    if (!f || !l || !c) return bad("null handle");
+    normalize_host(f, l_ms, cost, l, c, clamped);
+    return SAIR_OK;
+}
+
+sair_status sair_frontier_update(sair_frontier_t f, double l_ms, double cost, int* inserted,
+                                 int* clamped) {
+    if (!f) return bad("null handle");
+    return guard([&] {
+        double pl, pc;
+        int cl = 0;
+        normalize_host(f, l_ms, cost, &pl, &pc, &cl);
+        bool ins = sair::frontier_insert_one(f, pl, pc);
+        if (inserted) *inserted = ins;
+        if (clamped) *clamped = cl;
+    });
+}
+
+sair_status sair_frontier_insert_normalized(sair_frontier_t f, double l, double c, int* inserted) {
+    if (!f) return bad("null handle");
+    return guard([&] {
+        bool ins = sair::frontier_insert_one(f, l, c);
+        if (inserted) *inserted = ins;
+    });
+}
+
+sair_status sair_frontier_insert_batch(sair_frontier_t f, const double* pts, size_t T,
+                                       size_t* new_size) {
+    if (!f) return bad("null handle");
+    if (T && !pts) return bad("null input");
+    return guard([&] {
+        size_t F = sair::frontier_insert_batch(f, pts, T);
+        if (new_size) *new_size = F;
+    });
+}
+
+sair_status sair_frontier_size(sair_frontier_t f, size_t* F) {
+    if (!f || !F) return bad("null handle");
+    *F = f->F;
+    return SAIR_OK;
+}
+
+sair_status sair_frontier_points(sair_frontier_t f, double* l, double* c, size_t cap, size_t* F) {
+    if (!f) return bad("null handle");
+    if (F) *F = f->F;
+    if (l && c) {
+        if (cap < f->F) return bad("points: capacity too small");
+        std::memcpy(l, f->hl.data(), f->F * 8);
+        std::memcpy(c, f->hc.data(), f->F * 8);
+    }
+    return SAIR_OK;
+}
+
+sair_status sair_frontier_bounds(sair_frontier_t f, double* l_max, double* c_max) {
+    if (!f) return bad("null handle");
+    if (l_max) *l_max = f->l_max;
+    if (c_max) *c_max = f->c_max;
+    return SAIR_OK;
+}
+
+sair_status sair_frontier_hypervolume(sair_frontier_t f, double* out) {
+    if (!f || !out) return bad("null handle");
+    return guard([&] { *out = sair::frontier_point_query(f, 0.0, 0.0, sair::Q_HV, nullptr); });
+}
+
+sair_status sair_frontier_strictly_dominated(sair_frontier_t f, double l, double c, int* out) {
+    if (!f || !out) return bad("null handle");
+    return guard([&] { *out = sair::frontier_point_query(f, l, c, sair::Q_DOMINATED, nullptr) != 0.0; });
+}
+
+sair_status sair_frontier_contribution(sair_frontier_t f, double l, double c, double* out) {
+    if (!f || !out) return bad("null handle");
+    return guard([&] {
+        double dom = 0.0;
+        double v = sair::frontier_point_query(f, l, c, sair::Q_CONTRIB, &dom);
+        if (dom != 0.0)  // pareto.cpp:68-69
+            throw sair::Error(SAIR_ELOGIC,
+                              "contribution: point is dominated, caller must branch first");
+        *out = v;
+    });
+}
+
+sair_status sair_frontier_distance(sair_frontier_t f, double l, double c, double* out, int* has) {
+    if (!f || !out) return bad("null handle");
+    return guard([&] {
+        double v = sair::frontier_point_query(f, l, c, sair::Q_DISTANCE, nullptr);
+        if (has) *has = f->F > 0;
+        *out = f->F > 0 ? v : 0.0;
+    });
+}
+
+sair_status sair_frontier_reward(sair_frontier_t f, double l, double c, double* out) {
+    if (!f || !out) return bad("null handle");
+    return guard([&] { *out = sair::frontier_point_query(f, l, c, sair::Q_REWARD, nullptr); });
+}
+
+sair_status sair_frontier_score_batch(sair_frontier_t f, const double* pts, size_t T,
+                                      double* out_reward, uint8_t* out_dominated) {
+    if (!f) return bad("null handle");
+    if (T && (!pts || !out_reward)) return bad("null input");
+    return guard([&] { sair::frontier_score_batch(f, pts, T, out_reward, out_dominated); });
+}
+
+sair_status sair_frontier_score_batch_device(sair_frontier_t f, const double* pts, size_t T,
+                                             double* out_reward, uint8_t* out_dominated,
+                                             void* stream) {
+    if (!f) return bad("null handle");
+    if (T && (!pts || !out_reward)) return bad("null input");
+    return guard([&] {
+        sair::DeviceGuard g(f->device);
+        sair::frontier_score_batch_device(f, pts, T, out_reward, out_dominated,
+                                          static_cast<cudaStream_t>(stream));
+    });
+}
+
+sair_status sair_dominance_counts(const double* tuples, size_t T, int K, int device,
+                                  uint32_t* counts, uint8_t* member) {
+    if (T && !tuples) return bad("null input");
+    return guard([&] { sair::dominance_counts(tuples, T, K, device, counts, member); });
+}
+
+// ---------------------------------------------------------------- reward --
+
+sair_status sair_action_magnitude(const int32_t* deltas, size_t stages, double* out) {
+    if (!out || (stages && !deltas)) return bad("null input");
+    return guard([&] { *out = sair::action_magnitude(deltas, stages, 0); });
+}
+
+sair_status sair_compute_reward(const sair_reward_inputs* in, const int32_t* deltas, size_t stages,
+                                sair_frontier_t f, const sair_reward_config* cfg,
+                                sair_reward_breakdown* out) {
+    if (!in || !f || !cfg || !out || (stages && !deltas)) return bad("null input");
+    return guard([&] { sair::compute_reward_batch(in, deltas, stages, 1, f, cfg, out); });
+}
+
+sair_status sair_compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas,
+                                      size_t stages, size_t T, sair_frontier_t f,
+                                      const sair_reward_config* cfg, sair_reward_breakdown* out) {
+    if (!f || !cfg || (T && (!in || !out)) || (T && stages && !deltas)) return bad("null input");
+    return guard([&] { sair::compute_reward_batch(in, deltas, stages, T, f, cfg, out); });
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// internal.hpp -- host-side state behind the sair_* handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sair {
+
+// Grow-only device scratch buffer.
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+            SAIR_CUDA(cudaMalloc(&p, need));
+            bytes = need;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T) + 16)); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    ~DBuf() { release(); }
+};
+
+// Grow-only pinned host staging buffer.
+struct HBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        if (need > bytes) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            bytes = 0;
+            SAIR_CUDA(cudaMallocHost(&p, need));
+            bytes = need;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T) + 16)); }
+    ~HBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+// Host-maintained fp64 statistics (bit-identical to the reference's
+// ExperienceBuffer members sum_, sum_sq_, the reward total of loo_mean, and the
+// sigma cache; experience.hpp:82-88).
+struct StoreStats {
+    std::vector<double> sum, sum_sq, xabs;  // per dim; xabs = max |x| (filter bound)
+    double total = 0.0;                     // sum of rewards in index order
+    double rabs = 0.0;                      // max |reward| (filter bound)
+};
+
+}  // namespace sair
+
+// ------------------------------------------------------------------ store --
+struct sair_store_s {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    double r_min = 0.0;
+    uint64_t rejected = 0;
+    int d = 0;   // 0 until the first accepted row fixes it (experience.cpp:140-145)
+    int dp = 0;  // padded dimension of the fp32 page layout
+    size_t n = 0, cap = 0;
+    int64_t gbase = 0;  // global index of local record 0 (shard offset)
+
+    sair::StoreStats stats;
+    double cached_sigma = 0.0;  // experience.hpp:87
+    size_t stale = 0;           // experience.hpp:88
+
+    // device SoA
+    float* pages = nullptr;  // [cap/PAGE][dp][PAGE] fp32 filter copy
+    float* r32 = nullptr;    // [cap] fp32 rewards (filter)
+    double* r64 = nullptr;   // [cap] exact rewards
+    int32_t* rnd = nullptr;  // [cap] rounds (tie-break)
+    double* x64 = nullptr;   // [cap][d] exact contexts (record-major, refine/gather)
+
+    // scratch
+    sair::DBuf b_stage, b_cand, b_merged, b_thr, b_z, b_consts, b_out, b_exact, b_sigma, b_red;
+    sair::HBuf h_stage, h_out;
+    sair_select_stats last{};
+};
+
+// --------------------------------------------------------------- frontier --
+struct sair_frontier_s {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    double l_max = 1.0, c_max = 1.0;
+    size_t F = 0, cap = 0;
+    double* fl = nullptr;  // [cap] latency asc
+    double* fc = nullptr;  // [cap] cost (strictly desc)
+    double hv = 0.0;       // hypervolume() of the current points (host copy)
+    std::vector<double> hl, hc;  // host mirror for points()
+    sair::DBuf b_tmp, b_in, b_out, b_sort;
+    sair::HBuf h_io;
+};
+
+namespace sair {
+
+// store.cu
+void store_init(sair_store_s* s, double r_min, int device, size_t capacity_hint);
+void store_free(sair_store_s* s);
+void store_clone(const sair_store_s* s, sair_store_s* out);
+void store_reserve(sair_store_s* s, size_t need);
+size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
+                    const double* reward, const int32_t* round, uint8_t* accepted);
+void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int dim, int clustered);
+void store_standardize(const sair_store_s* s, const double* x, double* z);
+double store_effective_sigma(sair_store_s* s, double sigma_sim);
+void store_mean_sd(const sair_store_s* s, double* mean, double* sd);
+
+// select.cu
+void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
+                  const sair_select_config& cfg, int64_t* out_idx, double* out_sim, double* out_score, size_t* out_count,
+                  int64_t* out_nn, double* out_nn_sim);
+double store_surprisal(sair_store_s* s, size_t index, const double* x,
+                       const sair_select_config& cfg);
+
+// pareto.cu
+enum { Q_DOMINATED = 0, Q_CONTRIB = 1, Q_DISTANCE = 2, Q_REWARD = 3, Q_HV = 4 };
+void frontier_init(sair_frontier_s* f, double l_max, double c_max, int device);
+void frontier_free(sair_frontier_s* f);
+void frontier_clone(const sair_frontier_s* f, sair_frontier_s* o);
+bool frontier_insert_one(sair_frontier_s* f, double pl, double pc);
+size_t frontier_insert_batch(sair_frontier_s* f, const double* pts, size_t T);
+double frontier_point_query(sair_frontier_s* f, double pl, double pc, int op, double* aux);
+void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, double* out,
+                          uint8_t* dom);
+void frontier_score_batch_device(sair_frontier_s* f, const double* dpts, size_t T, double* dout,
+                                 uint8_t* ddom, cudaStream_t st);
+void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_t* counts,
+                      uint8_t* member);
+void compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas, size_t S, size_t T,
+                          sair_frontier_s* f, const sair_reward_config* cfg,
+                          sair_reward_breakdown* out);
+double action_magnitude(const int32_t* deltas, size_t S, int device);
+
+}  // namespace sair

@@ -1,0 +1,828 @@
+// pareto.cu -- Pareto-dominance reward shaping on the device.
+//
+// Restates ParetoFrontier (pareto.cpp:9-89) and compute_reward
+// (reward.cpp:9-44):
+//   K6  batch frontier maintenance: T sequential insert_normalized() calls are
+//       order-independent (the result is the non-dominated set of F u P with
+//       first occurrences of duplicates kept), so the batch is a radix sort by
+//       (latency, cost, arrival) + an exclusive prefix-min of cost + compaction.
+//   K8  per-tuple scoring against a sorted frontier: binary search for the
+//       dominance test, pruned bidirectional scan for the distance, the
+//       reference's own hypervolume sequence for the contribution.
+//   K7  k-objective dominance counts: per-objective dense ranks (exact
+//       comparisons on integers), sort by rank sum (a dominator has a strictly
+//       smaller sum), tiled pairwise tests with shared-memory j-tiles.
+//   reward: the five-term compute_reward per row, fused with K8.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "internal.hpp"
+
+
+namespace sair {
+
+// dominates, pareto.cpp:9-12
+__device__ __forceinline__ bool dom2(double pl, double pc, double ql, double qc) {
+    return pl <= ql && pc <= qc && (pl < ql || pc < qc);
+}
+
+// ------------------------------------------------------------- K8 helpers --
+
+struct FrontierView {
+    const double* l;
+    const double* c;
+    size_t F;
+    double hv;  // hypervolume of the view (reference sequence)
+};
+
+// first index with l[i] > x
+__device__ __forceinline__ size_t upper_bound_l(const FrontierView& f, double x) {
+    size_t lo = 0, hi = f.F;
+    while (lo < hi) {
+        size_t mid = (lo + hi) >> 1;
+        if (f.l[mid] > x) hi = mid; else lo = mid + 1;
+    }
+    return lo;
+}
+// first index with l[i] >= x
+__device__ __forceinline__ size_t lower_bound_l(const FrontierView& f, double x) {
+    size_t lo = 0, hi = f.F;
+    while (lo < hi) {
+        size_t mid = (lo + hi) >> 1;
+        if (f.l[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// strictly_dominated, pareto.cpp:31-34: the candidate dominator is the point
+// with the largest latency <= pl (the cheapest among those, costs descend).
+__device__ bool f_dominated(const FrontierView& f, double pl, double pc) {
+    size_t u = upper_bound_l(f, pl);
+    if (u == 0) return false;
+    return dom2(f.l[u - 1], f.c[u - 1], pl, pc);
+}
+
+// distance, pareto.cpp:75-84: min over points of dl^2 + dc^2, then sqrt.
+// Latencies are sorted, so scanning outwards from pl can stop once dl^2
+// alone reaches the best value; the minimum is the same value as the
+// reference's full scan.
+__device__ double f_distance(const FrontierView& f, double pl, double pc) {
+    double best = INFINITY;
+    size_t u = upper_bound_l(f, pl);
+    for (size_t i = u; i-- > 0;) {
+        double dl = dsub(pl, f.l[i]);
+        double dl2 = dmul(dl, dl);
+        if (dl2 >= best) break;
+        double dc = dsub(pc, f.c[i]);
+        double v = dadd(dl2, dmul(dc, dc));
+        best = fmin(best, v);
+    }
+    for (size_t i = u; i < f.F; ++i) {
+        double dl = dsub(pl, f.l[i]);
+        double dl2 = dmul(dl, dl);
+        if (dl2 >= best) break;
+        double dc = dsub(pc, f.c[i]);
+        double v = dadd(dl2, dmul(dc, dc));
+        best = fmin(best, v);
+    }
+    return sqrt(best);
+}
+
+// contribution, pareto.cpp:67-73, for a non-dominated p.  For small frontiers
+// the reference's exact sequence is replayed (copy, insert, hypervolume of the
+// result minus hypervolume()), so the value is bit-identical; for large ones
+// the exclusive area is summed locally over p's dominated run.
+__device__ double f_contribution(const FrontierView& f, double pl, double pc) {
+    size_t a = lower_bound_l(f, pl);
+    if (a < f.F && f.l[a] == pl && f.c[a] == pc) return 0.0;  // duplicate: no-op insert
+    if (f.F <= 64) {
+        // hypervolume (pareto.cpp:56-65) of: survivors l < pl, p, survivors l > pl
+        double hv = 0.0;
+        bool placed = false;
+        double cur_l = 0.0, cur_c = 0.0;
+        bool have = false;
+        auto emit = [&](double l, double c) {
+            if (have) hv = dadd(hv, dmul(dsub(l, cur_l), dsub(1.0, cur_c)));
+            cur_l = l;
+            cur_c = c;
+            have = true;
+        };
+        for (size_t i = 0; i < f.F; ++i) {
+            double l = f.l[i], c = f.c[i];
+            if (dom2(pl, pc, l, c)) continue;  // erased by insert_normalized
+            if (!placed && !(l < pl)) {
+                emit(pl, pc);
+                placed = true;
+            }
+            emit(l, c);
+        }
+        if (!placed) emit(pl, pc);
+        if (have) hv = dadd(hv, dmul(dsub(1.0, cur_l), dsub(1.0, cur_c)));
+        return dsub(hv, f.hv);
+    }
+    // exclusive area of [pl,1]x[pc,1] not covered by the frontier's boxes
+    double c_prev = a > 0 ? f.c[a - 1] : 1.0;
+    double l_next = a < f.F ? f.l[a] : 1.0;
+    double area = dmul(dsub(l_next, pl), dsub(fmin(c_prev, 1.0), pc));
+    for (size_t j = a; j < f.F && f.c[j] >= pc; ++j) {
+        double ln = j + 1 < f.F ? f.l[j + 1] : 1.0;
+        area = dadd(area, dmul(dsub(ln, f.l[j]), dsub(f.c[j], pc)));
+    }
+    return area;
+}
+
+// reward, pareto.cpp:86-89
+__device__ double f_reward(const FrontierView& f, double pl, double pc, bool* dominated) {
+    bool dm = f_dominated(f, pl, pc);
+    if (dominated) *dominated = dm;
+    if (!dm) return dadd(1.0, f_contribution(f, pl, pc));
+    return ddiv(0.8, dadd(1.0, f_distance(f, pl, pc)));
+}
+
+// normalize, pareto.cpp:20-29
+__device__ __forceinline__ void f_normalize(double l_max, double c_max, double l_ms,
+                                            double cost, double* pl, double* pc, bool* clamped) {
+    double l = ddiv(l_ms, l_max), c = ddiv(cost, c_max);
+    bool hit = false;
+    if (l > 1.0) { l = 1.0; hit = true; }
+    if (c > 1.0) { c = 1.0; hit = true; }
+    if (l < 0.0) l = 0.0;
+    if (c < 0.0) c = 0.0;
+    *pl = l;
+    *pc = c;
+    if (clamped) *clamped = hit;
+}
+
+// ----------------------------------------------------------------- kernels --
+
+__global__ void score_batch_kernel(FrontierView f, const double* __restrict__ pts, size_t T,
+                                   double* __restrict__ out, uint8_t* __restrict__ dom_out) {
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < T;
+         t += (size_t)gridDim.x * blockDim.x) {
+        bool dm;
+        out[t] = f_reward(f, pts[2 * t], pts[2 * t + 1], &dm);
+        if (dom_out) dom_out[t] = dm;
+    }
+}
+
+// op codes for the single-point query kernel
+
+__global__ void point_query_kernel(FrontierView f, double pl, double pc, int op,
+                                   double* __restrict__ out) {
+    if (threadIdx.x || blockIdx.x) return;
+    switch (op) {
+        case Q_DOMINATED: out[0] = f_dominated(f, pl, pc) ? 1.0 : 0.0; break;
+        case Q_CONTRIB:
+            out[1] = f_dominated(f, pl, pc) ? 1.0 : 0.0;
+            out[0] = out[1] != 0.0 ? 0.0 : f_contribution(f, pl, pc);
+            break;
+        case Q_DISTANCE: out[0] = f.F ? f_distance(f, pl, pc) : -1.0; break;
+        case Q_REWARD: out[0] = f_reward(f, pl, pc, nullptr); break;
+        case Q_HV: {
+            double hv = 0.0;  // pareto.cpp:56-65
+            for (size_t i = 0; i < f.F; ++i) {
+                double nl = i + 1 < f.F ? f.l[i + 1] : 1.0;
+                hv = dadd(hv, dmul(dsub(nl, f.l[i]), dsub(1.0, f.c[i])));
+            }
+            out[0] = hv;
+            break;
+        }
+    }
+}
+
+// insert_normalized, pareto.cpp:43-54, one point, one CTA: reject test, then
+// survivors (not dominated by p) compacted around p's lower_bound slot.
+__global__ void __launch_bounds__(1024)
+    insert_one_kernel(const double* __restrict__ fl, const double* __restrict__ fc, size_t F,
+                      double pl, double pc, double* __restrict__ ol, double* __restrict__ oc,
+                      unsigned long long* __restrict__ res /* [0]=inserted, [1]=newF */) {
+    __shared__ int s_reject;
+    __shared__ unsigned s_wsum[32];
+    __shared__ size_t s_base;
+    if (threadIdx.x == 0) {
+        s_reject = 0;
+        s_base = 0;
+    }
+    __syncthreads();
+    for (size_t i = threadIdx.x; i < F; i += blockDim.x)
+        if ((fl[i] == pl && fc[i] == pc) || dom2(fl[i], fc[i], pl, pc)) s_reject = 1;
+    __syncthreads();
+    if (s_reject) {
+        if (threadIdx.x == 0) {
+            res[0] = 0;
+            res[1] = F;
+        }
+        return;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    bool placed_total = false;
+    for (size_t c0 = 0; c0 < F; c0 += blockDim.x) {
+        size_t i = c0 + threadIdx.x;
+        bool keep = i < F && !dom2(pl, pc, fl[i], fc[i]);
+        bool before = keep && fl[i] < pl;
+        unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_wsum[warp] = __popc(bal);
+        __syncthreads();
+        unsigned off = 0, tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) off += s_wsum[w];
+            tot += s_wsum[w];
+        }
+        size_t rank = s_base + off + __popc(bal & ((1u << lane) - 1u));
+        if (keep) {
+            size_t pos = before ? rank : rank + 1;
+            ol[pos] = fl[i];
+            oc[pos] = fc[i];
+        }
+        // p goes right after the last survivor with l < pl
+        int nbefore = __syncthreads_count(before);
+        if (!placed_total && (size_t)nbefore < (size_t)tot) {
+            // survivors are sorted, so the first survivor with l >= pl is in this chunk
+            if (threadIdx.x == 0) {
+                ol[s_base + nbefore] = pl;
+                oc[s_base + nbefore] = pc;
+            }
+            placed_total = true;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (!placed_total) {
+            ol[s_base] = pl;
+            oc[s_base] = pc;
+        }
+        res[0] = 1;
+        res[1] = s_base + 1;
+    }
+}
+
+// ---- K6 batch insert --------------------------------------------------------
+
+__device__ __forceinline__ uint64_t ord64(double v) {
+    if (v == 0.0) v = 0.0;  // -0 and +0 compare equal in the reference
+    uint64_t u = (uint64_t)__double_as_longlong(v);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+__global__ void batch_keys_kernel(const double* __restrict__ l, const double* __restrict__ c,
+                                  size_t n, uint64_t* __restrict__ kl, uint64_t* __restrict__ kc,
+                                  uint32_t* __restrict__ pos) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        kl[i] = ord64(l[i]);
+        kc[i] = ord64(c[i]);
+        pos[i] = (uint32_t)i;
+    }
+}
+
+__global__ void gather_key_kernel(const uint64_t* __restrict__ key, const uint32_t* __restrict__ perm,
+                                  size_t n, uint64_t* __restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = key[perm[i]];
+}
+
+// sorted cost (by lexicographic order) for the prefix-min scan
+__global__ void sorted_cost_kernel(const double* __restrict__ c, const uint32_t* __restrict__ perm,
+                                   size_t n, double* __restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x)
+        out[i] = c[perm[i]];
+}
+
+struct MinOp {
+    __device__ __forceinline__ double operator()(double a, double b) const { return a < b ? a : b; }
+};
+
+// member = first of its duplicate run && cost < min cost of every
+// lexicographically smaller point
+__global__ void member_kernel(const double* __restrict__ l, const double* __restrict__ c,
+                              const uint32_t* __restrict__ perm, const double* __restrict__ pmin,
+                              size_t n, uint32_t* __restrict__ flag) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t p = perm[i];
+        bool first = i == 0 || !(l[perm[i - 1]] == l[p] && c[perm[i - 1]] == c[p]);
+        flag[i] = first && c[p] < pmin[i] ? 1u : 0u;
+    }
+}
+
+__global__ void compact_kernel(const double* __restrict__ l, const double* __restrict__ c,
+                               const uint32_t* __restrict__ perm, const uint32_t* __restrict__ flag,
+                               const uint32_t* __restrict__ slot, size_t n,
+                               double* __restrict__ ol, double* __restrict__ oc) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        if (!flag[i]) continue;
+        uint32_t p = perm[i];
+        ol[slot[i]] = l[p];
+        oc[slot[i]] = c[p];
+    }
+}
+
+// ---- K7 k-objective dominance counts ----------------------------------------
+
+__global__ void col_keys_kernel(const double* __restrict__ t, size_t T, int K, int k,
+                                uint64_t* __restrict__ key, uint32_t* __restrict__ pos) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x) {
+        key[i] = ord64(t[i * K + k]);
+        pos[i] = (uint32_t)i;
+    }
+}
+
+__global__ void new_value_kernel(const uint64_t* __restrict__ skey, size_t T,
+                                 uint32_t* __restrict__ flag) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x)
+        flag[i] = (i > 0 && skey[i] != skey[i - 1]) ? 1u : 0u;
+}
+
+__global__ void scatter_rank_kernel(const uint32_t* __restrict__ rank_sorted,
+                                    const uint32_t* __restrict__ perm, size_t T, int K, int k,
+                                    uint32_t* __restrict__ ranks, uint32_t* __restrict__ rsum) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t p = perm[i];
+        ranks[(size_t)p * K + k] = rank_sorted[i];
+        if (k == 0) rsum[p] = rank_sorted[i];
+        else rsum[p] += rank_sorted[i];
+    }
+}
+
+__global__ void pack_sorted_kernel(const uint32_t* __restrict__ ranks, const uint32_t* __restrict__ perm,
+                                   size_t T, int K, uint32_t* __restrict__ sranks) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t p = perm[i];
+        for (int k = 0; k < K; ++k) sranks[i * K + k] = ranks[(size_t)p * K + k];
+    }
+}
+
+// Tuples are sorted by rank sum.  j dominates i => sum_j < sum_i, and equal
+// tuples have equal sums, so every j that matters lies before the first
+// position whose sum exceeds the i-tile's largest sum.  One thread per i;
+// j-tiles staged in shared memory; dominance is `all(rj <= ri) && rj != ri`.
+template <int K>
+__global__ void __launch_bounds__(256)
+    dominance_kernel(const uint32_t* __restrict__ sr, const uint32_t* __restrict__ ssum,
+                     const uint32_t* __restrict__ perm, size_t T, int members_only,
+                     uint32_t* __restrict__ counts, uint8_t* __restrict__ member) {
+    constexpr int TILE = 256;
+    __shared__ uint32_t tj[TILE * K];
+    __shared__ uint32_t tp[TILE];
+    const size_t i0 = (size_t)blockIdx.x * TILE;
+    const size_t i = i0 + threadIdx.x;
+    const bool valid = i < T;
+    uint32_t ri[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) ri[k] = valid ? sr[i * K + k] : 0xFFFFFFFFu;
+    const uint32_t pi = valid ? perm[i] : 0xFFFFFFFFu;
+    // j range: [0, first position with sum > max sum of this tile)
+    const size_t ilast = min(i0 + TILE, T) - 1;
+    const uint32_t smax = ssum[ilast];
+    size_t lo = ilast, hi = T;  // first index with ssum > smax
+    while (lo < hi) {
+        size_t mid = (lo + hi) >> 1;
+        if (ssum[mid] > smax) hi = mid; else lo = mid + 1;
+    }
+    const size_t jend = lo;
+    uint32_t cnt = 0;
+    bool dup = false;
+    for (size_t j0 = 0; j0 < jend; j0 += TILE) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < TILE; t += blockDim.x) {
+            size_t j = j0 + t;
+#pragma unroll
+            for (int k = 0; k < K; ++k) tj[t * K + k] = j < jend ? sr[j * K + k] : 0xFFFFFFFFu;
+            tp[t] = j < jend ? perm[j] : 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        const int lim = (int)min((size_t)TILE, jend - j0);
+        for (int t = 0; t < lim; ++t) {
+            bool le = true, eq = true;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                uint32_t v = tj[t * K + k];
+                le &= v <= ri[k];
+                eq &= v == ri[k];
+            }
+            cnt += (le && !eq) ? 1u : 0u;
+            dup |= eq && tp[t] < pi;
+        }
+        if (members_only && __syncthreads_and(!valid || cnt > 0 || dup)) break;
+    }
+    if (valid) {
+        if (counts) counts[pi] = cnt;
+        if (member) member[pi] = (cnt == 0 && !dup) ? 1 : 0;
+    }
+}
+
+// ---- reward ---------------------------------------------------------------
+
+struct RewardCfg {
+    double t_sla, l_base, c_budget, w_l, w_c, w_p, r_max;
+};
+
+// action_magnitude, reward.cpp:9-19
+__device__ double action_mu(const int32_t* d, size_t S) {
+    double mu = 0.0;
+    int scaled = 0;
+    for (size_t s = 0; s < S; ++s) {
+        const int32_t* x = d + 4 * s;
+        mu = dadd(mu, (double)abs(x[0]));
+        double inner = dadd(dadd(ddiv((double)abs(x[1]), 500.0), ddiv((double)abs(x[2]), 256.0)),
+                            ddiv((double)abs(x[3]), 10.0));
+        mu = dadd(mu, dmul(0.5, inner));
+        scaled += (x[0] | x[1] | x[2] | x[3]) != 0;
+    }
+    return dadd(mu, dmul(0.5, (double)scaled));
+}
+
+__global__ void action_mu_kernel(const int32_t* __restrict__ d, size_t S, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *out = action_mu(d, S);
+}
+
+// compute_reward, reward.cpp:21-44 (config validity checked on the host)
+__global__ void reward_kernel(const double* __restrict__ in, const int32_t* __restrict__ deltas,
+                              size_t S, size_t T, FrontierView f, double l_max, double c_max,
+                              RewardCfg cfg, double* __restrict__ out) {
+    for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < T;
+         t += (size_t)gridDim.x * blockDim.x) {
+        const double lb = in[4 * t], la = in[4 * t + 1], cb = in[4 * t + 2], ca = in[4 * t + 3];
+        double latency = ddiv(dmul(cfg.w_l, dsub(lb, la)), cfg.l_base);
+        double cost = ddiv(dmul(-cfg.w_c, dsub(ca, cb)), cfg.c_budget);
+        double sla = 0.0;
+        if (la > cfg.t_sla) {
+            double ratio = ddiv(la, cfg.t_sla);
+            sla = dadd(-dmul(ratio, ratio), 1.0);
+        }
+        double sg = dsub(ddiv(lb, cfg.t_sla), 1.0);
+        if (sg < 0.0) sg = 0.0;  // std::max(0.0, .)
+        double proactive = dmul(dmul(sg, action_mu(deltas + t * S * 4, S)), cfg.w_p);
+        double pl, pc;
+        f_normalize(l_max, c_max, la, ca, &pl, &pc, nullptr);
+        double pareto = f_reward(f, pl, pc, nullptr);
+        double sum = dadd(dadd(dadd(dadd(latency, cost), sla), proactive), pareto);
+        double total = sum < -cfg.r_max ? -cfg.r_max : (cfg.r_max < sum ? cfg.r_max : sum);
+        double* o = out + 7 * t;
+        o[0] = latency;
+        o[1] = cost;
+        o[2] = sla;
+        o[3] = proactive;
+        o[4] = pareto;
+        o[5] = total;
+        o[6] = total != sum ? 1.0 : 0.0;
+    }
+}
+
+// ------------------------------------------------------------------- host --
+
+static int grid_for(size_t n, int threads = 256) {
+    return (int)std::max<size_t>(1, std::min<size_t>((n + threads - 1) / threads, 148 * 32));
+}
+
+static FrontierView view(const sair_frontier_s* f) { return FrontierView{f->fl, f->fc, f->F, f->hv}; }
+
+void frontier_init(sair_frontier_s* f, double l_max, double c_max, int device) {
+    // pareto.cpp:14-18
+    if (l_max <= 0.0 || c_max <= 0.0)
+        throw Error(SAIR_EINVAL, "ParetoFrontier: normalizers must be positive");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(SAIR_ECUDA, "no CUDA device (libsair has no CPU fallback)");
+    if (device < 0 || device >= ndev) throw Error(SAIR_EINVAL, "device ordinal out of range");
+    f->device = device;
+    f->l_max = l_max;
+    f->c_max = c_max;
+    DeviceGuard g(device);
+    SAIR_CUDA(cudaStreamCreateWithFlags(&f->st, cudaStreamNonBlocking));
+}
+
+void frontier_free(sair_frontier_s* f) {
+    DeviceGuard g(f->device);
+    if (f->st) cudaStreamSynchronize(f->st);
+    cudaFree(f->fl);
+    cudaFree(f->fc);
+    f->fl = f->fc = nullptr;
+    f->b_tmp.release();
+    f->b_in.release();
+    f->b_out.release();
+    f->b_sort.release();
+    if (f->st) cudaStreamDestroy(f->st);
+    f->st = nullptr;
+}
+
+static void reserve(sair_frontier_s* f, size_t need) {
+    if (need <= f->cap) return;
+    size_t cap = std::max<size_t>({need, f->cap * 2, 64});
+    double *l, *c;
+    SAIR_CUDA(cudaMalloc(&l, cap * 8));
+    SAIR_CUDA(cudaMalloc(&c, cap * 8));
+    if (f->F) {
+        SAIR_CUDA(cudaMemcpyAsync(l, f->fl, f->F * 8, cudaMemcpyDeviceToDevice, f->st));
+        SAIR_CUDA(cudaMemcpyAsync(c, f->fc, f->F * 8, cudaMemcpyDeviceToDevice, f->st));
+    }
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    cudaFree(f->fl);
+    cudaFree(f->fc);
+    f->fl = l;
+    f->fc = c;
+    f->cap = cap;
+}
+
+// refresh the host mirror and the cached hypervolume after a change
+static void sync_mirror(sair_frontier_s* f) {
+    f->hl.resize(f->F);
+    f->hc.resize(f->F);
+    if (f->F) {
+        SAIR_CUDA(cudaMemcpyAsync(f->hl.data(), f->fl, f->F * 8, cudaMemcpyDeviceToHost, f->st));
+        SAIR_CUDA(cudaMemcpyAsync(f->hc.data(), f->fc, f->F * 8, cudaMemcpyDeviceToHost, f->st));
+    }
+    double* d = f->b_tmp.as<double>(4);
+    point_query_kernel<<<1, 32, 0, f->st>>>(view(f), 0.0, 0.0, Q_HV, d);
+    SAIR_LAUNCH("point_query_kernel(hv)");
+    SAIR_CUDA(cudaMemcpyAsync(&f->hv, d, 8, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+}
+
+void frontier_clone(const sair_frontier_s* f, sair_frontier_s* o) {
+    frontier_init(o, f->l_max, f->c_max, f->device);
+    DeviceGuard g(f->device);
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    reserve(o, std::max<size_t>(f->F, 1));
+    if (f->F) {
+        SAIR_CUDA(cudaMemcpyAsync(o->fl, f->fl, f->F * 8, cudaMemcpyDeviceToDevice, o->st));
+        SAIR_CUDA(cudaMemcpyAsync(o->fc, f->fc, f->F * 8, cudaMemcpyDeviceToDevice, o->st));
+    }
+    SAIR_CUDA(cudaStreamSynchronize(o->st));
+    o->F = f->F;
+    o->hv = f->hv;
+    o->hl = f->hl;
+    o->hc = f->hc;
+}
+
+bool frontier_insert_one(sair_frontier_s* f, double pl, double pc) {
+    DeviceGuard g(f->device);
+    reserve(f, f->F + 1);
+    double* ol = f->b_out.as<double>(2 * (f->F + 1) + 4);
+    double* oc = ol + (f->F + 1);
+    auto* res = reinterpret_cast<unsigned long long*>(f->b_tmp.as<double>(4));
+    insert_one_kernel<<<1, 1024, 0, f->st>>>(f->fl, f->fc, f->F, pl, pc, ol, oc, res);
+    SAIR_LAUNCH("insert_one_kernel");
+    unsigned long long h[2];
+    SAIR_CUDA(cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    if (!h[0]) return false;
+    size_t nF = (size_t)h[1];
+    SAIR_CUDA(cudaMemcpyAsync(f->fl, ol, nF * 8, cudaMemcpyDeviceToDevice, f->st));
+    SAIR_CUDA(cudaMemcpyAsync(f->fc, oc, nF * 8, cudaMemcpyDeviceToDevice, f->st));
+    f->F = nF;
+    sync_mirror(f);
+    return true;
+}
+
+size_t frontier_insert_batch(sair_frontier_s* f, const double* pts, size_t T) {
+    if (T == 0) return f->F;
+    DeviceGuard g(f->device);
+    const size_t n = f->F + T;
+    if (n >= 0xFFFFFFFFull) throw Error(SAIR_EINVAL, "batch too large");
+    // layout: l[n], c[n], kl[n], kc[n], kt[n], pos[n], perm[n], perm2[n], pmin[n], flag[n], slot[n]
+    char* base = static_cast<char*>(f->b_in.get(n * (8 * 6 + 4 * 5) + 4096));
+    size_t off = 0;
+    auto take = [&](size_t b) {
+        char* p = base + off;
+        off += (b + 255) / 256 * 256;
+        return p;
+    };
+    double* l = reinterpret_cast<double*>(take(n * 8));
+    double* c = reinterpret_cast<double*>(take(n * 8));
+    uint64_t* kl = reinterpret_cast<uint64_t*>(take(n * 8));
+    uint64_t* kc = reinterpret_cast<uint64_t*>(take(n * 8));
+    uint64_t* kt = reinterpret_cast<uint64_t*>(take(n * 8));
+    double* pmin = reinterpret_cast<double*>(take(n * 8));
+    uint32_t* pos = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* perm = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* perm2 = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* flag = reinterpret_cast<uint32_t*>(take(n * 4));
+    uint32_t* slot = reinterpret_cast<uint32_t*>(take(n * 4));
+    // existing frontier first: it is the earliest arrival
+    if (f->F) {
+        SAIR_CUDA(cudaMemcpyAsync(l, f->fl, f->F * 8, cudaMemcpyDeviceToDevice, f->st));
+        SAIR_CUDA(cudaMemcpyAsync(c, f->fc, f->F * 8, cudaMemcpyDeviceToDevice, f->st));
+    }
+    {
+        double* h = f->h_io.as<double>(2 * T);
+        for (size_t t = 0; t < T; ++t) {
+            h[t] = pts[2 * t];
+            h[T + t] = pts[2 * t + 1];
+        }
+        SAIR_CUDA(cudaMemcpyAsync(l + f->F, h, T * 8, cudaMemcpyHostToDevice, f->st));
+        SAIR_CUDA(cudaMemcpyAsync(c + f->F, h + T, T * 8, cudaMemcpyHostToDevice, f->st));
+    }
+    batch_keys_kernel<<<grid_for(n), 256, 0, f->st>>>(l, c, n, kl, kc, pos);
+    SAIR_LAUNCH("batch_keys_kernel");
+    // LSD: stable by cost, then stable by latency -> (l, c, arrival)
+    size_t tmp = 0, tmp2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, kc, kt, pos, perm, (int)n);
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp2, kl, kt, perm2, perm, (int)n);
+    size_t tmp3 = 0;
+    cub::DeviceScan::ExclusiveScan(nullptr, tmp3, pmin, reinterpret_cast<double*>(kt), MinOp(), (double)INFINITY, (int)n);
+    size_t tmp4 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp4, flag, slot, (int)n);
+    void* dtmp = f->b_sort.get(std::max({tmp, tmp2, tmp3, tmp4}) + 256);
+    size_t tb = f->b_sort.bytes;
+    SAIR_CUDA(cub::DeviceRadixSort::SortPairs(dtmp, tb, kc, kt, pos, perm2, (int)n, 0, 64, f->st));
+    gather_key_kernel<<<grid_for(n), 256, 0, f->st>>>(kl, perm2, n, kc);  // kc := l-key in c-order
+    SAIR_LAUNCH("gather_key_kernel");
+    tb = f->b_sort.bytes;
+    SAIR_CUDA(cub::DeviceRadixSort::SortPairs(dtmp, tb, kc, kt, perm2, perm, (int)n, 0, 64, f->st));
+    sorted_cost_kernel<<<grid_for(n), 256, 0, f->st>>>(c, perm, n, pmin);
+    SAIR_LAUNCH("sorted_cost_kernel");
+    tb = f->b_sort.bytes;
+    SAIR_CUDA(cub::DeviceScan::ExclusiveScan(dtmp, tb, pmin, reinterpret_cast<double*>(kt), MinOp(),
+                                             (double)INFINITY, (int)n, f->st));
+    member_kernel<<<grid_for(n), 256, 0, f->st>>>(l, c, perm, reinterpret_cast<double*>(kt), n,
+                                                  flag);
+    SAIR_LAUNCH("member_kernel");
+    tb = f->b_sort.bytes;
+    SAIR_CUDA(cub::DeviceScan::ExclusiveSum(dtmp, tb, flag, slot, (int)n, f->st));
+    uint32_t last[2];
+    SAIR_CUDA(cudaMemcpyAsync(&last[0], slot + n - 1, 4, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaMemcpyAsync(&last[1], flag + n - 1, 4, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    const size_t nF = (size_t)last[0] + last[1];
+    reserve(f, nF);
+    compact_kernel<<<grid_for(n), 256, 0, f->st>>>(l, c, perm, flag, slot, n, f->fl, f->fc);
+    SAIR_LAUNCH("compact_kernel");
+    f->F = nF;
+    sync_mirror(f);
+    return nF;
+}
+
+double frontier_point_query(sair_frontier_s* f, double pl, double pc, int op, double* aux) {
+    DeviceGuard g(f->device);
+    double* d = f->b_tmp.as<double>(4);
+    point_query_kernel<<<1, 32, 0, f->st>>>(view(f), pl, pc, op, d);
+    SAIR_LAUNCH("point_query_kernel");
+    double h[2] = {0.0, 0.0};
+    SAIR_CUDA(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    if (aux) *aux = h[1];
+    return h[0];
+}
+
+void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, double* out,
+                          uint8_t* dom) {
+    if (T == 0) return;
+    DeviceGuard g(f->device);
+    char* base = static_cast<char*>(f->b_in.get(T * (16 + 8 + 1) + 1024));
+    double* dp = reinterpret_cast<double*>(base);
+    double* dout = dp + 2 * T;
+    uint8_t* ddom = reinterpret_cast<uint8_t*>(dout + T);
+    SAIR_CUDA(cudaMemcpyAsync(dp, pts, T * 16, cudaMemcpyHostToDevice, f->st));
+    score_batch_kernel<<<grid_for(T), 256, 0, f->st>>>(view(f), dp, T, dout, ddom);
+    SAIR_LAUNCH("score_batch_kernel");
+    SAIR_CUDA(cudaMemcpyAsync(out, dout, T * 8, cudaMemcpyDeviceToHost, f->st));
+    if (dom) SAIR_CUDA(cudaMemcpyAsync(dom, ddom, T, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+}
+
+// device-pointer variant (bench: tuples resident in HBM)
+void frontier_score_batch_device(sair_frontier_s* f, const double* dpts, size_t T, double* dout,
+                                 uint8_t* ddom, cudaStream_t st) {
+    score_batch_kernel<<<grid_for(T), 256, 0, st>>>(view(f), dpts, T, dout, ddom);
+    SAIR_LAUNCH("score_batch_kernel");
+}
+
+void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_t* counts,
+                      uint8_t* member) {
+    if (T == 0) return;
+    if (K < 1 || K > 8) throw Error(SAIR_EINVAL, "dominance: K must be in 1..8");
+    if (T >= 0xFFFFFFF0ull) throw Error(SAIR_EINVAL, "dominance: too many tuples");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(SAIR_ECUDA, "no CUDA device (libsair has no CPU fallback)");
+    DeviceGuard g(device);
+    cudaStream_t st;
+    SAIR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DBuf b_all, b_tmp;
+    char* base = static_cast<char*>(
+        b_all.get(T * (size_t)K * 8 + T * 8 * 2 + T * 4 * 6 + T * (size_t)K * 4 * 2 + T + 8192));
+    size_t off = 0;
+    auto take = [&](size_t b) {
+        char* p = base + off;
+        off += (b + 255) / 256 * 256;
+        return p;
+    };
+    double* dt = reinterpret_cast<double*>(take(T * K * 8));
+    uint64_t* key = reinterpret_cast<uint64_t*>(take(T * 8));
+    uint64_t* skey = reinterpret_cast<uint64_t*>(take(T * 8));
+    uint32_t* pos = reinterpret_cast<uint32_t*>(take(T * 4));
+    uint32_t* perm = reinterpret_cast<uint32_t*>(take(T * 4));
+    uint32_t* flag = reinterpret_cast<uint32_t*>(take(T * 4));
+    uint32_t* rk = reinterpret_cast<uint32_t*>(take(T * 4));
+    uint32_t* rsum = reinterpret_cast<uint32_t*>(take(T * 4));
+    uint32_t* ssum = reinterpret_cast<uint32_t*>(take(T * 4));
+    uint32_t* ranks = reinterpret_cast<uint32_t*>(take(T * K * 4));
+    uint32_t* sranks = reinterpret_cast<uint32_t*>(take(T * K * 4));
+    uint32_t* dcnt = reinterpret_cast<uint32_t*>(take(T * 4));
+    uint8_t* dmem = reinterpret_cast<uint8_t*>(take(T));
+    SAIR_CUDA(cudaMemcpyAsync(dt, tuples, T * K * 8, cudaMemcpyHostToDevice, st));
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, key, skey, pos, perm, (int)T);
+    cub::DeviceScan::InclusiveSum(nullptr, t2, flag, rk, (int)T);
+    cub::DeviceRadixSort::SortPairs(nullptr, t3, rsum, ssum, pos, perm, (int)T);
+    void* tmp = b_tmp.get(std::max({t1, t2, t3}) + 256);
+    const int gr = grid_for(T);
+    // dense ranks per objective: equal values share a rank, so comparisons on
+    // ranks are the exact fp64 comparisons of dominates()
+    for (int k = 0; k < K; ++k) {
+        col_keys_kernel<<<gr, 256, 0, st>>>(dt, T, K, k, key, pos);
+        size_t tb = b_tmp.bytes;
+        SAIR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, pos, perm, (int)T, 0, 64, st));
+        new_value_kernel<<<gr, 256, 0, st>>>(skey, T, flag);
+        tb = b_tmp.bytes;
+        SAIR_CUDA(cub::DeviceScan::InclusiveSum(tmp, tb, flag, rk, (int)T, st));
+        scatter_rank_kernel<<<gr, 256, 0, st>>>(rk, perm, T, K, k, ranks, rsum);
+    }
+    SAIR_LAUNCH("rank kernels");
+    // order by rank sum
+    {
+        batch_keys_kernel<<<gr, 256, 0, st>>>(dt, dt, T, key, skey, pos);  // pos = iota
+        size_t tb = b_tmp.bytes;
+        SAIR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, rsum, ssum, pos, perm, (int)T, 0, 32, st));
+        pack_sorted_kernel<<<gr, 256, 0, st>>>(ranks, perm, T, K, sranks);
+    }
+    const int members_only = counts == nullptr;
+    const int blocks = (int)((T + 255) / 256);
+    switch (K) {
+#define DK(KK) case KK: dominance_kernel<KK><<<blocks, 256, 0, st>>>(sranks, ssum, perm, T, members_only, dcnt, dmem); break;
+        DK(1) DK(2) DK(3) DK(4) DK(5) DK(6) DK(7) DK(8)
+#undef DK
+    }
+    SAIR_LAUNCH("dominance_kernel");
+    if (counts) SAIR_CUDA(cudaMemcpyAsync(counts, dcnt, T * 4, cudaMemcpyDeviceToHost, st));
+    if (member) SAIR_CUDA(cudaMemcpyAsync(member, dmem, T, cudaMemcpyDeviceToHost, st));
+    SAIR_CUDA(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+}
+
+static RewardCfg check_cfg(const sair_reward_config* c) {
+    // reward.cpp:22-26 (resolved_l_baseline: reward.hpp:17-19)
+    if (c->t_sla_ms <= 0.0) throw Error(SAIR_EINVAL, "reward: t_sla_ms must be positive");
+    double l_base = c->l_baseline_ms > 0.0 ? c->l_baseline_ms : 4.0 * c->t_sla_ms;
+    if (l_base <= 0.0 || c->c_budget <= 0.0)
+        throw Error(SAIR_EINVAL, "reward: normalizers must be positive");
+    return RewardCfg{c->t_sla_ms, l_base, c->c_budget, c->w_latency, c->w_cost, c->w_proactive,
+                     c->r_max};
+}
+
+void compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas, size_t S, size_t T,
+                          sair_frontier_s* f, const sair_reward_config* cfg,
+                          sair_reward_breakdown* out) {
+    RewardCfg rc = check_cfg(cfg);
+    if (T == 0) return;
+    DeviceGuard g(f->device);
+    size_t dbytes = T * S * 4 * 4;
+    char* base = static_cast<char*>(f->b_in.get(T * 32 + dbytes + T * 56 + 1024));
+    double* din = reinterpret_cast<double*>(base);
+    int32_t* dd = reinterpret_cast<int32_t*>(din + 4 * T);
+    double* dout = reinterpret_cast<double*>(base + T * 32 + (dbytes + 255) / 256 * 256);
+    SAIR_CUDA(cudaMemcpyAsync(din, in, T * 32, cudaMemcpyHostToDevice, f->st));
+    if (dbytes) SAIR_CUDA(cudaMemcpyAsync(dd, deltas, dbytes, cudaMemcpyHostToDevice, f->st));
+    reward_kernel<<<grid_for(T), 256, 0, f->st>>>(din, dd, S, T, view(f), f->l_max, f->c_max, rc,
+                                                  dout);
+    SAIR_LAUNCH("reward_kernel");
+    std::vector<double> h(7 * T);
+    SAIR_CUDA(cudaMemcpyAsync(h.data(), dout, T * 56, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    for (size_t t = 0; t < T; ++t) {
+        const double* o = h.data() + 7 * t;
+        out[t] = sair_reward_breakdown{o[0], o[1], o[2], o[3], o[4], o[5], o[6] != 0.0};
+    }
+}
+
+double action_magnitude(const int32_t* deltas, size_t S, int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(SAIR_ECUDA, "no CUDA device (libsair has no CPU fallback)");
+    DeviceGuard g(device);
+    DBuf b;
+    char* base = static_cast<char*>(b.get(S * 16 + 256));
+    double* dout = reinterpret_cast<double*>(base);
+    int32_t* dd = reinterpret_cast<int32_t*>(base + 64);
+    if (S) SAIR_CUDA(cudaMemcpy(dd, deltas, S * 16, cudaMemcpyHostToDevice));
+    action_mu_kernel<<<1, 32>>>(dd, S, dout);
+    SAIR_LAUNCH("action_mu_kernel");
+    double v = 0.0;
+    SAIR_CUDA(cudaMemcpy(&v, dout, 8, cudaMemcpyDeviceToHost));
+    return v;
+}
+
+}  // namespace sair

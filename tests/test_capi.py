@@ -1,0 +1,60 @@
+"""CPU-side checks of the drop-in boundary (no compute without a GPU)."""
+import ctypes as C
+import subprocess
+
+import pytest
+
+from paper_2601_22397_b200 import _lib
+
+
+def test_header_declares_the_boundary():
+    syms = _lib.header_symbols()
+    for s in ("sair_store_create", "sair_store_append", "sair_store_select",
+              "sair_store_effective_sigma", "sair_store_surprisal", "sair_store_nearest",
+              "sair_frontier_create", "sair_frontier_update", "sair_frontier_insert_batch",
+              "sair_frontier_score_batch", "sair_frontier_contribution",
+              "sair_dominance_counts", "sair_compute_reward", "sair_compute_reward_batch",
+              "sair_action_magnitude", "sair_last_error"):
+        assert s in syms
+    # the ctypes binding covers exactly the header
+    assert sorted(_lib.SIGNATURES) == syms
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.lib()
+    for s in _lib.header_symbols():
+        assert hasattr(L, s), s
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert set(_lib.header_symbols()) <= exported
+    # nothing but the C-ABI leaks out of the shared object
+    assert all(e.startswith("sair_") for e in exported), sorted(e for e in exported
+                                                                 if not e.startswith("sair_"))
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    L = _lib.lib()
+    h = C.c_void_p()
+    rc = L.sair_store_create(0.0, 0, 0, C.byref(h))
+    assert rc == _lib.SAIR_ECUDA
+    assert b"no CUDA device" in L.sair_last_error()
+    from paper_2601_22397_b200 import ExperienceBuffer, SairError
+    with pytest.raises(SairError):
+        ExperienceBuffer(0.0)
+
+
+def test_status_codes_for_bad_arguments():
+    L = _lib.lib()
+    assert L.sair_store_create(0.0, 0, 0, None) == _lib.SAIR_EINVAL
+    assert L.sair_store_size(None, None) == _lib.SAIR_EINVAL
+    assert L.sair_store_destroy(None) == _lib.SAIR_OK
