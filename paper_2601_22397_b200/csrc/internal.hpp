@@ -81,6 +81,11 @@ struct sair_store_s {
     int64_t gbase = 0;  // global index of local record 0 (shard offset)
 
     sair::StoreStats stats;
+    // per-dimension centring of the fp32 page copy: pages hold fp32(x - shift)
+    // (shift = the first stored row), keeping the filter's norm expansion well
+    // conditioned for uncentred features (memory_mb, cpu_millicores, ...)
+    std::vector<double> shift;
+    double* d_shift = nullptr;
     double cached_sigma = 0.0;  // experience.hpp:87
     size_t stale = 0;           // experience.hpp:88
 

@@ -713,7 +713,8 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
     SAIR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     DBuf b_all, b_tmp;
     char* base = static_cast<char*>(
-        b_all.get(T * (size_t)K * 8 + T * 8 * 2 + T * 4 * 6 + T * (size_t)K * 4 * 2 + T + 8192));
+        b_all.get(T * (size_t)K * 8 + T * 8 * 2 + T * 4 * 7 + T * (size_t)K * 4 * 2 + T +
+                  16 * 256));
     size_t off = 0;
     auto take = [&](size_t b) {
         char* p = base + off;

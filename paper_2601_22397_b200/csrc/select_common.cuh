@@ -1,0 +1,68 @@
+// select_common.cuh -- pieces shared by the fast (select.cu) and exact
+// (select_exact.cu) retrieval paths.
+#pragma once
+
+#include <vector>
+
+#include "internal.hpp"
+
+namespace sair {
+
+// Greedy pick key, experience.cpp:268-278: gain desc, then round asc, then the
+// first index scanned (index asc).  j < 0 marks "none".
+struct Best {
+    double g;
+    int32_t r;
+    int64_t i;
+    int j;
+};
+
+__device__ __forceinline__ bool better(const Best& a, const Best& b) {
+    if (a.j < 0) return false;
+    if (b.j < 0) return true;
+    if (a.g > b.g) return true;
+    if (a.g < b.g) return false;
+    if (a.r != b.r) return a.r < b.r;
+    return a.i < b.i;
+}
+
+__device__ __forceinline__ Best warp_best(Best b) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        Best c;
+        c.g = __shfl_xor_sync(0xffffffffu, b.g, o);
+        c.r = __shfl_xor_sync(0xffffffffu, b.r, o);
+        c.i = __shfl_xor_sync(0xffffffffu, b.i, o);
+        c.j = __shfl_xor_sync(0xffffffffu, b.j, o);
+        if (better(c, b)) b = c;
+    }
+    return b;
+}
+
+// Host-side per-call constants: the reference's standardize statistics and the
+// standardized queries (experience.cpp:159-166), sigma and 2 sigma^2 (:130).
+struct QueryPrep {
+    std::vector<double> mean, sd, z;  // z: [nq][d]
+    double sigma = 1.0, two_s2 = 2.0;
+};
+
+inline QueryPrep prep_queries(const sair_store_s* s, const double* q, size_t nq, double sigma) {
+    QueryPrep p;
+    const int d = s->d;
+    p.mean.resize(d);
+    p.sd.resize(d);
+    store_mean_sd(s, p.mean.data(), p.sd.data());
+    p.z.resize(nq * d);
+    for (size_t i = 0; i < nq; ++i)
+        for (int k = 0; k < d; ++k) p.z[i * d + k] = (q[i * d + k] - p.mean[k]) / p.sd[k];
+    p.sigma = sigma;
+    p.two_s2 = 2.0 * sigma * sigma;
+    return p;
+}
+
+// select_exact.cu: one query through the full fp64 pass.
+void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
+               double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,
+               size_t* o_cnt, int64_t* o_nn, double* o_nn_sim);
+
+}  // namespace sair

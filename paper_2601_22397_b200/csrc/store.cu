@@ -21,7 +21,8 @@ __global__ void scatter_rows_kernel(const double* __restrict__ sx, const double*
                                     const int32_t* __restrict__ sround, size_t n0, size_t cnt,
                                     int d, int dp, float* __restrict__ pages,
                                     float* __restrict__ r32, double* __restrict__ r64,
-                                    int32_t* __restrict__ rnd, double* __restrict__ x64) {
+                                    int32_t* __restrict__ rnd, double* __restrict__ x64,
+                                    const double* __restrict__ shift) {
     size_t total = cnt * (size_t)dp;
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
          t += (size_t)gridDim.x * blockDim.x) {
@@ -29,7 +30,8 @@ __global__ void scatter_rows_kernel(const double* __restrict__ sx, const double*
         int k = (int)(t % dp);
         size_t rec = n0 + i;
         double v = k < d ? sx[i * d + k] : 0.0;
-        pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] = (float)v;
+        pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] =
+            k < d ? (float)(v - shift[k]) : 0.f;
         if (k < d) x64[rec * d + k] = v;
         if (k == 0) {
             r64[rec] = sr[i];
@@ -64,7 +66,8 @@ __global__ void synth_rows_kernel(uint64_t seed, int clustered, int64_t gbase, s
                                   float* __restrict__ r32, double* __restrict__ r64,
                                   int32_t* __restrict__ rnd, double* __restrict__ x64,
                                   double* __restrict__ acc /* [2d + 1] sum, sum_sq, total */,
-                                  unsigned long long* __restrict__ amax /* [d + 1] */) {
+                                  unsigned long long* __restrict__ amax /* [d + 1] */,
+                                  const double* __restrict__ shift) {
     extern __shared__ double sh[];  // [2d+1] block partial sums
     __shared__ unsigned long long shmax[257];
     for (int t = threadIdx.x; t < 2 * d + 1; t += blockDim.x) sh[t] = 0.0;
@@ -89,7 +92,8 @@ __global__ void synth_rows_kernel(uint64_t seed, int clustered, int64_t gbase, s
             atomicAdd(&sh[d + k], v * v);
             atomicMax(&shmax[k], (unsigned long long)__double_as_longlong(fabs(v)));
         }
-        pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] = (float)v;
+        pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] =
+            k < d ? (float)(v - shift[k]) : 0.f;
         if (k == 0) {
             uint64_t h = splitmix64(g ^ synth_key(seed, 2));
             double r = (double)((h & 0xFFFFFull) + 8192ull) * 0x1p-20;
@@ -166,6 +170,8 @@ void store_free(sair_store_s* s) {
     DeviceGuard g(s->device);
     if (s->st) cudaStreamSynchronize(s->st);
     free_arrays(s);
+    cudaFree(s->d_shift);
+    s->d_shift = nullptr;
     for (auto* b : {&s->b_stage, &s->b_cand, &s->b_merged, &s->b_thr, &s->b_z, &s->b_consts,
                     &s->b_out, &s->b_exact, &s->b_sigma, &s->b_red})
         b->release();
@@ -211,7 +217,13 @@ void store_reserve(sair_store_s* s, size_t need) {
     s->cap = cap;
 }
 
-static void fix_dim(sair_store_s* s, int dim) {
+static void fix_dim(sair_store_s* s, int dim, const double* first_row) {
+    s->shift.assign(dim, 0.0);
+    if (first_row) s->shift.assign(first_row, first_row + dim);
+    if (s->d_shift) cudaFree(s->d_shift);
+    s->d_shift = nullptr;
+    SAIR_CUDA(cudaMalloc(&s->d_shift, dim * sizeof(double)));
+    SAIR_CUDA(cudaMemcpy(s->d_shift, s->shift.data(), dim * sizeof(double), cudaMemcpyHostToDevice));
     s->d = dim;
     s->dp = dp_bucket(dim);
     s->stats.sum.assign(dim, 0.0);
@@ -244,7 +256,7 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
             }
             // dimension fixed on first accepted row, experience.cpp:140-145
             if (s->n + k == 0) {
-                fix_dim(s, dim);
+                fix_dim(s, dim, ctx + i * (size_t)dim);
             } else if (dim != s->d) {
                 err = "experience store: context dimension changed";
                 break;
@@ -279,7 +291,7 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
             int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
             scatter_rows_kernel<<<blocks, 256, 0, s->st>>>(dx, dr, dround, s->n, k, s->d, s->dp,
                                                            s->pages, s->r32, s->r64, s->rnd,
-                                                           s->x64);
+                                                           s->x64, s->d_shift);
             SAIR_LAUNCH("scatter_rows_kernel");
             SAIR_CUDA(cudaStreamSynchronize(s->st));  // staging is reused next chunk
             s->n += k;
@@ -298,7 +310,7 @@ void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int di
     if (!(0x1p-7 > s->r_min))
         throw Error(SAIR_EINVAL, "synthetic rewards start at 2^-7: r_min must be below that");
     if (s->n == 0) {
-        fix_dim(s, dim);
+        fix_dim(s, dim, nullptr);
     } else if (dim != s->d) {
         throw Error(SAIR_EINVAL, "experience store: context dimension changed");
     }
@@ -311,7 +323,7 @@ void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int di
     int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 8);
     synth_rows_kernel<<<blocks, 256, (2 * dim + 1) * sizeof(double), s->st>>>(
         seed, clustered, s->gbase, s->n, count, s->d, s->dp, s->pages, s->r32, s->r64, s->rnd,
-        s->x64, acc, amax);
+        s->x64, acc, amax, s->d_shift);
     SAIR_LAUNCH("synth_rows_kernel");
     std::vector<double> h(3 * dim + 2);
     SAIR_CUDA(cudaMemcpyAsync(h.data(), acc, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -413,6 +425,13 @@ void store_clone(const sair_store_s* s, sair_store_s* o) {
     o->rejected = s->rejected;
     o->gbase = s->gbase;
     o->stats = s->stats;
+    o->shift = s->shift;
+    if (!s->shift.empty()) {
+        DeviceGuard g0(s->device);
+        SAIR_CUDA(cudaMalloc(&o->d_shift, s->shift.size() * sizeof(double)));
+        SAIR_CUDA(cudaMemcpy(o->d_shift, s->shift.data(), s->shift.size() * sizeof(double),
+                             cudaMemcpyHostToDevice));
+    }
     o->cached_sigma = s->cached_sigma;
     o->stale = s->stale;
     if (s->n == 0) {
