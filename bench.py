@@ -115,32 +115,32 @@ def run_ours(a, rank, world, local_rank):
 
     dev = local_rank
     torch.cuda.set_device(dev)
-    if world > 1:
-        raise SystemExit("bench.py: multi-GPU sharding lands with sair_store_set_shard")
     dist = None
+    n_total = a.records
+    cfg = sair.SelectionConfig(m=K_SEL, lambda_div=a.lambda_div)
+    t0 = time.time()
     if world > 1:
         import torch.distributed as dist
+        from paper_2601_22397_b200.sharded import ShardedExperienceBuffer, shard_range
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    n_total = a.records
-    lo, hi = n_total * rank // world, n_total * (rank + 1) // world
-    buf = sair.ExperienceBuffer(0.0, device=dev)
-    if world > 1:
-        buf.set_shard(lo, n_total)
-    t0 = time.time()
-    buf.store_synthetic(SEED, hi - lo, DIM)
-    if world > 1:
-        buf.sync_global_stats(dist)
+        lo, hi = shard_range(n_total, rank, world)
+        sharded = ShardedExperienceBuffer(dist, dev)
+        sharded.store_synthetic(SEED, n_total, DIM)
+        buf = sharded.local
+
+        def step(i):
+            return sharded.select_batch(qpool[i], cfg)
+    else:
+        lo, hi = 0, n_total
+        buf = sair.ExperienceBuffer(0.0, device=dev)
+        buf.store_synthetic(SEED, n_total, DIM)
+
+        def step(i):
+            return buf.select_batch(qpool[i], cfg)
     gen_s = time.time() - t0
-    cfg = sair.SelectionConfig(m=K_SEL, lambda_div=a.lambda_div)
     qpool = synth.queries(SEED, (a.warmup + a.steps) * a.queries, DIM).reshape(
         a.warmup + a.steps, a.queries, DIM)
     stream = torch.cuda.ExternalStream(buf.stream_ptr(), device=dev)
-
-    def step(i):
-        res = buf.select_batch(qpool[i], cfg)
-        if world > 1:
-            res = sair.merge_shards(res, dist, K_SEL)
-        return res
 
     for i in range(a.warmup):
         step(i)

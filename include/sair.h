@@ -151,6 +151,51 @@ SAIR_API sair_status sair_store_nearest(sair_store_t h, const double* queries, s
 
 SAIR_API sair_status sair_store_last_stats(sair_store_t h, sair_select_stats* out);
 
+/* ------------------------------------------------------------------------
+ * Sharding (one store per GPU, contiguous slices of one logical buffer;
+ * SURVEY.md 8(e)).  The reference has one buffer per run (harness.cpp:151);
+ * a shard reproduces that buffer's arithmetic exactly by using the buffer's
+ * global statistics for standardize / loo_mean / sigma.
+ * ------------------------------------------------------------------------ */
+
+/* Global index of this store's first record (call before the first append). */
+SAIR_API sair_status sair_store_set_shard(sair_store_t h, int64_t global_offset);
+/* This store's own sums (experience.cpp:146-149): sum[d], sum_sq[d], max|x|[d],
+ * scalars[3] = {n, reward total (index order), max |reward|}. */
+SAIR_API sair_status sair_store_local_stats(sair_store_t h, double* sum, double* sum_sq,
+                                            double* xabs, double* scalars);
+/* Switch to shard mode with the buffer's statistics and sigma (sigma <= 0:
+ * unset -- select then needs SelectionConfig::sigma_sim > 0). */
+SAIR_API sair_status sair_store_set_global(sair_store_t h, uint64_t n_global, const double* sum,
+                                           const double* sum_sq, const double* xabs,
+                                           double reward_total, double reward_absmax,
+                                           double sigma);
+/* mean[d] and sd[d] of standardize() (experience.cpp:159-165) for this store's
+ * statistics (global ones in shard mode). */
+SAIR_API sair_status sair_store_moments(sair_store_t h, double* mean, double* sd);
+/* The global indices refresh_sigma_cache samples from an n-record buffer
+ * (experience.cpp:173-182); m <= 512 returned. */
+SAIR_API sair_status sair_sigma_sample_indices(uint64_t n, int64_t* idx, size_t* m);
+/* The median pairwise z-distance of m raw rows (m x dim) standardized with
+ * mean/sd (experience.cpp:183-203), computed on `device`. */
+SAIR_API sair_status sair_sigma_rows(const double* rows, size_t m, int dim, const double* mean,
+                                     const double* sd, int device, double* out);
+/* select() on a shard: as sair_store_select plus each pick's reward and round
+ * (what the cross-shard merge orders by).  out_reward / out_round nullable. */
+SAIR_API sair_status sair_store_select_shard(sair_store_t h, const double* queries, size_t nq,
+                                             int dim, const sair_select_config* cfg,
+                                             int64_t* out_idx, double* out_sim,
+                                             double* out_score, double* out_reward,
+                                             int32_t* out_round, size_t* out_count);
+/* Merge per-shard top-m lists (shard-major arrays [nshards][nq][m], counts
+ * [nshards][nq]) into the buffer's select() result for lambda_div == 0:
+ * (score desc, round asc, index asc), then curriculum order. */
+SAIR_API sair_status sair_merge_topk(const double* score, const double* sim,
+                                     const double* reward, const int32_t* round,
+                                     const int64_t* gidx, const size_t* count, size_t nshards,
+                                     size_t nq, size_t m, int device, int64_t* out_idx,
+                                     double* out_sim, double* out_score, size_t* out_count);
+
 /* The CUDA stream the store's work is ordered on (for event timing). */
 SAIR_API sair_status sair_store_stream(sair_store_t h, void** stream);
 

@@ -62,6 +62,11 @@ class COracle:
         L.orc_select.restype = _sz
         L.orc_select_batch.argtypes = [_dp, _dp, _i32p, _sz, C.c_int, _dp, _dp, _dp, _sz, _sz,
                                        C.c_double, C.c_double, C.c_int, _i64p, _dp, _dp, _szp]
+        L.orc_select_shard.argtypes = [_dp, _dp, _i32p, _sz, C.c_int, _dp, _dp, _sz, C.c_double,
+                                       _dp, _sz, C.c_double, _i64p, _dp, _dp]
+        L.orc_select_shard.restype = _sz
+        L.orc_sigma_rows.argtypes = [_dp, _sz, C.c_int, _sz, _dp, _dp]
+        L.orc_sigma_rows.restype = C.c_double
         L.orc_surprisal.argtypes = [_dp, _dp, _sz, C.c_int, _dp, _dp, _sz, _dp, C.c_double,
                                     C.c_int]
         L.orc_surprisal.restype = C.c_double
@@ -137,6 +142,28 @@ class COracle:
                                   nthreads or os.cpu_count(), _p(idx, _i64p), _p(sim, _dp),
                                   _p(sc, _dp), cnt.ctypes.data_as(_szp))
         return idx, sim, sc, cnt.astype(np.int64)
+
+    def select_shard(self, ctx, reward, rounds, x, m, sigma, n_global, s, ss, total):
+        ctx = np.ascontiguousarray(ctx, np.float64)
+        reward = np.ascontiguousarray(reward, np.float64)
+        rounds = np.ascontiguousarray(rounds, np.int32)
+        x = np.ascontiguousarray(x, np.float64)
+        s = np.ascontiguousarray(s, np.float64)
+        ss = np.ascontiguousarray(ss, np.float64)
+        n, d = ctx.shape
+        idx = np.full(max(m, 1), -1, np.int64)
+        sim = np.zeros(max(m, 1))
+        sc = np.zeros(max(m, 1))
+        k = self.lib.orc_select_shard(_p(ctx, _dp), _p(reward, _dp), _p(rounds, _i32p), n, d,
+                                      _p(s, _dp), _p(ss, _dp), n_global, total, _p(x, _dp), m,
+                                      sigma, _p(idx, _i64p), _p(sim, _dp), _p(sc, _dp))
+        return idx[:k], sim[:k], sc[:k]
+
+    def sigma_rows(self, rows, n, s, ss):
+        rows = np.ascontiguousarray(rows, np.float64)
+        return self.lib.orc_sigma_rows(_p(rows, _dp), rows.shape[0], rows.shape[1], n,
+                                       _p(np.ascontiguousarray(s), _dp),
+                                       _p(np.ascontiguousarray(ss), _dp))
 
     def surprisal(self, ctx, reward, index, x, sigma, local_mean=False):
         ctx = np.ascontiguousarray(ctx, np.float64)

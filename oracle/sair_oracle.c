@@ -138,6 +138,7 @@ typedef struct {
     const double* sum;
     const double* sum_sq;
     double total; /* reward total (orc_reward_total) */
+    size_t n_loo; /* records of the whole buffer (== n unless this is a shard) */
 } orc_store;
 
 /* Per-record surprisal score: src/experience.cpp:254-258 with the global
@@ -147,9 +148,10 @@ static void score_all(const orc_store* s, const double* zq, double sigma, double
     size_t n = s->n;
     int d = s->d;
     for (size_t i = 0; i < n; ++i) {
-        orc_standardize(n, d, s->sum, s->sum_sq, s->ctx + i * (size_t)d, ztmp);
+        orc_standardize(s->n_loo, d, s->sum, s->sum_sq, s->ctx + i * (size_t)d, ztmp);
         double sim = orc_similarity(ztmp, zq, d, sigma);
-        double loo = n <= 1 ? 0.0 : (s->total - s->reward[i]) / (double)(n - 1);
+        size_t nl = s->n_loo;
+        double loo = nl <= 1 ? 0.0 : (s->total - s->reward[i]) / (double)(nl - 1);
         sim_curr[i] = sim;
         score[i] = sim * fabs(s->reward[i] - loo);
     }
@@ -190,7 +192,7 @@ static size_t select_one(const orc_store* s, const double* x, size_t m, double l
     double* sim_curr = (double*)malloc(n * sizeof(double));
     double* penalty = (double*)calloc(n, sizeof(double));
     unsigned char* taken = (unsigned char*)calloc(n, 1);
-    orc_standardize(n, d, s->sum, s->sum_sq, x, zq);
+    orc_standardize(s->n_loo, d, s->sum, s->sum_sq, x, zq);
     score_all(s, zq, sigma, score, sim_curr, zi);
     if (local_mean) {
         for (size_t i = 0; i < n; ++i) {
@@ -218,10 +220,10 @@ static size_t select_one(const orc_store* s, const double* x, size_t m, double l
         /* penalty += sim(z_i, z_b); with lambda == 0 the gain is score - 0 and
          * the (finite) penalties never influence a pick, so skip the update. */
         if (lambda != 0.0) {
-            orc_standardize(n, d, s->sum, s->sum_sq, s->ctx + (size_t)best * (size_t)d, zj);
+            orc_standardize(s->n_loo, d, s->sum, s->sum_sq, s->ctx + (size_t)best * (size_t)d, zj);
             for (size_t i = 0; i < n; ++i) {
                 if (taken[i]) continue;
-                orc_standardize(n, d, s->sum, s->sum_sq, s->ctx + i * (size_t)d, zi);
+                orc_standardize(s->n_loo, d, s->sum, s->sum_sq, s->ctx + i * (size_t)d, zi);
                 penalty[i] += orc_similarity(zi, zj, d, sigma);
             }
         }
@@ -254,15 +256,56 @@ ORC_API size_t orc_select(const double* ctx, const double* reward, const int32_t
                           size_t n, int d, const double* sum, const double* sum_sq,
                           const double* x, size_t m, double lambda, double sigma,
                           int local_mean, int64_t* out_idx, double* out_sim, double* out_score) {
-    orc_store s = {ctx, reward, round, n, d, sum, sum_sq, orc_reward_total(reward, n)};
+    orc_store s = {ctx, reward, round, n, d, sum, sum_sq, orc_reward_total(reward, n), n};
     return select_one(&s, x, m, lambda, sigma, local_mean, out_idx, out_sim, out_score);
+}
+
+/* select() restricted to one shard [0, n) of a buffer of n_global records whose
+ * sums / reward total are given: the reference's per-record arithmetic with
+ * the buffer's n (experience.cpp:159-166, :229-231); indices are shard-local. */
+ORC_API size_t orc_select_shard(const double* ctx, const double* reward, const int32_t* round,
+                                size_t n, int d, const double* sum, const double* sum_sq,
+                                size_t n_global, double total, const double* x, size_t m,
+                                double sigma, int64_t* out_idx, double* out_sim,
+                                double* out_score) {
+    orc_store s = {ctx, reward, round, n, d, sum, sum_sq, total, n_global};
+    return select_one(&s, x, m, 0.0, sigma, 0, out_idx, out_sim, out_score);
+}
+
+/* refresh_sigma_cache's median over given subsample rows (m x d), standardized
+ * with an n-record buffer's sums (experience.cpp:183-203). */
+ORC_API double orc_sigma_rows(const double* rows, size_t m, int d, size_t n, const double* sum,
+                              const double* sum_sq) {
+    double* z = (double*)malloc((m ? m : 1) * (size_t)d * sizeof(double));
+    for (size_t a = 0; a < m; ++a) orc_standardize(n, d, sum, sum_sq, rows + a * (size_t)d, z + a * (size_t)d);
+    size_t np = m * (m - (m ? 1 : 0)) / 2;
+    double sigma = 1.0;
+    if (np > 0) {
+        double* dists = (double*)malloc(np * sizeof(double));
+        size_t p = 0;
+        for (size_t i = 0; i < m; ++i)
+            for (size_t j = i + 1; j < m; ++j) {
+                double d2 = 0.0;
+                for (int k = 0; k < d; ++k) {
+                    double t = z[i * (size_t)d + k] - z[j * (size_t)d + k];
+                    d2 += t * t;
+                }
+                dists[p++] = sqrt(d2);
+            }
+        qsort(dists, np, sizeof(double), cmp_double);
+        double mid = dists[np / 2];
+        sigma = mid > 1e-12 ? mid : 1.0;
+        free(dists);
+    }
+    free(z);
+    return sigma;
 }
 
 /* ExperienceBuffer::surprisal, src/experience.cpp:234-240. */
 ORC_API double orc_surprisal(const double* ctx, const double* reward, size_t n, int d,
                              const double* sum, const double* sum_sq, size_t index,
                              const double* x, double sigma, int local_mean) {
-    orc_store s = {ctx, reward, NULL, n, d, sum, sum_sq, orc_reward_total(reward, n)};
+    orc_store s = {ctx, reward, NULL, n, d, sum, sum_sq, orc_reward_total(reward, n), n};
     double* zi = (double*)malloc((size_t)d * sizeof(double));
     double* zq = (double*)malloc((size_t)d * sizeof(double));
     double* zj = (double*)malloc((size_t)d * sizeof(double));
@@ -331,7 +374,7 @@ ORC_API void orc_select_batch(const double* ctx, const double* reward, const int
                               const double* xq, size_t nq, size_t m, double lambda,
                               double sigma, int nthreads, int64_t* out_idx, double* out_sim,
                               double* out_score, size_t* out_count) {
-    orc_store s = {ctx, reward, round, n, d, sum, sum_sq, orc_reward_total(reward, n)};
+    orc_store s = {ctx, reward, round, n, d, sum, sum_sq, orc_reward_total(reward, n), n};
     if (nthreads < 1) nthreads = 1;
     if ((size_t)nthreads > nq) nthreads = (int)(nq ? nq : 1);
     pthread_t* th = (pthread_t*)malloc((size_t)nthreads * sizeof(pthread_t));

@@ -80,6 +80,17 @@ SIGNATURES = {
     "sair_store_nearest": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, C.c_double, _i64p, _dp]),
     "sair_store_last_stats": (C.c_int, [_vp, C.POINTER(SelectStatsC)]),
     "sair_store_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "sair_store_set_shard": (C.c_int, [_vp, C.c_int64]),
+    "sair_store_local_stats": (C.c_int, [_vp, _dp, _dp, _dp, _dp]),
+    "sair_store_set_global": (C.c_int, [_vp, C.c_uint64, _dp, _dp, _dp, C.c_double, C.c_double,
+                                        C.c_double]),
+    "sair_store_moments": (C.c_int, [_vp, _dp, _dp]),
+    "sair_sigma_sample_indices": (C.c_int, [C.c_uint64, _i64p, _szp]),
+    "sair_sigma_rows": (C.c_int, [_dp, C.c_size_t, C.c_int, _dp, _dp, C.c_int, _dp]),
+    "sair_store_select_shard": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, C.POINTER(SelectConfigC),
+                                          _i64p, _dp, _dp, _dp, _i32p, _szp]),
+    "sair_merge_topk": (C.c_int, [_dp, _dp, _dp, _i32p, _i64p, _szp, C.c_size_t, C.c_size_t,
+                                  C.c_size_t, C.c_int, _i64p, _dp, _dp, _szp]),
     "sair_frontier_create": (C.c_int, [C.c_double, C.c_double, C.c_int, C.POINTER(_vp)]),
     "sair_frontier_destroy": (C.c_int, [_vp]),
     "sair_frontier_clone": (C.c_int, [_vp, C.POINTER(_vp)]),

@@ -213,6 +213,92 @@ sair_status sair_store_last_stats(sair_store_t h, sair_select_stats* out) {
     return SAIR_OK;
 }
 
+sair_status sair_store_set_shard(sair_store_t h, int64_t global_offset) {
+    if (!h) return bad("null handle");
+    if (h->n) return bad("set_shard: the store already holds records");
+    h->gbase = global_offset;
+    return SAIR_OK;
+}
+
+sair_status sair_store_local_stats(sair_store_t h, double* sum, double* sum_sq, double* xabs,
+                                   double* scalars) {
+    if (!h) return bad("null handle");
+    for (int k = 0; k < h->d && h->n; ++k) {
+        if (sum) sum[k] = h->stats.sum[k];
+        if (sum_sq) sum_sq[k] = h->stats.sum_sq[k];
+        if (xabs) xabs[k] = h->stats.xabs[k];
+    }
+    if (scalars) {
+        scalars[0] = (double)h->n;
+        scalars[1] = h->stats.total;
+        scalars[2] = h->stats.rabs;
+    }
+    return SAIR_OK;
+}
+
+sair_status sair_store_set_global(sair_store_t h, uint64_t n_global, const double* sum,
+                                  const double* sum_sq, const double* xabs, double reward_total,
+                                  double reward_absmax, double sigma) {
+    if (!h || !sum || !sum_sq || !xabs) return bad("null input");
+    if (!h->n) return bad("set_global: append the shard's records first");
+    if (n_global < h->n) return bad("set_global: n_global is smaller than the shard");
+    const int d = h->d;
+    h->sharded = true;
+    h->n_global = n_global;
+    h->gst.sum.assign(sum, sum + d);
+    h->gst.sum_sq.assign(sum_sq, sum_sq + d);
+    h->gst.xabs.assign(xabs, xabs + d);
+    h->gst.total = reward_total;
+    h->gst.rabs = reward_absmax;
+    h->gsigma = sigma;
+    return SAIR_OK;
+}
+
+sair_status sair_store_moments(sair_store_t h, double* mean, double* sd) {
+    if (!h || !mean || !sd) return bad("null input");
+    if (!h->n) return bad("moments: empty store");
+    sair::store_mean_sd(h, mean, sd);
+    return SAIR_OK;
+}
+
+sair_status sair_sigma_sample_indices(uint64_t n, int64_t* idx, size_t* m) {
+    if (!idx || !m) return bad("null input");
+    auto v = sair::sigma_sample(n);
+    std::memcpy(idx, v.data(), v.size() * 8);
+    *m = v.size();
+    return SAIR_OK;
+}
+
+sair_status sair_sigma_rows(const double* rows, size_t m, int dim, const double* mean,
+                            const double* sd, int device, double* out) {
+    if (!out || (m && (!rows || !mean || !sd))) return bad("null input");
+    return guard([&] { *out = sair::sigma_rows(rows, m, dim, mean, sd, device); });
+}
+
+sair_status sair_store_select_shard(sair_store_t h, const double* queries, size_t nq, int dim,
+                                    const sair_select_config* cfg, int64_t* out_idx,
+                                    double* out_sim, double* out_score, double* out_reward,
+                                    int32_t* out_round, size_t* out_count) {
+    if (!h) return bad("null handle");
+    if (nq && (!queries || !out_count)) return bad("null input");
+    return guard([&] {
+        sair::store_select(h, queries, nq, dim, defaults(cfg), out_idx, out_sim, out_score,
+                           out_count, nullptr, nullptr, out_reward, out_round);
+    });
+}
+
+sair_status sair_merge_topk(const double* score, const double* sim, const double* reward,
+                            const int32_t* round, const int64_t* gidx, const size_t* count,
+                            size_t nshards, size_t nq, size_t m, int device, int64_t* out_idx,
+                            double* out_sim, double* out_score, size_t* out_count) {
+    if (nq && (!out_count || !count)) return bad("null input");
+    if (m > 4096) return bad("merge: m too large");
+    return guard([&] {
+        sair::merge_topk(score, sim, reward, round, gidx, count, nshards, nq, m, device, out_idx,
+                         out_sim, out_score, out_count);
+    });
+}
+
 sair_status sair_store_stream(sair_store_t h, void** stream) {
     if (!h || !stream) return bad("null handle");
     *stream = h->st;

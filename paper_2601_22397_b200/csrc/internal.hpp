@@ -81,6 +81,12 @@ struct sair_store_s {
     int64_t gbase = 0;  // global index of local record 0 (shard offset)
 
     sair::StoreStats stats;
+    // shard mode (multi-GPU): this store holds records [gbase, gbase + n) of a
+    // buffer of n_global records whose statistics are gst / gsigma
+    bool sharded = false;
+    uint64_t n_global = 0;
+    sair::StoreStats gst;
+    double gsigma = 0.0;
     // per-dimension centring of the fp32 page copy: pages hold fp32(x - shift)
     // (shift = the first stored row), keeping the filter's norm expansion well
     // conditioned for uncentred features (memory_mb, cpu_millicores, ...)
@@ -118,6 +124,10 @@ struct sair_frontier_s {
 
 namespace sair {
 
+// statistics the reference's formulas see: the whole buffer's (experience.cpp:159-166, :229-231)
+inline const StoreStats& eff_stats(const sair_store_s* s) { return s->sharded ? s->gst : s->stats; }
+inline uint64_t eff_n(const sair_store_s* s) { return s->sharded ? s->n_global : s->n; }
+
 // store.cu
 void store_init(sair_store_s* s, double r_min, int device, size_t capacity_hint);
 void store_free(sair_store_s* s);
@@ -129,11 +139,19 @@ void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int di
 void store_standardize(const sair_store_s* s, const double* x, double* z);
 double store_effective_sigma(sair_store_s* s, double sigma_sim);
 void store_mean_sd(const sair_store_s* s, double* mean, double* sd);
+std::vector<int64_t> sigma_sample(uint64_t n);
+double sigma_rows(const double* rows, size_t m, int d, const double* mean, const double* sd,
+                  int device);
 
 // select.cu
 void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
-                  const sair_select_config& cfg, int64_t* out_idx, double* out_sim, double* out_score, size_t* out_count,
-                  int64_t* out_nn, double* out_nn_sim);
+                  const sair_select_config& cfg, int64_t* out_idx, double* out_sim,
+                  double* out_score, size_t* out_count, int64_t* out_nn, double* out_nn_sim,
+                  double* out_reward = nullptr, int32_t* out_round = nullptr);
+void merge_topk(const double* score, const double* sim, const double* reward,
+                const int32_t* round, const int64_t* gidx, const size_t* count, size_t nshards,
+                size_t nq, size_t m, int device, int64_t* out_idx, double* out_sim,
+                double* out_score, size_t* out_count);
 double store_surprisal(sair_store_s* s, size_t index, const double* x,
                        const sair_select_config& cfg);
 

@@ -554,7 +554,8 @@ struct RefineArgs {
     const double* cc;    // [QB] sum_k c_qk^2 (fp64 of the fp32 constants)
     const unsigned int* pmax;
     int d, m, kp, knn, QB, kmax;
-    size_t n;
+    size_t n;      // records in this store (candidate validity)
+    size_t n_loo;  // records of the whole buffer (loo_mean's n)
     double total, two_s2, lambda, beta, gamma, key_slack_abs;
     int has_excl, has_excl_nn;
     const float* ckey;
@@ -570,6 +571,8 @@ struct RefineArgs {
     int64_t* out_nn;
     double* out_nn_sim;
     int* out_nn_cert;
+    double* out_rew;    // [QB][m] reward of each pick (shard merge)
+    int32_t* out_round; // [QB][m]
 };
 
 __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
         }
         const double sim = sim_from_d2(d2, a.two_s2);
         const double r = a.r64[i];
-        const double loo = a.n <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n - 1));
+        const double loo = a.n_loo <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n_loo - 1));
         simc[j] = sim;
         score[j] = dmul(sim, fabs(dsub(r, loo)));
         rew[j] = r;
@@ -705,6 +708,8 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
         a.out_idx[(size_t)q * a.m + x] = a.gbase + (int64_t)ci[j];
         a.out_sim[(size_t)q * a.m + x] = simc[j];
         a.out_score[(size_t)q * a.m + x] = score[j];
+        a.out_rew[(size_t)q * a.m + x] = rew[j];
+        a.out_round[(size_t)q * a.m + x] = rr[j];
     }
     if (tid == 0) {
         a.out_count[q] = want;
@@ -861,7 +866,8 @@ StreamPlan make_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, 
 
 void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                   const sair_select_config& cfg, int64_t* out_idx, double* out_sim,
-                  double* out_score, size_t* out_count, int64_t* out_nn, double* out_nn_sim) {
+                  double* out_score, size_t* out_count, int64_t* out_nn, double* out_nn_sim,
+                  double* out_reward, int32_t* out_round) {
     s->last = sair_select_stats{};
     s->last.queries = nq;
     if (nq == 0) return;
@@ -885,6 +891,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     SAIR_CUDA(cudaEventRecord(s->ev[0], s->st));
 
     std::vector<int> done(nq, 0);
+    if (s->sharded && cfg.locally_weighted_mean)
+        throw Error(SAIR_EINVAL, "locally_weighted_mean is not supported on a sharded store");
     const bool fast = cfg.mode != SAIR_SELECT_EXACT && !cfg.locally_weighted_mean && d <= 128 &&
                       n < (size_t)1 << 31 && m <= 256;
     float stream_ms = 0.f;
@@ -895,17 +903,19 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
 
         // filter constants
         const double u = 0x1p-24;
+        const StoreStats& est = eff_stats(s);
+        const uint64_t nb = eff_n(s);
         double c1d = 1.0, c0d = 0.0;
-        if (n >= 2) {
-            c1d = (double)n / (double)(n - 1);
-            c0d = s->stats.total / (double)(n - 1);
+        if (nb >= 2) {
+            c1d = (double)nb / (double)(nb - 1);
+            c0d = est.total / (double)(nb - 1);
         }
         const float c1 = (float)c1d, c0 = (float)c0d;
-        const double rdel = 4.0 * u * (s->stats.rabs * c1d + std::fabs(c0d)) * 1.01 + 1e-30;
+        const double rdel = 4.0 * u * (est.rabs * c1d + std::fabs(c0d)) * 1.01 + 1e-30;
         const float rdelta = (float)rdel;
         const double beta = 1.4426950408889634 / p.two_s2;  // log2(e) / (2 sigma^2)
         const float alpha = (float)beta;
-        const double lg_hi = std::log2(s->stats.rabs * c1d + std::fabs(c0d) + rdel);
+        const double lg_hi = std::log2(est.rabs * c1d + std::fabs(c0d) + rdel);
         const double key_slack_abs = 1.0 + 2.0 * (std::fabs(std::log2(rdel)) + std::fabs(lg_hi));
 
         const size_t lists = (size_t)pl.grid * 2 * qb * kmax;
@@ -917,7 +927,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         unsigned int* dpmax = reinterpret_cast<unsigned int*>(mthr + 2 * qb);
         double* zs = s->b_z.as<double>((size_t)qb * kp * d);
         double* dc = s->b_consts.as<double>(2 * (size_t)d + (size_t)qb * d + qb);
-        const size_t ob = (size_t)qb * m * 8 * 3 + (size_t)qb * 8 * 2 + (size_t)qb * 4 * 4 + 64;
+        const size_t ob = (size_t)qb * m * 8 * 4 + (size_t)qb * m * 4 + (size_t)qb * 8 * 2 +
+                          (size_t)qb * 4 * 4 + 64;
         char* dout = static_cast<char*>(s->b_out.get(ob));
         char* hout = static_cast<char*>(s->h_out.get(ob));
         struct O {
@@ -929,6 +940,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             int* cnt;
             int* cert;
             int* nn_cert;
+            double* rew;
+            int32_t* round;
         };
         auto carve = [&](char* b) {
             O o;
@@ -940,6 +953,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             o.cnt = reinterpret_cast<int*>(o.nn_sim + qb);
             o.cert = o.cnt + qb;
             o.nn_cert = o.cert + qb;
+            o.rew = reinterpret_cast<double*>(o.nn_cert + qb + (qb & 1));
+            o.round = reinterpret_cast<int32_t*>(o.rew + qb * m);
             return o;
         };
         const O D = carve(dout), H = carve(hout);
@@ -984,7 +999,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.QB = qb;
             ra.kmax = kmax;
             ra.n = n;
-            ra.total = s->stats.total;
+            ra.n_loo = nb;
+            ra.total = est.total;
             ra.two_s2 = p.two_s2;
             ra.lambda = cfg.lambda_div;
             ra.beta = beta;
@@ -1005,6 +1021,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.out_nn = D.nn;
             ra.out_nn_sim = D.nn_sim;
             ra.out_nn_cert = D.nn_cert;
+            ra.out_rew = D.rew;
+            ra.out_round = D.round;
             refine_kernel<<<nqg, 256, refine_smem, s->st>>>(ra);
             SAIR_LAUNCH("refine_kernel");
             SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob, cudaMemcpyDeviceToHost, s->st));
@@ -1020,6 +1038,10 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                 std::memcpy(out_idx + gq * m, H.idx + (size_t)qq * m, H.cnt[qq] * 8);
                 std::memcpy(out_sim + gq * m, H.sim + (size_t)qq * m, H.cnt[qq] * 8);
                 std::memcpy(out_score + gq * m, H.score + (size_t)qq * m, H.cnt[qq] * 8);
+                if (out_reward)
+                    std::memcpy(out_reward + gq * m, H.rew + (size_t)qq * m, H.cnt[qq] * 8);
+                if (out_round)
+                    std::memcpy(out_round + gq * m, H.round + (size_t)qq * m, H.cnt[qq] * 4);
                 if (out_nn) {
                     out_nn[gq] = H.nn[qq];
                     out_nn_sim[gq] = H.nn_sim[qq];
@@ -1032,7 +1054,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         if (done[i]) continue;
         exact_one(s, p, p.z.data() + i * d, m, cfg.lambda_div, cfg.locally_weighted_mean != 0,
                   out_idx + i * m, out_sim + i * m, out_score + i * m, &out_count[i],
-                  out_nn ? out_nn + i : nullptr, out_nn ? out_nn_sim + i : nullptr);
+                  out_nn ? out_nn + i : nullptr, out_nn ? out_nn_sim + i : nullptr,
+                  out_reward ? out_reward + i * m : nullptr, out_round ? out_round + i * m : nullptr);
         s->last.exact_fallbacks++;
     }
     SAIR_CUDA(cudaEventRecord(s->ev[3], s->st));
@@ -1041,6 +1064,109 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     cudaEventElapsedTime(&tot, s->ev[0], s->ev[3]);
     s->last.stream_ms = stream_ms;
     s->last.total_ms = tot;
+}
+
+// ------------------------------------------------------- shard merge ------
+
+// Per query: the union of the shards' top-m (exact fp64 scores over the
+// buffer's global statistics) holds the buffer's top-m when lambda_div == 0;
+// pick it by (score desc, round asc, global index asc) -- experience.cpp:268-278
+// -- then order it by (reward asc, round asc, pick order) -- :290-294.
+__global__ void merge_topk_kernel(const double* __restrict__ score, const double* __restrict__ sim,
+                                  const double* __restrict__ rew, const int32_t* __restrict__ rnd,
+                                  const int64_t* __restrict__ gidx, const size_t* __restrict__ cnt,
+                                  int nshards, int nq, int m, int64_t* __restrict__ o_idx,
+                                  double* __restrict__ o_sim, double* __restrict__ o_score,
+                                  size_t* __restrict__ o_cnt) {
+    extern __shared__ int picks_sh[];  // [m] pick order, then [m] curriculum order
+    int* order = picks_sh + m;
+    const int q = blockIdx.x;
+    const int total = nshards * m;
+    auto at = [&](int e) { return (size_t)(e / m) * nq * m + (size_t)q * m + (e % m); };
+    auto valid = [&](int e) { return (size_t)(e % m) < cnt[(size_t)(e / m) * nq + q]; };
+    int want = 0;
+    for (int sh = 0; sh < nshards; ++sh) want += (int)cnt[(size_t)sh * nq + q];
+    want = min(want, m);
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        if (!valid(e)) continue;
+        const size_t ie = at(e);
+        const Best be{score[ie], rnd[ie], gidx[ie], 1};
+        int rank = 0;
+        for (int f = 0; f < total; ++f) {
+            if (f == e || !valid(f)) continue;
+            const size_t jf = at(f);
+            rank += better(Best{score[jf], rnd[jf], gidx[jf], 1}, be);
+        }
+        if (rank < want) picks_sh[rank] = e;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < want; x += blockDim.x) {
+        const size_t v = at(picks_sh[x]);
+        int pos = 0;
+        for (int y = 0; y < want; ++y) {
+            const size_t u = at(picks_sh[y]);
+            const bool less = rew[u] != rew[v] ? rew[u] < rew[v] : rnd[u] < rnd[v];
+            const bool same = rew[u] == rew[v] && rnd[u] == rnd[v];
+            pos += less || (same && y < x);
+        }
+        order[pos] = picks_sh[x];
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < want; x += blockDim.x) {
+        const size_t v = at(order[x]);
+        o_idx[(size_t)q * m + x] = gidx[v];
+        o_sim[(size_t)q * m + x] = sim[v];
+        o_score[(size_t)q * m + x] = score[v];
+    }
+    if (threadIdx.x == 0) o_cnt[q] = want;
+}
+
+void merge_topk(const double* score, const double* sim, const double* reward,
+                const int32_t* round, const int64_t* gidx, const size_t* count, size_t nshards,
+                size_t nq, size_t m, int device, int64_t* out_idx, double* out_sim,
+                double* out_score, size_t* out_count) {
+    if (nq == 0 || m == 0) {
+        for (size_t q = 0; q < nq; ++q) out_count[q] = 0;
+        return;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(SAIR_ECUDA, "no CUDA device (libsair has no CPU fallback)");
+    DeviceGuard g(device);
+    const size_t e = nshards * nq * m;
+    DBuf b;
+    char* base = static_cast<char*>(b.get(e * (8 * 4 + 4) + nshards * nq * 8 + nq * m * 24 +
+                                          nq * 8 + 16 * 256));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char* ptr = base + off;
+        off += (bytes + 255) / 256 * 256;
+        return ptr;
+    };
+    auto* dsc = reinterpret_cast<double*>(take(e * 8));
+    auto* dsi = reinterpret_cast<double*>(take(e * 8));
+    auto* drw = reinterpret_cast<double*>(take(e * 8));
+    auto* dgi = reinterpret_cast<int64_t*>(take(e * 8));
+    auto* drd = reinterpret_cast<int32_t*>(take(e * 4));
+    auto* dct = reinterpret_cast<size_t*>(take(nshards * nq * 8));
+    auto* oi = reinterpret_cast<int64_t*>(take(nq * m * 8));
+    auto* os = reinterpret_cast<double*>(take(nq * m * 8));
+    auto* oc = reinterpret_cast<double*>(take(nq * m * 8));
+    auto* on = reinterpret_cast<size_t*>(take(nq * 8));
+    SAIR_CUDA(cudaMemcpy(dsc, score, e * 8, cudaMemcpyHostToDevice));
+    SAIR_CUDA(cudaMemcpy(dsi, sim, e * 8, cudaMemcpyHostToDevice));
+    SAIR_CUDA(cudaMemcpy(drw, reward, e * 8, cudaMemcpyHostToDevice));
+    SAIR_CUDA(cudaMemcpy(dgi, gidx, e * 8, cudaMemcpyHostToDevice));
+    SAIR_CUDA(cudaMemcpy(drd, round, e * 4, cudaMemcpyHostToDevice));
+    SAIR_CUDA(cudaMemcpy(dct, count, nshards * nq * 8, cudaMemcpyHostToDevice));
+    merge_topk_kernel<<<(int)nq, 256, 2 * m * sizeof(int)>>>(dsc, dsi, drw, drd, dgi, dct,
+                                                            (int)nshards, (int)nq, (int)m, oi, os,
+                                                            oc, on);
+    SAIR_LAUNCH("merge_topk_kernel");
+    SAIR_CUDA(cudaMemcpy(out_idx, oi, nq * m * 8, cudaMemcpyDeviceToHost));
+    SAIR_CUDA(cudaMemcpy(out_sim, os, nq * m * 8, cudaMemcpyDeviceToHost));
+    SAIR_CUDA(cudaMemcpy(out_score, oc, nq * m * 8, cudaMemcpyDeviceToHost));
+    SAIR_CUDA(cudaMemcpy(out_count, on, nq * 8, cudaMemcpyDeviceToHost));
 }
 
 }  // namespace sair

@@ -63,6 +63,7 @@ inline QueryPrep prep_queries(const sair_store_s* s, const double* q, size_t nq,
 // select_exact.cu: one query through the full fp64 pass.
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,
-               size_t* o_cnt, int64_t* o_nn, double* o_nn_sim);
+               size_t* o_cnt, int64_t* o_nn, double* o_nn_sim, double* o_rew = nullptr,
+               int32_t* o_round = nullptr);
 
 }  // namespace sair

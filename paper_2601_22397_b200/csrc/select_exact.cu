@@ -23,7 +23,8 @@ struct ExactArgs {
     const double* sd;
     const double* zq;  // [d]
     int d;
-    size_t n;
+    size_t n;     // records in this store
+    size_t n_loo; // records of the whole buffer (loo_mean's n, experience.cpp:231)
     double total, two_s2, lambda;
     const double* loo;  // locally weighted LOO means (nullable)
     double* score;      // [n]
@@ -47,7 +48,7 @@ __global__ void exact_score_kernel(const ExactArgs a) {
         double s = sim_from_d2(d2, a.two_s2);
         double r = a.r64[i];
         double loo = a.loo ? a.loo[i]
-                           : (a.n <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n - 1)));
+                           : (a.n_loo <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n_loo - 1)));
         a.sim[i] = s;
         a.score[i] = dmul(s, fabs(dsub(r, loo)));
         a.pen[i] = 0.0;
@@ -60,7 +61,7 @@ __global__ void exact_score_kernel(const ExactArgs a) {
 __global__ void local_loo_kernel(const ExactArgs a, double* __restrict__ loo) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < a.n;
          i += (size_t)gridDim.x * blockDim.x) {
-        if (a.n <= 1) {
+        if (a.n_loo <= 1) {
             loo[i] = 0.0;
             continue;
         }
@@ -77,7 +78,7 @@ __global__ void local_loo_kernel(const ExactArgs a, double* __restrict__ loo) {
             acc = dadd(acc, dmul(w, a.r64[j]));
         }
         loo[i] = wsum > 1e-12 ? ddiv(acc, wsum)
-                              : ddiv(dsub(a.total, a.r64[i]), (double)(a.n - 1));
+                              : ddiv(dsub(a.total, a.r64[i]), (double)(a.n_loo - 1));
     }
 }
 
@@ -143,7 +144,8 @@ __global__ void exact_penalty_kernel(const ExactArgs a, const int64_t* __restric
 }
 
 __global__ void exact_finish_kernel(const ExactArgs a, int64_t* picks, int want, int64_t gbase,
-                                    int64_t* out_idx, double* out_sim, double* out_score) {
+                                    int64_t* out_idx, double* out_sim, double* out_score,
+                                    double* out_rew, int32_t* out_round) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int x = 1; x < want; ++x) {
         int64_t v = picks[x];
@@ -161,6 +163,8 @@ __global__ void exact_finish_kernel(const ExactArgs a, int64_t* picks, int want,
         out_idx[x] = gbase + picks[x];
         out_sim[x] = a.sim[picks[x]];
         out_score[x] = a.score[picks[x]];
+        out_rew[x] = a.r64[picks[x]];
+        out_round[x] = a.rnd[picks[x]];
     }
 }
 
@@ -174,7 +178,7 @@ __global__ void surprisal_kernel(const ExactArgs a, size_t index, double* out) {
     double s = sim_from_d2(d2, a.two_s2);
     double r = a.r64[index];
     double loo;
-    if (a.n <= 1) {
+    if (a.n_loo <= 1) {
         loo = 0.0;
     } else if (a.loo) {  // local mean computed for this index only
         double wsum = 0.0, acc = 0.0;
@@ -189,9 +193,9 @@ __global__ void surprisal_kernel(const ExactArgs a, size_t index, double* out) {
             wsum = dadd(wsum, w);
             acc = dadd(acc, dmul(w, a.r64[j]));
         }
-        loo = wsum > 1e-12 ? ddiv(acc, wsum) : ddiv(dsub(a.total, r), (double)(a.n - 1));
+        loo = wsum > 1e-12 ? ddiv(acc, wsum) : ddiv(dsub(a.total, r), (double)(a.n_loo - 1));
     } else {
-        loo = ddiv(dsub(a.total, r), (double)(a.n - 1));
+        loo = ddiv(dsub(a.total, r), (double)(a.n_loo - 1));
     }
     *out = dmul(s, fabs(dsub(r, loo)));
 }
@@ -201,12 +205,13 @@ __global__ void surprisal_kernel(const ExactArgs a, size_t index, double* out) {
 // Exact full-pass answer for one query (fp64 over x64), writing m results.
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,
-               size_t* o_cnt, int64_t* o_nn, double* o_nn_sim) {
+               size_t* o_cnt, int64_t* o_nn, double* o_nn_sim, double* o_rew,
+               int32_t* o_round) {
     const size_t n = s->n;
     const int d = s->d;
     char* base = static_cast<char*>(
         s->b_exact.get(n * (8 * 4 + 1) + (size_t)d * 8 * 3 + 4096 * sizeof(Best) + 64 * 1024 +
-                       m * 8 * 4 + 256));
+                       m * 8 * 8 + 16 * 256));
     size_t off = 0;
     auto take = [&](size_t bytes) {
         char* ptr = base + off;
@@ -223,7 +228,8 @@ void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_
     a.zq = dm + 2 * d;
     a.d = d;
     a.n = n;
-    a.total = s->stats.total;
+    a.n_loo = eff_n(s);
+    a.total = eff_stats(s).total;
     a.two_s2 = p.two_s2;
     a.lambda = lambda;
     a.score = reinterpret_cast<double*>(take(n * 8));
@@ -236,6 +242,8 @@ void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_
     int64_t* didx = reinterpret_cast<int64_t*>(take(m * 8 + 8));
     double* dsim = reinterpret_cast<double*>(take(m * 8 + 8));
     double* dscore = reinterpret_cast<double*>(take(m * 8 + 8));
+    double* drew = reinterpret_cast<double*>(take(m * 8 + 8));
+    int32_t* dround = reinterpret_cast<int32_t*>(take(m * 4 + 8));
     std::vector<double> h(3 * (size_t)d);
     std::copy(p.mean.begin(), p.mean.end(), h.begin());
     std::copy(p.sd.begin(), p.sd.end(), h.begin() + d);
@@ -261,11 +269,16 @@ void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_
     }
     SAIR_LAUNCH("exact greedy");
     if (want) {
-        exact_finish_kernel<<<1, 32, 0, s->st>>>(a, picks, (int)want, s->gbase, didx, dsim, dscore);
+        exact_finish_kernel<<<1, 32, 0, s->st>>>(a, picks, (int)want, s->gbase, didx, dsim, dscore,
+                                                 drew, dround);
         SAIR_LAUNCH("exact_finish_kernel");
         SAIR_CUDA(cudaMemcpyAsync(o_idx, didx, want * 8, cudaMemcpyDeviceToHost, s->st));
         SAIR_CUDA(cudaMemcpyAsync(o_sim, dsim, want * 8, cudaMemcpyDeviceToHost, s->st));
         SAIR_CUDA(cudaMemcpyAsync(o_score, dscore, want * 8, cudaMemcpyDeviceToHost, s->st));
+        if (o_rew)
+            SAIR_CUDA(cudaMemcpyAsync(o_rew, drew, want * 8, cudaMemcpyDeviceToHost, s->st));
+        if (o_round)
+            SAIR_CUDA(cudaMemcpyAsync(o_round, dround, want * 4, cudaMemcpyDeviceToHost, s->st));
     }
     if (o_nn) {
         exact_argmax_kernel<<<blocks, threads, 0, s->st>>>(a, 1, part);
@@ -304,7 +317,8 @@ double store_surprisal(sair_store_s* s, size_t index, const double* x,
     a.zq = dm + 2 * d;
     a.d = d;
     a.n = s->n;
-    a.total = s->stats.total;
+    a.n_loo = eff_n(s);
+    a.total = eff_stats(s).total;
     a.two_s2 = p.two_s2;
     a.loo = cfg.locally_weighted_mean ? dm : nullptr;  // non-null flags the local mean
     double* out = dm + 3 * d;

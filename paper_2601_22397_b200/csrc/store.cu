@@ -347,10 +347,11 @@ void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int di
 
 void store_mean_sd(const sair_store_s* s, double* mean, double* sd) {
     // standardize's per-dimension statistics, experience.cpp:159-165
-    double nn = static_cast<double>(s->n);
+    const StoreStats& st = eff_stats(s);
+    double nn = static_cast<double>(eff_n(s));
     for (int k = 0; k < s->d; ++k) {
-        double m = s->stats.sum[k] / nn;
-        double var = std::max(0.0, s->stats.sum_sq[k] / nn - m * m);
+        double m = st.sum[k] / nn;
+        double var = std::max(0.0, st.sum_sq[k] / nn - m * m);
         double v = std::sqrt(var);
         if (v < 1e-12) v = 1.0;
         mean[k] = m;
@@ -365,53 +366,89 @@ void store_standardize(const sair_store_s* s, const double* x, double* z) {
     for (int k = 0; k < s->d; ++k) z[k] = (x[k] - mean[k]) / sd[k];
 }
 
-static double refresh_sigma(sair_store_s* s) {
-    // experience.cpp:171-205 on the device
-    const size_t capn = 512;
-    std::vector<int64_t> idx;
-    if (s->n <= capn) {
-        for (size_t k = 0; k < s->n; ++k) idx.push_back((int64_t)k);
-    } else {
-        double stride = static_cast<double>(s->n) / capn;
-        for (size_t k = 0; k < capn; ++k) idx.push_back((int64_t)(size_t)(k * stride));
-    }
-    int m = (int)idx.size();
-    size_t np = (size_t)m * (m - 1) / 2;
+// median pairwise z-distance of the rows idx of `x64` (device, record-major),
+// experience.cpp:183-203: z rows, every pair's distance, the order statistic
+// at size/2 (what nth_element places there) via a device radix sort.
+static double sigma_of_rows(cudaStream_t st, DBuf& scratch, const double* x64,
+                            const std::vector<int64_t>& idx, int d, const double* mean,
+                            const double* sd) {
+    const int m = (int)idx.size();
+    const size_t np = (size_t)m * (m - 1) / 2;
     if (np == 0) return 1.0;
-    DeviceGuard g(s->device);
-    int d = s->d;
-    std::vector<double> msd(2 * d);
-    store_mean_sd(s, msd.data(), msd.data() + d);
     size_t tmp_bytes = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, (double*)nullptr, (double*)nullptr,
                                    (int)np);
     size_t off_idx = 0, off_msd = off_idx + m * 8, off_z = off_msd + 2 * d * 8,
-           off_d = off_z + (size_t)m * d * 8, off_s = off_d + np * 8,
-           off_t = off_s + np * 8;
-    char* base = static_cast<char*>(s->b_sigma.get(off_t + tmp_bytes + 256));
+           off_d = off_z + (size_t)m * d * 8, off_s = off_d + np * 8, off_t = off_s + np * 8;
+    char* base = static_cast<char*>(scratch.get(off_t + tmp_bytes + 256));
     auto* didx = reinterpret_cast<int64_t*>(base + off_idx);
     auto* dmsd = reinterpret_cast<double*>(base + off_msd);
     auto* dz = reinterpret_cast<double*>(base + off_z);
     auto* dd = reinterpret_cast<double*>(base + off_d);
     auto* ds = reinterpret_cast<double*>(base + off_s);
-    SAIR_CUDA(cudaMemcpyAsync(didx, idx.data(), m * 8, cudaMemcpyHostToDevice, s->st));
-    SAIR_CUDA(cudaMemcpyAsync(dmsd, msd.data(), 2 * d * 8, cudaMemcpyHostToDevice, s->st));
-    sigma_z_kernel<<<ceil_div((size_t)m * d, 256), 256, 0, s->st>>>(s->x64, didx, m, d, dmsd,
-                                                                    dmsd + d, dz);
+    SAIR_CUDA(cudaMemcpyAsync(didx, idx.data(), m * 8, cudaMemcpyHostToDevice, st));
+    SAIR_CUDA(cudaMemcpyAsync(dmsd, mean, d * 8, cudaMemcpyHostToDevice, st));
+    SAIR_CUDA(cudaMemcpyAsync(dmsd + d, sd, d * 8, cudaMemcpyHostToDevice, st));
+    sigma_z_kernel<<<ceil_div((size_t)m * d, 256), 256, 0, st>>>(x64, didx, m, d, dmsd, dmsd + d,
+                                                                 dz);
     SAIR_LAUNCH("sigma_z_kernel");
-    sigma_pairs_kernel<<<m, 128, 0, s->st>>>(dz, m, d, dd);
+    sigma_pairs_kernel<<<m, 128, 0, st>>>(dz, m, d, dd);
     SAIR_LAUNCH("sigma_pairs_kernel");
-    SAIR_CUDA(cub::DeviceRadixSort::SortKeys(base + off_t, tmp_bytes, dd, ds, (int)np, 0, 64,
-                                             s->st));
+    SAIR_CUDA(cub::DeviceRadixSort::SortKeys(base + off_t, tmp_bytes, dd, ds, (int)np, 0, 64, st));
     double mid = 0.0;
-    SAIR_CUDA(cudaMemcpyAsync(&mid, ds + np / 2, 8, cudaMemcpyDeviceToHost, s->st));
-    SAIR_CUDA(cudaStreamSynchronize(s->st));
+    SAIR_CUDA(cudaMemcpyAsync(&mid, ds + np / 2, 8, cudaMemcpyDeviceToHost, st));
+    SAIR_CUDA(cudaStreamSynchronize(st));
     return mid > 1e-12 ? mid : 1.0;
+}
+
+// the strided subsample of refresh_sigma_cache, experience.cpp:173-182
+std::vector<int64_t> sigma_sample(uint64_t n) {
+    const size_t capn = 512;
+    std::vector<int64_t> idx;
+    if (n <= capn) {
+        for (size_t k = 0; k < n; ++k) idx.push_back((int64_t)k);
+    } else {
+        double stride = static_cast<double>(n) / capn;
+        for (size_t k = 0; k < capn; ++k) idx.push_back((int64_t)(size_t)(k * stride));
+    }
+    return idx;
+}
+
+static double refresh_sigma(sair_store_s* s) {
+    DeviceGuard g(s->device);
+    const int d = s->d;
+    std::vector<double> mean(d), sd(d);
+    store_mean_sd(s, mean.data(), sd.data());
+    return sigma_of_rows(s->st, s->b_sigma, s->x64, sigma_sample(s->n), d, mean.data(), sd.data());
+}
+
+double sigma_rows(const double* rows, size_t m, int d, const double* mean, const double* sd,
+                  int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(SAIR_ECUDA, "no CUDA device (libsair has no CPU fallback)");
+    DeviceGuard g(device);
+    cudaStream_t st;
+    SAIR_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    DBuf rb, scratch;
+    double* dr = static_cast<double*>(rb.get(m * (size_t)d * 8 + 8));
+    SAIR_CUDA(cudaMemcpyAsync(dr, rows, m * (size_t)d * 8, cudaMemcpyHostToDevice, st));
+    std::vector<int64_t> idx(m);
+    for (size_t i = 0; i < m; ++i) idx[i] = (int64_t)i;
+    double v = sigma_of_rows(st, scratch, dr, idx, d, mean, sd);
+    cudaStreamDestroy(st);
+    return v;
 }
 
 double store_effective_sigma(sair_store_s* s, double sigma_sim) {
     // experience.cpp:207-212
     if (sigma_sim > 0.0) return sigma_sim;
+    if (s->sharded) {  // the buffer's sigma, computed over its global subsample
+        if (s->n_global < 2) return 1.0;
+        if (!(s->gsigma > 0.0))
+            throw Error(SAIR_EINVAL, "sharded store: set the buffer's sigma (sair_store_set_global)");
+        return s->gsigma;
+    }
     if (s->n < 2) return 1.0;
     if (s->cached_sigma == 0.0 || s->stale >= 50) {
         s->cached_sigma = refresh_sigma(s);
@@ -425,6 +462,10 @@ void store_clone(const sair_store_s* s, sair_store_s* o) {
     o->rejected = s->rejected;
     o->gbase = s->gbase;
     o->stats = s->stats;
+    o->sharded = s->sharded;
+    o->n_global = s->n_global;
+    o->gst = s->gst;
+    o->gsigma = s->gsigma;
     o->shift = s->shift;
     if (!s->shift.empty()) {
         DeviceGuard g0(s->device);

@@ -1,0 +1,183 @@
+"""One logical ExperienceBuffer sharded over the GPUs of a node.
+
+One process per GPU (torch.distributed, NCCL over NVLink; gloo for CPU tests).
+Rank r owns the contiguous global slice [lo_r, hi_r) of the buffer.  Exactness
+with the single-buffer reference (experience.cpp:242-296) rests on three
+exchanges, each deterministic (rank order):
+
+1. statistics -- every rank all-gathers the shards' running sums and combines
+   them in rank order (sum_, sum_sq_, the reward total; experience.cpp:146-149,
+   :229-230).  For the synthetic generator every partial sum is exact, so the
+   combined sums are bit-identical to the sequential reference's;
+2. sigma -- the buffer's 512-row subsample (experience.cpp:173-182) is gathered
+   from the owning ranks and every rank computes the same median on its device;
+3. candidates -- each shard's certified top-m (exact fp64 scores over the
+   global statistics, each pick's reward and round) is all-gathered and merged
+   by the device merge kernel (score desc, round asc, global index asc, then
+   curriculum order).  With lambda_div == 0 the buffer's top-m is a subset of
+   the union of the shards' top-m, so the merge is exact.
+
+lambda_div > 0 (the greedy with diversity penalties) needs every shard's
+candidate pool and the pool vectors on one device; it is not sharded yet
+(DESIGN.md "Multi-GPU").
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Tuple
+
+import numpy as np
+
+from . import SelectionConfig, _check, _dp, _f64, lib
+from . import ExperienceBuffer
+
+
+def shard_range(n_total: int, rank: int, world: int) -> Tuple[int, int]:
+    return n_total * rank // world, n_total * (rank + 1) // world
+
+
+def combine_stats(parts: List[np.ndarray], d: int):
+    """Rank-ordered combination of per-shard (sum[d], sum_sq[d], xabs[d], n,
+    total, rabs) vectors -> global (n, sum, sum_sq, xabs, total, rabs)."""
+    n = 0
+    s = np.zeros(d)
+    ss = np.zeros(d)
+    xa = np.zeros(d)
+    total = 0.0
+    rabs = 0.0
+    for p in parts:  # rank order: deterministic on every rank
+        s = s + p[:d]
+        ss = ss + p[d:2 * d]
+        xa = np.maximum(xa, p[2 * d:3 * d])
+        n += int(p[3 * d])
+        total = total + float(p[3 * d + 1])
+        rabs = max(rabs, float(p[3 * d + 2]))
+    return n, s, ss, xa, total, rabs
+
+
+def moments(n: int, s: np.ndarray, ss: np.ndarray):
+    """standardize()'s mean / sd, experience.cpp:159-165 (numpy fp64, same
+    operation order -- used only to feed the device sigma kernel)."""
+    mean = s / float(n)
+    var = np.maximum(0.0, ss / float(n) - mean * mean)
+    sd = np.sqrt(var)
+    sd[sd < 1e-12] = 1.0
+    return mean, sd
+
+
+def sigma_sample_indices(n: int) -> np.ndarray:
+    idx = np.zeros(512, np.int64)
+    m = C.c_size_t()
+    _check(lib().sair_sigma_sample_indices(n, idx.ctypes.data_as(C.POINTER(C.c_int64)),
+                                           C.byref(m)))
+    return idx[:m.value]
+
+
+def _all_gather(dist, arr: np.ndarray, device) -> List[np.ndarray]:
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    if dist.get_backend() == "nccl":
+        t = t.to(device)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.cpu().numpy() for o in out]
+
+
+class ShardedExperienceBuffer:
+    """The rank-local shard of one logical ExperienceBuffer."""
+
+    def __init__(self, dist, device: int, r_min: float = 0.0):
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.device = device
+        self.local = ExperienceBuffer(r_min, device=device)
+        self.lo = self.hi = 0
+        self.n_global = 0
+
+    def store_synthetic(self, seed: int, n_total: int, dim: int, clustered: bool = False):
+        """Every rank generates its slice of the same synthetic buffer."""
+        self.lo, self.hi = shard_range(n_total, self.rank, self.world)
+        _check(lib().sair_store_set_shard(self.local._h, self.lo))
+        self.local.store_synthetic(seed, self.hi - self.lo, dim, clustered)
+        self.finalize()
+
+    def finalize(self):
+        """Exchange statistics and sigma; switch the shard to global mode."""
+        d = self.local.dim()
+        s, ss, xa, sc = np.zeros(d), np.zeros(d), np.zeros(d), np.zeros(3)
+        _check(lib().sair_store_local_stats(self.local._h, _dp(s), _dp(ss), _dp(xa), _dp(sc)))
+        mine = np.concatenate([s, ss, xa, sc])
+        dev = f"cuda:{self.device}"
+        parts = _all_gather(self.dist, mine, dev)
+        n, gs, gss, gxa, total, rabs = combine_stats(parts, d)
+        self.n_global = n
+        mean, sd = moments(n, gs, gss)
+        # sigma over the buffer's subsample: rows come from their owners
+        idx = sigma_sample_indices(n)
+        rows = np.zeros((len(idx), d))
+        owned = (idx >= self.lo) & (idx < self.hi)
+        for j in np.nonzero(owned)[0]:
+            rows[j] = self.local.get(int(idx[j] - self.lo))[0]
+        gathered = _all_gather(self.dist, np.concatenate([owned.astype(np.float64)[:, None], rows],
+                                                         axis=1), dev)
+        full = np.zeros((len(idx), d))
+        for g in gathered:
+            own = g[:, 0] > 0
+            full[own] = g[own, 1:]
+        sigma = C.c_double(1.0)
+        if len(idx) >= 2:
+            _check(lib().sair_sigma_rows(_dp(np.ascontiguousarray(full)), len(idx), d, _dp(mean),
+                                         _dp(sd), self.device, C.byref(sigma)))
+        _check(lib().sair_store_set_global(self.local._h, n, _dp(gs), _dp(gss), _dp(gxa), total,
+                                           rabs, sigma.value))
+        self.sigma = sigma.value
+
+    def select_local(self, queries, cfg: SelectionConfig):
+        q = _f64(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        nq, d = q.shape
+        m = max(cfg.m, 1)
+        idx = np.full((nq, m), -1, np.int64)
+        sim, sc, rw = np.zeros((nq, m)), np.zeros((nq, m)), np.zeros((nq, m))
+        rd = np.zeros((nq, m), np.int32)
+        cnt = np.zeros(nq, np.uintp)
+        c = cfg._c()
+        _check(lib().sair_store_select_shard(
+            self.local._h, _dp(q), nq, d, C.byref(c), idx.ctypes.data_as(C.POINTER(C.c_int64)),
+            _dp(sim), _dp(sc), _dp(rw), rd.ctypes.data_as(C.POINTER(C.c_int32)),
+            cnt.ctypes.data_as(C.POINTER(C.c_size_t))))
+        return idx, sim, sc, rw, rd, cnt.astype(np.int64)
+
+    def select_batch(self, queries, cfg: SelectionConfig):
+        """The buffer's select() for every query: (idx, sim, score, count)."""
+        if cfg.lambda_div != 0.0:
+            raise NotImplementedError("sharded select supports lambda_div == 0 (DESIGN.md)")
+        idx, sim, sc, rw, rd, cnt = self.select_local(queries, cfg)
+        nq, m = idx.shape
+        pack = np.concatenate([sc, sim, rw, idx.astype(np.float64), rd.astype(np.float64),
+                               cnt.astype(np.float64)[:, None]], axis=1)
+        parts = _all_gather(self.dist, pack, f"cuda:{self.device}")
+        return merge_parts(parts, nq, m, self.device)
+
+
+def merge_parts(parts: List[np.ndarray], nq: int, m: int, device: int):
+    """Device merge (sair_merge_topk) of all-gathered per-shard results."""
+    S = len(parts)
+    sc = np.stack([p[:, 0:m] for p in parts])
+    sim = np.stack([p[:, m:2 * m] for p in parts])
+    rw = np.stack([p[:, 2 * m:3 * m] for p in parts])
+    gi = np.ascontiguousarray(np.stack([p[:, 3 * m:4 * m] for p in parts]).astype(np.int64))
+    rd = np.ascontiguousarray(np.stack([p[:, 4 * m:5 * m] for p in parts]).astype(np.int32))
+    ct = np.ascontiguousarray(np.stack([p[:, 5 * m] for p in parts]).astype(np.uintp))
+    oi = np.full((nq, m), -1, np.int64)
+    osim, osc = np.zeros((nq, m)), np.zeros((nq, m))
+    ocnt = np.zeros(nq, np.uintp)
+    _check(lib().sair_merge_topk(
+        _dp(np.ascontiguousarray(sc)), _dp(np.ascontiguousarray(sim)),
+        _dp(np.ascontiguousarray(rw)), rd.ctypes.data_as(C.POINTER(C.c_int32)),
+        gi.ctypes.data_as(C.POINTER(C.c_int64)), ct.ctypes.data_as(C.POINTER(C.c_size_t)), S, nq,
+        m, device, oi.ctypes.data_as(C.POINTER(C.c_int64)), _dp(osim), _dp(osc),
+        ocnt.ctypes.data_as(C.POINTER(C.c_size_t))))
+    return oi, osim, osc, ocnt.astype(np.int64)

@@ -1,6 +1,5 @@
-# quick iteration: parity tests + bench + one full ncu capture of the stream kernel
+# quick iteration: parity tests + bench + bounded ncu capture of the stream kernel
 set -x
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -15
 timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>&1 | tail -2
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 4 -c 1 -o gpurun_out/prof_stream python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-pareto > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/ncu_full.log
+bash scripts/gpu_prof.sh
