@@ -128,6 +128,11 @@ SAIR_API sair_status sair_store_standardize(sair_store_t h, const double* x, int
  * 512-subsample pairwise median on the device. */
 SAIR_API sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double* out);
 
+/* similarity(a, b, sigma), experience.cpp:121-131: SAIR_EINVAL when the
+ * lengths differ or sigma <= 0. */
+SAIR_API sair_status sair_similarity(const double* a, size_t len_a, const double* b, size_t len_b,
+                                     double sigma, double* out);
+
 /* ExperienceBuffer::surprisal, experience.cpp:234-240 (SAIR_ERANGE on a bad index). */
 SAIR_API sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, int dim,
                                           const sair_select_config* cfg, double* out);

@@ -73,6 +73,7 @@ SIGNATURES = {
     "sair_store_get": (C.c_int, [_vp, C.c_size_t, _dp, _dp, _i32p]),
     "sair_store_standardize": (C.c_int, [_vp, _dp, C.c_int, _dp]),
     "sair_store_effective_sigma": (C.c_int, [_vp, C.c_double, _dp]),
+    "sair_similarity": (C.c_int, [_dp, C.c_size_t, _dp, C.c_size_t, C.c_double, _dp]),
     "sair_store_surprisal": (C.c_int, [_vp, C.c_size_t, _dp, C.c_int,
                                        C.POINTER(SelectConfigC), _dp]),
     "sair_store_select": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, C.POINTER(SelectConfigC),

@@ -165,6 +165,15 @@ sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double*
     return guard([&] { *out = sair::store_effective_sigma(h, sigma_sim); });
 }
 
+sair_status sair_similarity(const double* a, size_t len_a, const double* b, size_t len_b,
+                            double sigma, double* out) {
+    if (!out) return bad("null output");
+    // experience.cpp:122-124: the dimension check, then the sigma check
+    if (len_a != len_b) return bad("similarity: dimension mismatch");
+    if (sigma <= 0.0) return bad("similarity: sigma must be positive");
+    return guard([&] { *out = sair::similarity(a, b, (int)len_a, sigma, 0); });
+}
+
 sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, int dim,
                                  const sair_select_config* cfg, double* out) {
     if (!h || !out) return bad("null handle");

@@ -173,5 +173,6 @@ void compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas, s
                           sair_frontier_s* f, const sair_reward_config* cfg,
                           sair_reward_breakdown* out);
 double action_magnitude(const int32_t* deltas, size_t S, int device);
+double similarity(const double* a, const double* b, int d, double sigma, int device);
 
 }  // namespace sair
