@@ -26,11 +26,13 @@
 // Queries that cannot be certified are answered by the full fp64 pass
 // (select_exact.cu).  The exactness argument is DESIGN.md "Exactness".
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <cstring>
 #include <vector>
 
 #include "select_common.cuh"
+#include "warp_topk.cuh"
 
 namespace sair {
 
@@ -66,114 +68,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
-}
-
-// ------------------------------------------------- warp radix-select (smem) --
-
-// One 8-bit digit step of a descending radix select over `cnt` entries: finds
-// the bin (from the top) holding rank r.  Returns the bin; r is reduced by the
-// count above it; *binc gets the bin's population.
-template <class Get>
-__device__ __forceinline__ int warp_digit(Get get, int cnt, uint32_t prefix, uint32_t pmask,
-                                          int shift, int& r, uint32_t* hist, int lane,
-                                          uint32_t* binc) {
-    for (int b = lane; b < 256; b += 32) hist[b] = 0;
-    __syncwarp();
-    for (int i = lane; i < cnt; i += 32) {
-        uint32_t u;
-        if (get(i, u) && (u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
-    }
-    __syncwarp();
-    uint32_t loc[8], sum = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        loc[j] = hist[255 - (lane * 8 + j)];
-        sum += loc[j];
-    }
-    uint32_t incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    const uint32_t excl = incl - sum;
-    const unsigned own = __ballot_sync(0xffffffffu, excl < (uint32_t)r && (uint32_t)r <= incl);
-    const int owner = __ffs(own) - 1;
-    int bin = 0;
-    uint32_t above = 0, pop = 0;
-    if (lane == owner) {
-        uint32_t c = excl;
-        for (int j = 0; j < 8; ++j) {
-            if (c + loc[j] >= (uint32_t)r) {
-                bin = 255 - (lane * 8 + j);
-                above = c;
-                pop = loc[j];
-                break;
-            }
-            c += loc[j];
-        }
-    }
-    bin = __shfl_sync(0xffffffffu, bin, owner);
-    above = __shfl_sync(0xffffffffu, above, owner);
-    *binc = __shfl_sync(0xffffffffu, pop, owner);
-    r -= (int)above;
-    __syncwarp();
-    return bin;
-}
-
-// Keep the K largest entries of a candidate list by (key desc, idx asc),
-// compacted in place to [0, K).  Returns the ordinal of the K-th key.
-__device__ __noinline__ uint32_t warp_keep_topk(float* key, uint32_t* idx, int cnt, int K, uint32_t* hist,
-                                   int lane) {
-    uint32_t prefix = 0, pmask = 0, binc = 0;
-    int r = K;
-    auto by_key = [&](int i, uint32_t& u) {
-        u = f2ord(key[i]);
-        return true;
-    };
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        int bin = warp_digit(by_key, cnt, prefix, pmask, shift, r, hist, lane, &binc);
-        prefix |= (uint32_t)bin << shift;
-        pmask |= 255u << shift;
-    }
-    const uint32_t T = prefix;
-    uint32_t TI = 0;  // ties at T are kept when ~idx >= TI
-    if ((int)binc > r) {
-        uint32_t pre = 0, pm = 0;
-        auto by_idx = [&](int i, uint32_t& u) {
-            u = ~idx[i];
-            return f2ord(key[i]) == T;
-        };
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            int bin = warp_digit(by_idx, cnt, pre, pm, shift, r, hist, lane, &binc);
-            pre |= (uint32_t)bin << shift;
-            pm |= 255u << shift;
-        }
-        TI = pre;
-    }
-    int w = 0;  // in-place compaction: writes never pass the read position
-    for (int base = 0; base < cnt; base += 32) {
-        const int i = base + lane;
-        float kk = 0.f;
-        uint32_t ii = 0;
-        bool keep = false;
-        if (i < cnt) {
-            kk = key[i];
-            ii = idx[i];
-            const uint32_t u = f2ord(kk);
-            keep = u > T || (u == T && ~ii >= TI);
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        __syncwarp();
-        if (keep) {
-            const int pos = w + __popc(bal & ((1u << lane) - 1u));
-            key[pos] = kk;
-            idx[pos] = ii;
-        }
-        w += __popc(bal);
-        __syncwarp();
-    }
-    return T;
 }
 
 // ------------------------------------------------------------ K3 stream --
@@ -597,7 +491,8 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
     // d2 error bound of the filter: E_q = gamma (sqrt(Pmax) + sqrt(C_q))^2
     const double pmx = (double)__uint_as_float(*a.pmax);
     const double sq = sqrt(pmx) + sqrt(a.cc[q]);
-    const double Eq = a.gamma * sq * sq + 1e-30;
+    // + the TF32 rounding of the stored records: d2_true >= d2 (1 - 2^-11) - 2^-11 P
+    const double Eq = a.gamma * sq * sq + 0x1p-11 * pmx * (1.0 + 1e-6) + 1e-30;
 
     // exact score of every candidate: experience.cpp:254-258 with the
     // reference's rounding sequence (standardize :162-166, similarity
@@ -743,7 +638,7 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
         if (a.has_excl_nn) {
             // excluded records have d2_32 >= D = -U_nn, so true d2 >= D - E_q
             const double D = -(double)a.cthr[a.QB + q];
-            const double lo = fmax(D - Eq, 0.0);
+            const double lo = fmax(D * (1.0 - 0x1p-11) - Eq, 0.0);
             cert = c.g > exp(-lo / a.two_s2) * (1.0 + 1e-12);
         }
         a.out_nn[q] = a.gbase + c.i;
@@ -897,9 +792,23 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                       n < (size_t)1 << 31 && m <= 256;
     float stream_ms = 0.f;
     if (fast) {
-        const StreamPlan pl = make_plan(s, nq, m, cfg.lambda_div, out_nn != nullptr);
+        // tensor-core streaming kernel when the shape fits,
+        // the CUDA-core kernel otherwise or when SAIR_NO_MMA is set
+        MmaPlan mp{};
+        const bool use_mma = std::getenv("SAIR_NO_MMA") == nullptr &&
+                             make_mma_plan(s, nq, m, cfg.lambda_div, out_nn != nullptr, &mp);
+        StreamPlan pl = make_plan(s, nq, m, cfg.lambda_div, out_nn != nullptr);
+        if (use_mma) {
+            pl.dp = mp.dp;
+            pl.qb = mp.qb;
+            pl.kp = mp.kp;
+            pl.knn = mp.knn;
+            pl.kmax = mp.kmax;
+            pl.grid = mp.grid;
+        }
         const int qb = pl.qb, kp = pl.kp, knn = pl.knn, kmax = pl.kmax;
         FillFn fill = pick_fill(pl.dp, qb);
+        MmaFillFn mfill = use_mma ? pick_mma_fill(mp.dp, qb) : nullptr;
 
         // filter constants
         const double u = 0x1p-24;
@@ -914,7 +823,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         const double rdel = 4.0 * u * (est.rabs * c1d + std::fabs(c0d)) * 1.01 + 1e-30;
         const float rdelta = (float)rdel;
         const double beta = 1.4426950408889634 / p.two_s2;  // log2(e) / (2 sigma^2)
-        const float alpha = (float)beta;
+        const float alpha = (float)(beta * (1.0 - 0x1p-11));  // TF32 storage, see Eq
         const double lg_hi = std::log2(est.rabs * c1d + std::fabs(c0d) + rdel);
         const double key_slack_abs = 1.0 + 2.0 * (std::fabs(std::log2(rdel)) + std::fabs(lg_hi));
 
@@ -975,7 +884,10 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             }
             SAIR_CUDA(cudaMemsetAsync(dpmax, 0, 4, s->st));
             SAIR_CUDA(cudaEventRecord(s->ev[1], s->st));
-            fill(s, pl, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
+            if (use_mma)
+                mfill(s, mp, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
+            else
+                fill(s, pl, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
             SAIR_CUDA(cudaEventRecord(s->ev[2], s->st));
             s->last.stream_launches++;
             for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
@@ -1004,7 +916,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.two_s2 = p.two_s2;
             ra.lambda = cfg.lambda_div;
             ra.beta = beta;
-            ra.gamma = (pl.dp + 16) * u;
+            ra.gamma = use_mma ? (pl.dp + 24) * u + 0x1p-20 : (pl.dp + 16) * u;
             ra.key_slack_abs = key_slack_abs;
             ra.has_excl = n > (size_t)kp;
             ra.has_excl_nn = n > (size_t)knn;

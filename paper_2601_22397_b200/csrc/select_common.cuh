@@ -60,6 +60,18 @@ inline QueryPrep prep_queries(const sair_store_s* s, const double* q, size_t nq,
     return p;
 }
 
+// select_mma.cu: the tcgen05 streaming kernel (plan + launcher)
+struct MmaPlan {
+    int dp, qb, kp, knn, kmax, nst, cap_sel, cap_nn, grid;
+    size_t smem;
+};
+using MmaFillFn = void (*)(sair_store_s*, const MmaPlan&, const QueryPrep&, const double*, int,
+                           float, float, float, float, float*, uint32_t*, unsigned int*,
+                           std::vector<double>&);
+MmaFillFn pick_mma_fill(int dp, int qb);
+bool make_mma_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
+                   MmaPlan* pl);
+
 // select_exact.cu: one query through the full fp64 pass.
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,

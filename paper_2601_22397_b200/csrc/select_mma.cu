@@ -1,0 +1,558 @@
+// select_mma.cu -- K3 on the 5th-generation tensor cores.
+//
+// The streaming filter's dominant work is the contraction
+//   D[record][q] = sum_k x[record][k] * b[k][q],   b[k][q] = -2 c_qk / sd_k
+// (the cross term of ||y - c_q||^2).  Here it runs as tcgen05.mma kind::tf32:
+//
+//   warp 8 (producer)  TMA tensor copies (cp.async.bulk.tensor.3d, 128-byte
+//                      swizzle with 32-byte atoms) of 32-record x DP-dimension
+//                      boxes straight from the page layout into a 3-deep
+//                      shared-memory ring; a box is exactly one MN-major
+//                      SWIZZLE_128B_BASE32B UMMA operand block (the layout
+//                      tcgen05 requires for MN-major tf32).
+//   warp 9 (MMA)       allocates TMEM, and one elected lane issues
+//                      M=128 (records) x N=16 x K=8 MMAs per page: A = the
+//                      page tile (MN-major, records contiguous), B = the query
+//                      constants split hi/lo in TF32 (K-major, 16 columns: 8
+//                      hi + 8 lo), D accumulates in TMEM; tcgen05.commit
+//                      signals the consumers.
+//   warps 0-7          P = ||y||^2 on the CUDA cores from the same shared tile
+//   (consumers)        (one record per thread), D from TMEM (tcgen05.ld
+//                      32x32b.x16, lane = record), then keys, thresholds and
+//                      candidate lists exactly as the CUDA-core kernel.
+//
+// Records are stored rounded to TF32 (cvt.rna at append), so the MMA sees the
+// stored values exactly and P, D describe the same vector; the rounding is a
+// bounded input perturbation the certification accounts for.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cstring>
+#include <vector>
+
+#include "select_common.cuh"
+#include "warp_topk.cuh"
+
+namespace sair {
+
+
+namespace {
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_W_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra LAB_W_%=;\n"
+        "}\n" ::"r"(su32(b)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+// UMMA shared-memory descriptor (sm_100): start >> 4, LBO >> 4, SBO >> 4,
+// version 1, layout type in bits 61-63 (2 = SWIZZLE_128B, 0 = none).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                              uint32_t layout) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)(layout & 7u) << 61;
+    return d;
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+constexpr int MW = 8;                  // consumer warps
+constexpr int MMA_THREADS = MW * 32 + 64;  // + producer warp + MMA warp
+constexpr int PAGES_PER_STAGE = 1;
+constexpr int TMEM_COLS = 128;
+// instruction descriptor: D f32, A/B tf32, A MN-major, B K-major, N=16, M=128
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((16u >> 3) << 17) |
+                           ((128u >> 4) << 24);
+
+}  // namespace
+
+template <int DP, int QB>
+struct MmaArgs {
+    const float* r32;
+    uint32_t n, npages;
+    float c1, c0, rdelta, alpha;
+    int kp, knn, nst, cap_sel, cap_nn, kmax;
+    float* out_key;  // [grid][2*QB][kmax]
+    uint32_t* out_idx;
+    unsigned int* pmax;
+    const float* b;   // [2][DP][QB] hi / lo TF32 parts of -2 c_qk / sd_k (device)
+    float s[DP];      // 1 / sd (0 on padding)
+    float cc[QB];     // sum_k c_qk^2
+};
+
+template <int DP, int QB>
+__global__ void __launch_bounds__(MMA_THREADS, 1)
+    stream_mma_kernel(const __grid_constant__ CUtensorMap tmap,
+                      const __grid_constant__ MmaArgs<DP, QB> a) {
+    constexpr int BOX_BYTES = 32 * DP * 4;              // 32 records x DP dims
+    constexpr int PAGE_BYTES = 4 * BOX_BYTES;           // 4 boxes = 128 records
+    constexpr int STAGE_BYTES = PAGES_PER_STAGE * PAGE_BYTES;
+    constexpr int KSTEPS = DP / 8;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the SWIZZLE_128B atoms
+    // (offsetting smem_raw keeps the pointer in the shared window: LDS, not LD)
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nl = a.knn ? 2 * QB : QB;
+    unsigned char* stage = smem;
+    float* btile = reinterpret_cast<float*>(stage + (size_t)a.nst * STAGE_BYTES);  // KSTEPS x 512 B
+    float* ss = btile + KSTEPS * 128;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ss + DP);
+    uint64_t* empty = full + 8;
+    uint64_t* tfull = empty + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 8);
+    float* thr = reinterpret_cast<float*>(tmem_slot + 4);
+    int* cnt = reinterpret_cast<int*>(thr + 2 * QB);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(cnt + 2 * QB);
+    float* lkey = reinterpret_cast<float*>(hist + MW * 256);
+    const int total_cap = QB * a.cap_sel + (a.knn ? QB * a.cap_nn : 0);
+    uint32_t* lidx = reinterpret_cast<uint32_t*>(lkey + total_cap);
+    auto lbase = [&](int L) { return L < QB ? L * a.cap_sel : QB * a.cap_sel + (L - QB) * a.cap_nn; };
+    auto lcap = [&](int L) { return L < QB ? a.cap_sel : a.cap_nn; };
+    auto lk = [&](int L) { return L < QB ? a.kp : a.knn; };
+
+    // B operand: K-major, no swizzle; per K-step a 16 (N) x 8 (K) tile of four
+    // 8x16B core matrices: (n%8)*16 + (n/8)*256 + (k%4)*4 + (k/4)*128 bytes
+    for (int i = tid; i < KSTEPS * 16 * 8; i += MMA_THREADS) {
+        const int ks = i / 128, n = (i / 8) % 16, k = i % 8;
+        const int dim = ks * 8 + k;
+        float v = 0.f;
+        if (n < QB) v = a.b[dim * QB + n];
+        else if (n >= 8 && n - 8 < QB) v = a.b[(DP + dim) * QB + n - 8];
+        const int off = ks * 512 + (n % 8) * 16 + (n / 8) * 256 + (k % 4) * 4 + (k / 4) * 128;
+        btile[off / 4] = v;
+    }
+    for (int i = tid; i < DP; i += MMA_THREADS) ss[i] = a.s[i];
+    if (tid < 2 * QB) {
+        thr[tid] = -FLT_MAX;
+        cnt[tid] = 0;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < a.nst; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], MW / 2);  // one half of the consumers reads each stage
+            bar_init(&tfull[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // generic-proxy writes of the B tiles must be visible to the tensor core
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == MW + 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const uint32_t nrounds = (a.npages + PAGES_PER_STAGE - 1) / PAGES_PER_STAGE;
+    const uint32_t G = gridDim.x, r0 = blockIdx.x;
+    const uint32_t mine = r0 < nrounds ? (nrounds - 1 - r0) / G + 1 : 0;
+
+    if (warp == MW) {
+        // ---------------- producer: TMA tensor loads ----------------
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (uint32_t it = 0; it < mine; ++it) {
+                const uint32_t p0 = (r0 + it * G) * PAGES_PER_STAGE;
+                const uint32_t np = min((uint32_t)PAGES_PER_STAGE, a.npages - p0);
+                if (it >= (uint32_t)a.nst) bar_wait(&empty[s], ph ^ 1u);
+                bar_expect_tx(&full[s], np * PAGE_BYTES);
+                for (uint32_t pp = 0; pp < np; ++pp)
+                    for (int b = 0; b < 4; ++b)
+                        tma_load_3d(stage + (size_t)s * STAGE_BYTES + pp * PAGE_BYTES + b * BOX_BYTES,
+                                    &tmap, &full[s], 32 * b, 0, (int)(p0 + pp));
+                if (++s == a.nst) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == MW + 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t bbase = su32(btile);
+            for (uint32_t it = 0; it < mine; ++it) {
+                bar_wait(&full[s], ph);
+                tc_fence_after();
+                for (int pp = 0; pp < PAGES_PER_STAGE; ++pp) {
+                    const uint32_t abase = su32(stage + (size_t)s * STAGE_BYTES + pp * PAGE_BYTES);
+                    const uint32_t dcol = tmem + (uint32_t)((s * PAGES_PER_STAGE + pp) * 16);
+#pragma unroll
+                    for (int ks = 0; ks < KSTEPS; ++ks) {
+                        // A: MN-major SWIZZLE_128B_BASE32B (the only MN-major layout for
+                        // tf32): LBO = next 32-record block, SBO = next 4-dimension atom
+                        const uint64_t ad = umma_desc(abase + ks * 1024, BOX_BYTES, 512, 1);
+                        const uint64_t bd = umma_desc(bbase + ks * 512, 128, 256, 0);
+                        umma_tf32(dcol, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+                    }
+                }
+                umma_commit(&tfull[s]);
+                if (++s == a.nst) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        // warp w reads TMEM lane quarter w % 4 of every stage with parity w / 4;
+        // the two halves of the consumers work on consecutive stages at once
+        const int pp = 0;
+        const int par = warp >> 2;
+        const int quarter = warp & 3;
+        const int rloc = quarter * 32 + lane;  // record within the page
+        float thr_r[2 * QB];
+#pragma unroll
+        for (int L = 0; L < 2 * QB; ++L) thr_r[L] = -FLT_MAX;
+        float pmax = 0.f;
+        int s = par % a.nst;
+        uint32_t ph = (uint32_t)(par / a.nst) & 1u;
+        const uint32_t rounds = (mine + 1) / 2;  // barrier rounds of two stages
+        for (uint32_t rr = 0; rr < rounds; ++rr) {
+            const uint32_t it = 2 * rr + par;
+            const bool live = it < mine;  // the odd half may idle in the last round
+            const uint32_t page = live ? (r0 + it * G) * PAGES_PER_STAGE + pp : 0;
+            const uint32_t rec = page * PAGE + rloc;
+            const bool valid = live && rec < a.n;
+            if (live) {
+            const float r = valid ? __ldg(a.r32 + rec) : 0.f;
+            bar_wait(&full[s], ph);
+            // P from the swizzled box: row k at k*128 B, 32-B chunk (lane/8) ^ (k%4)
+            const unsigned char* box = stage + (size_t)s * STAGE_BYTES + pp * PAGE_BYTES +
+                                       quarter * BOX_BYTES;
+            float P = 0.f;
+#pragma unroll
+            for (int k = 0; k < DP; ++k) {
+                const float x = *reinterpret_cast<const float*>(
+                    box + k * 128 + ((((lane >> 3) ^ (k & 3)) << 5) | ((lane & 7) << 2)));
+                const float y = __fmul_rn(x, ss[k]);
+                P = fmaf(y, y, P);
+            }
+            bar_wait(&tfull[s], ph);
+            tc_fence_after();
+            float acc[16];
+            tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) +
+                          (uint32_t)((s * PAGES_PER_STAGE + pp) * 16),
+                      acc);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&empty[s]);
+            if (valid) pmax = fmaxf(pmax, P);
+            const float lg = log2f(fabsf(fmaf(r, a.c1, -a.c0)) + a.rdelta);
+            float key[2 * QB];
+            uint32_t pm = 0;
+#pragma unroll
+            for (int q = 0; q < QB; ++q) {
+                const float d2 = (P + a.cc[q]) + (acc[q] + acc[8 + q]);
+                key[q] = fmaf(-d2, a.alpha, lg);
+                key[QB + q] = -d2;
+                pm |= (key[q] > thr_r[q] ? 1u : 0u) << q;
+                pm |= (key[QB + q] > thr_r[QB + q] ? 1u : 0u) << (QB + q);
+            }
+            if (!a.knn) pm &= (1u << QB) - 1u;
+            if (!valid) pm = 0;
+            if (__any_sync(0xffffffffu, pm)) {
+#pragma unroll
+                for (int L = 0; L < 2 * QB; ++L) {
+                    const bool pass = (pm >> L) & 1u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, pass);
+                    if (bal) {
+                        const int leader = __ffs(bal) - 1;
+                        int base = 0;
+                        if (lane == leader) base = atomicAdd(&cnt[L], __popc(bal));
+                        base = __shfl_sync(0xffffffffu, base, leader);
+                        if (pass) {
+                            const int pos = lbase(L) + base + __popc(bal & ((1u << lane) - 1u));
+                            lkey[pos] = key[L];
+                            lidx[pos] = rec;
+                        }
+                    }
+                }
+            }
+            }  // live
+            // consumers-only barrier: lists settle, compact if the next stage could overflow
+            asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
+            bool need = false;
+            for (int L = 0; L < nl; ++L) need |= cnt[L] > lcap(L) - MW * 32;
+            if (need) {
+                for (int L = warp; L < nl; L += MW) {
+                    if (cnt[L] > lcap(L) - MW * 32) {
+                        const uint32_t T = warp_keep_topk(lkey + lbase(L), lidx + lbase(L), cnt[L],
+                                                          lk(L), hist + warp * 256, lane);
+                        if (lane == 0) {
+                            cnt[L] = lk(L);
+                            thr[L] = ord2f(T);
+                        }
+                    }
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
+#pragma unroll
+                for (int L = 0; L < 2 * QB; ++L) thr_r[L] = thr[L];
+            }
+            // this half consumes every other stage: advance the ring by two
+            for (int t = 0; t < 2; ++t)
+                if (++s == a.nst) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+        }
+        for (int L = warp; L < nl; L += MW) {
+            if (cnt[L] > lk(L)) {
+                warp_keep_topk(lkey + lbase(L), lidx + lbase(L), cnt[L], lk(L), hist + warp * 256,
+                               lane);
+                if (lane == 0) cnt[L] = lk(L);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+        if (lane == 0) atomicMax(a.pmax, __float_as_uint(pmax));
+        asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
+        for (int L = 0; L < nl; ++L) {
+            const size_t row = ((size_t)blockIdx.x * 2 * QB + L) * a.kmax;
+            for (int j = tid; j < lk(L); j += MW * 32) {
+                const bool have = j < cnt[L];
+                a.out_key[row + j] = have ? lkey[lbase(L) + j] : -INFINITY;
+                a.out_idx[row + j] = have ? lidx[lbase(L) + j] : 0xFFFFFFFFu - (uint32_t)(row + j);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == MW + 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(TMEM_COLS));
+    }
+}
+
+// ------------------------------------------------------------------- host --
+
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SAIR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            throw Error(SAIR_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+// 3-D view of the page array: (record-in-page 128, dimension dp, page)
+CUtensorMap make_page_map(const float* pages, int dp, uint32_t npages) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    const cuuint64_t dims[3] = {128, (cuuint64_t)dp, npages};
+    const cuuint64_t strides[2] = {128 * 4, (cuuint64_t)dp * 128 * 4};
+    const cuuint32_t box[3] = {32, (cuuint32_t)dp, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(pages), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(SAIR_ECUDA, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+inline float tf32_trunc(double v) {
+    float f = (float)v;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u &= 0xFFFFE000u;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+template <int DP, int QB>
+void mma_fill_and_launch(sair_store_s* s, const MmaPlan& pl, const QueryPrep& p, const double* zgrp,
+                         int nqg, float c1, float c0, float rdelta, float alpha, float* ck,
+                         uint32_t* ci, unsigned int* pmax, std::vector<double>& cc_out) {
+    MmaArgs<DP, QB> a{};
+    a.r32 = s->r32;
+    a.n = (uint32_t)s->n;
+    a.npages = (uint32_t)((s->n + PAGE - 1) / PAGE);
+    a.c1 = c1;
+    a.c0 = c0;
+    a.rdelta = rdelta;
+    a.alpha = alpha;
+    a.kp = pl.kp;
+    a.knn = pl.knn;
+    a.nst = pl.nst;
+    a.cap_sel = pl.cap_sel;
+    a.cap_nn = pl.cap_nn;
+    a.kmax = pl.kmax;
+    a.out_key = ck;
+    a.out_idx = ci;
+    a.pmax = pmax;
+    const int d = s->d;
+    for (int k = 0; k < DP; ++k) a.s[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
+    cc_out.assign(QB, 0.0);
+    float* hb = s->h_mmab.as<float>(2 * DP * QB);
+    for (int q = 0; q < QB; ++q) {
+        const double* z = zgrp + (size_t)(q < nqg ? q : 0) * d;
+        double cc = 0.0;
+        for (int k = 0; k < DP; ++k) {
+            float c = 0.f;
+            if (k < d) c = (float)((p.mean[k] - s->shift[k]) / p.sd[k] + z[k]);
+            cc += (double)c * (double)c;
+            const double bk = k < d ? -2.0 * (double)c * (double)a.s[k] : 0.0;
+            const float hi = tf32_trunc(bk);
+            hb[k * QB + q] = hi;
+            hb[(DP + k) * QB + q] = tf32_trunc(bk - (double)hi);
+        }
+        a.cc[q] = (float)cc;
+        cc_out[q] = cc;
+    }
+    float* db = s->b_mmab.as<float>(2 * DP * QB);
+    SAIR_CUDA(cudaMemcpyAsync(db, hb, 2 * DP * QB * sizeof(float), cudaMemcpyHostToDevice, s->st));
+    a.b = db;
+    // the tensor map is rebuilt only when the page array moved or grew
+    const uint32_t npages = a.npages;
+    if (s->tmap_for != s->pages || s->tmap_pages != npages || s->tmap_dp != DP) {
+        CUtensorMap m = make_page_map(s->pages, DP, npages);
+        std::memcpy(s->tmap, &m, sizeof(m));
+        s->tmap_for = s->pages;
+        s->tmap_pages = npages;
+        s->tmap_dp = DP;
+    }
+    CUtensorMap m;
+    std::memcpy(&m, s->tmap, sizeof(m));
+    SAIR_CUDA(cudaFuncSetAttribute(stream_mma_kernel<DP, QB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    stream_mma_kernel<DP, QB><<<pl.grid, MMA_THREADS, pl.smem, s->st>>>(m, a);
+    SAIR_LAUNCH("stream_mma_kernel");
+}
+
+template <int DP>
+MmaFillFn mma_pick_qb(int qb) {
+    switch (qb) {
+        case 1: return mma_fill_and_launch<DP, 1>;
+        case 2: return mma_fill_and_launch<DP, 2>;
+        case 4: return mma_fill_and_launch<DP, 4>;
+        default: return mma_fill_and_launch<DP, 8>;
+    }
+}
+
+}  // namespace
+
+MmaFillFn pick_mma_fill(int dp, int qb) {
+    switch (dp) {
+        case 8: return mma_pick_qb<8>(qb);
+        case 16: return mma_pick_qb<16>(qb);
+        case 32: return mma_pick_qb<32>(qb);
+        case 64: return mma_pick_qb<64>(qb);
+        default: return nullptr;
+    }
+}
+
+bool make_mma_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
+                   MmaPlan* pl) {
+    if (s->dp < 8 || s->dp > 64) return false;
+    pl->dp = s->dp;
+    pl->qb = nq >= 8 ? 8 : (nq >= 4 ? 4 : (nq >= 2 ? 2 : 1));
+    pl->kp = 32;
+    const size_t want_pool = lambda != 0.0 ? 4 * m : 2 * m;
+    while ((size_t)pl->kp < want_pool && pl->kp < 512) pl->kp <<= 1;
+    pl->knn = nn ? 16 : 0;
+    pl->kmax = std::max(pl->kp, pl->knn);
+    pl->cap_sel = pl->kp + MW * 32 + 64;
+    pl->cap_nn = pl->knn + MW * 32 + 64;
+    const size_t stage = (size_t)PAGES_PER_STAGE * 4 * 32 * pl->dp * 4;  // 32 KB at dp = 64
+    const size_t fixed = 1024 /* alignment slack */ + (size_t)(pl->dp / 8) * 512 + pl->dp * 4 +
+                         24 * 8 + 16 + 2 * 16 * 4 + MW * 256 * 4 +
+                         (size_t)pl->qb * pl->cap_sel * 8 + (nn ? (size_t)pl->qb * pl->cap_nn * 8 : 0);
+    const size_t limit = 227 * 1024;
+    // deep ring of one-page stages: up to 160 KB in flight (<= 8 stages: TMEM columns)
+    pl->nst = (int)std::min<size_t>(8, std::max<size_t>(2, 192 * 1024 / stage));
+    while (pl->nst > 2 && fixed + pl->nst * stage > limit) --pl->nst;
+    if (fixed + pl->nst * stage > limit) return false;
+    if (pl->nst * PAGES_PER_STAGE * 16 > TMEM_COLS) return false;
+    pl->smem = fixed + pl->nst * stage;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    const size_t npages = (s->n + PAGE - 1) / PAGE;
+    const size_t nrounds = (npages + PAGES_PER_STAGE - 1) / PAGES_PER_STAGE;
+    pl->grid = (int)std::max<size_t>(1, std::min<size_t>(nrounds, (size_t)nsm));
+    return true;
+}
+
+}  // namespace sair

@@ -16,6 +16,14 @@ namespace sair {
 
 // ---------------------------------------------------------------- kernels --
 
+// the fp32 page copy holds TF32-rounded values (round to nearest): the
+// tensor-core filter then reads the stored values exactly (select_mma.cu)
+__device__ __forceinline__ float to_tf32(double v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"((float)v));
+    return __uint_as_float(r);
+}
+
 // Scatter `cnt` staged rows (fp64, record-major) into the store at [n0, n0+cnt).
 __global__ void scatter_rows_kernel(const double* __restrict__ sx, const double* __restrict__ sr,
                                     const int32_t* __restrict__ sround, size_t n0, size_t cnt,
@@ -31,7 +39,7 @@ __global__ void scatter_rows_kernel(const double* __restrict__ sx, const double*
         size_t rec = n0 + i;
         double v = k < d ? sx[i * d + k] : 0.0;
         pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] =
-            k < d ? (float)(v - shift[k]) : 0.f;
+            k < d ? to_tf32(v - shift[k]) : 0.f;
         if (k < d) x64[rec * d + k] = v;
         if (k == 0) {
             r64[rec] = sr[i];
@@ -93,7 +101,7 @@ __global__ void synth_rows_kernel(uint64_t seed, int clustered, int64_t gbase, s
             atomicMax(&shmax[k], (unsigned long long)__double_as_longlong(fabs(v)));
         }
         pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] =
-            k < d ? (float)(v - shift[k]) : 0.f;
+            k < d ? to_tf32(v - shift[k]) : 0.f;
         if (k == 0) {
             uint64_t h = splitmix64(g ^ synth_key(seed, 2));
             double r = (double)((h & 0xFFFFFull) + 8192ull) * 0x1p-20;
