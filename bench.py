@@ -192,8 +192,12 @@ def run_ours(a, rank, world, local_rank):
         traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
     fallbacks = sum(s["exact_fallbacks"] for s in stats)
     certified = sum(s["certified"] for s in stats)
-    gpu_launches = sum(3 * s["stream_launches"] + s["exact_fallbacks"] * (3 + 3 * K_SEL)
-                       for s in stats)
+    # per query group: [sample_keys, sample_kth,] stream, merge, refine
+    gpu_launches = sum((5 if s["tensor_core"] else 3) * s["stream_launches"]
+                       + s["exact_fallbacks"] * (3 + 3 * K_SEL) for s in stats)
+    tc = all(s["tensor_core"] for s in stats)
+    kname = f"sair::stream_mma_kernel<{dp},8> (tcgen05)" if tc else f"sair::stream_kernel<{dp},8>"
+    prepass_ms = sum(s["prepass_ms"] for s in stats) / max(launches, 1)
 
     out = {
         "metric": "retrieval queries/s @16M exps k=32",
@@ -217,7 +221,9 @@ def run_ours(a, rank, world, local_rank):
         "gpu_launches": gpu_launches,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                     "kernel": "sair::stream_kernel<64,8>", "peak_kind": peak_kind,
+                     "kernel": kname, "peak_kind": peak_kind,
+                     "prepass_ms_per_launch": round(prepass_ms, 4),
+                     "call_device_ms": round(sum(s["total_ms"] for s in stats) / max(len(stats), 1), 4),
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": round(per_launch_s * 1e3, 4)},
         "certified_queries": certified, "exact_fallbacks": fallbacks,

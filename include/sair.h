@@ -77,6 +77,8 @@ typedef struct {
     int stream_launches;    /* streaming-kernel launches */
     float stream_ms;        /* device time of the streaming kernels (CUDA events) */
     float total_ms;         /* device time of the whole call */
+    float prepass_ms;       /* device time of the threshold sample pre-pass (tensor-core path) */
+    int tensor_core;        /* 1 when the tcgen05 streaming kernel ran */
 } sair_select_stats;
 
 SAIR_API const char* sair_last_error(void);

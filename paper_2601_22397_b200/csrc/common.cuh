@@ -55,6 +55,20 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
     return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
 }
 
+// Float index of (record, dimension) in the page array.  A page is 4 blocks of
+// 32 records; a block is dp rows (one per dimension) of 128 bytes, stored
+// pre-swizzled: the 32-byte chunk j of row k holds records 8*(j ^ (k % 4)) ..
+// +7.  This is exactly the tcgen05 SWIZZLE_128B_BASE32B image of an MN-major
+// TF32 operand block, so one contiguous bulk copy of a page lands a ready UMMA
+// operand in shared memory (select_mma.cu), and a warp reading one dimension
+// of 32 records still touches 32 distinct banks.
+__host__ __device__ __forceinline__ size_t page_index(size_t rec, int k, int dp) {
+    const size_t page = rec / PAGE;
+    const uint32_t slot = (uint32_t)(rec % PAGE), b = slot >> 5, t = slot & 31u;
+    return page * (size_t)dp * PAGE + (size_t)b * dp * 32 + (size_t)k * 32 +
+           ((((t >> 3) ^ ((uint32_t)k & 3u)) << 3) | (t & 7u));
+}
+
 inline int ceil_div(size_t a, size_t b) { return (int)((a + b - 1) / b); }
 
 // smallest supported padded dimension bucket for the streaming kernel

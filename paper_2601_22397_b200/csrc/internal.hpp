@@ -71,7 +71,7 @@ struct StoreStats {
 struct sair_store_s {
     int device = 0;
     cudaStream_t st = nullptr;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 
     double r_min = 0.0;
     uint64_t rejected = 0;
@@ -102,16 +102,13 @@ struct sair_store_s {
     int32_t* rnd = nullptr;  // [cap] rounds (tie-break)
     double* x64 = nullptr;   // [cap][d] exact contexts (record-major, refine/gather)
 
-    // TMA tensor map of `pages` for the tcgen05 kernel (rebuilt when pages move)
-    alignas(64) unsigned char tmap[128] = {};
-    const void* tmap_for = nullptr;
-    uint32_t tmap_pages = 0;
-    int tmap_dp = 0;
-
     // scratch
     sair::DBuf b_stage, b_cand, b_merged, b_thr, b_z, b_consts, b_out, b_exact, b_sigma, b_red;
-    sair::HBuf h_stage, h_out, h_mmab;
-    sair::DBuf b_mmab;  // tensor-core B operand constants
+    sair::HBuf h_stage, h_out, h_mmab, h_consts;
+    sair::DBuf b_mmab;    // tensor-core B operand constants, t0, dropped
+    sair::DBuf b_sample;  // sample pre-pass keys
+    const float* mma_t0 = nullptr;
+    const unsigned int* mma_dropped = nullptr;
     sair_select_stats last{};
 };
 

@@ -187,9 +187,10 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
                     if (it * NH + h >= (uint32_t)a.nst) mbar_wait(&empty[s], ph ^ 1u);
                     mbar_expect_tx(&full[s], np * DH * PAGE * 4);
                     for (uint32_t p = 0; p < np; ++p)
-                        bulk_g2s(stage + (size_t)s * STAGE_FLOATS + p * DH * PAGE,
-                                 a.pages + ((size_t)(p0 + p) * DP + h * DH) * PAGE, DH * PAGE * 4,
-                                 &full[s]);
+                        for (int b = 0; b < 4; ++b)  // rows h*DH.. of each 32-record block
+                            bulk_g2s(stage + (size_t)s * STAGE_FLOATS + p * DH * PAGE + b * DH * 32,
+                                     a.pages + (size_t)(p0 + p) * DP * PAGE + b * DP * 32 + h * DH * 32,
+                                     DH * 32 * 4, &full[s]);
                     if (++s == a.nst) {
                         s = 0;
                         ph ^= 1u;
@@ -261,12 +262,15 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
 #pragma unroll 1
         for (int h = 0; h < NH; ++h) {
             mbar_wait(&full[s], ph);
-            const float* xp = stage + (size_t)s * STAGE_FLOATS + pg * DH * PAGE + slot;
+            // pre-swizzled block rows (page_index): records t, t+1 share a chunk
+            const float* xp = stage + (size_t)s * STAGE_FLOATS + pg * DH * PAGE + (slot >> 5) * DH * 32;
+            const int t8 = (slot & 31) >> 3, t7 = slot & 7;
             const float* ch = cs + h * DH * QB;
             const float* sh = ss + h * DH;
 #pragma unroll
             for (int k = 0; k < DH; ++k) {
-                const float2 x = *reinterpret_cast<const float2*>(xp + k * PAGE);
+                const float2 x = *reinterpret_cast<const float2*>(
+                    xp + k * 32 + (((t8 ^ (k & 3)) << 3) | t7));
                 float c[QB];
                 load_consts<QB>(ch + k * QB, c);
                 const float sk = sh[k];
@@ -336,8 +340,12 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
 
 // ------------------------------------------------------------ merge --------
 
+constexpr unsigned long long PAD_TOP = 0x007FFFFFull;  // f2ord(-inf): padding entries
+
 // Global top-K (key desc, idx asc) of list L across all CTAs, sorted, plus the
-// K-th key (the filter threshold U of every record outside the pool).
+// K-th key (the filter threshold U of every record outside the pool).  Padding
+// entries (key -inf) are skipped; histogram updates are warp-aggregated
+// because the keys of one list share their leading digits.
 __global__ void __launch_bounds__(1024)
     merge_kernel(const float* __restrict__ in_key, const uint32_t* __restrict__ in_idx, int G,
                  int lists_stride, int kmax, int QB, int kp, int knn, float* __restrict__ out_key,
@@ -346,26 +354,46 @@ __global__ void __launch_bounds__(1024)
     const int K = L < QB ? kp : knn;
     const int total = G * K;
     __shared__ uint32_t hist[256];
-    __shared__ uint32_t sh_bin, sh_r, sh_pop, sh_cnt;
+    __shared__ uint32_t sh_bin, sh_r, sh_pop, sh_cnt, sh_valid;
     __shared__ unsigned long long skey[512];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     auto comp = [&](int e) {
         const int g = e / K, j = e - g * K;
         const size_t off = ((size_t)g * lists_stride + L) * kmax + j;
         return ((unsigned long long)f2ord(in_key[off]) << 32) | (unsigned long long)(~in_idx[off]);
     };
+    if (tid == 0) {
+        sh_cnt = 0;
+        sh_valid = 0;
+    }
     unsigned long long prefix = 0, pmask = 0;
     uint32_t r = (uint32_t)K;
+    bool all_valid = false;
     for (int shift = 56; shift >= 0; shift -= 8) {
         for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
         __syncthreads();
-        for (int e = tid; e < total; e += blockDim.x) {
-            const unsigned long long u = comp(e);
-            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+        uint32_t nvalid = 0;
+        for (int e0 = tid - lane; e0 < total; e0 += blockDim.x) {
+            const int e = e0 + lane;
+            uint32_t bin = 256;
+            if (e < total) {
+                const unsigned long long u = comp(e);
+                if ((u >> 32) > PAD_TOP && (u & pmask) == prefix) bin = (uint32_t)(u >> shift) & 255u;
+            }
+            const unsigned peers = __match_any_sync(0xffffffffu, bin);
+            if (bin < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+            nvalid += bin < 256;
+        }
+        if (shift == 56) {
+            for (int o = 16; o; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+            if (lane == 0 && nvalid) atomicAdd(&sh_valid, nvalid);
         }
         __syncthreads();
+        if (shift == 56 && sh_valid <= (uint32_t)K) {  // every valid entry is kept
+            all_valid = true;
+            break;
+        }
         if (tid < 32) {
-            const int lane = tid;
             uint32_t loc[8], sum = 0;
             for (int j = 0; j < 8; ++j) {
                 loc[j] = hist[255 - (lane * 8 + j)];
@@ -402,16 +430,20 @@ __global__ void __launch_bounds__(1024)
             break;
         }
     }
-    // composites are unique: exactly K entries match (u & pmask) >= prefix
+    // composites are unique: exactly K entries (or every valid one) qualify
     int P = 1;
     while (P < K) P <<= 1;
-    if (tid == 0) sh_cnt = 0;
     for (int j = tid; j < P; j += blockDim.x) skey[j] = 0ull;
     __syncthreads();
     for (int e = tid; e < total; e += blockDim.x) {
         const unsigned long long u = comp(e);
-        if ((u & pmask) >= prefix) skey[atomicAdd(&sh_cnt, 1u)] = u;
+        if ((u >> 32) > PAD_TOP && (all_valid || (u & pmask) >= prefix))
+            skey[atomicAdd(&sh_cnt, 1u)] = u;
     }
+    __syncthreads();
+    // short lists: unique padding composites (key -inf, idx >= n, skipped by refine)
+    for (int j = (int)sh_cnt + tid; j < K; j += blockDim.x)
+        skey[j] = (PAD_TOP << 32) | (unsigned long long)(uint32_t)j;
     __syncthreads();
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -436,6 +468,205 @@ __global__ void __launch_bounds__(1024)
     if (tid == 0) out_thr[L] = ord2f((uint32_t)(skey[K - 1] >> 32));
 }
 
+// Global top-K of list L for lists of at most 1024 * ITEMS entries, one block
+// per list, entries held in registers.  The refine kernel is order-agnostic
+// (every tie-break ends on the record index), so the K winners are written
+// unsorted.  Selection: one histogram over the ordinal range actually present
+// (lo..hi of this list's keys, 2048 bins), the boundary bin resolved by rank
+// counting on the composites; a radix select on the registers only when the
+// boundary bin is very crowded (many equal keys).
+template <int ITEMS>
+__global__ void __launch_bounds__(1024)
+    merge_reg_kernel(const float* __restrict__ in_key, const uint32_t* __restrict__ in_idx, int G,
+                     int lists_stride, int kmax, int QB, int kp, int knn,
+                     float* __restrict__ out_key, uint32_t* __restrict__ out_idx,
+                     float* __restrict__ out_thr) {
+    constexpr int NB = 2048, BCAP = 1024;
+    const int L = blockIdx.x;
+    const int K = L < QB ? kp : knn;
+    const int total = G * K;
+    __shared__ uint32_t hist[NB];
+    __shared__ unsigned long long skey[512];
+    __shared__ unsigned long long sb[BCAP];
+    __shared__ uint32_t sh_valid, sh_lo, sh_hi, sh_bin, sh_above, sh_cnt, sh_nb;
+    __shared__ unsigned long long sh_kth;
+    const int tid = threadIdx.x, lane = tid & 31;
+    unsigned long long v[ITEMS];
+    uint32_t nvalid = 0, lo = 0xFFFFFFFFu, hi = 0;
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        const int e = tid + it * 1024;
+        v[it] = 0ull;  // empty
+        if (e < total) {
+            const int g = e / K, j = e - g * K;
+            const size_t off = ((size_t)g * lists_stride + L) * kmax + j;
+            const uint32_t o = f2ord(in_key[off]);
+            if (o > (uint32_t)PAD_TOP) {
+                v[it] = ((unsigned long long)o << 32) | (unsigned long long)(~in_idx[off]);
+                ++nvalid;
+                lo = min(lo, o);
+                hi = max(hi, o);
+            }
+        }
+    }
+    if (tid == 0) {
+        sh_valid = 0;
+        sh_lo = 0xFFFFFFFFu;
+        sh_hi = 0;
+        sh_cnt = 0;
+        sh_nb = 0;
+        sh_kth = ~0ull;
+    }
+    for (int b = tid; b < NB; b += blockDim.x) hist[b] = 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    __syncthreads();
+    if (lane == 0 && nvalid) {
+        atomicAdd(&sh_valid, nvalid);
+        atomicMin(&sh_lo, lo);
+        atomicMax(&sh_hi, hi);
+    }
+    __syncthreads();
+    const uint32_t V = sh_valid;
+    bool take_all = V <= (uint32_t)K;
+    bool radix = false;
+    if (!take_all) {
+        // bin = (ord - lo) >> sh < NB
+        const uint32_t span = sh_hi - sh_lo;
+        const int sh = span < NB ? 0 : (32 - __clz(span)) - 11;
+        const uint32_t blo = sh_lo;
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it)
+            if (v[it]) atomicAdd(&hist[((uint32_t)(v[it] >> 32) - blo) >> sh], 1u);
+        __syncthreads();
+        if (tid < 32) {
+            // lane l owns bins [NB - 64 (l + 1), NB - 64 l): counts from the top
+            uint32_t sum = 0;
+            for (int j = 0; j < NB / 32; ++j) sum += hist[NB - 1 - (lane * (NB / 32) + j)];
+            uint32_t incl = sum;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const uint32_t excl = incl - sum;
+            const unsigned own = __ballot_sync(0xffffffffu, excl < (uint32_t)K && (uint32_t)K <= incl);
+            if (lane == __ffs(own) - 1) {
+                uint32_t c = excl;
+                for (int j = 0; j < NB / 32; ++j) {
+                    const int b = NB - 1 - (lane * (NB / 32) + j);
+                    if (c + hist[b] >= (uint32_t)K) {
+                        sh_bin = (uint32_t)b;
+                        sh_above = c;
+                        break;
+                    }
+                    c += hist[b];
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t bstar = sh_bin, above = sh_above;
+        radix = hist[bstar] > (uint32_t)BCAP;
+        if (!radix) {
+            // bins above the boundary are in; the boundary bin goes to sb
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                if (!v[it]) continue;
+                const uint32_t b = ((uint32_t)(v[it] >> 32) - blo) >> sh;
+                if (b > bstar) skey[atomicAdd(&sh_cnt, 1u)] = v[it];
+                else if (b == bstar) sb[atomicAdd(&sh_nb, 1u)] = v[it];
+            }
+            __syncthreads();
+            // the boundary entries of rank < K - above (composites are unique)
+            const uint32_t need = (uint32_t)K - above, nb = sh_nb;
+            for (uint32_t t = tid; t < nb; t += blockDim.x) {
+                const unsigned long long u = sb[t];
+                uint32_t rank = 0;
+                for (uint32_t j = 0; j < nb; ++j) rank += sb[j] > u;
+                if (rank < need) skey[above + rank] = u;
+                if (rank == need - 1) sh_kth = u;
+            }
+            __syncthreads();
+        }
+    }
+    if (radix) {
+        // crowded boundary: 8-bit radix select over the composites
+        unsigned long long prefix = 0, pmask = 0;
+        uint32_t r = (uint32_t)K;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
+            __syncthreads();
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                const unsigned long long u = v[it];
+                if (u && (u & pmask) == prefix) atomicAdd(&hist[(uint32_t)(u >> shift) & 255u], 1u);
+            }
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t c = 0;
+                for (int b = 255; b >= 0; --b) {
+                    if (c + hist[b] >= r) {
+                        sh_bin = (uint32_t)b;
+                        sh_above = r - c;
+                        break;
+                    }
+                    c += hist[b];
+                }
+            }
+            __syncthreads();
+            prefix |= (unsigned long long)sh_bin << shift;
+            pmask |= 255ull << shift;
+            r = sh_above;
+            __syncthreads();
+        }
+        // prefix is now the K-th composite itself
+        if (tid == 0) {
+            sh_cnt = 0;
+            sh_kth = prefix;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it)
+            if (v[it] && v[it] >= prefix) skey[atomicAdd(&sh_cnt, 1u)] = v[it];
+        __syncthreads();
+    }
+    if (take_all) {
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it)
+            if (v[it]) skey[atomicAdd(&sh_cnt, 1u)] = v[it];
+        __syncthreads();
+    }
+    const int have = take_all ? (int)V : K;
+    for (int j = tid; j < K; j += blockDim.x) {
+        const size_t o = (size_t)L * kmax + j;
+        if (j < have) {
+            out_key[o] = ord2f((uint32_t)(skey[j] >> 32));
+            out_idx[o] = ~(uint32_t)(skey[j] & 0xffffffffu);
+        } else {  // unique padding, idx >= n (skipped by refine)
+            out_key[o] = -INFINITY;
+            out_idx[o] = 0xFFFFFFFFu - (uint32_t)j;
+        }
+    }
+    if (tid == 0) out_thr[L] = take_all ? -INFINITY : ord2f((uint32_t)(sh_kth >> 32));
+}
+
+// one merge launch: the register kernel when every list fits, else the global one
+void launch_merge(cudaStream_t st, const float* ck, const uint32_t* ci, int G, int lists, int kmax,
+                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr) {
+    const int nb = knn ? 2 * qb : qb;
+    const size_t total = (size_t)G * std::max(kp, knn);
+    if (total <= 4 * 1024)
+        merge_reg_kernel<4><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, qb, kp, knn, mk, mi, mthr);
+    else if (total <= 16 * 1024)
+        merge_reg_kernel<16><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, qb, kp, knn, mk, mi, mthr);
+    else
+        merge_kernel<<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, qb, kp, knn, mk, mi, mthr);
+    SAIR_LAUNCH("merge_kernel");
+}
+
 // ------------------------------------------------------------ refine -------
 
 struct RefineArgs {
@@ -455,6 +686,8 @@ struct RefineArgs {
     const float* ckey;
     const uint32_t* cidx;  // merged, sorted [2QB][kmax]
     const float* cthr;     // [2QB]
+    const float* t0;                // [2QB] stream-pass start thresholds (MMA path) or null
+    const unsigned int* dropped;    // [2QB] max ordinal key dropped on a full list, or null
     double* zs;            // scratch [QB][kp][d]
     int64_t gbase;
     int64_t* out_idx;  // [QB][m]
@@ -469,6 +702,16 @@ struct RefineArgs {
     int32_t* out_round; // [QB][m]
 };
 
+// Largest key any record outside list L's pool can have: the merged K'-th key,
+// the stream pass's start threshold (records at or below it were never
+// listed) and the largest key dropped on a full list.
+__device__ __forceinline__ double excl_bound(const RefineArgs& a, int L, float kth) {
+    double U = (double)kth;
+    if (a.t0) U = fmax(U, (double)a.t0[L]);
+    if (a.dropped && a.dropped[L]) U = fmax(U, (double)ord2f(a.dropped[L]));
+    return U;
+}
+
 __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
     const int q = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -481,12 +724,25 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
     int* taken = rr + a.kp;
     int* picks = taken + a.kp;
     int* order = picks + a.kp;
+    double* nnsim = reinterpret_cast<double*>(order + a.kp + (a.kp & 1));  // [knn]
+    double* sqbuf = nnsim + a.knn;  // [warps][8][d + 1]
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(sqbuf + (blockDim.x >> 5) * 8 * (a.d + 1));
     __shared__ Best wb[8];
-    __shared__ int s_cert;
+    __shared__ int s_cert, s_valid;
     const int d = a.d;
     const double* zq = a.zq + (size_t)q * d;
     double* zs = a.zs + (size_t)q * a.kp * d;
-    const uint32_t* ci = a.cidx + (size_t)q * a.kmax;
+    __shared__ float s_thr[2];
+    const uint32_t* ci = sidx;           // select candidates, merged (smem)
+    const uint32_t* ni = sidx + a.kp;    // veto candidates
+    {
+        for (int j = tid; j < a.kp; j += blockDim.x) sidx[j] = a.cidx[(size_t)q * a.kmax + j];
+        for (int j = tid; j < a.knn; j += blockDim.x)
+            sidx[a.kp + j] = a.cidx[(size_t)(a.QB + q) * a.kmax + j];
+        if (tid == 0) s_thr[0] = a.cthr[q];
+        if (tid == 1 && a.knn) s_thr[1] = a.cthr[a.QB + q];
+    }
+    __syncthreads();
 
     // d2 error bound of the filter: E_q = gamma (sqrt(Pmax) + sqrt(C_q))^2
     const double pmx = (double)__uint_as_float(*a.pmax);
@@ -496,42 +752,96 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
 
     // exact score of every candidate: experience.cpp:254-258 with the
     // reference's rounding sequence (standardize :162-166, similarity
-    // :125-130, loo_mean :229-231)
-    for (int j = tid; j < a.kp; j += blockDim.x) {
-        const uint32_t i = ci[j];
-        pen[j] = 0.0;
-        if (i >= a.n) {
-            score[j] = -INFINITY;
-            rr[j] = INT32_MAX;
-            taken[j] = 1;
-            continue;
+    // :125-130, loo_mean :229-231).  Select and veto candidates form one work
+    // list; a warp takes 8 at a time: its lanes compute the squared
+    // differences of all 8 rows in parallel, then 8 lanes each sum one row in
+    // k order (the order the reference's loop rounds in).
+    const int nwarps = blockDim.x >> 5;
+    const int nitems = a.kp + a.knn;
+    const int ld = d + 1;  // padded row: lanes summing different rows hit distinct banks
+    double* sqw = sqbuf + (size_t)warp * 8 * ld;
+    for (int base = warp * 8; base < nitems; base += 8 * nwarps) {
+        const int nb = min(8, nitems - base);
+        // UN loads in flight per lane before any of the dependent fp64 math
+        constexpr int UN = 8;
+        for (int e0 = lane; e0 < nb * d; e0 += 32 * UN) {
+            double xv[UN];
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                const int e = e0 + 32 * u;
+                xv[u] = 0.0;
+                if (e < nb * d) {
+                    const int b = e / d, k = e - b * d;
+                    const uint32_t i = sidx[base + b];
+                    if (i < a.n) xv[u] = a.x64[(size_t)i * d + k];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UN; ++u) {
+                const int e = e0 + 32 * u;
+                if (e >= nb * d) break;
+                const int b = e / d, k = e - b * d;
+                const int it = base + b;
+                double v = 0.0;
+                if (sidx[it] < a.n) {
+                    const double z = ddiv(dsub(xv[u], a.mean[k]), a.sd[k]);
+                    if (it < a.kp) zs[(size_t)it * d + k] = z;
+                    const double t = dsub(z, zq[k]);
+                    v = dmul(t, t);
+                }
+                sqw[b * ld + k] = v;
+            }
         }
-        taken[j] = 0;
-        double d2 = 0.0;
-        for (int k = 0; k < d; ++k) {
-            const double z = ddiv(dsub(a.x64[(size_t)i * d + k], a.mean[k]), a.sd[k]);
-            zs[(size_t)j * d + k] = z;
-            const double t = dsub(z, zq[k]);
-            d2 = dadd(d2, dmul(t, t));
+        __syncwarp();
+        if (lane < nb) {
+            const int it = base + lane;
+            const bool sel = it < a.kp;
+            const uint32_t i = sidx[it];
+            double d2 = 0.0;
+            for (int k = 0; k < d; ++k) d2 = dadd(d2, sqw[lane * ld + k]);
+            if (sel) {
+                const int j = it;
+                pen[j] = 0.0;
+                if (i >= a.n) {
+                    score[j] = -INFINITY;
+                    rr[j] = INT32_MAX;
+                    taken[j] = 1;
+                } else {
+                    const double sim = sim_from_d2(d2, a.two_s2);
+                    const double r = a.r64[i];
+                    const double loo =
+                        a.n_loo <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n_loo - 1));
+                    taken[j] = 0;
+                    simc[j] = sim;
+                    score[j] = dmul(sim, fabs(dsub(r, loo)));
+                    rew[j] = r;
+                    rr[j] = a.rnd[i];
+                }
+            } else {
+                nnsim[it - a.kp] = i < a.n ? sim_from_d2(d2, a.two_s2) : -1.0;
+            }
         }
-        const double sim = sim_from_d2(d2, a.two_s2);
-        const double r = a.r64[i];
-        const double loo = a.n_loo <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n_loo - 1));
-        simc[j] = sim;
-        score[j] = dmul(sim, fabs(dsub(r, loo)));
-        rew[j] = r;
-        rr[j] = a.rnd[i];
+        __syncwarp();
     }
-    if (tid == 0) s_cert = 1;
+    if (tid == 0) {
+        s_cert = 1;
+        s_valid = 0;
+    }
+    __syncthreads();
+    for (int j = tid; j < a.kp; j += blockDim.x)
+        if (!taken[j]) atomicAdd(&s_valid, 1);
     __syncthreads();
 
     // every record outside the pool has score <= 2^(U + E_q beta + slack)
     double bound = -1.0;
     if (a.has_excl) {
-        const double U = (double)a.cthr[q];
+        const double U = excl_bound(a, q, s_thr[0]);
         bound = exp2(U + Eq * a.beta + 1e-5 * (fabs(U) + a.key_slack_abs));
     }
-    const int want = (int)min((size_t)a.m, a.n);
+    // the pool always holds min(K', n) >= min(m, n) valid records; the cap
+    // only guards against an inconsistent pool (no pick may index past it)
+    const int want = (int)min(min((size_t)a.m, a.n), (size_t)s_valid);
+    if (want < (int)min((size_t)a.m, a.n) && tid == 0) s_cert = 0;
     if (a.lambda == 0.0) {
         // gain == score: the greedy picks are the top-`want` by (score desc,
         // round asc, index asc) -- one rank per candidate, no loop
@@ -612,18 +922,11 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
     }
     if (a.knn == 0) return;
     // nearest record by exact similarity; first index wins ties (policy.cpp:146-153)
-    const uint32_t* ni = a.cidx + (size_t)(a.QB + q) * a.kmax;
     Best b{0.0, 0, 0, -1};
     for (int j = tid; j < a.knn; j += blockDim.x) {
         const uint32_t i = ni[j];
         if (i >= a.n) continue;
-        double d2 = 0.0;
-        for (int k = 0; k < d; ++k) {
-            const double z = ddiv(dsub(a.x64[(size_t)i * d + k], a.mean[k]), a.sd[k]);
-            const double t = dsub(z, zq[k]);
-            d2 = dadd(d2, dmul(t, t));
-        }
-        const Best c{sim_from_d2(d2, a.two_s2), 0, (int64_t)i, j};
+        const Best c{nnsim[j], 0, (int64_t)i, j};
         if (better(c, b)) b = c;
     }
     b = warp_best(b);
@@ -637,7 +940,7 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
         int cert = 1;
         if (a.has_excl_nn) {
             // excluded records have d2_32 >= D = -U_nn, so true d2 >= D - E_q
-            const double D = -(double)a.cthr[a.QB + q];
+            const double D = -excl_bound(a, a.QB + q, s_thr[1]);
             const double lo = fmax(D * (1.0 - 0x1p-11) - Eq, 0.0);
             cert = c.g > exp(-lo / a.two_s2) * (1.0 + 1e-12);
         }
@@ -790,7 +1093,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         throw Error(SAIR_EINVAL, "locally_weighted_mean is not supported on a sharded store");
     const bool fast = cfg.mode != SAIR_SELECT_EXACT && !cfg.locally_weighted_mean && d <= 128 &&
                       n < (size_t)1 << 31 && m <= 256;
-    float stream_ms = 0.f;
+    float stream_ms = 0.f, prepass_ms = 0.f;
     if (fast) {
         // tensor-core streaming kernel when the shape fits,
         // the CUDA-core kernel otherwise or when SAIR_NO_MMA is set
@@ -867,14 +1170,19 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             return o;
         };
         const O D = carve(dout), H = carve(hout);
-        std::vector<double> hc(2 * (size_t)d + (size_t)qb * d + qb), cc;
-        std::copy(p.mean.begin(), p.mean.end(), hc.begin());
-        std::copy(p.sd.begin(), p.sd.end(), hc.begin() + d);
-        const size_t refine_smem = (size_t)kp * (8 * 4 + 4 * 4) + 64;
+        // pinned, so the copy never stages through pageable memory
+        const size_t nhc = 2 * (size_t)d + (size_t)qb * d + qb;
+        double* hc = s->h_consts.as<double>(nhc);
+        std::vector<double> cc;
+        std::copy(p.mean.begin(), p.mean.end(), hc);
+        std::copy(p.sd.begin(), p.sd.end(), hc + d);
+        const size_t refine_smem = (size_t)kp * (8 * 4 + 4 * 4) + 16 + (size_t)knn * 8 +
+                                   (size_t)8 * 8 * (d + 1) * 8 + (size_t)(kp + knn) * 4 + 64;
         SAIR_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)refine_smem));
         s->last.candidates = kp;
         s->last.qb = qb;
+        s->last.tensor_core = use_mma ? 1 : 0;
         for (size_t g0 = 0; g0 < nq; g0 += qb) {
             const int nqg = (int)std::min<size_t>(qb, nq - g0);
             const double* zgrp = p.z.data() + g0 * d;
@@ -891,10 +1199,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             SAIR_CUDA(cudaEventRecord(s->ev[2], s->st));
             s->last.stream_launches++;
             for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
-            SAIR_CUDA(cudaMemcpyAsync(dc, hc.data(), hc.size() * 8, cudaMemcpyHostToDevice, s->st));
-            merge_kernel<<<knn ? 2 * qb : qb, 1024, 0, s->st>>>(ck, ci, pl.grid, 2 * qb, kmax, qb,
-                                                               kp, knn, mk, mi, mthr);
-            SAIR_LAUNCH("merge_kernel");
+            SAIR_CUDA(cudaMemcpyAsync(dc, hc, nhc * 8, cudaMemcpyHostToDevice, s->st));
+            launch_merge(s->st, ck, ci, pl.grid, 2 * qb, kmax, qb, kp, knn, mk, mi, mthr);
             RefineArgs ra{};
             ra.x64 = s->x64;
             ra.r64 = s->r64;
@@ -923,6 +1229,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.ckey = mk;
             ra.cidx = mi;
             ra.cthr = mthr;
+            ra.t0 = use_mma ? s->mma_t0 : nullptr;
+            ra.dropped = use_mma ? s->mma_dropped : nullptr;
             ra.zs = zs;
             ra.gbase = s->gbase;
             ra.out_idx = D.idx;
@@ -940,7 +1248,14 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob, cudaMemcpyDeviceToHost, s->st));
             SAIR_CUDA(cudaStreamSynchronize(s->st));
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, s->ev[1], s->ev[2]);
+            if (use_mma) {
+                float pre = 0.f;
+                cudaEventElapsedTime(&pre, s->ev[1], s->ev[4]);
+                cudaEventElapsedTime(&ms, s->ev[4], s->ev[2]);
+                prepass_ms += pre;
+            } else {
+                cudaEventElapsedTime(&ms, s->ev[1], s->ev[2]);
+            }
             stream_ms += ms;
             for (int qq = 0; qq < nqg; ++qq) {
                 const size_t gq = g0 + qq;
@@ -975,6 +1290,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     float tot = 0.f;
     cudaEventElapsedTime(&tot, s->ev[0], s->ev[3]);
     s->last.stream_ms = stream_ms;
+    s->last.prepass_ms = prepass_ms;
     s->last.total_ms = tot;
 }
 

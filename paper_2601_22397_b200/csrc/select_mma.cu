@@ -4,12 +4,12 @@
 //   D[record][q] = sum_k x[record][k] * b[k][q],   b[k][q] = -2 c_qk / sd_k
 // (the cross term of ||y - c_q||^2).  Here it runs as tcgen05.mma kind::tf32:
 //
-//   warp 8 (producer)  TMA tensor copies (cp.async.bulk.tensor.3d, 128-byte
-//                      swizzle with 32-byte atoms) of 32-record x DP-dimension
-//                      boxes straight from the page layout into a 3-deep
-//                      shared-memory ring; a box is exactly one MN-major
-//                      SWIZZLE_128B_BASE32B UMMA operand block (the layout
-//                      tcgen05 requires for MN-major tf32).
+//   warp 8 (producer)  one bulk copy (cp.async.bulk, the TMA engine) per page
+//                      into a 5-deep shared-memory ring.  Pages are stored
+//                      pre-swizzled (common.cuh page_index): a page is four
+//                      32-record blocks, each exactly the MN-major
+//                      SWIZZLE_128B_BASE32B operand image tcgen05 requires for
+//                      TF32, so the copy lands a ready UMMA operand.
 //   warp 9 (MMA)       allocates TMEM, and one elected lane issues
 //                      M=128 (records) x N=16 x K=8 MMAs per page: A = the
 //                      page tile (MN-major, records contiguous), B = the query
@@ -24,9 +24,8 @@
 // Records are stored rounded to TF32 (cvt.rna at append), so the MMA sees the
 // stored values exactly and P, D describe the same vector; the rounding is a
 // bounded input perturbation the certification accounts for.
-#include <cuda.h>
-
 #include <algorithm>
+#include <cstdlib>
 #include <cfloat>
 #include <cstring>
 #include <vector>
@@ -64,12 +63,12 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, int c2) {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar))
         : "memory");
 }
 // UMMA shared-memory descriptor (sm_100): start >> 4, LBO >> 4, SBO >> 4,
@@ -131,13 +130,17 @@ constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((1
 
 template <int DP, int QB>
 struct MmaArgs {
+    const float* pages;
     const float* r32;
     uint32_t n, npages;
     float c1, c0, rdelta, alpha;
     int kp, knn, nst, cap_sel, cap_nn, kmax;
+    int probe;       // diagnostics only (SAIR_PROBE): 1 = skip inserts/barriers
     float* out_key;  // [grid][2*QB][kmax]
     uint32_t* out_idx;
     unsigned int* pmax;
+    const float* t0;        // [2QB] starting thresholds (sample pre-pass)
+    unsigned int* dropped;  // [2QB] max ordinal of a key dropped on a full list
     const float* b;   // [2][DP][QB] hi / lo TF32 parts of -2 c_qk / sd_k (device)
     float s[DP];      // 1 / sd (0 on padding)
     float cc[QB];     // sum_k c_qk^2
@@ -145,8 +148,7 @@ struct MmaArgs {
 
 template <int DP, int QB>
 __global__ void __launch_bounds__(MMA_THREADS, 1)
-    stream_mma_kernel(const __grid_constant__ CUtensorMap tmap,
-                      const __grid_constant__ MmaArgs<DP, QB> a) {
+    stream_mma_kernel(const __grid_constant__ MmaArgs<DP, QB> a) {
     constexpr int BOX_BYTES = 32 * DP * 4;              // 32 records x DP dims
     constexpr int PAGE_BYTES = 4 * BOX_BYTES;           // 4 boxes = 128 records
     constexpr int STAGE_BYTES = PAGES_PER_STAGE * PAGE_BYTES;
@@ -225,10 +227,10 @@ __global__ void __launch_bounds__(MMA_THREADS, 1)
                 const uint32_t np = min((uint32_t)PAGES_PER_STAGE, a.npages - p0);
                 if (it >= (uint32_t)a.nst) bar_wait(&empty[s], ph ^ 1u);
                 bar_expect_tx(&full[s], np * PAGE_BYTES);
+                // pages are stored pre-swizzled: one contiguous bulk copy per page
                 for (uint32_t pp = 0; pp < np; ++pp)
-                    for (int b = 0; b < 4; ++b)
-                        tma_load_3d(stage + (size_t)s * STAGE_BYTES + pp * PAGE_BYTES + b * BOX_BYTES,
-                                    &tmap, &full[s], 32 * b, 0, (int)(p0 + pp));
+                    bulk_g2s(stage + (size_t)s * STAGE_BYTES + pp * PAGE_BYTES,
+                             a.pages + (size_t)(p0 + pp) * DP * PAGE, PAGE_BYTES, &full[s]);
                 if (++s == a.nst) {
                     s = 0;
                     ph ^= 1u;
@@ -271,33 +273,35 @@ __global__ void __launch_bounds__(MMA_THREADS, 1)
         const int par = warp >> 2;
         const int quarter = warp & 3;
         const int rloc = quarter * 32 + lane;  // record within the page
+        // Fixed thresholds from the sample pre-pass (T0 <= the global K'-th
+        // key): lists are append-only, so consumers never synchronise while
+        // streaming.  A record that finds its list full is dropped and only
+        // its key is remembered (the bound then covers it).
         float thr_r[2 * QB];
 #pragma unroll
-        for (int L = 0; L < 2 * QB; ++L) thr_r[L] = -FLT_MAX;
+        for (int L = 0; L < 2 * QB; ++L) thr_r[L] = L < nl ? a.t0[L] : FLT_MAX;
+        const unsigned lt_mask = (1u << lane) - 1u;
         float pmax = 0.f;
         int s = par % a.nst;
         uint32_t ph = (uint32_t)(par / a.nst) & 1u;
-        const uint32_t rounds = (mine + 1) / 2;  // barrier rounds of two stages
-        for (uint32_t rr = 0; rr < rounds; ++rr) {
-            const uint32_t it = 2 * rr + par;
-            const bool live = it < mine;  // the odd half may idle in the last round
-            const uint32_t page = live ? (r0 + it * G) * PAGES_PER_STAGE + pp : 0;
+        for (uint32_t it = par; it < mine; it += 2) {
+            const uint32_t page = (r0 + it * G) * PAGES_PER_STAGE + pp;
             const uint32_t rec = page * PAGE + rloc;
-            const bool valid = live && rec < a.n;
-            if (live) {
+            const bool valid = rec < a.n;
             const float r = valid ? __ldg(a.r32 + rec) : 0.f;
             bar_wait(&full[s], ph);
-            // P from the swizzled box: row k at k*128 B, 32-B chunk (lane/8) ^ (k%4)
+            // P from the pre-swizzled block: row k at k*128 B, 32-B chunk (lane/8) ^ (k%4)
             const unsigned char* box = stage + (size_t)s * STAGE_BYTES + pp * PAGE_BYTES +
                                        quarter * BOX_BYTES;
-            float P = 0.f;
+            float Pp[4] = {0.f, 0.f, 0.f, 0.f};  // four chains, not one serial FFMA chain
 #pragma unroll
             for (int k = 0; k < DP; ++k) {
                 const float x = *reinterpret_cast<const float*>(
                     box + k * 128 + ((((lane >> 3) ^ (k & 3)) << 5) | ((lane & 7) << 2)));
                 const float y = __fmul_rn(x, ss[k]);
-                P = fmaf(y, y, P);
+                Pp[k & 3] = fmaf(y, y, Pp[k & 3]);
             }
+            const float P = (Pp[0] + Pp[1]) + (Pp[2] + Pp[3]);
             bar_wait(&tfull[s], ph);
             tc_fence_after();
             float acc[16];
@@ -319,8 +323,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1)
                 pm |= (key[q] > thr_r[q] ? 1u : 0u) << q;
                 pm |= (key[QB + q] > thr_r[QB + q] ? 1u : 0u) << (QB + q);
             }
-            if (!a.knn) pm &= (1u << QB) - 1u;
-            if (!valid) pm = 0;
+            if (!valid || a.probe) pm = 0;
             if (__any_sync(0xffffffffu, pm)) {
 #pragma unroll
                 for (int L = 0; L < 2 * QB; ++L) {
@@ -332,32 +335,16 @@ __global__ void __launch_bounds__(MMA_THREADS, 1)
                         if (lane == leader) base = atomicAdd(&cnt[L], __popc(bal));
                         base = __shfl_sync(0xffffffffu, base, leader);
                         if (pass) {
-                            const int pos = lbase(L) + base + __popc(bal & ((1u << lane) - 1u));
-                            lkey[pos] = key[L];
-                            lidx[pos] = rec;
+                            const int slot = base + __popc(bal & lt_mask);
+                            if (slot < lcap(L)) {
+                                lkey[lbase(L) + slot] = key[L];
+                                lidx[lbase(L) + slot] = rec;
+                            } else {
+                                atomicMax(&a.dropped[L], f2ord(key[L]));
+                            }
                         }
                     }
                 }
-            }
-            }  // live
-            // consumers-only barrier: lists settle, compact if the next stage could overflow
-            asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
-            bool need = false;
-            for (int L = 0; L < nl; ++L) need |= cnt[L] > lcap(L) - MW * 32;
-            if (need) {
-                for (int L = warp; L < nl; L += MW) {
-                    if (cnt[L] > lcap(L) - MW * 32) {
-                        const uint32_t T = warp_keep_topk(lkey + lbase(L), lidx + lbase(L), cnt[L],
-                                                          lk(L), hist + warp * 256, lane);
-                        if (lane == 0) {
-                            cnt[L] = lk(L);
-                            thr[L] = ord2f(T);
-                        }
-                    }
-                }
-                asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
-#pragma unroll
-                for (int L = 0; L < 2 * QB; ++L) thr_r[L] = thr[L];
             }
             // this half consumes every other stage: advance the ring by two
             for (int t = 0; t < 2; ++t)
@@ -366,16 +353,20 @@ __global__ void __launch_bounds__(MMA_THREADS, 1)
                     ph ^= 1u;
                 }
         }
-        for (int L = warp; L < nl; L += MW) {
-            if (cnt[L] > lk(L)) {
-                warp_keep_topk(lkey + lbase(L), lidx + lbase(L), cnt[L], lk(L), hist + warp * 256,
-                               lane);
-                if (lane == 0) cnt[L] = lk(L);
-            }
-        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
         if (lane == 0) atomicMax(a.pmax, __float_as_uint(pmax));
+        asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
+        // one compaction per list at the end
+        for (int L = warp; L < nl; L += MW) {
+            const int c = min(cnt[L], lcap(L));
+            if (c > lk(L)) {
+                warp_keep_topk(lkey + lbase(L), lidx + lbase(L), c, lk(L), hist + warp * 256, lane);
+                if (lane == 0) cnt[L] = lk(L);
+            } else if (lane == 0) {
+                cnt[L] = c;
+            }
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(MW * 32) : "memory");
         for (int L = 0; L < nl; ++L) {
             const size_t row = ((size_t)blockIdx.x * 2 * QB + L) * a.kmax;
@@ -395,43 +386,143 @@ __global__ void __launch_bounds__(MMA_THREADS, 1)
     }
 }
 
+// ------------------------------------------------------ sample pre-pass --
+// Page maxima of every list's key over a strided page sample (CUDA cores, the
+// stream pass's formula).  The K'-th largest of K' or more page maxima is the
+// key of K' distinct records, so it is <= the store's K'-th key: a safe start
+// threshold for the stream pass.  One block = one sampled page.
+template <int DP, int QB>
+__global__ void __launch_bounds__(PAGE)
+    sample_keys_kernel(const float* __restrict__ pages, const float* __restrict__ r32, uint32_t n,
+                       uint32_t npages, uint32_t sample_pages,
+                       const float* __restrict__ consts /* s[DP] | c2[DP][QB] | cc[QB] */,
+                       float c1, float c0, float rdelta, float alpha, float* __restrict__ pmaxk) {
+    __shared__ float sc[DP + DP * QB + QB];
+    __shared__ float wmax[4][2 * QB];
+    for (int i = threadIdx.x; i < DP + DP * QB + QB; i += PAGE) sc[i] = consts[i];
+    __syncthreads();
+    const uint32_t page = (uint32_t)((uint64_t)blockIdx.x * npages / sample_pages);
+    const uint32_t rec = page * PAGE + threadIdx.x;
+    const bool valid = rec < n;
+    float P = 0.f, D[QB];
+#pragma unroll
+    for (int q = 0; q < QB; ++q) D[q] = 0.f;
+    if (valid) {
+        // all DP loads in flight at once: the pass is latency-bound, not bandwidth-bound
+        float x[DP];
+#pragma unroll
+        for (int k = 0; k < DP; ++k) x[k] = __ldg(pages + page_index(rec, k, DP));
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+            const float y = __fmul_rn(x[k], sc[k]);
+            P = fmaf(y, y, P);
+#pragma unroll
+            for (int q = 0; q < QB; ++q) D[q] = fmaf(y, sc[DP + k * QB + q], D[q]);
+        }
+    }
+    const float r = valid ? __ldg(r32 + rec) : 0.f;
+    const float lg = log2f(fabsf(fmaf(r, c1, -c0)) + rdelta);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < QB; ++q) {
+        const float d2 = (P + sc[DP + DP * QB + q]) + D[q];
+        float ks = valid ? fmaf(-d2, alpha, lg) : -INFINITY;
+        float kn = valid ? -d2 : -INFINITY;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            ks = fmaxf(ks, __shfl_xor_sync(0xffffffffu, ks, o));
+            kn = fmaxf(kn, __shfl_xor_sync(0xffffffffu, kn, o));
+        }
+        if (lane == 0) {
+            wmax[w][q] = ks;
+            wmax[w][QB + q] = kn;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * QB) {
+        const int L = threadIdx.x;
+        pmaxk[(size_t)L * sample_pages + blockIdx.x] =
+            fmaxf(fmaxf(wmax[0][L], wmax[1][L]), fmaxf(wmax[2][L], wmax[3][L]));
+    }
+}
+
+// t0[L] <= the K-th largest of list L's S <= 1024 page maxima: one histogram
+// over the ordinal range present (2048 bins); the lower edge of the bin where
+// the count from the top reaches K is a lower bound of the K-th value.  It is
+// then lowered by a relative 1e-4 so formula differences only loosen it.
+__global__ void __launch_bounds__(1024)
+    sample_kth_kernel(const float* __restrict__ pmaxk, uint32_t S, int QB, int kp, int knn,
+                      float* __restrict__ t0) {
+    constexpr int NB = 2048;
+    __shared__ uint32_t hist[NB];
+    __shared__ uint32_t sh_lo, sh_hi, sh_bin;
+    const int L = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const int K = L < QB ? kp : knn;
+    if ((uint32_t)K > S || K == 0 || S > 1024) {
+        if (tid == 0) t0[L] = -FLT_MAX;
+        return;
+    }
+    const bool have = (uint32_t)tid < S;
+    const uint32_t o = have ? f2ord(pmaxk[(size_t)L * S + tid]) : 0u;
+    const bool valid = have && o > 0x007FFFFFu;  // not -inf (empty page)
+    uint32_t lo = valid ? o : 0xFFFFFFFFu, hi = valid ? o : 0u;
+    for (int b = tid; b < NB; b += blockDim.x) hist[b] = 0;
+    if (tid == 0) {
+        sh_lo = 0xFFFFFFFFu;
+        sh_hi = 0;
+        sh_bin = 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+    }
+    __syncthreads();
+    if (lane == 0) {
+        atomicMin(&sh_lo, lo);
+        atomicMax(&sh_hi, hi);
+    }
+    __syncthreads();
+    const uint32_t blo = sh_lo, span = sh_hi - sh_lo;
+    const int sh = span < NB ? 0 : (32 - __clz(span)) - 11;
+    if (valid) atomicAdd(&hist[(o - blo) >> sh], 1u);
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t sum = 0;
+        for (int j = 0; j < NB / 32; ++j) sum += hist[NB - 1 - (lane * (NB / 32) + j)];
+        uint32_t incl = sum;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
+        }
+        const uint32_t excl = incl - sum;
+        const unsigned own = __ballot_sync(0xffffffffu, excl < (uint32_t)K && (uint32_t)K <= incl);
+        if (lane == __ffs(own) - 1) {
+            uint32_t c = excl;
+            for (int j = 0; j < NB / 32; ++j) {
+                const int b = NB - 1 - (lane * (NB / 32) + j);
+                c += hist[b];
+                if (c >= (uint32_t)K) {
+                    sh_bin = (uint32_t)b;
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (sh_bin == 0xFFFFFFFFu) {  // fewer than K non-empty sampled pages
+            t0[L] = -FLT_MAX;
+        } else {
+            const float v = ord2f(blo + (sh_bin << sh));
+            t0[L] = v - 1e-4f * (fabsf(v) + 1.f);
+        }
+    }
+}
+
 // ------------------------------------------------------------------- host --
 
 namespace {
-
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiled encoder() {
-    static EncodeTiled fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        SAIR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-        if (q != cudaDriverEntryPointSuccess || !p)
-            throw Error(SAIR_ECUDA, "cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<EncodeTiled>(p);
-    }
-    return fn;
-}
-
-// 3-D view of the page array: (record-in-page 128, dimension dp, page)
-CUtensorMap make_page_map(const float* pages, int dp, uint32_t npages) {
-    CUtensorMap m;
-    std::memset(&m, 0, sizeof(m));
-    const cuuint64_t dims[3] = {128, (cuuint64_t)dp, npages};
-    const cuuint64_t strides[2] = {128 * 4, (cuuint64_t)dp * 128 * 4};
-    const cuuint32_t box[3] = {32, (cuuint32_t)dp, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(pages), dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Error(SAIR_ECUDA, "cuTensorMapEncodeTiled failed");
-    return m;
-}
 
 inline float tf32_trunc(double v) {
     float f = (float)v;
@@ -447,7 +538,9 @@ void mma_fill_and_launch(sair_store_s* s, const MmaPlan& pl, const QueryPrep& p,
                          int nqg, float c1, float c0, float rdelta, float alpha, float* ck,
                          uint32_t* ci, unsigned int* pmax, std::vector<double>& cc_out) {
     MmaArgs<DP, QB> a{};
+    a.pages = s->pages;
     a.r32 = s->r32;
+    a.probe = std::getenv("SAIR_PROBE") ? 1 : 0;
     a.n = (uint32_t)s->n;
     a.npages = (uint32_t)((s->n + PAGE - 1) / PAGE);
     a.c1 = c1;
@@ -466,7 +559,7 @@ void mma_fill_and_launch(sair_store_s* s, const MmaPlan& pl, const QueryPrep& p,
     const int d = s->d;
     for (int k = 0; k < DP; ++k) a.s[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
     cc_out.assign(QB, 0.0);
-    float* hb = s->h_mmab.as<float>(2 * DP * QB);
+    float* hb = s->h_mmab.as<float>(2 * DP * QB + DP + DP * QB + QB + 64);
     for (int q = 0; q < QB; ++q) {
         const double* z = zgrp + (size_t)(q < nqg ? q : 0) * d;
         double cc = 0.0;
@@ -482,23 +575,43 @@ void mma_fill_and_launch(sair_store_s* s, const MmaPlan& pl, const QueryPrep& p,
         a.cc[q] = (float)cc;
         cc_out[q] = cc;
     }
-    float* db = s->b_mmab.as<float>(2 * DP * QB);
-    SAIR_CUDA(cudaMemcpyAsync(db, hb, 2 * DP * QB * sizeof(float), cudaMemcpyHostToDevice, s->st));
-    a.b = db;
-    // the tensor map is rebuilt only when the page array moved or grew
-    const uint32_t npages = a.npages;
-    if (s->tmap_for != s->pages || s->tmap_pages != npages || s->tmap_dp != DP) {
-        CUtensorMap m = make_page_map(s->pages, DP, npages);
-        std::memcpy(s->tmap, &m, sizeof(m));
-        s->tmap_for = s->pages;
-        s->tmap_pages = npages;
-        s->tmap_dp = DP;
+    // device constants: B hi/lo | sample consts (s, -2c, cc) | t0[16] | dropped[16]
+    const size_t nb = 2 * DP * QB, nsc = DP + DP * QB + QB;
+    for (int k = 0; k < DP; ++k) {
+        hb[nb + k] = a.s[k];
+        for (int q = 0; q < QB; ++q) {
+            const double* z = zgrp + (size_t)(q < nqg ? q : 0) * d;
+            const float c = k < d ? (float)((p.mean[k] - s->shift[k]) / p.sd[k] + z[k]) : 0.f;
+            hb[nb + DP + k * QB + q] = -2.f * c;
+        }
     }
-    CUtensorMap m;
-    std::memcpy(&m, s->tmap, sizeof(m));
+    for (int q = 0; q < QB; ++q) hb[nb + DP + DP * QB + q] = a.cc[q];
+    float* db = s->b_mmab.as<float>(nb + nsc + 32 + 64);
+    float* dsc = db + nb;
+    float* dt0 = dsc + nsc;
+    unsigned int* ddrop = reinterpret_cast<unsigned int*>(dt0 + 16);
+    SAIR_CUDA(cudaMemcpyAsync(db, hb, (nb + nsc) * sizeof(float), cudaMemcpyHostToDevice, s->st));
+    SAIR_CUDA(cudaMemsetAsync(ddrop, 0, 16 * sizeof(unsigned int), s->st));
+    a.b = db;
+    a.t0 = dt0;
+    a.dropped = ddrop;
+    s->mma_t0 = dt0;
+    s->mma_dropped = ddrop;
+    // sample pre-pass over spages strided pages (all pages of a small store)
+    const uint32_t npg = a.npages;
+    const uint32_t kl = (uint32_t)std::max(pl.kp, pl.knn);
+    uint32_t spages = std::min<uint32_t>(npg, std::max<uint32_t>(2 * kl, std::min<uint32_t>(1024, npg / 32)));
+    float* dkeys = s->b_sample.as<float>((size_t)2 * QB * spages);
+    sample_keys_kernel<DP, QB><<<spages, PAGE, 0, s->st>>>(s->pages, s->r32, a.n, npg, spages, dsc,
+                                                          c1, c0, rdelta, alpha, dkeys);
+    SAIR_LAUNCH("sample_keys_kernel");
+    sample_kth_kernel<<<pl.knn ? 2 * QB : QB, 1024, 0, s->st>>>(
+        dkeys, spages, QB, pl.kp, pl.knn, dt0);
+    SAIR_LAUNCH("sample_kth_kernel");
+    SAIR_CUDA(cudaEventRecord(s->ev[4], s->st));
     SAIR_CUDA(cudaFuncSetAttribute(stream_mma_kernel<DP, QB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    stream_mma_kernel<DP, QB><<<pl.grid, MMA_THREADS, pl.smem, s->st>>>(m, a);
+    stream_mma_kernel<DP, QB><<<pl.grid, MMA_THREADS, pl.smem, s->st>>>(a);
     SAIR_LAUNCH("stream_mma_kernel");
 }
 
@@ -534,8 +647,9 @@ bool make_mma_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bo
     while ((size_t)pl->kp < want_pool && pl->kp < 512) pl->kp <<= 1;
     pl->knn = nn ? 16 : 0;
     pl->kmax = std::max(pl->kp, pl->knn);
-    pl->cap_sel = pl->kp + MW * 32 + 64;
-    pl->cap_nn = pl->knn + MW * 32 + 64;
+    // append-only lists above the sample threshold (overflow is tracked, not lost)
+    pl->cap_sel = std::max(4 * pl->kp, 512);
+    pl->cap_nn = nn ? std::max(4 * pl->knn, 256) : 0;
     const size_t stage = (size_t)PAGES_PER_STAGE * 4 * 32 * pl->dp * 4;  // 32 KB at dp = 64
     const size_t fixed = 1024 /* alignment slack */ + (size_t)(pl->dp / 8) * 512 + pl->dp * 4 +
                          24 * 8 + 16 + 2 * 16 * 4 + MW * 256 * 4 +

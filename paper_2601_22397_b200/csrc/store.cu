@@ -38,7 +38,7 @@ __global__ void scatter_rows_kernel(const double* __restrict__ sx, const double*
         int k = (int)(t % dp);
         size_t rec = n0 + i;
         double v = k < d ? sx[i * d + k] : 0.0;
-        pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] =
+        pages[page_index(rec, k, dp)] =
             k < d ? to_tf32(v - shift[k]) : 0.f;
         if (k < d) x64[rec * d + k] = v;
         if (k == 0) {
@@ -100,7 +100,7 @@ __global__ void synth_rows_kernel(uint64_t seed, int clustered, int64_t gbase, s
             atomicAdd(&sh[d + k], v * v);
             atomicMax(&shmax[k], (unsigned long long)__double_as_longlong(fabs(v)));
         }
-        pages[(rec / PAGE) * (size_t)dp * PAGE + (size_t)k * PAGE + rec % PAGE] =
+        pages[page_index(rec, k, dp)] =
             k < d ? to_tf32(v - shift[k]) : 0.f;
         if (k == 0) {
             uint64_t h = splitmix64(g ^ synth_key(seed, 2));
@@ -181,7 +181,7 @@ void store_free(sair_store_s* s) {
     cudaFree(s->d_shift);
     s->d_shift = nullptr;
     for (auto* b : {&s->b_stage, &s->b_cand, &s->b_merged, &s->b_thr, &s->b_z, &s->b_consts,
-                    &s->b_out, &s->b_exact, &s->b_sigma, &s->b_red})
+                    &s->b_out, &s->b_exact, &s->b_sigma, &s->b_red, &s->b_mmab, &s->b_sample})
         b->release();
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
