@@ -78,7 +78,7 @@ typedef struct {
     float stream_ms;        /* device time of the streaming kernels (CUDA events) */
     float total_ms;         /* device time of the whole call */
     float prepass_ms;       /* device time of the threshold sample pre-pass (tensor-core path) */
-    int tensor_core;        /* 1 when the tcgen05 streaming kernel ran */
+    int tensor_core;        /* 1: tcgen05 8-query stream pass; 2: tcgen05 wide (32-128 query) pass */
 } sair_select_stats;
 
 SAIR_API const char* sair_last_error(void);

@@ -273,7 +273,8 @@ class ExperienceBuffer:
         return v.value
 
     def select_batch(self, queries, cfg: Optional[SelectionConfig] = None, nearest=False):
-        """select() for every row of `queries` in one device pass per 8 queries.
+        """select() for every row of `queries`: one device pass per 128 queries
+        (tensor-core wide pass, Q >= 32) or per 8 (Q < 32).
         Returns (idx[nq, m], sim[nq, m], score[nq, m], count[nq]) and, with
         nearest=True, also (nn_idx[nq], nn_sim[nq]) of the veto scan."""
         cfg = cfg or SelectionConfig()

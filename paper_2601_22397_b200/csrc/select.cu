@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "select_common.cuh"
+#include "topk_select.cuh"
 #include "warp_topk.cuh"
 
 namespace sair {
@@ -340,7 +341,6 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
 
 // ------------------------------------------------------------ merge --------
 
-constexpr unsigned long long PAD_TOP = 0x007FFFFFull;  // f2ord(-inf): padding entries
 
 // Global top-K (key desc, idx asc) of list L across all CTAs, sorted, plus the
 // K-th key (the filter threshold U of every record outside the pool).  Padding
@@ -468,189 +468,23 @@ __global__ void __launch_bounds__(1024)
     if (tid == 0) out_thr[L] = ord2f((uint32_t)(skey[K - 1] >> 32));
 }
 
-// Global top-K of list L for lists of at most 1024 * ITEMS entries, one block
-// per list, entries held in registers.  The refine kernel is order-agnostic
-// (every tie-break ends on the record index), so the K winners are written
-// unsorted.  Selection: one histogram over the ordinal range actually present
-// (lo..hi of this list's keys, 2048 bins), the boundary bin resolved by rank
-// counting on the composites; a radix select on the registers only when the
-// boundary bin is very crowded (many equal keys).
 template <int ITEMS>
 __global__ void __launch_bounds__(1024)
     merge_reg_kernel(const float* __restrict__ in_key, const uint32_t* __restrict__ in_idx, int G,
                      int lists_stride, int kmax, int QB, int kp, int knn,
                      float* __restrict__ out_key, uint32_t* __restrict__ out_idx,
                      float* __restrict__ out_thr) {
-    constexpr int NB = 2048, BCAP = 1024;
     const int L = blockIdx.x;
     const int K = L < QB ? kp : knn;
-    const int total = G * K;
-    __shared__ uint32_t hist[NB];
-    __shared__ unsigned long long skey[512];
-    __shared__ unsigned long long sb[BCAP];
-    __shared__ uint32_t sh_valid, sh_lo, sh_hi, sh_bin, sh_above, sh_cnt, sh_nb;
-    __shared__ unsigned long long sh_kth;
-    const int tid = threadIdx.x, lane = tid & 31;
-    unsigned long long v[ITEMS];
-    uint32_t nvalid = 0, lo = 0xFFFFFFFFu, hi = 0;
-#pragma unroll
-    for (int it = 0; it < ITEMS; ++it) {
-        const int e = tid + it * 1024;
-        v[it] = 0ull;  // empty
-        if (e < total) {
-            const int g = e / K, j = e - g * K;
-            const size_t off = ((size_t)g * lists_stride + L) * kmax + j;
-            const uint32_t o = f2ord(in_key[off]);
-            if (o > (uint32_t)PAD_TOP) {
-                v[it] = ((unsigned long long)o << 32) | (unsigned long long)(~in_idx[off]);
-                ++nvalid;
-                lo = min(lo, o);
-                hi = max(hi, o);
-            }
-        }
-    }
-    if (tid == 0) {
-        sh_valid = 0;
-        sh_lo = 0xFFFFFFFFu;
-        sh_hi = 0;
-        sh_cnt = 0;
-        sh_nb = 0;
-        sh_kth = ~0ull;
-    }
-    for (int b = tid; b < NB; b += blockDim.x) hist[b] = 0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
-        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    }
-    __syncthreads();
-    if (lane == 0 && nvalid) {
-        atomicAdd(&sh_valid, nvalid);
-        atomicMin(&sh_lo, lo);
-        atomicMax(&sh_hi, hi);
-    }
-    __syncthreads();
-    const uint32_t V = sh_valid;
-    bool take_all = V <= (uint32_t)K;
-    bool radix = false;
-    if (!take_all) {
-        // bin = (ord - lo) >> sh < NB
-        const uint32_t span = sh_hi - sh_lo;
-        const int sh = span < NB ? 0 : (32 - __clz(span)) - 11;
-        const uint32_t blo = sh_lo;
-#pragma unroll
-        for (int it = 0; it < ITEMS; ++it)
-            if (v[it]) atomicAdd(&hist[((uint32_t)(v[it] >> 32) - blo) >> sh], 1u);
-        __syncthreads();
-        if (tid < 32) {
-            // lane l owns bins [NB - 64 (l + 1), NB - 64 l): counts from the top
-            uint32_t sum = 0;
-            for (int j = 0; j < NB / 32; ++j) sum += hist[NB - 1 - (lane * (NB / 32) + j)];
-            uint32_t incl = sum;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const uint32_t excl = incl - sum;
-            const unsigned own = __ballot_sync(0xffffffffu, excl < (uint32_t)K && (uint32_t)K <= incl);
-            if (lane == __ffs(own) - 1) {
-                uint32_t c = excl;
-                for (int j = 0; j < NB / 32; ++j) {
-                    const int b = NB - 1 - (lane * (NB / 32) + j);
-                    if (c + hist[b] >= (uint32_t)K) {
-                        sh_bin = (uint32_t)b;
-                        sh_above = c;
-                        break;
-                    }
-                    c += hist[b];
-                }
-            }
-        }
-        __syncthreads();
-        const uint32_t bstar = sh_bin, above = sh_above;
-        radix = hist[bstar] > (uint32_t)BCAP;
-        if (!radix) {
-            // bins above the boundary are in; the boundary bin goes to sb
-#pragma unroll
-            for (int it = 0; it < ITEMS; ++it) {
-                if (!v[it]) continue;
-                const uint32_t b = ((uint32_t)(v[it] >> 32) - blo) >> sh;
-                if (b > bstar) skey[atomicAdd(&sh_cnt, 1u)] = v[it];
-                else if (b == bstar) sb[atomicAdd(&sh_nb, 1u)] = v[it];
-            }
-            __syncthreads();
-            // the boundary entries of rank < K - above (composites are unique)
-            const uint32_t need = (uint32_t)K - above, nb = sh_nb;
-            for (uint32_t t = tid; t < nb; t += blockDim.x) {
-                const unsigned long long u = sb[t];
-                uint32_t rank = 0;
-                for (uint32_t j = 0; j < nb; ++j) rank += sb[j] > u;
-                if (rank < need) skey[above + rank] = u;
-                if (rank == need - 1) sh_kth = u;
-            }
-            __syncthreads();
-        }
-    }
-    if (radix) {
-        // crowded boundary: 8-bit radix select over the composites
-        unsigned long long prefix = 0, pmask = 0;
-        uint32_t r = (uint32_t)K;
-        for (int shift = 56; shift >= 0; shift -= 8) {
-            for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0;
-            __syncthreads();
-#pragma unroll
-            for (int it = 0; it < ITEMS; ++it) {
-                const unsigned long long u = v[it];
-                if (u && (u & pmask) == prefix) atomicAdd(&hist[(uint32_t)(u >> shift) & 255u], 1u);
-            }
-            __syncthreads();
-            if (tid == 0) {
-                uint32_t c = 0;
-                for (int b = 255; b >= 0; --b) {
-                    if (c + hist[b] >= r) {
-                        sh_bin = (uint32_t)b;
-                        sh_above = r - c;
-                        break;
-                    }
-                    c += hist[b];
-                }
-            }
-            __syncthreads();
-            prefix |= (unsigned long long)sh_bin << shift;
-            pmask |= 255ull << shift;
-            r = sh_above;
-            __syncthreads();
-        }
-        // prefix is now the K-th composite itself
-        if (tid == 0) {
-            sh_cnt = 0;
-            sh_kth = prefix;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int it = 0; it < ITEMS; ++it)
-            if (v[it] && v[it] >= prefix) skey[atomicAdd(&sh_cnt, 1u)] = v[it];
-        __syncthreads();
-    }
-    if (take_all) {
-#pragma unroll
-        for (int it = 0; it < ITEMS; ++it)
-            if (v[it]) skey[atomicAdd(&sh_cnt, 1u)] = v[it];
-        __syncthreads();
-    }
-    const int have = take_all ? (int)V : K;
-    for (int j = tid; j < K; j += blockDim.x) {
-        const size_t o = (size_t)L * kmax + j;
-        if (j < have) {
-            out_key[o] = ord2f((uint32_t)(skey[j] >> 32));
-            out_idx[o] = ~(uint32_t)(skey[j] & 0xffffffffu);
-        } else {  // unique padding, idx >= n (skipped by refine)
-            out_key[o] = -INFINITY;
-            out_idx[o] = 0xFFFFFFFFu - (uint32_t)j;
-        }
-    }
-    if (tid == 0) out_thr[L] = take_all ? -INFINITY : ord2f((uint32_t)(sh_kth >> 32));
+    auto load = [&](int e, float& key, uint32_t& idx) {
+        const int g = e / K, j = e - g * K;
+        const size_t off = ((size_t)g * lists_stride + L) * kmax + j;
+        key = in_key[off];
+        idx = in_idx[off];
+        return true;
+    };
+    block_topk<ITEMS>(load, G * K, K, out_key + (size_t)L * kmax, out_idx + (size_t)L * kmax,
+                      out_thr + L);
 }
 
 // one merge launch: the register kernel when every list fits, else the global one
@@ -1098,10 +932,21 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         // tensor-core streaming kernel when the shape fits,
         // the CUDA-core kernel otherwise or when SAIR_NO_MMA is set
         MmaPlan mp{};
-        const bool use_mma = std::getenv("SAIR_NO_MMA") == nullptr &&
+        WidePlan wp{};
+        const bool no_tc = std::getenv("SAIR_NO_MMA") != nullptr;
+        const bool use_wide =
+            !no_tc && make_wide_plan(s, nq, m, cfg.lambda_div, out_nn != nullptr, &wp);
+        const bool use_mma = !no_tc && !use_wide &&
                              make_mma_plan(s, nq, m, cfg.lambda_div, out_nn != nullptr, &mp);
         StreamPlan pl = make_plan(s, nq, m, cfg.lambda_div, out_nn != nullptr);
-        if (use_mma) {
+        if (use_wide) {
+            pl.dp = wp.dp;
+            pl.qb = wp.qw;
+            pl.kp = wp.kp;
+            pl.knn = wp.knn;
+            pl.kmax = wp.kmax;
+            pl.grid = wp.grid;
+        } else if (use_mma) {
             pl.dp = mp.dp;
             pl.qb = mp.qb;
             pl.kp = mp.kp;
@@ -1110,8 +955,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             pl.grid = mp.grid;
         }
         const int qb = pl.qb, kp = pl.kp, knn = pl.knn, kmax = pl.kmax;
-        FillFn fill = pick_fill(pl.dp, qb);
+        FillFn fill = use_wide ? nullptr : pick_fill(pl.dp, qb);
         MmaFillFn mfill = use_mma ? pick_mma_fill(mp.dp, qb) : nullptr;
+        WideFn wfill = use_wide ? pick_wide(wp.dp, qb) : nullptr;
 
         // filter constants
         const double u = 0x1p-24;
@@ -1130,7 +976,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         const double lg_hi = std::log2(est.rabs * c1d + std::fabs(c0d) + rdel);
         const double key_slack_abs = 1.0 + 2.0 * (std::fabs(std::log2(rdel)) + std::fabs(lg_hi));
 
-        const size_t lists = (size_t)pl.grid * 2 * qb * kmax;
+        const size_t lists = use_wide ? 1 : (size_t)pl.grid * 2 * qb * kmax;
         float* ck = s->b_cand.as<float>(lists * 2);
         uint32_t* ci = reinterpret_cast<uint32_t*>(ck + lists);
         float* mk = s->b_merged.as<float>((size_t)2 * qb * kmax * 2 + 2 * qb + 4);
@@ -1182,7 +1028,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                                        (int)refine_smem));
         s->last.candidates = kp;
         s->last.qb = qb;
-        s->last.tensor_core = use_mma ? 1 : 0;
+        s->last.tensor_core = use_wide ? 2 : (use_mma ? 1 : 0);
         for (size_t g0 = 0; g0 < nq; g0 += qb) {
             const int nqg = (int)std::min<size_t>(qb, nq - g0);
             const double* zgrp = p.z.data() + g0 * d;
@@ -1192,15 +1038,18 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             }
             SAIR_CUDA(cudaMemsetAsync(dpmax, 0, 4, s->st));
             SAIR_CUDA(cudaEventRecord(s->ev[1], s->st));
-            if (use_mma)
+            if (use_wide)  // sample + stream + per-list top-K' (records ev[4], ev[2])
+                wfill(s, wp, p, zgrp, nqg, c1, c0, rdelta, alpha, mk, mi, mthr, dpmax, cc);
+            else if (use_mma)
                 mfill(s, mp, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
             else
                 fill(s, pl, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
-            SAIR_CUDA(cudaEventRecord(s->ev[2], s->st));
+            if (!use_wide) SAIR_CUDA(cudaEventRecord(s->ev[2], s->st));
             s->last.stream_launches++;
             for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
             SAIR_CUDA(cudaMemcpyAsync(dc, hc, nhc * 8, cudaMemcpyHostToDevice, s->st));
-            launch_merge(s->st, ck, ci, pl.grid, 2 * qb, kmax, qb, kp, knn, mk, mi, mthr);
+            if (!use_wide)
+                launch_merge(s->st, ck, ci, pl.grid, 2 * qb, kmax, qb, kp, knn, mk, mi, mthr);
             RefineArgs ra{};
             ra.x64 = s->x64;
             ra.r64 = s->r64;
@@ -1222,15 +1071,18 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.two_s2 = p.two_s2;
             ra.lambda = cfg.lambda_div;
             ra.beta = beta;
-            ra.gamma = use_mma ? (pl.dp + 24) * u + 0x1p-20 : (pl.dp + 16) * u;
+            // fp32 error of the filter's d2; the wide pass
+            // accumulates the hi and lo products in one chain of 2 dp / 8 MMAs
+            ra.gamma = use_wide ? (2 * pl.dp + 32) * u + 0x1p-20
+                                : (use_mma ? (pl.dp + 24) * u + 0x1p-20 : (pl.dp + 16) * u);
             ra.key_slack_abs = key_slack_abs;
             ra.has_excl = n > (size_t)kp;
             ra.has_excl_nn = n > (size_t)knn;
             ra.ckey = mk;
             ra.cidx = mi;
             ra.cthr = mthr;
-            ra.t0 = use_mma ? s->mma_t0 : nullptr;
-            ra.dropped = use_mma ? s->mma_dropped : nullptr;
+            ra.t0 = use_mma || use_wide ? s->mma_t0 : nullptr;
+            ra.dropped = use_mma || use_wide ? s->mma_dropped : nullptr;
             ra.zs = zs;
             ra.gbase = s->gbase;
             ra.out_idx = D.idx;
@@ -1248,7 +1100,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob, cudaMemcpyDeviceToHost, s->st));
             SAIR_CUDA(cudaStreamSynchronize(s->st));
             float ms = 0.f;
-            if (use_mma) {
+            if (use_mma || use_wide) {
                 float pre = 0.f;
                 cudaEventElapsedTime(&pre, s->ev[1], s->ev[4]);
                 cudaEventElapsedTime(&ms, s->ev[4], s->ev[2]);

@@ -72,6 +72,20 @@ MmaFillFn pick_mma_fill(int dp, int qb);
 bool make_mma_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                    MmaPlan* pl);
 
+// select_wide.cu: the tcgen05 large-batch streaming filter (QW = 32/64/128
+// queries per pass) -> merged per-query top-K' lists for the refine kernel
+struct WidePlan {
+    int dp, qw, kp, knn, kmax, nst, grid;
+    size_t smem;
+    uint32_t cap, spages;
+};
+using WideFn = void (*)(sair_store_s*, const WidePlan&, const QueryPrep&, const double*, int, float,
+                        float, float, float, float*, uint32_t*, float*, unsigned int*,
+                        std::vector<double>&);
+WideFn pick_wide(int dp, int qw);
+bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
+                    WidePlan* pl);
+
 // select_exact.cu: one query through the full fp64 pass.
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,

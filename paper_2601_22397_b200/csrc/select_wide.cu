@@ -1,0 +1,686 @@
+// select_wide.cu -- K4: the large-batch streaming filter on the tensor cores.
+//
+// For Q >= 32 queries per call the Q x N similarity contraction is a real GEMM
+// (SURVEY.md 8(a) A9 "K4", configs 2/4/5), so one pass over the store serves
+// QW = 32/64/128 queries at once instead of one pass per 8 (select_mma.cu):
+//
+//   warp 8 (producer)  one bulk copy (TMA engine) per page into an NST-deep
+//                      shared-memory ring; pages are stored as ready MN-major
+//                      SWIZZLE_128B_BASE32B TF32 operand blocks (common.cuh).
+//   warp 9 (MMA)       per page 2 x DP/8 tcgen05.mma kind::tf32, M = 128
+//                      records x N = QW queries x K = 8: A = the page tile,
+//                      B = the query constants -2 c_qk / sd_k split hi + lo in
+//                      TF32, both halves accumulating into the same TMEM
+//                      columns (fp32).  The records are TF32-exact (stored
+//                      rounded), so the split keeps the fp32 filter tolerance.
+//   warps 0-7          two groups of four lane quarters take alternate pages:
+//                      P = ||y||^2 from the shared tile, then 32 TMEM columns
+//                      at a time (tcgen05.ld 32x32b.x32): key = log2 residual
+//                      - alpha d2 per (record, query).
+//
+// Two launches per query group, the same kernel in two modes:
+//   sample  a strided 1/16 of the pages; each warp writes the per-query
+//           maximum key of its 32 records (a transpose-reduce over the warp),
+//           so the K'-th largest of those maxima is <= the store's K'-th key
+//           (they belong to distinct records) -> the start threshold t0.
+//   stream  every page; a record whose key beats t0 is appended to its
+//           query's global candidate list (atomic slot; a full list only
+//           records the largest key it dropped, which the certification
+//           bound then covers).
+// list_topk_kernel selects each list's top-K' and the refine kernel
+// (select.cu) finishes exactly as for the 8-query path.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "select_common.cuh"
+#include "topk_select.cuh"
+#include "umma.cuh"
+
+namespace sair {
+
+using namespace umma;
+
+namespace {
+
+constexpr int WW = 8;                        // consumer warps
+constexpr int WIDE_THREADS = WW * 32 + 64;   // + producer warp + MMA warp
+
+struct WideArgs {
+    const float* pages;
+    const float* r32;
+    uint32_t n, npages;
+    float c1, c0, rdelta, alpha;
+    int nst, knn, mode;       // mode 0 = sample, 1 = stream
+    uint32_t spages;          // sample mode: sampled pages (page = i * npages / spages)
+    const float* consts;      // B tiles (hi, lo; smem image) | s [DP] | cc [QW] | t0 [2QW]
+    float* smax;              // sample out [2QW][4 * spages]
+    float* lkey;              // stream out: per-CTA lists [grid][2QW][cap]
+    uint32_t* lidx;
+    uint32_t* lcnt;           // [grid][2QW] entries in each CTA list
+    unsigned int* dropped;    // [2QW] max ordinal of a key dropped on a full list
+    uint32_t cap;             // per-CTA list capacity
+    unsigned int* pmax;       // max P over records (float bits)
+    uint32_t tcols;           // TMEM columns allocated (power of two >= nst * QW)
+    int probe;                // diagnostics (SAIR_PROBE_WIDE): 1 no consumer math,
+                              // 2 P only, 3 + TMEM loads, 4 + loose test, no appends
+};
+
+// Candidate append: the slot comes from a shared-memory counter (no global
+// round trip on the consumer's critical path), the entry is a fire-and-forget
+// global store into this CTA's list; a full list keeps only the largest key
+// it dropped (shared atomicMax, folded into the global bound at the end).
+__device__ __forceinline__ void list_append(const WideArgs& a, uint32_t* scnt, uint32_t* sdrop,
+                                            int nl, int L, float key, uint32_t rec) {
+    const uint32_t slot = atomicAdd(&scnt[L], 1u);
+    if (slot < a.cap) {
+        const size_t o = ((size_t)blockIdx.x * nl + L) * a.cap + slot;
+        a.lkey[o] = key;
+        a.lidx[o] = rec;
+    } else {
+        atomicMax(&sdrop[L], f2ord(key));
+    }
+}
+
+// lane l ends with max over the warp of v[l] (31 shuffles for 32 columns)
+__device__ __forceinline__ float transpose_max(float (&v)[32], int lane) {
+#pragma unroll
+    for (int s = 16; s; s >>= 1) {
+        const bool upper = lane & s;
+#pragma unroll
+        for (int i = 0; i < s; ++i) {
+            const float send = upper ? v[i] : v[i + s];
+            const float keep = upper ? v[i + s] : v[i];
+            v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, s));
+        }
+    }
+    return v[0];
+}
+
+template <int DP, int QW>
+__global__ void __launch_bounds__(WIDE_THREADS, 1)
+    stream_wide_kernel(const __grid_constant__ WideArgs a) {
+    constexpr int BOX_BYTES = 32 * DP * 4;     // 32 records x DP dims
+    constexpr int PAGE_BYTES = 4 * BOX_BYTES;  // 128 records
+    constexpr int KSTEPS = DP / 8;
+    constexpr int BT_BYTES = QW * 32;          // one K-step B tile: QW rows x 8 tf32
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned char* stage = smem;
+    float* btile = reinterpret_cast<float*>(stage + (size_t)a.nst * PAGE_BYTES);  // [2][KSTEPS]
+    float* ss = btile + 2 * KSTEPS * BT_BYTES / 4;
+    float* scc = ss + DP;
+    float* sthr = scc + QW;
+    float* sB = sthr + 2 * QW;   // loose pre-test constants per list (see the consumers)
+    float* sM = sB + 2 * QW;     // [2] max |B| per list kind
+    uint32_t* scnt = reinterpret_cast<uint32_t*>(sM + 4);  // [2QW] CTA list fill
+    uint32_t* sdrop = scnt + 2 * QW;                       // [2QW] dropped max ordinal
+    uint64_t* full = reinterpret_cast<uint64_t*>(sdrop + 2 * QW);
+    uint64_t* empty = full + 8;
+    uint64_t* tfull = empty + 8;
+    uint64_t* tempty = tfull + 8;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 8);
+
+    // B operand, K-major without swizzle, arranged on the host in shared-memory
+    // order (per K-step QW/8 groups of two 8x16B core matrices): a straight
+    // coalesced copy
+    {
+        const float4* src = reinterpret_cast<const float4*>(a.consts);
+        float4* dst = reinterpret_cast<float4*>(btile);
+        for (int i = tid; i < 2 * KSTEPS * BT_BYTES / 16; i += WIDE_THREADS) dst[i] = src[i];
+    }
+    const float* cs = a.consts + 2 * DP * QW;
+    for (int i = tid; i < DP; i += WIDE_THREADS) ss[i] = cs[i];
+    for (int i = tid; i < QW; i += WIDE_THREADS) scc[i] = cs[DP + i];
+    for (int i = tid; i < 2 * QW; i += WIDE_THREADS)
+        sthr[i] = (i < QW || a.knn) ? cs[DP + QW + i] : FLT_MAX;
+    for (int i = tid; i < 4 * QW; i += WIDE_THREADS) scnt[i] = 0;  // scnt and sdrop
+    __syncthreads();
+    // Loose pre-test: the exact-formula test
+    //   fma(-((P + cc_q) + D), alpha, lg) > thr_q         (selection list)
+    //   -((P + cc_q) + D) > thrn_q                        (veto list)
+    // implies  D + B_q < A + e  with B_q = thr_q / alpha + cc_q, A = lg / alpha - P
+    // (veto: B = thrn_q + cc_q, A = -P) and e = 2^-19 (|A| + P + max|B|), a
+    // margin far above the fp32 rounding of both forms.  The hot loop runs
+    // the loose test (2 instructions per pair); the rare warp whose records
+    // pass re-runs the exact formula for that chunk.
+    if (warp == 0) {
+        float mb[2] = {0.f, 0.f};
+        for (int i = lane; i < 2 * QW; i += 32) {
+            const int q = i < QW ? i : i - QW;
+            const float B = i < QW ? sthr[i] / a.alpha + scc[q] : sthr[i] + scc[q];
+            sB[i] = B;
+            mb[i >= QW] = fmaxf(mb[i >= QW], fabsf(B));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mb[0] = fmaxf(mb[0], __shfl_xor_sync(0xffffffffu, mb[0], o));
+            mb[1] = fmaxf(mb[1], __shfl_xor_sync(0xffffffffu, mb[1], o));
+        }
+        if (lane == 0) {
+            sM[0] = mb[0];
+            sM[1] = mb[1];
+        }
+    }
+    if (tid == 0) {
+        for (int s = 0; s < a.nst; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 4);   // the four warps of the group reading the stage
+            bar_init(&tfull[s], 1);
+            bar_init(&tempty[s], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == WW + 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(tmem_slot)),
+                     "r"(a.tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const uint32_t units = a.mode == 0 ? a.spages : a.npages;
+    const uint32_t G = gridDim.x, r0 = blockIdx.x;
+    const uint32_t mine = r0 < units ? (units - 1 - r0) / G + 1 : 0;
+    auto page_of = [&](uint32_t it) -> uint32_t {
+        const uint32_t u = r0 + it * G;
+        return a.mode == 0 ? (uint32_t)((uint64_t)u * a.npages / a.spages) : u;
+    };
+
+    if (warp == WW) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (uint32_t it = 0; it < mine; ++it) {
+                if (it >= (uint32_t)a.nst) bar_wait(&empty[s], ph ^ 1u);
+                bar_expect_tx(&full[s], PAGE_BYTES);
+                bulk_g2s(stage + (size_t)s * PAGE_BYTES, a.pages + (size_t)page_of(it) * DP * PAGE,
+                         PAGE_BYTES, &full[s]);
+                if (++s == a.nst) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == WW + 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            // D f32, A/B tf32, A MN-major, B K-major, N = QW, M = 128
+            constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
+                                       ((uint32_t)(QW >> 3) << 17) | ((128u >> 4) << 24);
+            int s = 0;
+            uint32_t ph = 0;
+            const uint32_t bbase = su32(btile);
+            for (uint32_t it = 0; it < mine; ++it) {
+                bar_wait(&full[s], ph);
+                if (it >= (uint32_t)a.nst) bar_wait(&tempty[s], ph ^ 1u);
+                tc_fence_after();
+                const uint32_t abase = su32(stage + (size_t)s * PAGE_BYTES);
+                const uint32_t dcol = tmem + (uint32_t)(s * QW);
+#pragma unroll
+                for (int ks = 0; ks < KSTEPS; ++ks) {
+                    const uint64_t ad = umma_desc(abase + ks * 1024, BOX_BYTES, 512, 1);
+                    const uint64_t bh = umma_desc(bbase + ks * BT_BYTES, 128, 256, 0);
+                    const uint64_t bl = umma_desc(bbase + (KSTEPS + ks) * BT_BYTES, 128, 256, 0);
+                    umma_tf32(dcol, ad, bh, IDESC, ks > 0 ? 1u : 0u);
+                    umma_tf32(dcol, ad, bl, IDESC, 1u);
+                }
+                umma_commit(&tfull[s]);
+                if (++s == a.nst) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        const int par = warp >> 2, quarter = warp & 3;
+        const int rloc = quarter * 32 + lane;
+        float pmax = 0.f;
+        int s = par % a.nst;
+        uint32_t ph = (uint32_t)(par / a.nst) & 1u;
+        for (uint32_t it = par; it < mine; it += 2) {
+            const uint32_t page = page_of(it);
+            const uint32_t rec = page * PAGE + rloc;
+            const bool valid = rec < a.n;
+            const float r = valid ? __ldg(a.r32 + rec) : 0.f;
+            bar_wait(&full[s], ph);
+            const unsigned char* box = stage + (size_t)s * PAGE_BYTES + quarter * BOX_BYTES;
+            float Pp[4] = {0.f, 0.f, 0.f, 0.f};
+            if (a.probe != 1) {
+#pragma unroll
+                for (int k = 0; k < DP; ++k) {
+                    const float x = *reinterpret_cast<const float*>(
+                        box + k * 128 + ((((lane >> 3) ^ (k & 3)) << 5) | ((lane & 7) << 2)));
+                    const float y = __fmul_rn(x, ss[k]);
+                    Pp[k & 3] = fmaf(y, y, Pp[k & 3]);
+                }
+            }
+            const float P = (Pp[0] + Pp[1]) + (Pp[2] + Pp[3]);
+            bar_wait(&tfull[s], ph);
+            tc_fence_after();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&empty[s]);  // the MMA is done with the shared tile
+            if (a.probe == 1 || a.probe == 2) {
+                if (P == 12345.f) a.pmax[1] = 1;  // keep P live
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&tempty[s]);
+                for (int t = 0; t < 2; ++t)
+                    if (++s == a.nst) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                continue;
+            }
+            if (valid) pmax = fmaxf(pmax, P);
+            const float lg = log2f(fabsf(fmaf(r, a.c1, -a.c0)) + a.rdelta);
+            // loose pre-test bounds; an invalid record never passes
+            const float A = lg / a.alpha - P;
+            const float Asel = valid ? A + 0x1p-19f * (fabsf(A) + P + sM[0]) : -INFINITY;
+            const float Ann = valid ? -P + 0x1p-19f * (2.f * P + sM[1]) : -INFINITY;
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(s * QW);
+#pragma unroll 1
+            for (int c0 = 0; c0 < QW; c0 += 32) {
+                float acc[32];
+                tmem_ld32(taddr + c0, acc);
+                if (a.probe == 3) {
+                    float t = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) t += acc[j];
+                    if (t == 12345.f) a.pmax[1] = 1;
+                } else if (a.mode == 1) {
+                    // four independent predicate chains
+                    bool h0 = false, h1 = false, h2 = false, h3 = false;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 b4 = *reinterpret_cast<const float4*>(sB + c0 + j);
+                        h0 |= acc[j] + b4.x < Asel;
+                        h1 |= acc[j + 1] + b4.y < Asel;
+                        h2 |= acc[j + 2] + b4.z < Asel;
+                        h3 |= acc[j + 3] + b4.w < Asel;
+                    }
+                    const bool hit = (h0 | h1) | (h2 | h3);
+                    bool hitn = false;
+                    if (a.knn) {
+                        h0 = h1 = h2 = h3 = false;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 b4 = *reinterpret_cast<const float4*>(sB + QW + c0 + j);
+                            h0 |= acc[j] + b4.x < Ann;
+                            h1 |= acc[j + 1] + b4.y < Ann;
+                            h2 |= acc[j + 2] + b4.z < Ann;
+                            h3 |= acc[j + 3] + b4.w < Ann;
+                        }
+                        hitn = (h0 | h1) | (h2 | h3);
+                    }
+                    if (a.probe == 4) {
+                        if (hit && P == 12345.f) a.pmax[1] = 1;
+                    } else if (__any_sync(0xffffffffu, hit | hitn)) {
+                        // rare: which columns passed, then the exact formula (the
+                        // stream pass's key) on each such column, reloaded from
+                        // TMEM with a warp-uniform column address
+                        uint32_t ms = 0, mn = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            ms |= acc[j] + sB[c0 + j] < Asel ? 1u << j : 0u;
+                            if (a.knn) mn |= acc[j] + sB[QW + c0 + j] < Ann ? 1u << j : 0u;
+                        }
+                        uint32_t U = __reduce_or_sync(0xffffffffu, ms | mn);
+                        while (U) {
+                            const int j = __ffs(U) - 1;
+                            U &= U - 1;
+                            const float v = tmem_ld1(taddr + c0 + j);
+                            const float d2 = (P + scc[c0 + j]) + v;
+                            const float key = fmaf(-d2, a.alpha, lg);
+                            if (((ms >> j) & 1u) && key > sthr[c0 + j])
+                                list_append(a, scnt, sdrop, 2 * QW, c0 + j, key, rec);
+                            if (((mn >> j) & 1u) && -d2 > sthr[QW + c0 + j])
+                                list_append(a, scnt, sdrop, 2 * QW, QW + c0 + j, -d2, rec);
+                        }
+                    }
+                } else {
+                    float kn[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float d2 = (P + scc[c0 + j]) + acc[j];
+                        acc[j] = valid ? fmaf(-d2, a.alpha, lg) : -INFINITY;
+                        kn[j] = valid ? -d2 : -INFINITY;
+                    }
+                    const uint32_t S4 = 4 * a.spages, col = r0 + it * G;
+                    const float mk = transpose_max(acc, lane);
+                    a.smax[(size_t)(c0 + lane) * S4 + 4 * col + quarter] = mk;
+                    if (a.knn) {
+                        const float mn = transpose_max(kn, lane);
+                        a.smax[(size_t)(QW + c0 + lane) * S4 + 4 * col + quarter] = mn;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&tempty[s]);
+            for (int t = 0; t < 2; ++t)
+                if (++s == a.nst) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+        }
+        if (a.mode == 1) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+            if (lane == 0) atomicMax(a.pmax, __float_as_uint(pmax));
+            asm volatile("bar.sync 1, %0;" ::"n"(WW * 32) : "memory");
+            for (int L = tid; L < 2 * QW; L += WW * 32) {
+                a.lcnt[(size_t)blockIdx.x * 2 * QW + L] = min(scnt[L], a.cap);
+                if (sdrop[L]) atomicMax(&a.dropped[L], sdrop[L]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == WW + 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tcols));
+    }
+}
+
+// t0[L] <= the K-th largest of list L's S block maxima (S up to 4 * 8192):
+// one histogram over the ordinal range present; the lower edge of the bin
+// where the count from the top reaches K, lowered by a relative 1e-6.
+// Fewer than K non-empty maxima: no threshold (-FLT_MAX).
+__global__ void __launch_bounds__(1024)
+    wide_kth_kernel(const float* __restrict__ smax, uint32_t S, int QW, int kp, int knn,
+                    float* __restrict__ t0) {
+    constexpr int NB = 2048;
+    __shared__ uint32_t hist[NB];
+    __shared__ uint32_t sh_lo, sh_hi, sh_bin, sh_valid;
+    const int L = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    const uint32_t K = (uint32_t)(L < QW ? kp : knn);
+    const float* v = smax + (size_t)L * S;
+    for (int b = tid; b < NB; b += blockDim.x) hist[b] = 0;
+    if (tid == 0) {
+        sh_lo = 0xFFFFFFFFu;
+        sh_hi = 0;
+        sh_bin = 0xFFFFFFFFu;
+        sh_valid = 0;
+    }
+    __syncthreads();
+    uint32_t lo = 0xFFFFFFFFu, hi = 0, nv = 0;
+    for (uint32_t i = tid; i < S; i += blockDim.x) {
+        const uint32_t o = f2ord(v[i]);
+        if (o > (uint32_t)PAD_TOP) {
+            lo = min(lo, o);
+            hi = max(hi, o);
+            ++nv;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+        nv += __shfl_xor_sync(0xffffffffu, nv, d);
+    }
+    if (lane == 0) {
+        atomicMin(&sh_lo, lo);
+        atomicMax(&sh_hi, hi);
+        atomicAdd(&sh_valid, nv);
+    }
+    __syncthreads();
+    if (K == 0 || sh_valid < K) {
+        if (tid == 0) t0[L] = -FLT_MAX;
+        return;
+    }
+    const uint32_t blo = sh_lo, span = sh_hi - sh_lo;
+    const int sh = span < NB ? 0 : (32 - __clz(span)) - 11;
+    for (uint32_t i = tid; i < S; i += blockDim.x) {
+        const uint32_t o = f2ord(v[i]);
+        if (o > (uint32_t)PAD_TOP) atomicAdd(&hist[(o - blo) >> sh], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+        uint32_t sum = 0;
+        for (int j = 0; j < NB / 32; ++j) sum += hist[NB - 1 - (lane * (NB / 32) + j)];
+        uint32_t incl = sum;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
+        }
+        const uint32_t excl = incl - sum;
+        const unsigned own = __ballot_sync(0xffffffffu, excl < K && K <= incl);
+        if (lane == __ffs(own) - 1) {
+            uint32_t c = excl;
+            for (int j = 0; j < NB / 32; ++j) {
+                const int b = NB - 1 - (lane * (NB / 32) + j);
+                c += hist[b];
+                if (c >= K) {
+                    sh_bin = (uint32_t)b;
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const float e = ord2f(blo + (sh_bin << sh));
+        t0[L] = e - 1e-6f * (fabsf(e) + 1.f);
+    }
+}
+
+// top-K' of one global candidate list (one block per list)
+template <int ITEMS>
+__global__ void __launch_bounds__(1024)
+    list_topk_kernel(const float* __restrict__ lkey, const uint32_t* __restrict__ lidx,
+                     const uint32_t* __restrict__ lcnt, uint32_t cap, int G, int QW, int kp,
+                     int knn, int kmax, float* __restrict__ out_key,
+                     uint32_t* __restrict__ out_idx, float* __restrict__ out_thr) {
+    const int L = blockIdx.x;
+    const int K = L < QW ? kp : knn;
+    auto load = [&](int e, float& key, uint32_t& idx) {
+        const int g = e / (int)cap, j = e - g * (int)cap;
+        const size_t row = (size_t)g * 2 * QW + L;
+        if ((uint32_t)j >= lcnt[row]) return false;
+        key = lkey[row * cap + j];
+        idx = lidx[row * cap + j];
+        return true;
+    };
+    block_topk<ITEMS>(load, G * (int)cap, K, out_key + (size_t)L * kmax, out_idx + (size_t)L * kmax,
+                      out_thr + L);
+}
+
+inline float tf32_trunc(double v) {
+    float f = (float)v;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u &= 0xFFFFE000u;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+template <int DP, int QW>
+void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, const double* zgrp,
+                   int nqg, float c1, float c0, float rdelta, float alpha, float* mk,
+                   uint32_t* mi, float* mthr, unsigned int* pmax, std::vector<double>& cc_out) {
+    const int d = s->d;
+    const size_t nc = 2 * (size_t)DP * QW + DP + QW + 2 * QW;
+    float* hb = s->h_mmab.as<float>(nc + 64);
+    float* sv = hb + 2 * (size_t)DP * QW;
+    float* ccv = sv + DP;
+    for (int k = 0; k < DP; ++k) sv[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
+    cc_out.assign(QW, 0.0);
+    for (int q = 0; q < QW; ++q) {
+        // padded query slots repeat query 0 (their lists are never read)
+        const double* z = zgrp + (size_t)(q < nqg ? q : 0) * d;
+        double cc = 0.0;
+        for (int k = 0; k < DP; ++k) {
+            float c = 0.f;
+            if (k < d) c = (float)((p.mean[k] - s->shift[k]) / p.sd[k] + z[k]);
+            cc += (double)c * (double)c;
+            const double bk = k < d ? -2.0 * (double)c * (double)sv[k] : 0.0;
+            const float hi = tf32_trunc(bk);
+            // smem image of the K-major B tiles: (q % 8) * 16 + (q / 8) * 256 +
+            // (k % 4) * 4 + (k / 4) * 128 bytes within K-step k / 8
+            const size_t off = (size_t)(k / 8) * QW * 8 + (q % 8) * 4 + (q / 8) * 64 +
+                               (k % 4) + ((k % 8) / 4) * 32;
+            hb[off] = hi;
+            hb[(size_t)DP * QW + off] = tf32_trunc(bk - (double)hi);
+        }
+        ccv[q] = (float)cc;
+        cc_out[q] = cc;
+    }
+    // device: consts | lists | counters
+    const size_t L = 2 * (size_t)QW;
+    const size_t S4 = 4 * (size_t)pl.spages;
+    char* base = static_cast<char*>(s->b_mmab.get(nc * 4 + 256 + L * 8 + S4 * L * 4 + 256));
+    float* dc = reinterpret_cast<float*>(base);
+    float* dt0 = dc + 2 * (size_t)DP * QW + DP + QW;  // the t0 slot of consts
+    uint32_t* dcnt = reinterpret_cast<uint32_t*>(base + ((nc * 4 + 255) & ~(size_t)255));
+    unsigned int* ddrop = dcnt + L;
+    float* dsmax = reinterpret_cast<float*>(ddrop + L);
+    const size_t lent = (size_t)pl.grid * L * pl.cap;
+    char* lists = static_cast<char*>(s->b_sample.get(lent * 8 + (size_t)pl.grid * L * 4 + 256));
+    float* lkey = reinterpret_cast<float*>(lists);
+    uint32_t* lidx = reinterpret_cast<uint32_t*>(lists + lent * 4);
+    uint32_t* gcnt = lidx + lent;
+    SAIR_CUDA(cudaMemcpyAsync(dc, hb, (nc - L) * sizeof(float), cudaMemcpyHostToDevice, s->st));
+    SAIR_CUDA(cudaMemsetAsync(dcnt, 0, 2 * L * sizeof(uint32_t), s->st));
+
+    WideArgs a{};
+    a.pages = s->pages;
+    a.r32 = s->r32;
+    a.n = (uint32_t)s->n;
+    a.npages = (uint32_t)((s->n + PAGE - 1) / PAGE);
+    a.c1 = c1;
+    a.c0 = c0;
+    a.rdelta = rdelta;
+    a.alpha = alpha;
+    a.nst = pl.nst;
+    a.knn = pl.knn ? 1 : 0;
+    a.spages = pl.spages;
+    a.consts = dc;
+    a.smax = dsmax;
+    a.lkey = lkey;
+    a.lidx = lidx;
+    a.lcnt = gcnt;
+    a.dropped = ddrop;
+    a.cap = pl.cap;
+    a.pmax = pmax;
+    a.probe = std::getenv("SAIR_PROBE_WIDE") ? std::atoi(std::getenv("SAIR_PROBE_WIDE")) : 0;
+    a.tcols = 32;
+    while (a.tcols < (uint32_t)(pl.nst * QW)) a.tcols <<= 1;
+    SAIR_CUDA(cudaFuncSetAttribute(stream_wide_kernel<DP, QW>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    // sample pass -> t0 (written into the consts the stream pass reads)
+    a.mode = 0;
+    stream_wide_kernel<DP, QW><<<(int)std::min<uint32_t>(pl.spages, (uint32_t)pl.grid),
+                                 WIDE_THREADS, pl.smem, s->st>>>(a);
+    SAIR_LAUNCH("stream_wide_kernel(sample)");
+    wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(dsmax, (uint32_t)S4, QW, pl.kp,
+                                                             pl.knn, dt0);
+    SAIR_LAUNCH("wide_kth_kernel");
+    SAIR_CUDA(cudaEventRecord(s->ev[4], s->st));
+    a.mode = 1;
+    stream_wide_kernel<DP, QW><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
+    SAIR_LAUNCH("stream_wide_kernel(stream)");
+    SAIR_CUDA(cudaEventRecord(s->ev[2], s->st));
+    const int nl = pl.knn ? 2 * QW : QW;
+    if ((size_t)pl.grid * pl.cap <= 4096)
+        list_topk_kernel<4><<<nl, 1024, 0, s->st>>>(lkey, lidx, gcnt, pl.cap, pl.grid, QW, pl.kp,
+                                                     pl.knn, pl.kmax, mk, mi, mthr);
+    else
+        list_topk_kernel<16><<<nl, 1024, 0, s->st>>>(lkey, lidx, gcnt, pl.cap, pl.grid, QW,
+                                                      pl.kp, pl.knn, pl.kmax, mk, mi, mthr);
+    SAIR_LAUNCH("list_topk_kernel");
+    if (std::getenv("SAIR_WIDE_DEBUG")) {  // diagnostics: list fill and thresholds
+        std::vector<uint32_t> hc((size_t)pl.grid * L), hd(L);
+        std::vector<float> ht(L);
+        SAIR_CUDA(cudaMemcpyAsync(hc.data(), gcnt, hc.size() * 4, cudaMemcpyDeviceToHost, s->st));
+        SAIR_CUDA(cudaMemcpyAsync(hd.data(), ddrop, L * 4, cudaMemcpyDeviceToHost, s->st));
+        SAIR_CUDA(cudaMemcpyAsync(ht.data(), dt0, L * 4, cudaMemcpyDeviceToHost, s->st));
+        SAIR_CUDA(cudaStreamSynchronize(s->st));
+        uint64_t tot = 0, mx = 0, nd = 0;
+        for (int i = 0; i < QW; ++i) {
+            uint64_t c = 0;
+            for (int g = 0; g < pl.grid; ++g) c += hc[(size_t)g * L + i];
+            tot += c;
+            mx = std::max<uint64_t>(mx, c);
+            nd += hd[i] != 0;
+        }
+        fprintf(stderr, "[wide] QW=%d spages=%u lists: mean %.1f max %llu dropped-lists %llu t0[0]=%g\n",
+                QW, pl.spages, (double)tot / QW, (unsigned long long)mx, (unsigned long long)nd,
+                (double)ht[0]);
+    }
+    s->mma_t0 = dt0;
+    s->mma_dropped = ddrop;
+}
+
+template <int DP>
+WideFn wide_pick_qw(int qw) {
+    switch (qw) {
+        case 32: return wide_launch_t<DP, 32>;
+        case 64: return wide_launch_t<DP, 64>;
+        default: return wide_launch_t<DP, 128>;
+    }
+}
+
+size_t wide_smem(int dp, int qw, int nst) {
+    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + 2 * (size_t)(dp / 8) * qw * 32 + dp * 4 +
+           qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 + 32 * 8 + 16;
+}
+
+}  // namespace
+
+WideFn pick_wide(int dp, int qw) {
+    switch (dp) {
+        case 8: return wide_pick_qw<8>(qw);
+        case 16: return wide_pick_qw<16>(qw);
+        case 32: return wide_pick_qw<32>(qw);
+        case 64: return wide_pick_qw<64>(qw);
+        default: return nullptr;
+    }
+}
+
+bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
+                    WidePlan* pl) {
+    if (std::getenv("SAIR_NO_WIDE") || nq < 32 || s->dp < 8 || s->dp > 64) return false;
+    pl->dp = s->dp;
+    pl->qw = nq >= 128 ? 128 : (nq >= 64 ? 64 : 32);
+    pl->kp = 32;
+    const size_t want_pool = lambda != 0.0 ? 4 * m : 2 * m;
+    while ((size_t)pl->kp < want_pool && pl->kp < 512) pl->kp <<= 1;
+    pl->knn = nn ? 16 : 0;
+    pl->kmax = std::max(pl->kp, pl->knn);
+    const size_t npages = (s->n + PAGE - 1) / PAGE;
+    // below ~64k records the 8-query pass is as fast and the per-CTA lists
+    // could not hold a threshold-less sample
+    if (npages < 512) return false;
+    // Sample size: a sample of S pages leaves ~K' npages / S candidates per
+    // list, and each costs the stream pass a slow chunk (~1/8 page of work
+    // for 128 lists); S = sqrt(10 K' npages) balances the two (28% of the
+    // pages at 1M records, 7% at 16M).
+    pl->spages = (uint32_t)std::min<size_t>(
+        npages, std::min<size_t>(
+                    16384, std::max<size_t>(64, (size_t)std::sqrt(10.0 * pl->kp * npages))));
+    pl->cap = 96;  // per CTA and list: ~16 K' / 148 expected (148 x 96 <= 16384)
+    const size_t limit = 227 * 1024;
+    // TMEM: nst stages x QW columns <= 512
+    pl->nst = std::min(8, 512 / pl->qw);
+    while (pl->nst > 2 && wide_smem(pl->dp, pl->qw, pl->nst) > limit) --pl->nst;
+    if (wide_smem(pl->dp, pl->qw, pl->nst) > limit) return false;
+    pl->smem = wide_smem(pl->dp, pl->qw, pl->nst);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    pl->grid = (int)std::max<size_t>(1, std::min<size_t>(npages, (size_t)nsm));
+    return true;
+}
+
+}  // namespace sair
