@@ -47,8 +47,12 @@ using namespace umma;
 
 namespace {
 
-constexpr int WW = 8;                        // consumer warps
-constexpr int WIDE_THREADS = WW * 32 + 64;   // + producer warp + MMA warp
+// warp roles: 0-7 epilogue (two groups of four TMEM lane quarters), 8-15
+// record constants (two groups; they own the shared page stage), 16
+// producer, 17 MMA
+constexpr int WE = 8;
+constexpr int W_REC = 8, W_PROD = 16, W_MMA = 17;
+constexpr int WIDE_THREADS = 18 * 32;
 
 struct WideArgs {
     const float* pages;
@@ -66,8 +70,7 @@ struct WideArgs {
     uint32_t cap;             // per-CTA list capacity
     unsigned int* pmax;       // max P over records (float bits)
     uint32_t tcols;           // TMEM columns allocated (power of two >= nst * QW)
-    int probe;                // diagnostics (SAIR_PROBE_WIDE): 1 no consumer math,
-                              // 2 P only, 3 + TMEM loads, 4 + loose test, no appends
+    int probe;                // diagnostics (SAIR_PROBE_WIDE=1): skip the epilogue math
 };
 
 // Candidate append: the slot comes from a shared-memory counter (no global
@@ -111,12 +114,14 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nst = a.nst, PR = 2 * a.nst;  // smem/TMEM stages, record-constant slots
     unsigned char* stage = smem;
-    float* btile = reinterpret_cast<float*>(stage + (size_t)a.nst * PAGE_BYTES);  // [2][KSTEPS]
-    float* ss = btile + 2 * KSTEPS * BT_BYTES / 4;
+    float* btile = reinterpret_cast<float*>(stage + (size_t)nst * PAGE_BYTES);  // [2][KSTEPS]
+    float* prec = btile + 2 * KSTEPS * BT_BYTES / 4;  // [PR][4][PAGE]: Asel, Ann, P, lg
+    float* ss = prec + (size_t)PR * 4 * PAGE;
     float* scc = ss + DP;
     float* sthr = scc + QW;
-    float* sB = sthr + 2 * QW;   // loose pre-test constants per list (see the consumers)
+    float* sB = sthr + 2 * QW;   // loose pre-test constants per list (see below)
     float* sM = sB + 2 * QW;     // [2] max |B| per list kind
     uint32_t* scnt = reinterpret_cast<uint32_t*>(sM + 4);  // [2QW] CTA list fill
     uint32_t* sdrop = scnt + 2 * QW;                       // [2QW] dropped max ordinal
@@ -124,7 +129,8 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 8;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 8);
+    uint64_t* pready = tempty + 8;  // [16]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pready + 16);
 
     // B operand, K-major without swizzle, arranged on the host in shared-memory
     // order (per K-step QW/8 groups of two 8x16B core matrices): a straight
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     // (veto: B = thrn_q + cc_q, A = -P) and e = 2^-19 (|A| + P + max|B|), a
     // margin far above the fp32 rounding of both forms.  The hot loop runs
     // the loose test (2 instructions per pair); the rare warp whose records
-    // pass re-runs the exact formula for that chunk.
+    // pass re-runs the exact formula on the passing columns.
     if (warp == 0) {
         float mb[2] = {0.f, 0.f};
         for (int i = lane; i < 2 * QW; i += 32) {
@@ -168,16 +174,17 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         }
     }
     if (tid == 0) {
-        for (int s = 0; s < a.nst; ++s) {
+        for (int s = 0; s < nst; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&empty[s], 4);   // the four warps of the group reading the stage
+            bar_init(&empty[s], 4);   // the four record-constant warps
             bar_init(&tfull[s], 1);
-            bar_init(&tempty[s], 4);
+            bar_init(&tempty[s], 4);  // the four epilogue warps of the page's group
         }
+        for (int p = 0; p < PR; ++p) bar_init(&pready[p], 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (warp == WW + 1) {
+    if (warp == W_MMA) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          su32(tmem_slot)),
                      "r"(a.tcols));
@@ -196,34 +203,28 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         return a.mode == 0 ? (uint32_t)((uint64_t)u * a.npages / a.spages) : u;
     };
 
-    if (warp == WW) {
-        // ---------------- producer ----------------
+    if (warp == W_PROD) {
+        // ---------------- producer: one bulk copy per page ----------------
         if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
             for (uint32_t it = 0; it < mine; ++it) {
-                if (it >= (uint32_t)a.nst) bar_wait(&empty[s], ph ^ 1u);
+                const uint32_t s = it % nst, ph = (it / nst) & 1u;
+                if (it >= (uint32_t)nst) bar_wait(&empty[s], ph ^ 1u);
                 bar_expect_tx(&full[s], PAGE_BYTES);
                 bulk_g2s(stage + (size_t)s * PAGE_BYTES, a.pages + (size_t)page_of(it) * DP * PAGE,
                          PAGE_BYTES, &full[s]);
-                if (++s == a.nst) {
-                    s = 0;
-                    ph ^= 1u;
-                }
             }
         }
-    } else if (warp == WW + 1) {
+    } else if (warp == W_MMA) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             // D f32, A/B tf32, A MN-major, B K-major, N = QW, M = 128
             constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
                                        ((uint32_t)(QW >> 3) << 17) | ((128u >> 4) << 24);
-            int s = 0;
-            uint32_t ph = 0;
             const uint32_t bbase = su32(btile);
             for (uint32_t it = 0; it < mine; ++it) {
+                const uint32_t s = it % nst, ph = (it / nst) & 1u;
                 bar_wait(&full[s], ph);
-                if (it >= (uint32_t)a.nst) bar_wait(&tempty[s], ph ^ 1u);
+                if (it >= (uint32_t)nst) bar_wait(&tempty[s], ph ^ 1u);
                 tc_fence_after();
                 const uint32_t abase = su32(stage + (size_t)s * PAGE_BYTES);
                 const uint32_t dcol = tmem + (uint32_t)(s * QW);
@@ -236,151 +237,141 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                     umma_tf32(dcol, ad, bl, IDESC, 1u);
                 }
                 umma_commit(&tfull[s]);
-                if (++s == a.nst) {
-                    s = 0;
-                    ph ^= 1u;
-                }
             }
         }
-    } else {
-        // ---------------- consumers ----------------
-        const int par = warp >> 2, quarter = warp & 3;
-        const int rloc = quarter * 32 + lane;
+    } else if (warp >= W_REC) {
+        // ---------------- record constants: P, lg, pre-test bounds ----------------
+        // These warps own the shared page stage: P = ||y||^2 needs the page, the
+        // epilogue only TMEM, so the stage is released as soon as the MMA is done.
+        const int quarter = warp & 3, rloc = quarter * 32 + lane;
         float pmax = 0.f;
-        int s = par % a.nst;
-        uint32_t ph = (uint32_t)(par / a.nst) & 1u;
-        for (uint32_t it = par; it < mine; it += 2) {
-            const uint32_t page = page_of(it);
-            const uint32_t rec = page * PAGE + rloc;
+        for (uint32_t it = (warp - W_REC) >> 2; it < mine; it += 2) {
+            const uint32_t s = it % nst, ph = (it / nst) & 1u;
+            const uint32_t rec = page_of(it) * PAGE + rloc;
             const bool valid = rec < a.n;
             const float r = valid ? __ldg(a.r32 + rec) : 0.f;
             bar_wait(&full[s], ph);
             const unsigned char* box = stage + (size_t)s * PAGE_BYTES + quarter * BOX_BYTES;
             float Pp[4] = {0.f, 0.f, 0.f, 0.f};
-            if (a.probe != 1) {
 #pragma unroll
-                for (int k = 0; k < DP; ++k) {
-                    const float x = *reinterpret_cast<const float*>(
-                        box + k * 128 + ((((lane >> 3) ^ (k & 3)) << 5) | ((lane & 7) << 2)));
-                    const float y = __fmul_rn(x, ss[k]);
-                    Pp[k & 3] = fmaf(y, y, Pp[k & 3]);
-                }
+            for (int k = 0; k < DP; ++k) {
+                const float x = *reinterpret_cast<const float*>(
+                    box + k * 128 + ((((lane >> 3) ^ (k & 3)) << 5) | ((lane & 7) << 2)));
+                const float y = __fmul_rn(x, ss[k]);
+                Pp[k & 3] = fmaf(y, y, Pp[k & 3]);
             }
             const float P = (Pp[0] + Pp[1]) + (Pp[2] + Pp[3]);
-            bar_wait(&tfull[s], ph);
-            tc_fence_after();
-            __syncwarp();
-            if (lane == 0) bar_arrive(&empty[s]);  // the MMA is done with the shared tile
-            if (a.probe == 1 || a.probe == 2) {
-                if (P == 12345.f) a.pmax[1] = 1;  // keep P live
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) bar_arrive(&tempty[s]);
-                for (int t = 0; t < 2; ++t)
-                    if (++s == a.nst) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
-                continue;
-            }
             if (valid) pmax = fmaxf(pmax, P);
             const float lg = log2f(fabsf(fmaf(r, a.c1, -a.c0)) + a.rdelta);
-            // loose pre-test bounds; an invalid record never passes
             const float A = lg / a.alpha - P;
-            const float Asel = valid ? A + 0x1p-19f * (fabsf(A) + P + sM[0]) : -INFINITY;
-            const float Ann = valid ? -P + 0x1p-19f * (2.f * P + sM[1]) : -INFINITY;
+            float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
+            // an invalid record never passes a pre-test
+            pr[rloc] = valid ? A + 0x1p-19f * (fabsf(A) + P + sM[0]) : -INFINITY;
+            pr[PAGE + rloc] = valid ? -P + 0x1p-19f * (2.f * P + sM[1]) : -INFINITY;
+            pr[2 * PAGE + rloc] = P;
+            pr[3 * PAGE + rloc] = valid ? lg : -INFINITY;
+            __syncwarp();
+            if (lane == 0) bar_arrive(&pready[it % PR]);
+            bar_wait(&tfull[s], ph);  // the MMA is done reading the stage
+            __syncwarp();
+            if (lane == 0) bar_arrive(&empty[s]);
+        }
+        if (a.mode == 1) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+            if (lane == 0) atomicMax(a.pmax, __float_as_uint(pmax));
+        }
+    } else {
+        // ---------------- epilogue: two groups of four lane quarters ----------------
+        const int par = warp >> 2, quarter = warp & 3;
+        const int rloc = quarter * 32 + lane;
+        for (uint32_t it = par; it < mine; it += 2) {
+            const uint32_t s = it % nst, ph = (it / nst) & 1u;
+            const uint32_t rec = page_of(it) * PAGE + rloc;
+            bar_wait(&pready[it % PR], (it / PR) & 1u);
+            const float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
+            const float Asel = pr[rloc], Ann = pr[PAGE + rloc];
+            const float P = pr[2 * PAGE + rloc], lg = pr[3 * PAGE + rloc];
+            bar_wait(&tfull[s], ph);
+            tc_fence_after();
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(s * QW);
+            if (a.probe != 1) {
 #pragma unroll 1
-            for (int c0 = 0; c0 < QW; c0 += 32) {
-                float acc[32];
-                tmem_ld32(taddr + c0, acc);
-                if (a.probe == 3) {
-                    float t = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) t += acc[j];
-                    if (t == 12345.f) a.pmax[1] = 1;
-                } else if (a.mode == 1) {
-                    // four independent predicate chains
-                    bool h0 = false, h1 = false, h2 = false, h3 = false;
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        const float4 b4 = *reinterpret_cast<const float4*>(sB + c0 + j);
-                        h0 |= acc[j] + b4.x < Asel;
-                        h1 |= acc[j + 1] + b4.y < Asel;
-                        h2 |= acc[j + 2] + b4.z < Asel;
-                        h3 |= acc[j + 3] + b4.w < Asel;
-                    }
-                    const bool hit = (h0 | h1) | (h2 | h3);
-                    bool hitn = false;
-                    if (a.knn) {
-                        h0 = h1 = h2 = h3 = false;
+                for (int c0 = 0; c0 < QW; c0 += 32) {
+                    float acc[32];
+                    tmem_ld32(taddr + c0, acc);
+                    if (a.mode == 1) {
+                        // four independent predicate chains
+                        bool h0 = false, h1 = false, h2 = false, h3 = false;
 #pragma unroll
                         for (int j = 0; j < 32; j += 4) {
-                            const float4 b4 = *reinterpret_cast<const float4*>(sB + QW + c0 + j);
-                            h0 |= acc[j] + b4.x < Ann;
-                            h1 |= acc[j + 1] + b4.y < Ann;
-                            h2 |= acc[j + 2] + b4.z < Ann;
-                            h3 |= acc[j + 3] + b4.w < Ann;
+                            const float4 b4 = *reinterpret_cast<const float4*>(sB + c0 + j);
+                            h0 |= acc[j] + b4.x < Asel;
+                            h1 |= acc[j + 1] + b4.y < Asel;
+                            h2 |= acc[j + 2] + b4.z < Asel;
+                            h3 |= acc[j + 3] + b4.w < Asel;
                         }
-                        hitn = (h0 | h1) | (h2 | h3);
-                    }
-                    if (a.probe == 4) {
-                        if (hit && P == 12345.f) a.pmax[1] = 1;
-                    } else if (__any_sync(0xffffffffu, hit | hitn)) {
-                        // rare: which columns passed, then the exact formula (the
-                        // stream pass's key) on each such column, reloaded from
-                        // TMEM with a warp-uniform column address
-                        uint32_t ms = 0, mn = 0;
+                        if (a.knn) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                const float4 b4 =
+                                    *reinterpret_cast<const float4*>(sB + QW + c0 + j);
+                                h0 |= acc[j] + b4.x < Ann;
+                                h1 |= acc[j + 1] + b4.y < Ann;
+                                h2 |= acc[j + 2] + b4.z < Ann;
+                                h3 |= acc[j + 3] + b4.w < Ann;
+                            }
+                        }
+                        if (__any_sync(0xffffffffu, (h0 | h1) | (h2 | h3))) {
+                            // rare: which columns passed, then the exact formula (the
+                            // stream pass's key) on each such column, reloaded from
+                            // TMEM with a warp-uniform column address
+                            uint32_t ms = 0, mn = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                ms |= acc[j] + sB[c0 + j] < Asel ? 1u << j : 0u;
+                                if (a.knn) mn |= acc[j] + sB[QW + c0 + j] < Ann ? 1u << j : 0u;
+                            }
+                            uint32_t U = __reduce_or_sync(0xffffffffu, ms | mn);
+                            while (U) {
+                                const int j = __ffs(U) - 1;
+                                U &= U - 1;
+                                const float v = tmem_ld1(taddr + c0 + j);
+                                const float d2 = (P + scc[c0 + j]) + v;
+                                const float key = fmaf(-d2, a.alpha, lg);
+                                if (((ms >> j) & 1u) && key > sthr[c0 + j])
+                                    list_append(a, scnt, sdrop, 2 * QW, c0 + j, key, rec);
+                                if (((mn >> j) & 1u) && -d2 > sthr[QW + c0 + j])
+                                    list_append(a, scnt, sdrop, 2 * QW, QW + c0 + j, -d2, rec);
+                            }
+                        }
+                    } else {
+                        // sample: per-query maximum over this warp's 32 records
+                        float kn[32];
+                        const bool valid = lg != -INFINITY;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            ms |= acc[j] + sB[c0 + j] < Asel ? 1u << j : 0u;
-                            if (a.knn) mn |= acc[j] + sB[QW + c0 + j] < Ann ? 1u << j : 0u;
+                            const float d2 = (P + scc[c0 + j]) + acc[j];
+                            acc[j] = valid ? fmaf(-d2, a.alpha, lg) : -INFINITY;
+                            kn[j] = valid ? -d2 : -INFINITY;
                         }
-                        uint32_t U = __reduce_or_sync(0xffffffffu, ms | mn);
-                        while (U) {
-                            const int j = __ffs(U) - 1;
-                            U &= U - 1;
-                            const float v = tmem_ld1(taddr + c0 + j);
-                            const float d2 = (P + scc[c0 + j]) + v;
-                            const float key = fmaf(-d2, a.alpha, lg);
-                            if (((ms >> j) & 1u) && key > sthr[c0 + j])
-                                list_append(a, scnt, sdrop, 2 * QW, c0 + j, key, rec);
-                            if (((mn >> j) & 1u) && -d2 > sthr[QW + c0 + j])
-                                list_append(a, scnt, sdrop, 2 * QW, QW + c0 + j, -d2, rec);
+                        const uint32_t S4 = 4 * a.spages, col = r0 + it * G;
+                        const float mk = transpose_max(acc, lane);
+                        a.smax[(size_t)(c0 + lane) * S4 + 4 * col + quarter] = mk;
+                        if (a.knn) {
+                            const float mn = transpose_max(kn, lane);
+                            a.smax[(size_t)(QW + c0 + lane) * S4 + 4 * col + quarter] = mn;
                         }
-                    }
-                } else {
-                    float kn[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float d2 = (P + scc[c0 + j]) + acc[j];
-                        acc[j] = valid ? fmaf(-d2, a.alpha, lg) : -INFINITY;
-                        kn[j] = valid ? -d2 : -INFINITY;
-                    }
-                    const uint32_t S4 = 4 * a.spages, col = r0 + it * G;
-                    const float mk = transpose_max(acc, lane);
-                    a.smax[(size_t)(c0 + lane) * S4 + 4 * col + quarter] = mk;
-                    if (a.knn) {
-                        const float mn = transpose_max(kn, lane);
-                        a.smax[(size_t)(QW + c0 + lane) * S4 + 4 * col + quarter] = mn;
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) bar_arrive(&tempty[s]);
-            for (int t = 0; t < 2; ++t)
-                if (++s == a.nst) {
-                    s = 0;
-                    ph ^= 1u;
-                }
         }
         if (a.mode == 1) {
-#pragma unroll
-            for (int o = 16; o; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
-            if (lane == 0) atomicMax(a.pmax, __float_as_uint(pmax));
-            asm volatile("bar.sync 1, %0;" ::"n"(WW * 32) : "memory");
-            for (int L = tid; L < 2 * QW; L += WW * 32) {
+            asm volatile("bar.sync 1, %0;" ::"n"(WE * 32) : "memory");
+            for (int L = tid; L < 2 * QW; L += WE * 32) {
                 a.lcnt[(size_t)blockIdx.x * 2 * QW + L] = min(scnt[L], a.cap);
                 if (sdrop[L]) atomicMax(&a.dropped[L], sdrop[L]);
             }
@@ -388,7 +379,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == WW + 1) {
+    if (warp == W_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tcols));
     }
@@ -633,8 +624,9 @@ WideFn wide_pick_qw(int qw) {
 }
 
 size_t wide_smem(int dp, int qw, int nst) {
-    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + 2 * (size_t)(dp / 8) * qw * 32 + dp * 4 +
-           qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 + 32 * 8 + 16;
+    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + 2 * (size_t)(dp / 8) * qw * 32 +
+           (size_t)2 * nst * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 +
+           48 * 8 + 16;
 }
 
 }  // namespace
