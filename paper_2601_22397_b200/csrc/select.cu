@@ -516,6 +516,7 @@ struct RefineArgs {
     size_t n;      // records in this store (candidate validity)
     size_t n_loo;  // records of the whole buffer (loo_mean's n)
     double total, two_s2, lambda, beta, gamma, key_slack_abs;
+    double bq_rel;  // relative rounding of the MMA's query operand (wide pass), else 0
     int has_excl, has_excl_nn;
     const float* ckey;
     const uint32_t* cidx;  // merged, sorted [2QB][kmax]
@@ -582,7 +583,9 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
     const double pmx = (double)__uint_as_float(*a.pmax);
     const double sq = sqrt(pmx) + sqrt(a.cc[q]);
     // + the TF32 rounding of the stored records: d2_true >= d2 (1 - 2^-11) - 2^-11 P
-    const double Eq = a.gamma * sq * sq + 0x1p-11 * pmx * (1.0 + 1e-6) + 1e-30;
+    // + the rounded query operand: |<x, b' - b>| <= bq_rel sqrt(P C_q)
+    const double Eq = a.gamma * sq * sq + 0x1p-11 * pmx * (1.0 + 1e-6) +
+                      a.bq_rel * sqrt(pmx * a.cc[q]) + 1e-30;
 
     // exact score of every candidate: experience.cpp:254-258 with the
     // reference's rounding sequence (standardize :162-166, similarity
@@ -985,10 +988,15 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         unsigned int* dpmax = reinterpret_cast<unsigned int*>(mthr + 2 * qb);
         double* zs = s->b_z.as<double>((size_t)qb * kp * d);
         double* dc = s->b_consts.as<double>(2 * (size_t)d + (size_t)qb * d + qb);
-        const size_t ob = (size_t)qb * m * 8 * 4 + (size_t)qb * m * 4 + (size_t)qb * 8 * 2 +
-                          (size_t)qb * 4 * 4 + 64;
-        char* dout = static_cast<char*>(s->b_out.get(ob));
-        char* hout = static_cast<char*>(s->h_out.get(ob));
+        const size_t ngroups = (nq + qb - 1) / qb;
+        // Every group's kernels are enqueued back to back on the store's stream
+        // (device scratch is reused in stream order); each group has its own
+        // pinned staging, output slice and events, and the host synchronises
+        // once, after one device-to-host copy of all outputs.
+        const size_t ob = ((size_t)qb * m * 8 * 4 + (size_t)qb * m * 4 + (size_t)qb * 8 * 2 +
+                           (size_t)qb * 4 * 4 + 64 + 255) & ~(size_t)255;
+        char* dout = static_cast<char*>(s->b_out.get(ob * ngroups));
+        char* hout = static_cast<char*>(s->h_out.get(ob * ngroups));
         struct O {
             int64_t* idx;
             double* sim;
@@ -1015,13 +1023,17 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             o.round = reinterpret_cast<int32_t*>(o.rew + qb * m);
             return o;
         };
-        const O D = carve(dout), H = carve(hout);
-        // pinned, so the copy never stages through pageable memory
+        // pinned, so the copies never stage through pageable memory
         const size_t nhc = 2 * (size_t)d + (size_t)qb * d + qb;
-        double* hc = s->h_consts.as<double>(nhc);
+        double* hc_all = s->h_consts.as<double>(nhc * ngroups);
+        const size_t hstride = ((size_t)3 * pl.dp * qb + pl.dp + 4 * (size_t)qb + 256 + 63) & ~(size_t)63;
+        float* hstage_all = use_mma || use_wide ? s->h_mmab.as<float>(hstride * ngroups) : nullptr;
+        while (s->gev.size() < 3 * ngroups) {
+            cudaEvent_t e;
+            SAIR_CUDA(cudaEventCreate(&e));
+            s->gev.push_back(e);
+        }
         std::vector<double> cc;
-        std::copy(p.mean.begin(), p.mean.end(), hc);
-        std::copy(p.sd.begin(), p.sd.end(), hc + d);
         const size_t refine_smem = (size_t)kp * (8 * 4 + 4 * 4) + 16 + (size_t)knn * 8 +
                                    (size_t)8 * 8 * (d + 1) * 8 + (size_t)(kp + knn) * 4 + 64;
         SAIR_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1029,22 +1041,29 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         s->last.candidates = kp;
         s->last.qb = qb;
         s->last.tensor_core = use_wide ? 2 : (use_mma ? 1 : 0);
-        for (size_t g0 = 0; g0 < nq; g0 += qb) {
+        for (size_t g = 0; g < ngroups; ++g) {
+            const size_t g0 = g * qb;
             const int nqg = (int)std::min<size_t>(qb, nq - g0);
             const double* zgrp = p.z.data() + g0 * d;
+            double* hc = hc_all + g * nhc;
+            std::copy(p.mean.begin(), p.mean.end(), hc);
+            std::copy(p.sd.begin(), p.sd.end(), hc + d);
             for (int qq = 0; qq < qb; ++qq) {
                 const double* z = zgrp + (size_t)(qq < nqg ? qq : 0) * d;
                 for (int k = 0; k < d; ++k) hc[2 * (size_t)d + (size_t)qq * d + k] = z[k];
             }
+            const GroupIo io{hstage_all ? hstage_all + g * hstride : nullptr, s->gev[3 * g + 1],
+                             s->gev[3 * g + 2]};
+            const O D = carve(dout + g * ob);
             SAIR_CUDA(cudaMemsetAsync(dpmax, 0, 4, s->st));
-            SAIR_CUDA(cudaEventRecord(s->ev[1], s->st));
-            if (use_wide)  // sample + stream + per-list top-K' (records ev[4], ev[2])
-                wfill(s, wp, p, zgrp, nqg, c1, c0, rdelta, alpha, mk, mi, mthr, dpmax, cc);
+            SAIR_CUDA(cudaEventRecord(s->gev[3 * g], s->st));
+            if (use_wide)  // sample + stream + per-list top-K' (records e_mid, e_end)
+                wfill(s, wp, p, zgrp, nqg, c1, c0, rdelta, alpha, mk, mi, mthr, dpmax, cc, io);
             else if (use_mma)
-                mfill(s, mp, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
+                mfill(s, mp, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc, io);
             else
                 fill(s, pl, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
-            if (!use_wide) SAIR_CUDA(cudaEventRecord(s->ev[2], s->st));
+            if (!use_wide) SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
             s->last.stream_launches++;
             for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
             SAIR_CUDA(cudaMemcpyAsync(dc, hc, nhc * 8, cudaMemcpyHostToDevice, s->st));
@@ -1076,6 +1095,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.gamma = use_wide ? (2 * pl.dp + 32) * u + 0x1p-20
                                 : (use_mma ? (pl.dp + 24) * u + 0x1p-20 : (pl.dp + 16) * u);
             ra.key_slack_abs = key_slack_abs;
+            ra.bq_rel = use_wide ? wide_bq_rel() : 0.0;
             ra.has_excl = n > (size_t)kp;
             ra.has_excl_nn = n > (size_t)knn;
             ra.ckey = mk;
@@ -1097,16 +1117,21 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.out_round = D.round;
             refine_kernel<<<nqg, 256, refine_smem, s->st>>>(ra);
             SAIR_LAUNCH("refine_kernel");
-            SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob, cudaMemcpyDeviceToHost, s->st));
-            SAIR_CUDA(cudaStreamSynchronize(s->st));
+        }
+        SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob * ngroups, cudaMemcpyDeviceToHost, s->st));
+        SAIR_CUDA(cudaStreamSynchronize(s->st));
+        for (size_t g = 0; g < ngroups; ++g) {
+            const size_t g0 = g * qb;
+            const int nqg = (int)std::min<size_t>(qb, nq - g0);
+            const O H = carve(hout + g * ob);
             float ms = 0.f;
             if (use_mma || use_wide) {
                 float pre = 0.f;
-                cudaEventElapsedTime(&pre, s->ev[1], s->ev[4]);
-                cudaEventElapsedTime(&ms, s->ev[4], s->ev[2]);
+                cudaEventElapsedTime(&pre, s->gev[3 * g], s->gev[3 * g + 1]);
+                cudaEventElapsedTime(&ms, s->gev[3 * g + 1], s->gev[3 * g + 2]);
                 prepass_ms += pre;
             } else {
-                cudaEventElapsedTime(&ms, s->ev[1], s->ev[2]);
+                cudaEventElapsedTime(&ms, s->gev[3 * g], s->gev[3 * g + 2]);
             }
             stream_ms += ms;
             for (int qq = 0; qq < nqg; ++qq) {

@@ -60,6 +60,13 @@ inline QueryPrep prep_queries(const sair_store_s* s, const double* q, size_t nq,
     return p;
 }
 
+// Per query group: pinned staging for the launcher's constants and the
+// events it records (end of the threshold pre-pass, end of the stream pass).
+struct GroupIo {
+    float* hstage;
+    cudaEvent_t e_mid, e_end;
+};
+
 // select_mma.cu: the tcgen05 streaming kernel (plan + launcher)
 struct MmaPlan {
     int dp, qb, kp, knn, kmax, nst, cap_sel, cap_nn, grid;
@@ -67,7 +74,7 @@ struct MmaPlan {
 };
 using MmaFillFn = void (*)(sair_store_s*, const MmaPlan&, const QueryPrep&, const double*, int,
                            float, float, float, float, float*, uint32_t*, unsigned int*,
-                           std::vector<double>&);
+                           std::vector<double>&, const GroupIo&);
 MmaFillFn pick_mma_fill(int dp, int qb);
 bool make_mma_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                    MmaPlan* pl);
@@ -81,8 +88,9 @@ struct WidePlan {
 };
 using WideFn = void (*)(sair_store_s*, const WidePlan&, const QueryPrep&, const double*, int, float,
                         float, float, float, float*, uint32_t*, float*, unsigned int*,
-                        std::vector<double>&);
+                        std::vector<double>&, const GroupIo&);
 WideFn pick_wide(int dp, int qw);
+double wide_bq_rel();  // relative error bound of the wide pass's query operand
 bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                     WidePlan* pl);
 

@@ -459,7 +459,8 @@ inline float tf32_trunc(double v) {
 template <int DP, int QB>
 void mma_fill_and_launch(sair_store_s* s, const MmaPlan& pl, const QueryPrep& p, const double* zgrp,
                          int nqg, float c1, float c0, float rdelta, float alpha, float* ck,
-                         uint32_t* ci, unsigned int* pmax, std::vector<double>& cc_out) {
+                         uint32_t* ci, unsigned int* pmax, std::vector<double>& cc_out,
+                         const GroupIo& io) {
     MmaArgs<DP, QB> a{};
     a.pages = s->pages;
     a.r32 = s->r32;
@@ -482,7 +483,7 @@ void mma_fill_and_launch(sair_store_s* s, const MmaPlan& pl, const QueryPrep& p,
     const int d = s->d;
     for (int k = 0; k < DP; ++k) a.s[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
     cc_out.assign(QB, 0.0);
-    float* hb = s->h_mmab.as<float>(2 * DP * QB + DP + DP * QB + QB + 64);
+    float* hb = io.hstage;  // 2 DP QB + DP + DP QB + QB floats
     for (int q = 0; q < QB; ++q) {
         const double* z = zgrp + (size_t)(q < nqg ? q : 0) * d;
         double cc = 0.0;
@@ -531,7 +532,7 @@ void mma_fill_and_launch(sair_store_s* s, const MmaPlan& pl, const QueryPrep& p,
     sample_kth_kernel<<<pl.knn ? 2 * QB : QB, 1024, 0, s->st>>>(
         dkeys, spages, QB, pl.kp, pl.knn, dt0);
     SAIR_LAUNCH("sample_kth_kernel");
-    SAIR_CUDA(cudaEventRecord(s->ev[4], s->st));
+    SAIR_CUDA(cudaEventRecord(io.e_mid, s->st));
     SAIR_CUDA(cudaFuncSetAttribute(stream_mma_kernel<DP, QB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     stream_mma_kernel<DP, QB><<<pl.grid, MMA_THREADS, pl.smem, s->st>>>(a);

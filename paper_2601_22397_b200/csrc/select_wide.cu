@@ -53,6 +53,10 @@ namespace {
 constexpr int WE = 8;
 constexpr int W_REC = 8, W_PROD = 16, W_MMA = 17;
 constexpr int WIDE_THREADS = 18 * 32;
+// B operand parts: 1 = the query constants rounded to nearest TF32 (the
+// perturbation is a bounded query error the certification carries, DESIGN.md
+// "K4"); 2 = hi + lo split, two MMAs per K-step
+constexpr int WB = 1;
 
 struct WideArgs {
     const float* pages;
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     const int nst = a.nst, PR = 2 * a.nst;  // smem/TMEM stages, record-constant slots
     unsigned char* stage = smem;
     float* btile = reinterpret_cast<float*>(stage + (size_t)nst * PAGE_BYTES);  // [2][KSTEPS]
-    float* prec = btile + 2 * KSTEPS * BT_BYTES / 4;  // [PR][4][PAGE]: Asel, Ann, P, lg
+    float* prec = btile + WB * KSTEPS * BT_BYTES / 4;  // [PR][4][PAGE]: Asel, Ann, P, lg
     float* ss = prec + (size_t)PR * 4 * PAGE;
     float* scc = ss + DP;
     float* sthr = scc + QW;
@@ -138,9 +142,9 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     {
         const float4* src = reinterpret_cast<const float4*>(a.consts);
         float4* dst = reinterpret_cast<float4*>(btile);
-        for (int i = tid; i < 2 * KSTEPS * BT_BYTES / 16; i += WIDE_THREADS) dst[i] = src[i];
+        for (int i = tid; i < WB * KSTEPS * BT_BYTES / 16; i += WIDE_THREADS) dst[i] = src[i];
     }
-    const float* cs = a.consts + 2 * DP * QW;
+    const float* cs = a.consts + WB * DP * QW;
     for (int i = tid; i < DP; i += WIDE_THREADS) ss[i] = cs[i];
     for (int i = tid; i < QW; i += WIDE_THREADS) scc[i] = cs[DP + i];
     for (int i = tid; i < 2 * QW; i += WIDE_THREADS)
@@ -231,10 +235,12 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
 #pragma unroll
                 for (int ks = 0; ks < KSTEPS; ++ks) {
                     const uint64_t ad = umma_desc(abase + ks * 1024, BOX_BYTES, 512, 1);
-                    const uint64_t bh = umma_desc(bbase + ks * BT_BYTES, 128, 256, 0);
-                    const uint64_t bl = umma_desc(bbase + (KSTEPS + ks) * BT_BYTES, 128, 256, 0);
-                    umma_tf32(dcol, ad, bh, IDESC, ks > 0 ? 1u : 0u);
-                    umma_tf32(dcol, ad, bl, IDESC, 1u);
+#pragma unroll
+                    for (int h = 0; h < WB; ++h) {
+                        const uint64_t bd =
+                            umma_desc(bbase + (h * KSTEPS + ks) * BT_BYTES, 128, 256, 0);
+                        umma_tf32(dcol, ad, bd, IDESC, ks > 0 || h > 0 ? 1u : 0u);
+                    }
                 }
                 umma_commit(&tfull[s]);
             }
@@ -497,14 +503,25 @@ inline float tf32_trunc(double v) {
     return f;
 }
 
+// round to the nearest TF32 (ties to even): |error| <= 2^-11 |v|
+inline float tf32_rn(double v) {
+    float f = (float)v;
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
 template <int DP, int QW>
 void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, const double* zgrp,
                    int nqg, float c1, float c0, float rdelta, float alpha, float* mk,
-                   uint32_t* mi, float* mthr, unsigned int* pmax, std::vector<double>& cc_out) {
+                   uint32_t* mi, float* mthr, unsigned int* pmax, std::vector<double>& cc_out,
+                   const GroupIo& io) {
     const int d = s->d;
-    const size_t nc = 2 * (size_t)DP * QW + DP + QW + 2 * QW;
-    float* hb = s->h_mmab.as<float>(nc + 64);
-    float* sv = hb + 2 * (size_t)DP * QW;
+    const size_t nc = WB * (size_t)DP * QW + DP + QW + 2 * QW;
+    float* hb = io.hstage;  // nc floats
+    float* sv = hb + WB * (size_t)DP * QW;
     float* ccv = sv + DP;
     for (int k = 0; k < DP; ++k) sv[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
     cc_out.assign(QW, 0.0);
@@ -517,13 +534,17 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
             if (k < d) c = (float)((p.mean[k] - s->shift[k]) / p.sd[k] + z[k]);
             cc += (double)c * (double)c;
             const double bk = k < d ? -2.0 * (double)c * (double)sv[k] : 0.0;
-            const float hi = tf32_trunc(bk);
             // smem image of the K-major B tiles: (q % 8) * 16 + (q / 8) * 256 +
             // (k % 4) * 4 + (k / 4) * 128 bytes within K-step k / 8
             const size_t off = (size_t)(k / 8) * QW * 8 + (q % 8) * 4 + (q / 8) * 64 +
                                (k % 4) + ((k % 8) / 4) * 32;
-            hb[off] = hi;
-            hb[(size_t)DP * QW + off] = tf32_trunc(bk - (double)hi);
+            if (WB == 1) {
+                hb[off] = tf32_rn(bk);
+            } else {
+                const float hi = tf32_trunc(bk);
+                hb[off] = hi;
+                hb[(size_t)DP * QW + off] = tf32_trunc(bk - (double)hi);
+            }
         }
         ccv[q] = (float)cc;
         cc_out[q] = cc;
@@ -533,7 +554,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     const size_t S4 = 4 * (size_t)pl.spages;
     char* base = static_cast<char*>(s->b_mmab.get(nc * 4 + 256 + L * 8 + S4 * L * 4 + 256));
     float* dc = reinterpret_cast<float*>(base);
-    float* dt0 = dc + 2 * (size_t)DP * QW + DP + QW;  // the t0 slot of consts
+    float* dt0 = dc + WB * (size_t)DP * QW + DP + QW;  // the t0 slot of consts
     uint32_t* dcnt = reinterpret_cast<uint32_t*>(base + ((nc * 4 + 255) & ~(size_t)255));
     unsigned int* ddrop = dcnt + L;
     float* dsmax = reinterpret_cast<float*>(ddrop + L);
@@ -578,11 +599,11 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(dsmax, (uint32_t)S4, QW, pl.kp,
                                                              pl.knn, dt0);
     SAIR_LAUNCH("wide_kth_kernel");
-    SAIR_CUDA(cudaEventRecord(s->ev[4], s->st));
+    SAIR_CUDA(cudaEventRecord(io.e_mid, s->st));
     a.mode = 1;
     stream_wide_kernel<DP, QW><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
     SAIR_LAUNCH("stream_wide_kernel(stream)");
-    SAIR_CUDA(cudaEventRecord(s->ev[2], s->st));
+    SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
     const int nl = pl.knn ? 2 * QW : QW;
     if ((size_t)pl.grid * pl.cap <= 4096)
         list_topk_kernel<4><<<nl, 1024, 0, s->st>>>(lkey, lidx, gcnt, pl.cap, pl.grid, QW, pl.kp,
@@ -624,7 +645,7 @@ WideFn wide_pick_qw(int qw) {
 }
 
 size_t wide_smem(int dp, int qw, int nst) {
-    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + 2 * (size_t)(dp / 8) * qw * 32 +
+    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + WB * (size_t)(dp / 8) * qw * 32 +
            (size_t)2 * nst * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 +
            48 * 8 + 16;
 }
@@ -640,6 +661,8 @@ WideFn pick_wide(int dp, int qw) {
         default: return nullptr;
     }
 }
+
+double wide_bq_rel() { return WB == 1 ? 0x1p-10 * 1.01 : 0.0; }
 
 bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                     WidePlan* pl) {

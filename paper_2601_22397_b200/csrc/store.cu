@@ -185,6 +185,8 @@ void store_free(sair_store_s* s) {
         b->release();
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : s->gev) cudaEventDestroy(e);
+    s->gev.clear();
     if (s->st) cudaStreamDestroy(s->st);
     s->st = nullptr;
 }

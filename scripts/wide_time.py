@@ -6,7 +6,7 @@ sys.path.insert(0, ".")
 import paper_2601_22397_b200 as sair
 from paper_2601_22397_b200 import synth
 
-for n, nq in [(1 << 20, 256), (1 << 21, 512), (1 << 24, 128), (1 << 24, 8)]:
+for n, nq in [(1 << 20, 256), (1 << 21, 512), (1 << 24, 128), (1 << 24, 8), (1 << 24, 4096)]:
     db = sair.ExperienceBuffer(0.0)
     db.store_synthetic(2026, n, 64)
     xq = synth.queries(7, nq * 4, 64).reshape(4, nq, 64)
