@@ -47,12 +47,12 @@ using namespace umma;
 
 namespace {
 
-// warp roles: 0-7 epilogue (two groups of four TMEM lane quarters), 8-15
-// record constants (two groups; they own the shared page stage), 16
-// producer, 17 MMA
+// warp roles: 0-7 epilogue (two groups of four TMEM lane quarters), 8-11
+// record constants (two pairs taking alternate pages; they own the shared
+// page stage), 12 producer, 13 MMA
 constexpr int WE = 8;
-constexpr int W_REC = 8, W_PROD = 16, W_MMA = 17;
-constexpr int WIDE_THREADS = 18 * 32;
+constexpr int W_REC = 8, W_PROD = 12, W_MMA = 13;
+constexpr int WIDE_THREADS = 14 * 32;
 // B operand parts: 1 = the query constants rounded to nearest TF32 (the
 // perturbation is a bounded query error the certification carries, DESIGN.md
 // "K4"); 2 = hi + lo split, two MMAs per K-step
@@ -180,11 +180,11 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < nst; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&empty[s], 4);   // the four record-constant warps
+            bar_init(&empty[s], 2);   // the record-constant warp pair of the page
             bar_init(&tfull[s], 1);
             bar_init(&tempty[s], 4);  // the four epilogue warps of the page's group
         }
-        for (int p = 0; p < PR; ++p) bar_init(&pready[p], 4);
+        for (int p = 0; p < PR; ++p) bar_init(&pready[p], 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -249,33 +249,54 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         // ---------------- record constants: P, lg, pre-test bounds ----------------
         // These warps own the shared page stage: P = ||y||^2 needs the page, the
         // epilogue only TMEM, so the stage is released as soon as the MMA is done.
-        const int quarter = warp & 3, rloc = quarter * 32 + lane;
+        // A pair of warps per page (the pairs take alternate pages); a thread owns
+        // two row-adjacent records: one LDS.64 and one FMUL2 + FFMA2 per dimension.
+        const int w = warp - W_REC, half = w & 1;
+        const int box_i = 2 * half + (lane >> 4), l16 = lane & 15;
+        const int rloc = box_i * 32 + 2 * l16;  // records rloc, rloc + 1 of the page
         float pmax = 0.f;
-        for (uint32_t it = (warp - W_REC) >> 2; it < mine; it += 2) {
+        for (uint32_t it = (uint32_t)(w >> 1); it < mine; it += 2) {
             const uint32_t s = it % nst, ph = (it / nst) & 1u;
             const uint32_t rec = page_of(it) * PAGE + rloc;
-            const bool valid = rec < a.n;
-            const float r = valid ? __ldg(a.r32 + rec) : 0.f;
+            const bool v0 = rec < a.n, v1 = rec + 1 < a.n;
+            float2 r2 = make_float2(0.f, 0.f);
+            if (v1) r2 = __ldg(reinterpret_cast<const float2*>(a.r32 + rec));
+            else if (v0) r2.x = __ldg(a.r32 + rec);
             bar_wait(&full[s], ph);
-            const unsigned char* box = stage + (size_t)s * PAGE_BYTES + quarter * BOX_BYTES;
-            float Pp[4] = {0.f, 0.f, 0.f, 0.f};
+            const unsigned char* box = stage + (size_t)s * PAGE_BYTES + box_i * BOX_BYTES;
+            float2 Pa = make_float2(0.f, 0.f), Pb = Pa;
 #pragma unroll
-            for (int k = 0; k < DP; ++k) {
-                const float x = *reinterpret_cast<const float*>(
-                    box + k * 128 + ((((lane >> 3) ^ (k & 3)) << 5) | ((lane & 7) << 2)));
-                const float y = __fmul_rn(x, ss[k]);
-                Pp[k & 3] = fmaf(y, y, Pp[k & 3]);
+            for (int k = 0; k < DP; k += 2) {
+                const float2 xa = *reinterpret_cast<const float2*>(
+                    box + k * 128 + ((((l16 >> 2) ^ (k & 3)) << 5) | ((l16 & 3) << 3)));
+                const float2 xb = *reinterpret_cast<const float2*>(
+                    box + (k + 1) * 128 + ((((l16 >> 2) ^ ((k + 1) & 3)) << 5) | ((l16 & 3) << 3)));
+                const float2 ya = __fmul2_rn(xa, make_float2(ss[k], ss[k]));
+                const float2 yb = __fmul2_rn(xb, make_float2(ss[k + 1], ss[k + 1]));
+                Pa = __ffma2_rn(ya, ya, Pa);
+                Pb = __ffma2_rn(yb, yb, Pb);
             }
-            const float P = (Pp[0] + Pp[1]) + (Pp[2] + Pp[3]);
-            if (valid) pmax = fmaxf(pmax, P);
-            const float lg = log2f(fabsf(fmaf(r, a.c1, -a.c0)) + a.rdelta);
-            const float A = lg / a.alpha - P;
+            const float2 P2 = __fadd2_rn(Pa, Pb);
             float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
-            // an invalid record never passes a pre-test
-            pr[rloc] = valid ? A + 0x1p-19f * (fabsf(A) + P + sM[0]) : -INFINITY;
-            pr[PAGE + rloc] = valid ? -P + 0x1p-19f * (2.f * P + sM[1]) : -INFINITY;
-            pr[2 * PAGE + rloc] = P;
-            pr[3 * PAGE + rloc] = valid ? lg : -INFINITY;
+            float2 oa, on, op, ol;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const bool valid = e ? v1 : v0;
+                const float P = e ? P2.y : P2.x, r = e ? r2.y : r2.x;
+                if (valid) pmax = fmaxf(pmax, P);
+                const float lg = log2f(fabsf(fmaf(r, a.c1, -a.c0)) + a.rdelta);
+                const float A = lg / a.alpha - P;
+                // an invalid record never passes a pre-test
+                const float as = valid ? A + 0x1p-19f * (fabsf(A) + P + sM[0]) : -INFINITY;
+                const float an = valid ? -P + 0x1p-19f * (2.f * P + sM[1]) : -INFINITY;
+                const float lv = valid ? lg : -INFINITY;
+                if (e) { oa.y = as; on.y = an; op.y = P; ol.y = lv; }
+                else { oa.x = as; on.x = an; op.x = P; ol.x = lv; }
+            }
+            *reinterpret_cast<float2*>(pr + rloc) = oa;
+            *reinterpret_cast<float2*>(pr + PAGE + rloc) = on;
+            *reinterpret_cast<float2*>(pr + 2 * PAGE + rloc) = op;
+            *reinterpret_cast<float2*>(pr + 3 * PAGE + rloc) = ol;
             __syncwarp();
             if (lane == 0) bar_arrive(&pready[it % PR]);
             bar_wait(&tfull[s], ph);  // the MMA is done reading the stage
@@ -307,28 +328,36 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                     float acc[32];
                     tmem_ld32(taddr + c0, acc);
                     if (a.mode == 1) {
-                        // four independent predicate chains
-                        bool h0 = false, h1 = false, h2 = false, h3 = false;
+                        // min over the chunk of D + B (FADD2 + 3-input min: one
+                        // instruction per pair), two independent chains per list
+                        float m0 = INFINITY, m1 = INFINITY;
 #pragma unroll
                         for (int j = 0; j < 32; j += 4) {
                             const float4 b4 = *reinterpret_cast<const float4*>(sB + c0 + j);
-                            h0 |= acc[j] + b4.x < Asel;
-                            h1 |= acc[j + 1] + b4.y < Asel;
-                            h2 |= acc[j + 2] + b4.z < Asel;
-                            h3 |= acc[j + 3] + b4.w < Asel;
+                            const float2 u = __fadd2_rn(make_float2(acc[j], acc[j + 1]),
+                                                        make_float2(b4.x, b4.y));
+                            const float2 v = __fadd2_rn(make_float2(acc[j + 2], acc[j + 3]),
+                                                        make_float2(b4.z, b4.w));
+                            m0 = fminf(m0, fminf(u.x, u.y));
+                            m1 = fminf(m1, fminf(v.x, v.y));
                         }
+                        bool hit = fminf(m0, m1) < Asel;
                         if (a.knn) {
+                            m0 = m1 = INFINITY;
 #pragma unroll
                             for (int j = 0; j < 32; j += 4) {
                                 const float4 b4 =
                                     *reinterpret_cast<const float4*>(sB + QW + c0 + j);
-                                h0 |= acc[j] + b4.x < Ann;
-                                h1 |= acc[j + 1] + b4.y < Ann;
-                                h2 |= acc[j + 2] + b4.z < Ann;
-                                h3 |= acc[j + 3] + b4.w < Ann;
+                                const float2 u = __fadd2_rn(make_float2(acc[j], acc[j + 1]),
+                                                            make_float2(b4.x, b4.y));
+                                const float2 v = __fadd2_rn(make_float2(acc[j + 2], acc[j + 3]),
+                                                            make_float2(b4.z, b4.w));
+                                m0 = fminf(m0, fminf(u.x, u.y));
+                                m1 = fminf(m1, fminf(v.x, v.y));
                             }
+                            hit |= fminf(m0, m1) < Ann;
                         }
-                        if (__any_sync(0xffffffffu, (h0 | h1) | (h2 | h3))) {
+                        if (__any_sync(0xffffffffu, hit)) {
                             // rare: which columns passed, then the exact formula (the
                             // stream pass's key) on each such column, reloaded from
                             // TMEM with a warp-uniform column address
