@@ -1,12 +1,16 @@
 #!/usr/bin/env python
 """Benchmark: surprisal-guided retrieval over a 16M x 64 experience store
 (BASELINE.json metric "retrieval queries/s @16M exps k=32; Pareto-scored
-tuples/s; % HBM roofline").
+tuples/s; % HBM roofline"; configs[3]: 16M experiences, 4096 queries/batch,
+k=32).
 
-A step = one select() pass of Q=8 queries (k = m = 32, lambda_div = 0, the
-fused veto scan off) over the whole device-resident store.  The Pareto half
-(4M 2-objective tuples: frontier maintenance + per-tuple reward) is measured in
-the same run and reported under "pareto".
+A step = one select() of a Q=4096 query batch (k = m = 32, lambda_div = 0, the
+fused veto scan off) over the whole device-resident store: 32 wide tensor-core
+passes of 128 queries (select_wide.cu).  Also measured in the same run:
+"hbm_target" -- Q=8 queries per step, the single HBM-bound pass of the north
+star's >= 70% HBM target (select_mma.cu); "config2" -- configs[1], 1M x 64
+with 256-query batches; "pareto" -- configs[2], 4M 2-objective tuples
+(frontier maintenance + per-tuple reward) and k-D dominance counts.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -34,7 +38,8 @@ sys.path.insert(0, str(ROOT))
 
 N_RECORDS = 16 * 1024 * 1024
 DIM = 64
-Q = 8
+Q = 4096
+Q_HBM = 8
 K_SEL = 32
 SEED = 2026
 PARETO_T = 4 * 1024 * 1024
@@ -108,6 +113,37 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ ours ---
 
+def _launches(stats):
+    """Our kernels per select() call, from its stats: per query group the
+    threshold pre-pass (2), the stream pass and the list merge (wide: per-list
+    top-K') and refine; 3 + 3m per exact fallback query."""
+    per = {2: 5, 1: 5, 0: 3}
+    return sum(per[s["tensor_core"]] * s["stream_launches"] + s["exact_fallbacks"] * (3 + 3 * K_SEL)
+               for s in stats)
+
+
+def _stream_roofline(stats, n_local, hbm_peak, peak_kind, bf16_peak, qw):
+    """Roofline of the dominant kernel (the stream pass): algorithmic bytes =
+    records x (4 d_pad + 4) per launch / its CUDA-event time."""
+    launches = sum(s["stream_launches"] for s in stats)
+    stream_ms = sum(s["stream_ms"] for s in stats)
+    dp = 64 if DIM > 32 else 32
+    alg_bytes = n_local * (4 * dp + 4)
+    per_launch_s = stream_ms / 1e3 / max(launches, 1)
+    achieved = alg_bytes / per_launch_s / 1e9
+    out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+           "frac": round(achieved / hbm_peak, 4), "peak_kind": peak_kind,
+           "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(per_launch_s * 1e3, 4),
+           "prepass_ms_per_launch": round(sum(s["prepass_ms"] for s in stats) / max(launches, 1), 4)}
+    if qw:
+        # the same launch as a GEMM: 2 x records x d_pad x QW TF32 flops
+        tf = 2.0 * n_local * dp * qw / per_launch_s / 1e12
+        out["tensor"] = {"achieved_tflops": round(tf, 1), "tf32_peak_tflops": round(bf16_peak / 2, 1),
+                         "frac": round(tf / (bf16_peak / 2), 4),
+                         "peak_note": "TF32 dense = measured bf16 / 2 (nominal ratio)"}
+    return out
+
+
 def run_ours(a, rank, world, local_rank):
     import torch
     import paper_2601_22397_b200 as sair
@@ -128,47 +164,54 @@ def run_ours(a, rank, world, local_rank):
         sharded.store_synthetic(SEED, n_total, DIM)
         buf = sharded.local
 
-        def step(i):
-            return sharded.select_batch(qpool[i], cfg)
+        def select(q):
+            return sharded.select_batch(q, cfg)
     else:
         lo, hi = 0, n_total
         buf = sair.ExperienceBuffer(0.0, device=dev)
         buf.store_synthetic(SEED, n_total, DIM)
 
-        def step(i):
-            return buf.select_batch(qpool[i], cfg)
+        def select(q):
+            return buf.select_batch(q, cfg)
     gen_s = time.time() - t0
     qpool = synth.queries(SEED, (a.warmup + a.steps) * a.queries, DIM).reshape(
         a.warmup + a.steps, a.queries, DIM)
     stream = torch.cuda.ExternalStream(buf.stream_ptr(), device=dev)
+    hbm_peak, bf16_peak, peak_kind = measured_peaks()
 
-    for i in range(a.warmup):
-        step(i)
-    stats = []
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clk:
+    def timed(qs, steps):
+        """device time (CUDA events on the store's stream, max over ranks)"""
+        stats = []
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for i in range(a.warmup, a.warmup + a.steps):
-            step(i)
+        for i in range(steps):
+            select(qs[i])
             stats.append(buf.last_stats())
         e1.record(stream)
         torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        if dist:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, stats
+
+    for i in range(a.warmup):
+        select(qpool[i])
+    with ClockSampler(dev) as clk:
+        ms, stats = timed(qpool[a.warmup:], a.steps)
     value = a.steps * a.queries / (ms / 1e3)
 
-    # e2e: the public API with host buffers, wall clock (copies inside)
+    # e2e: the public API with host queries and host results, wall clock
+    # (host->device query copy and device->host result copy inside every step)
     t0 = time.perf_counter()
     for i in range(a.warmup, a.warmup + a.steps):
-        step(i)
+        select(qpool[i])
     if dist:
         dist.barrier()
     e2e_s = time.perf_counter() - t0
@@ -178,26 +221,31 @@ def run_ours(a, rank, world, local_rank):
         e2e_s = float(t.item())
     e2e = a.steps * a.queries / e2e_s
 
-    # roofline of the dominant kernel (stream_kernel), CUDA events around each launch
-    launches = sum(s["stream_launches"] for s in stats)
-    stream_ms = sum(s["stream_ms"] for s in stats)
+    qw = stats[0]["qb"] if stats[0]["tensor_core"] == 2 else 0
+    roof = _stream_roofline(stats, hi - lo, hbm_peak, peak_kind, bf16_peak, qw)
+    tc = stats[0]["tensor_core"]
     dp = 64 if DIM > 32 else 32
-    alg_bytes = (hi - lo) * (4 * dp + 4)  # fp32 page row + fp32 reward per record
-    per_launch_s = stream_ms / 1e3 / max(launches, 1)
-    hbm_peak, _, peak_kind = measured_peaks()
-    achieved = alg_bytes / per_launch_s / 1e9
-    traffic = None
+    roof["kernel"] = (f"sair::stream_wide_kernel<{dp},{qw}> (tcgen05, {qw} queries/pass)" if tc == 2
+                      else f"sair::stream_mma_kernel<{dp},8> (tcgen05)" if tc == 1
+                      else f"sair::stream_kernel<{dp},8>")
     tp = ROOT / "profiles" / "stream_kernel_traffic.json"
+    roof["traffic"] = None
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
-    fallbacks = sum(s["exact_fallbacks"] for s in stats)
-    certified = sum(s["certified"] for s in stats)
-    # per query group: [sample_keys, sample_kth,] stream, merge, refine
-    gpu_launches = sum((5 if s["tensor_core"] else 3) * s["stream_launches"]
-                       + s["exact_fallbacks"] * (3 + 3 * K_SEL) for s in stats)
-    tc = all(s["tensor_core"] for s in stats)
-    kname = f"sair::stream_mma_kernel<{dp},8> (tcgen05)" if tc else f"sair::stream_kernel<{dp},8>"
-    prepass_ms = sum(s["prepass_ms"] for s in stats) / max(launches, 1)
+        tj = json.loads(tp.read_text()).get(roof["kernel"].split(" ")[0], {})
+        roof["traffic"] = tj.get("dram_bytes_per_launch")
+        roof["traffic_source"] = tj.get("source")
+    gpu_launches = _launches(stats) + (a.steps if dist else 0)
+
+    # the north star's HBM target: Q = 8 queries per step, one memory-bound pass
+    qh = synth.queries(SEED + 7, (3 + a.steps) * Q_HBM, DIM).reshape(3 + a.steps, Q_HBM, DIM)
+    for i in range(3):
+        select(qh[i])
+    ms_h, st_h = timed(qh[3:], a.steps)
+    roof_h = _stream_roofline(st_h, hi - lo, hbm_peak, peak_kind, bf16_peak, 0)
+    roof_h["kernel"] = f"sair::stream_mma_kernel<{dp},8> (tcgen05)"
+    hbm_target = {"queries_per_step": Q_HBM, "value": round(a.steps * Q_HBM / (ms_h / 1e3), 2),
+                  "unit": "queries/s", "ms_per_step": round(ms_h / a.steps, 4), "roofline": roof_h,
+                  "certified_queries": sum(s["certified"] for s in st_h)}
 
     out = {
         "metric": "retrieval queries/s @16M exps k=32",
@@ -208,27 +256,25 @@ def run_ours(a, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 filter + f64 refine",
+        "dtype": "f32/tf32 filter + f64 refine",
         "data": "synthetic (device-generated, synth.py; store 16M x 64, i.i.d. Irwin-Hall contexts)",
-        "config": {"workload": f"config 4 north-star HBM target: {n_total} records x d={DIM}, "
-                               f"Q={a.queries} queries/step, k={K_SEL}, lambda_div={a.lambda_div}",
+        "config": {"workload": f"configs[3]: {n_total} records x d={DIM}, Q={a.queries} "
+                               f"queries/step, k={K_SEL}, lambda_div={a.lambda_div}",
                    "records": n_total, "dim": DIM, "queries_per_step": a.queries, "k": K_SEL,
                    "lambda_div": a.lambda_div, "parallelism": f"record shards x{world}",
-                   "l2": "inputs larger than L2 (4.4 GB store vs 126 MB L2)"},
+                   "l2": "inputs larger than L2 (4.4 GB store streamed per pass vs 126 MB L2)"},
         "e2e": {"value": round(e2e, 2), "unit": "queries/s",
                 "h2d_bytes_per_step": a.queries * DIM * 8,
                 "d2h_bytes_per_step": a.queries * K_SEL * 24 + a.queries * 8},
         "gpu_launches": gpu_launches,
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
-                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                     "kernel": kname, "peak_kind": peak_kind,
-                     "prepass_ms_per_launch": round(prepass_ms, 4),
-                     "call_device_ms": round(sum(s["total_ms"] for s in stats) / max(len(stats), 1), 4),
-                     "algorithmic_bytes_per_launch": alg_bytes,
-                     "avg_launch_ms": round(per_launch_s * 1e3, 4)},
-        "certified_queries": certified, "exact_fallbacks": fallbacks,
+        "roofline": roof,
+        "certified_queries": sum(s["certified"] for s in stats),
+        "exact_fallbacks": sum(s["exact_fallbacks"] for s in stats),
         "store_build_s": round(gen_s, 3),
+        "hbm_target": hbm_target,
     }
+    if rank == 0 and world == 1 and not a.no_pareto:
+        out["config2"] = bench_config2(dev, a.steps)
     if rank == 0 and not a.no_pareto:
         out["pareto"] = bench_pareto(dev)
     if rank == 0:
@@ -238,6 +284,39 @@ def run_ours(a, rank, world, local_rank):
     if dist:
         dist.destroy_process_group()
     return out
+
+
+def bench_config2(dev, steps):
+    """configs[1]: 1M x 64 store, 256-query batches, k = 32, one GPU."""
+    import torch
+    import paper_2601_22397_b200 as sair
+    from paper_2601_22397_b200 import synth
+    n, nq = 1 << 20, 256
+    buf = sair.ExperienceBuffer(0.0, device=dev)
+    buf.store_synthetic(SEED + 1, n, DIM)
+    cfg = sair.SelectionConfig(m=K_SEL, lambda_div=0.0)
+    qs = synth.queries(SEED + 2, (3 + steps) * nq, DIM).reshape(3 + steps, nq, DIM)
+    for i in range(3):
+        buf.select_batch(qs[i], cfg)
+    stream = torch.cuda.ExternalStream(buf.stream_ptr(), device=dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stats = []
+    e0.record(stream)
+    for i in range(3, 3 + steps):
+        buf.select_batch(qs[i], cfg)
+        stats.append(buf.last_stats())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    hbm_peak, bf16_peak, peak_kind = measured_peaks()
+    qw = stats[0]["qb"] if stats[0]["tensor_core"] == 2 else 0
+    roof = _stream_roofline(stats, n, hbm_peak, peak_kind, bf16_peak, qw)
+    del buf
+    return {"workload": f"configs[1]: {n} records x d={DIM}, {nq}-query batch, k={K_SEL}",
+            "value": round(steps * nq / (ms / 1e3), 1), "unit": "queries/s",
+            "ms_per_step": round(ms / steps, 4), "roofline": roof,
+            "certified_queries": sum(s["certified"] for s in stats)}
 
 
 def bench_pareto(dev):
@@ -341,6 +420,7 @@ def run_reference(a):
         return {"impl": "reference", "unavailable": "oracle/_ref/libsair_ref.so not built"}
     ref = Ref()
     threads = min(os.cpu_count() or 1, a.queries)
+    q_s = min(a.queries, 2 * threads)  # bounded sample of each step's query batch
     sizes = (4096, 8192)
     per_q = {}
     for n_s in sizes:
@@ -348,15 +428,13 @@ def run_reference(a):
         b.store_many(synth.contexts(SEED, 0, n_s, DIM), synth.rewards(SEED, 0, n_s),
                      synth.rounds(0, n_s))
         b.effective_sigma(0.0)
-        xq = synth.queries(SEED, a.queries * (a.warmup + a.steps), DIM)
+        xq = synth.queries(SEED, q_s * (a.warmup + a.steps), DIM)
         for i in range(a.warmup):
-            b.select_batch(xq[i * a.queries:(i + 1) * a.queries], K_SEL, a.lambda_div, 0.0,
-                           nthreads=threads)
+            b.select_batch(xq[i * q_s:(i + 1) * q_s], K_SEL, a.lambda_div, 0.0, nthreads=threads)
         t0 = time.perf_counter()
         for i in range(a.warmup, a.warmup + a.steps):
-            b.select_batch(xq[i * a.queries:(i + 1) * a.queries], K_SEL, a.lambda_div, 0.0,
-                           nthreads=threads)
-        per_q[n_s] = (time.perf_counter() - t0) / (a.steps * a.queries) * threads
+            b.select_batch(xq[i * q_s:(i + 1) * q_s], K_SEL, a.lambda_div, 0.0, nthreads=threads)
+        per_q[n_s] = (time.perf_counter() - t0) / (a.steps * q_s) * threads
     # t(n) = c1 n + c2 n^2 per query per thread
     n1, n2 = sizes
     t1, t2 = per_q[n1], per_q[n2]
@@ -365,7 +443,7 @@ def run_reference(a):
     c2 = max(c2, 0.0)
     t_full = max(c1, 0.0) * N_RECORDS + c2 * N_RECORDS ** 2
     value = threads / t_full
-    sample = (f"literal reference select, {a.steps} steps x {a.queries} queries on {threads} "
+    sample = (f"literal reference select, {a.steps} steps x {q_s} of the {a.queries} queries on {threads} "
               f"threads at n={n1} ({t1 * 1e3:.1f} ms/query) and n={n2} ({t2 * 1e3:.1f} ms/query), "
               f"extrapolated to N={N_RECORDS} by t(n) = c1 n + c2 n^2")
     return {
@@ -374,8 +452,8 @@ def run_reference(a):
         "ms_per_step": t_full / threads * a.queries * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (synth.py)", "impl": "reference",
-        "config": {"workload": f"config 4 north-star HBM target: {N_RECORDS} records x d={DIM}, "
-                               f"Q={a.queries} queries/step, k={K_SEL}, lambda_div={a.lambda_div}"},
+        "config": {"workload": f"configs[3]: {N_RECORDS} records x d={DIM}, Q={a.queries} "
+                               f"queries/step, k={K_SEL}, lambda_div={a.lambda_div}"},
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
                          "kind": "reference", "sample": sample, "cpu_model": _cpu_model()},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
