@@ -122,13 +122,13 @@ def test_sharded_protocol_matches_single_buffer_cpu(orc):
         assert np.array_equal([v for _, v in got], sc)
 
 
-def _gpu_worker(rank, world, port, q):
+def _gpu_worker(rank, world, port, q, nq=10):
     from paper_2601_22397_b200 import SelectionConfig
     from paper_2601_22397_b200.sharded import ShardedExperienceBuffer
     _init(rank, world, port)
     buf = ShardedExperienceBuffer(dist, device=0)
     buf.store_synthetic(SEED, 200000, 32)
-    xq = synth.queries(SEED, 10, 32)
+    xq = synth.queries(SEED, nq, 32)
     out = buf.select_batch(xq, SelectionConfig(m=32, lambda_div=0.0))
     if rank == 0:
         q.put((buf.sigma,) + tuple(out))
@@ -136,7 +136,8 @@ def _gpu_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_sharded_select_on_device_matches_single_store():
+@pytest.mark.parametrize("nq", [10, 160])  # the 8-query pass / the wide tensor-core pass
+def test_sharded_select_on_device_matches_single_store(nq):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2601_22397_b200 as sair
@@ -144,7 +145,7 @@ def test_sharded_select_on_device_matches_single_store():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, nq)) for r in range(world)]
     for p in procs:
         p.start()
     sigma, idx, sim, sc, cnt = q.get(timeout=300)
@@ -154,7 +155,7 @@ def test_sharded_select_on_device_matches_single_store():
     one = sair.ExperienceBuffer(0.0)
     one.store_synthetic(SEED, 200000, 32)
     assert sigma == one.effective_sigma()
-    i1, s1, c1, n1 = one.select_batch(synth.queries(SEED, 10, 32),
+    i1, s1, c1, n1 = one.select_batch(synth.queries(SEED, nq, 32),
                                       sair.SelectionConfig(m=32, lambda_div=0.0))
     assert np.array_equal(cnt, n1)
     assert np.array_equal(idx, i1)
