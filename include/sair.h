@@ -267,6 +267,13 @@ SAIR_API sair_status sair_frontier_score_batch_device(sair_frontier_t f, const d
  * counts / member nullable (member-only mode exits early). */
 SAIR_API sair_status sair_dominance_counts(const double* tuples, size_t T, int K, int device,
                                            uint32_t* counts, uint8_t* member);
+/* The same counts split into `nparts` parts of equal pairwise work (a rank of
+ * a multi-GPU job computes part = its rank over the all-gathered tuples):
+ * entries outside the part are 0, so the parts combine by a sum (SURVEY.md
+ * 8(e): dominance counts need every pair across shards). */
+SAIR_API sair_status sair_dominance_counts_part(const double* tuples, size_t T, int K, int device,
+                                                int part, int nparts, uint32_t* counts,
+                                                uint8_t* member);
 
 /* ------------------------------------------------------------------------
  * Reward -- compute_reward / action_magnitude (reward.hpp:42-48)

@@ -476,17 +476,23 @@ class ParetoFrontier:
                                                       dom_ptr or None, stream or None))
 
 
-def dominance_counts(tuples, device: int = 0, counts: bool = True):
-    """K-objective dominance counts and frontier membership (see sair.h)."""
+def dominance_counts(tuples, device: int = 0, counts: bool = True, part: int = 0,
+                     nparts: int = 1):
+    """K-objective dominance counts and frontier membership (see sair.h).
+    With nparts > 1 only part `part` of the pairwise work is done (entries
+    outside it are 0; the parts of all ranks combine by a sum)."""
     t = _f64(tuples)
     if t.ndim != 2:
         raise InvalidArgument(_lib.SAIR_EINVAL, "tuples must be T x K")
     T, K = t.shape
     cnt = np.zeros(T, np.uint32) if counts else None
     mem = np.zeros(T, np.uint8)
-    _check(lib().sair_dominance_counts(
-        _dp(t), T, K, device, cnt.ctypes.data_as(C.POINTER(C.c_uint32)) if counts else None,
-        mem.ctypes.data_as(C.POINTER(C.c_uint8))))
+    cp = cnt.ctypes.data_as(C.POINTER(C.c_uint32)) if counts else None
+    mp = mem.ctypes.data_as(C.POINTER(C.c_uint8))
+    if nparts == 1:
+        _check(lib().sair_dominance_counts(_dp(t), T, K, device, cp, mp))
+    else:
+        _check(lib().sair_dominance_counts_part(_dp(t), T, K, device, part, nparts, cp, mp))
     return cnt, mem.astype(bool)
 
 

@@ -116,6 +116,8 @@ SIGNATURES = {
     "sair_frontier_score_batch_device": (C.c_int, [_vp, C.c_void_p, C.c_size_t, C.c_void_p,
                                                    C.c_void_p, C.c_void_p]),
     "sair_dominance_counts": (C.c_int, [_dp, C.c_size_t, C.c_int, C.c_int, _u32p, _u8p]),
+    "sair_dominance_counts_part": (C.c_int, [_dp, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             _u32p, _u8p]),
     "sair_action_magnitude": (C.c_int, [_i32p, C.c_size_t, _dp]),
     "sair_compute_reward": (C.c_int, [C.POINTER(RewardInputsC), _i32p, C.c_size_t, _vp,
                                       C.POINTER(RewardConfigC), C.POINTER(RewardBreakdownC)]),

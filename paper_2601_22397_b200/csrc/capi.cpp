@@ -490,6 +490,12 @@ sair_status sair_dominance_counts(const double* tuples, size_t T, int K, int dev
     return guard([&] { sair::dominance_counts(tuples, T, K, device, counts, member); });
 }
 
+sair_status sair_dominance_counts_part(const double* tuples, size_t T, int K, int device, int part,
+                                       int nparts, uint32_t* counts, uint8_t* member) {
+    if (T && !tuples) return bad("null input");
+    return guard([&] { sair::dominance_counts(tuples, T, K, device, counts, member, part, nparts); });
+}
+
 // ---------------------------------------------------------------- reward --
 
 sair_status sair_action_magnitude(const int32_t* deltas, size_t stages, double* out) {

@@ -173,7 +173,7 @@ void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
 void frontier_score_batch_device(sair_frontier_s* f, const double* dpts, size_t T, double* dout,
                                  uint8_t* ddom, cudaStream_t st);
 void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_t* counts,
-                      uint8_t* member);
+                      uint8_t* member, int part = 0, int nparts = 1);
 void compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas, size_t S, size_t T,
                           sair_frontier_s* f, const sair_reward_config* cfg,
                           sair_reward_breakdown* out);

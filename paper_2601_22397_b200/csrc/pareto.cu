@@ -17,6 +17,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "internal.hpp"
@@ -371,12 +372,12 @@ __global__ void pack_sorted_kernel(const uint32_t* __restrict__ ranks, const uin
 template <int K>
 __global__ void __launch_bounds__(256)
     dominance_kernel(const uint32_t* __restrict__ sr, const uint32_t* __restrict__ ssum,
-                     const uint32_t* __restrict__ perm, size_t T, int members_only,
+                     const uint32_t* __restrict__ perm, size_t T, size_t i_begin, int members_only,
                      uint32_t* __restrict__ counts, uint8_t* __restrict__ member) {
     constexpr int TILE = 256;
     __shared__ uint32_t tj[TILE * K];
     __shared__ uint32_t tp[TILE];
-    const size_t i0 = (size_t)blockIdx.x * TILE;
+    const size_t i0 = i_begin + (size_t)blockIdx.x * TILE;
     const size_t i = i0 + threadIdx.x;
     const bool valid = i < T;
     uint32_t ri[K];
@@ -701,8 +702,10 @@ void frontier_score_batch_device(sair_frontier_s* f, const double* dpts, size_t 
 }
 
 void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_t* counts,
-                      uint8_t* member) {
+                      uint8_t* member, int part, int nparts) {
     if (T == 0) return;
+    if (nparts < 1 || part < 0 || part >= nparts)
+        throw Error(SAIR_EINVAL, "dominance: part must be in [0, nparts)");
     if (K < 1 || K > 8) throw Error(SAIR_EINVAL, "dominance: K must be in 1..8");
     if (T >= 0xFFFFFFF0ull) throw Error(SAIR_EINVAL, "dominance: too many tuples");
     int ndev = 0;
@@ -761,9 +764,24 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
         pack_sorted_kernel<<<gr, 256, 0, st>>>(ranks, perm, T, K, sranks);
     }
     const int members_only = counts == nullptr;
-    const int blocks = (int)((T + 255) / 256);
-    switch (K) {
-#define DK(KK) case KK: dominance_kernel<KK><<<blocks, 256, 0, st>>>(sranks, ssum, perm, T, members_only, dcnt, dmem); break;
+    // Part p of n: the sorted positions [T sqrt(p/n), T sqrt((p+1)/n)) in whole
+    // tiles.  Tile i scans ~i earlier tuples (sorted by rank sum), so the
+    // pairwise work up to position x grows as x^2 and these parts carry equal
+    // shares of it.  Tuples outside the part get count 0 / member 0, so the
+    // parts of all n ranks combine by a sum.
+    const size_t tiles = (T + 255) / 256;
+    auto bound = [&](int q) {
+        return std::min(tiles, (size_t)std::ceil((double)tiles * std::sqrt((double)q / nparts)));
+    };
+    const size_t t_lo = nparts == 1 ? 0 : bound(part), t_hi = nparts == 1 ? tiles : bound(part + 1);
+    if (nparts > 1) {
+        SAIR_CUDA(cudaMemsetAsync(dcnt, 0, T * 4, st));
+        SAIR_CUDA(cudaMemsetAsync(dmem, 0, T, st));
+    }
+    const int blocks = (int)(t_hi - t_lo);
+    const size_t i_begin = t_lo * 256;
+    if (blocks > 0) switch (K) {
+#define DK(KK) case KK: dominance_kernel<KK><<<blocks, 256, 0, st>>>(sranks, ssum, perm, T, i_begin, members_only, dcnt, dmem); break;
         DK(1) DK(2) DK(3) DK(4) DK(5) DK(6) DK(7) DK(8)
 #undef DK
     }

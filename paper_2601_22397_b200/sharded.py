@@ -20,6 +20,14 @@ exchanges, each deterministic (rank order):
 lambda_div > 0 (the greedy with diversity penalties) needs every shard's
 candidate pool and the pool vectors on one device; it is not sharded yet
 (DESIGN.md "Multi-GPU").
+
+Pareto: outcome tuples are sharded the same way.  The
+frontier of a union is the frontier of the union of the shards' frontiers, so
+each rank reduces its tuples to a local frontier on its device (K6), the
+local frontiers are all-gathered (a few hundred points) and every rank inserts
+them, in rank order, into its copy of the global frontier; scoring is then
+rank-local.  Dominance counts need every pair: the tuples are all-gathered and
+each rank computes an equal-work part of the pairwise counts; the parts sum.
 """
 from __future__ import annotations
 
@@ -29,7 +37,7 @@ from typing import List, Tuple
 import numpy as np
 
 from . import SelectionConfig, _check, _dp, _f64, lib
-from . import ExperienceBuffer
+from . import ExperienceBuffer, ParetoFrontier, dominance_counts
 
 
 def shard_range(n_total: int, rank: int, world: int) -> Tuple[int, int]:
@@ -181,3 +189,70 @@ def merge_parts(parts: List[np.ndarray], nq: int, m: int, device: int):
         m, device, oi.ctypes.data_as(C.POINTER(C.c_int64)), _dp(osim), _dp(osc),
         ocnt.ctypes.data_as(C.POINTER(C.c_size_t))))
     return oi, osim, osc, ocnt.astype(np.int64)
+
+
+# ------------------------------------------------------------------ pareto --
+
+def all_gather_rows(dist, arr: np.ndarray, device) -> List[np.ndarray]:
+    """All-gather of row blocks whose row count differs per rank (rank order)."""
+    import torch
+    arr = np.ascontiguousarray(arr, dtype=np.float64)
+    width = arr.shape[1]
+    sizes = _all_gather(dist, np.array([arr.shape[0]], np.int64), device)
+    mx = max(int(x[0]) for x in sizes)
+    pad = np.zeros((max(mx, 1), width))
+    pad[:arr.shape[0]] = arr
+    parts = _all_gather(dist, pad, device)
+    return [p[:int(n[0])] for p, n in zip(parts, sizes)]
+
+
+def combine_parts(dist, counts: np.ndarray, member: np.ndarray, device):
+    """Sum of the ranks' partial dominance counts / memberships."""
+    parts = _all_gather(dist, np.concatenate([counts.astype(np.float64),
+                                              member.astype(np.float64)]), device)
+    tot = np.sum(parts, axis=0)
+    T = len(counts)
+    return tot[:T].astype(np.uint32), tot[T:] > 0
+
+
+class ShardedParetoFrontier:
+    """ParetoFrontier (pareto.hpp:24-70) over outcome tuples sharded by rank."""
+
+    def __init__(self, dist, device: int, latency_max_ms: float = 1.0, cost_max: float = 1.0):
+        self.dist = dist
+        self.device = device
+        self.bounds = (latency_max_ms, cost_max)
+        self.front = ParetoFrontier(latency_max_ms, cost_max, device=device)
+
+    def insert_batch(self, local_pts) -> int:
+        """Sequential insert_normalized() of every rank's tuples (in any order:
+        the result is the non-dominated set of the distinct points)."""
+        local = ParetoFrontier(*self.bounds, device=self.device)
+        local.insert_batch(_f64(local_pts).reshape(-1, 2))
+        fl, fc = local.points_array()
+        parts = all_gather_rows(self.dist, np.stack([fl, fc], axis=1).reshape(-1, 2),
+                                f"cuda:{self.device}")
+        return self.front.insert_batch(np.concatenate(parts) if parts else np.zeros((0, 2)))
+
+    def score_batch(self, local_pts):
+        """reward() of this rank's tuples against the global frontier."""
+        return self.front.score_batch(local_pts)
+
+    def points_array(self):
+        return self.front.points_array()
+
+    def hypervolume(self) -> float:
+        return self.front.hypervolume()
+
+
+def sharded_dominance_counts(dist, local_tuples, device: int):
+    """Dominance counts of this rank's tuples against the whole sharded set:
+    (counts, member) for the local rows, and the global frontier size."""
+    t = _f64(local_tuples)
+    parts = all_gather_rows(dist, t, f"cuda:{device}")
+    allt = np.concatenate(parts)
+    cnt, mem = dominance_counts(allt, device=device, part=dist.get_rank(),
+                                nparts=dist.get_world_size())
+    cnt, mem = combine_parts(dist, cnt, mem, f"cuda:{device}")
+    lo = sum(len(p) for p in parts[:dist.get_rank()])
+    return cnt[lo:lo + len(t)], mem[lo:lo + len(t)], int(mem.sum())

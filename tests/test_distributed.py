@@ -160,3 +160,96 @@ def test_sharded_select_on_device_matches_single_store(nq):
     assert np.array_equal(cnt, n1)
     assert np.array_equal(idx, i1)
     assert np.array_equal(sc, c1) and np.array_equal(sim, s1)
+
+
+# ------------------------------------------------------------------ pareto --
+
+T_P, K_P = 6000, 3
+
+
+def _pareto_cpu_worker(rank, world, port, q):
+    from oracle.oracle import COracle
+    from paper_2601_22397_b200.sharded import all_gather_rows, combine_parts
+    _init(rank, world, port)
+    orc = COracle()
+    lo, hi = shard_range(T_P, rank, world)
+    pts = synth.tuples(SEED, T_P, 2, "grid")[lo:hi]
+    # each rank's device frontier (K6) is restated by the oracle
+    fl, fc, _ = orc.frontier_from_points(pts)
+    parts = all_gather_rows(dist, np.stack([fl, fc], axis=1), "cpu")
+    gl, gc, _ = orc.frontier_from_points(np.concatenate(parts))
+    # dominance counts: all-gather, this rank's part (a stripe here), sum
+    tk = synth.tuples(SEED + 1, T_P, K_P, "grid")[lo:hi]
+    allt = np.concatenate(all_gather_rows(dist, tk, "cpu"))
+    cnt, mem = orc.dominance_counts(allt)
+    mine = np.arange(len(allt)) % world == rank
+    cnt, mem = combine_parts(dist, np.where(mine, cnt, 0), np.where(mine, mem, False), "cpu")
+    if rank == 0:
+        q.put((gl, gc, cnt, mem))
+    dist.destroy_process_group()
+
+
+def test_sharded_pareto_protocol_cpu(orc):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pareto_cpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    gl, gc, cnt, mem = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    fl, fc, _ = orc.frontier_from_points(synth.tuples(SEED, T_P, 2, "grid"))
+    assert np.array_equal(gl, fl) and np.array_equal(gc, fc)
+    c1, m1 = orc.dominance_counts(synth.tuples(SEED + 1, T_P, K_P, "grid"))
+    assert np.array_equal(cnt, c1) and np.array_equal(mem, m1)
+
+
+def _pareto_gpu_worker(rank, world, port, q):
+    from paper_2601_22397_b200.sharded import ShardedParetoFrontier, sharded_dominance_counts
+    _init(rank, world, port)
+    T = 200000
+    lo, hi = shard_range(T, rank, world)
+    pts = synth.tuples(SEED, T, 2, "grid")[lo:hi]
+    f = ShardedParetoFrontier(dist, 0, 1.0, 1.0)
+    f.insert_batch(pts)
+    probe = synth.tuples(SEED + 2, 5000, 2, "uniform")
+    rw, dom = f.score_batch(probe)
+    tk = synth.tuples(SEED + 1, 100000, 4, "grid")
+    klo, khi = shard_range(len(tk), rank, world)
+    cnt, mem, nf = sharded_dominance_counts(dist, tk[klo:khi], 0)
+    parts = [None] * world
+    dist.all_gather_object(parts, (cnt, mem))
+    if rank == 0:
+        l, c = f.points_array()
+        q.put((l, c, rw, dom, np.concatenate([p[0] for p in parts]),
+               np.concatenate([p[1] for p in parts]), nf))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_pareto_on_device_matches_single():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2601_22397_b200 as sair
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pareto_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    l, c, rw, dom, cnt, mem, nf = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    one = sair.ParetoFrontier(1.0, 1.0)
+    one.insert_batch(synth.tuples(SEED, 200000, 2, "grid"))
+    l1, c1 = one.points_array()
+    assert np.array_equal(l, l1) and np.array_equal(c, c1)
+    r1, d1 = one.score_batch(synth.tuples(SEED + 2, 5000, 2, "uniform"))
+    assert np.array_equal(rw, r1) and np.array_equal(dom, d1)
+    cf, mf = sair.dominance_counts(synth.tuples(SEED + 1, 100000, 4, "grid"))
+    assert np.array_equal(cnt, cf) and np.array_equal(mem, mf) and nf == int(mf.sum())
