@@ -79,6 +79,7 @@ typedef struct {
     float total_ms;         /* device time of the whole call */
     float prepass_ms;       /* device time of the threshold sample pre-pass (tensor-core path) */
     int tensor_core;        /* 1: tcgen05 8-query stream pass; 2: tcgen05 wide (32-128 query) pass */
+    int small;              /* 1: the whole call ran as the one-launch exact small-store select */
 } sair_select_stats;
 
 SAIR_API const char* sair_last_error(void);

@@ -33,7 +33,7 @@ class SelectStatsC(C.Structure):
     _fields_ = [("queries", C.c_size_t), ("certified", C.c_size_t),
                 ("exact_fallbacks", C.c_size_t), ("candidates", C.c_size_t), ("qb", C.c_int),
                 ("stream_launches", C.c_int), ("stream_ms", C.c_float), ("total_ms", C.c_float),
-                ("prepass_ms", C.c_float), ("tensor_core", C.c_int)]
+                ("prepass_ms", C.c_float), ("tensor_core", C.c_int), ("small", C.c_int)]
 
 
 class RewardConfigC(C.Structure):

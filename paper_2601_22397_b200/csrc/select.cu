@@ -928,6 +928,27 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     std::vector<int> done(nq, 0);
     if (s->sharded && cfg.locally_weighted_mean)
         throw Error(SAIR_EINVAL, "locally_weighted_mean is not supported on a sharded store");
+    // Small stores (<= 64k records): the whole exact select in one clustered
+    // launch (select_small.cu) when the filter cannot pay off -- lambda > 0
+    // (the greedy's diversity penalties defeat a fixed candidate pool), the
+    // exact mode, or a store small enough that one exact pass is the cheaper
+    // launch sequence.
+    const bool small_ok = !cfg.locally_weighted_mean && small_select_fits(s, m) &&
+                          std::getenv("SAIR_NO_SMALL") == nullptr;
+    if (small_ok && (cfg.lambda_div != 0.0 || cfg.mode == SAIR_SELECT_EXACT || n <= SMALL_DIRECT_N)) {
+        std::vector<size_t> all(nq);
+        for (size_t i = 0; i < nq; ++i) all[i] = i;
+        small_select(s, p, all, m, cfg.lambda_div, out_nn != nullptr, out_idx, out_sim, out_score,
+                     out_count, out_nn, out_nn_sim, out_reward, out_round);
+        s->last.exact_fallbacks = 0;
+        s->last.small = 1;
+        SAIR_CUDA(cudaEventRecord(s->ev[3], s->st));
+        SAIR_CUDA(cudaEventSynchronize(s->ev[3]));
+        float tot = 0.f;
+        cudaEventElapsedTime(&tot, s->ev[0], s->ev[3]);
+        s->last.total_ms = tot;
+        return;
+    }
     const bool fast = cfg.mode != SAIR_SELECT_EXACT && !cfg.locally_weighted_mean && d <= 128 &&
                       n < (size_t)1 << 31 && m <= 256;
     float stream_ms = 0.f, prepass_ms = 0.f;
@@ -1153,6 +1174,15 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                 s->last.certified++;
             }
         }
+    }
+    if (small_ok) {  // the uncertified queries of a small store: one clustered launch
+        std::vector<size_t> rest;
+        for (size_t i = 0; i < nq; ++i)
+            if (!done[i]) rest.push_back(i);
+        small_select(s, p, rest, m, cfg.lambda_div, out_nn != nullptr, out_idx, out_sim,
+                     out_score, out_count, out_nn, out_nn_sim, out_reward, out_round);
+        s->last.exact_fallbacks += rest.size();
+        for (size_t i : rest) done[i] = 1;
     }
     for (size_t i = 0; i < nq; ++i) {
         if (done[i]) continue;

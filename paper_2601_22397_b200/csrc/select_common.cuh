@@ -94,6 +94,15 @@ double wide_bq_rel();  // relative error bound of the wide pass's query operand
 bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                     WidePlan* pl);
 
+// select_small.cu: exact select() of small stores (<= 64k records), one
+// clustered launch for all given queries
+constexpr size_t SMALL_DIRECT_N = 4096;  // lambda == 0: below this, skip the filter
+bool small_select_fits(const sair_store_s* s, size_t m);
+void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>& qidx, size_t m,
+                  double lambda, bool want_nn, int64_t* out_idx, double* out_sim,
+                  double* out_score, size_t* out_count, int64_t* out_nn, double* out_nn_sim,
+                  double* out_reward, int32_t* out_round);
+
 // select_exact.cu: one query through the full fp64 pass.
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,
