@@ -124,6 +124,25 @@ SAIR_API sair_status sair_store_get(sair_store_t h, size_t index, double* ctx, d
                                     int32_t* round);
 
 /* ExperienceBuffer::standardize, experience.cpp:155-169 (fp64, host-kept sums). */
+/* Bulk device->host copy of records [offset, offset + count) (each pointer
+ * nullable): ctx [count][dim], reward [count], round [count]. */
+SAIR_API sair_status sair_store_export(sair_store_t h, size_t offset, size_t count, double* ctx,
+                                       double* reward, int32_t* round);
+
+/* ExperienceBuffer::load(path, r_min, corrupt_lines) (experience.hpp:76-77,
+ * experience.cpp:243-271) into a new device store: the JSONL lines are parsed
+ * on `nthreads` host threads (0 = all) with the reference's parser and
+ * store()'s semantics are applied in line order (gate, dimension fixed by the
+ * first accepted row -- a change is SAIR_EINVAL), then one bulk append.
+ * SAIR_EIO when the file cannot be read. */
+SAIR_API sair_status sair_store_load_jsonl(const char* path, double r_min, int device, int nthreads,
+                                           size_t* corrupt_lines, sair_store_t* out);
+/* ExperienceBuffer::persist(path) (experience.cpp:232-241) from the device
+ * store (one bulk export); the device store holds no source / action, so
+ * those are written empty ("" and []) -- a host mirror with them persists
+ * itself (the C++ drop-in, the Python wrapper with keep_mirror). */
+SAIR_API sair_status sair_store_persist_jsonl(sair_store_t h, const char* path);
+
 SAIR_API sair_status sair_store_standardize(sair_store_t h, const double* x, int dim, double* z);
 
 /* ExperienceBuffer::effective_sigma, experience.cpp:207-212, including the

@@ -300,6 +300,10 @@ class Ref:
         L.ref_compute_reward.argtypes = [_dp, _i32p, _sz, C.c_void_p, _dp, _dp]
         L.ref_action_magnitude.argtypes = [_i32p, _sz]
         L.ref_action_magnitude.restype = C.c_double
+        L.ref_buffer_load.argtypes = [C.c_char_p, C.c_double, _szp]
+        L.ref_buffer_load.restype = C.c_void_p
+        L.ref_buffer_persist.argtypes = [C.c_void_p, C.c_char_p]
+        L.ref_buffer_get.argtypes = [C.c_void_p, _sz, _dp, _dp, C.POINTER(C.c_int)]
 
     def _chk(self, rc):
         if rc:
@@ -336,6 +340,27 @@ class RefBuffer:
 
     def size(self):
         return self.L.ref_buffer_size(self.h)
+
+    @classmethod
+    def load(cls, ref: "Ref", path, r_min=0.0):
+        """ExperienceBuffer::load (experience.cpp:243-271): (buffer, corrupt)."""
+        bad = C.c_size_t()
+        h = ref.lib.ref_buffer_load(str(path).encode(), r_min, C.byref(bad))
+        if not h:
+            raise ValueError(ref.lib.ref_last_error().decode())
+        o = cls.__new__(cls)
+        o.ref, o.L, o.h = ref, ref.lib, h
+        return o, bad.value
+
+    def persist(self, path):
+        self.ref._chk(self.L.ref_buffer_persist(self.h, str(path).encode()))
+
+    def get(self, i, d):
+        ctx = np.zeros(d)
+        r = C.c_double()
+        rd = C.c_int()
+        self.ref._chk(self.L.ref_buffer_get(self.h, i, _p(ctx, _dp), C.byref(r), C.byref(rd)))
+        return ctx, r.value, rd.value
 
     def rejected(self):
         return self.L.ref_buffer_rejected(self.h)

@@ -89,6 +89,27 @@ REF_API int ref_buffer_store_many(void* h, const double* ctx, std::size_t n, int
     });
 }
 
+// persistence (experience.cpp:232-271), for the persistence parity tests
+REF_API void* ref_buffer_load(const char* path, double r_min, std::size_t* corrupt) {
+    try {
+        return new ExperienceBuffer(ExperienceBuffer::load(path, r_min, corrupt));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+REF_API int ref_buffer_persist(void* h, const char* path) {
+    return guard([&] { static_cast<ExperienceBuffer*>(h)->persist(path); });
+}
+REF_API int ref_buffer_get(void* h, std::size_t i, double* ctx, double* reward, int* round) {
+    return guard([&] {
+        const Experience& e = static_cast<ExperienceBuffer*>(h)->all().at(i);
+        std::copy(e.context.begin(), e.context.end(), ctx);
+        *reward = e.reward;
+        *round = e.round;
+    });
+}
+
 REF_API std::size_t ref_buffer_size(void* h) { return static_cast<ExperienceBuffer*>(h)->size(); }
 REF_API uint64_t ref_buffer_rejected(void* h) {
     return static_cast<ExperienceBuffer*>(h)->rejected();

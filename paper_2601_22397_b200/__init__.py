@@ -172,6 +172,38 @@ class ExperienceBuffer:
 
     __copy__ = copy
 
+    @classmethod
+    def load(cls, path: str, r_min: float = 0.0, device: int = 0, nthreads: int = 0):
+        """ExperienceBuffer::load (experience.cpp:243-271) into the device store:
+        returns (buffer, corrupt_lines).  Parsed on all host threads, one bulk
+        append; no host mirror (use get(i) / export())."""
+        h = C.c_void_p()
+        bad = C.c_size_t()
+        _check(lib().sair_store_load_jsonl(str(path).encode(), r_min, device, nthreads,
+                                           C.byref(bad), C.byref(h)))
+        o = cls.__new__(cls)
+        o._h = h
+        o._items = []
+        o._mirror = False
+        return o, bad.value
+
+    def persist(self, path: str):
+        """ExperienceBuffer::persist (experience.cpp:232-241) from the device store
+        (source / action are not held on the device and are written empty)."""
+        _check(lib().sair_store_persist_jsonl(self._h, str(path).encode()))
+
+    def export(self, offset: int = 0, count: Optional[int] = None):
+        """Bulk copy of records [offset, offset + count): (contexts, rewards, rounds)."""
+        n = self.size()
+        count = n - offset if count is None else count
+        d = max(self.dim(), 1)
+        ctx = np.zeros((count, d))
+        rw = np.zeros(count)
+        rd = np.zeros(count, np.int32)
+        _check(lib().sair_store_export(self._h, offset, count, _dp(ctx), _dp(rw),
+                                       rd.ctypes.data_as(C.POINTER(C.c_int32))))
+        return ctx, rw, rd
+
     def store(self, e: Experience) -> bool:
         """experience.cpp:135-153: False (and counted) when reward <= r_min."""
         x = _f64(e.context)

@@ -80,6 +80,10 @@ SIGNATURES = {
     "sair_store_select": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, C.POINTER(SelectConfigC),
                                     _i64p, _dp, _dp, _szp, _i64p, _dp]),
     "sair_store_nearest": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, C.c_double, _i64p, _dp]),
+    "sair_store_export": (C.c_int, [_vp, C.c_size_t, C.c_size_t, _dp, _dp, C.POINTER(C.c_int32)]),
+    "sair_store_load_jsonl": (C.c_int, [C.c_char_p, C.c_double, C.c_int, C.c_int,
+                                        C.POINTER(C.c_size_t), C.POINTER(_vp)]),
+    "sair_store_persist_jsonl": (C.c_int, [_vp, C.c_char_p]),
     "sair_store_last_stats": (C.c_int, [_vp, C.POINTER(SelectStatsC)]),
     "sair_store_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "sair_store_set_shard": (C.c_int, [_vp, C.c_int64]),

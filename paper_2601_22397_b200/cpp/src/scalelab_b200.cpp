@@ -204,6 +204,7 @@ ExperienceBuffer ExperienceBuffer::load(const std::string& path, double r_min,
     ExperienceBuffer buf(r_min);
     std::size_t bad = 0;
     std::string line;
+    std::vector<Experience> rows;
     while (std::getline(in, line)) {
         if (line.empty()) continue;
         try {
@@ -221,10 +222,38 @@ ExperienceBuffer ExperienceBuffer::load(const std::string& path, double r_min,
                 d.rate_ratio_tenths = s.at("rate_ratio_tenths").get<int>();
                 e.action.stages.push_back(d);
             }
-            buf.store(std::move(e));
+            rows.push_back(std::move(e));
         } catch (const nlohmann::json::exception&) {
             ++bad;
         }
+    }
+    // store() of every parsed row in line order as ONE device append: the gate
+    // and the dimension rule are applied here first (a change throws, as the
+    // reference's store() inside load() does), rejected rows keep their place
+    int dim = -1;
+    for (const auto& e : rows) {
+        if (!(e.reward > r_min)) continue;
+        if (dim < 0) dim = static_cast<int>(e.context.size());
+        else if (static_cast<int>(e.context.size()) != dim)
+            throw std::invalid_argument("experience store: context dimension changed");
+    }
+    if (!rows.empty() && dim != 0) {
+        const int d = dim > 0 ? dim : 1;
+        std::vector<double> ctx(rows.size() * static_cast<std::size_t>(d), 0.0), rew(rows.size());
+        std::vector<int32_t> rnd(rows.size());
+        std::vector<uint8_t> acc(rows.size(), 0);
+        for (std::size_t i = 0; i < rows.size(); ++i) {
+            rew[i] = rows[i].reward;
+            rnd[i] = rows[i].round;
+            if (rows[i].reward > r_min)
+                std::copy(rows[i].context.begin(), rows[i].context.end(), ctx.begin() + i * d);
+        }
+        check(sair_store_append(buf.h_, ctx.data(), rows.size(), d, rew.data(), rnd.data(),
+                                acc.data(), nullptr));
+        for (std::size_t i = 0; i < rows.size(); ++i)
+            if (acc[i]) buf.items_.push_back(std::move(rows[i]));
+    } else {
+        for (auto& e : rows) buf.store(std::move(e));  // empty contexts: one at a time
     }
     if (corrupt_lines) *corrupt_lines = bad;
     return buf;

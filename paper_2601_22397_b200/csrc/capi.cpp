@@ -43,6 +43,10 @@ sair_select_config defaults(const sair_select_config* c) {
 extern "C" {
 
 const char* sair_last_error(void) { return g_err.c_str(); }
+sair_status sair_internal_fail(sair_status code, const char* msg) {  // hidden: persist.cpp
+    g_err = msg;
+    return code;
+}
 int sair_version(void) { return 1; }
 
 sair_status sair_device_count(int* out) {
@@ -143,6 +147,27 @@ sair_status sair_store_get(sair_store_t h, size_t index, double* ctx, double* re
             SAIR_CUDA(cudaMemcpyAsync(reward, h->r64 + index, 8, cudaMemcpyDeviceToHost, h->st));
         if (round)
             SAIR_CUDA(cudaMemcpyAsync(round, h->rnd + index, 4, cudaMemcpyDeviceToHost, h->st));
+        SAIR_CUDA(cudaStreamSynchronize(h->st));
+    });
+}
+
+sair_status sair_store_export(sair_store_t h, size_t offset, size_t count, double* ctx,
+                              double* reward, int32_t* round) {
+    if (!h) return bad("null handle");
+    return guard([&] {
+        if (offset > h->n || count > h->n - offset)
+            throw sair::Error(SAIR_ERANGE, "export range outside the store");
+        if (count == 0) return;
+        sair::DeviceGuard g(h->device);
+        if (ctx)
+            SAIR_CUDA(cudaMemcpyAsync(ctx, h->x64 + offset * h->d, count * h->d * 8,
+                                      cudaMemcpyDeviceToHost, h->st));
+        if (reward)
+            SAIR_CUDA(cudaMemcpyAsync(reward, h->r64 + offset, count * 8, cudaMemcpyDeviceToHost,
+                                      h->st));
+        if (round)
+            SAIR_CUDA(cudaMemcpyAsync(round, h->rnd + offset, count * 4, cudaMemcpyDeviceToHost,
+                                      h->st));
         SAIR_CUDA(cudaStreamSynchronize(h->st));
     });
 }

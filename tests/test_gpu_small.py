@@ -30,7 +30,7 @@ class env:
 
 
 @pytest.mark.parametrize("n,d,m,lam", [(60000, 23, 8, 0.1), (60000, 23, 32, 0.5), (20000, 64, 15, 0.1),
-                                       (9000, 32, 8, 0.0), (1500, 5, 40, 0.1)])
+                                       (3000, 32, 8, 0.0), (1500, 5, 40, 0.1)])
 def test_small_equals_multi_launch_exact(n, d, m, lam):
     db = ExperienceBuffer(0.0)
     db.store_synthetic(n + d, n, d, clustered=True)
