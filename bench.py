@@ -355,6 +355,21 @@ def bench_pareto(dev):
                 "frontier_insert_tuples_per_s": round(PARETO_T / ins_s, 1),
                 "frontier_insert_s_e2e": round(ins_s, 4),
                 "score_hbm_gbs": round(PARETO_T * (16 + 8 + 1) / (sc_ms / 1e3) / 1e9, 1)})
+    # prefix-sequential replay: 4M rounds, 85 % updating
+    rng = np.random.default_rng(SEED)
+    T = PARETO_T
+    inputs = np.stack([rng.uniform(100, 2500, T), rng.uniform(50, 2600, T),
+                       rng.uniform(0.5, 10, T), rng.uniform(0.5, 11, T)], 1)
+    deltas = np.zeros((T, 3, 4), np.int32)
+    upd = (rng.uniform(size=T) < 0.85).astype(np.uint8)
+    fr = sair.ParetoFrontier(2000.0, 10.0, device=dev)
+    sair.compute_reward_replay(inputs[:4096], deltas[:4096], upd[:4096], fr, sair.RewardConfig())
+    fr = sair.ParetoFrontier(2000.0, 10.0, device=dev)
+    t0 = time.perf_counter()
+    sair.compute_reward_replay(inputs, deltas, upd, fr, sair.RewardConfig())
+    dt = time.perf_counter() - t0
+    res["replay"] = {"rounds": T, "s_e2e": round(dt, 4), "rounds_per_s": round(T / dt, 1),
+                     "final_frontier": fr.size()}
     for K in (2, 3, 4):
         T = 262144
         t = synth.tuples(SEED + K, T, K, "uniform")

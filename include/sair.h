@@ -331,6 +331,18 @@ SAIR_API sair_status sair_compute_reward_batch(const sair_reward_inputs* in,
                                                sair_frontier_t f, const sair_reward_config* cfg,
                                                sair_reward_breakdown* out);
 
+/* Prefix-sequential replay (scalelab_cli.cpp:118-147
+ * cmd_replay, harness.cpp:250-251): row t's compute_reward is scored against
+ * the frontier `f` as updated by the rows s < t with update[s] != 0, and then
+ * f.update(l_after_t, c_after_t) when update[t] != 0 -- the sequential loop's
+ * results, computed by parallel replayers from prefix frontiers.  On return f
+ * holds the final frontier. */
+SAIR_API sair_status sair_compute_reward_replay(const sair_reward_inputs* in,
+                                                const int32_t* deltas, size_t stages, size_t T,
+                                                const uint8_t* update, sair_frontier_t f,
+                                                const sair_reward_config* cfg,
+                                                sair_reward_breakdown* out);
+
 #ifdef __cplusplus
 }
 #endif

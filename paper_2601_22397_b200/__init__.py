@@ -30,6 +30,7 @@ __all__ = [
     "StageDelta", "ParetoFrontier", "ObjectivePoint", "dominates", "RewardConfig",
     "RewardInputs", "RewardBreakdown", "compute_reward", "compute_reward_batch",
     "action_magnitude", "context_features", "dominance_counts", "SairError", "InvalidArgument",
+    "compute_reward_replay",
     "LogicError", "OutOfRange", "SELECT_AUTO", "SELECT_EXACT",
 ]
 
@@ -609,5 +610,25 @@ def compute_reward_batch(inputs, deltas, frontier: ParetoFrontier, cfg: RewardCo
     _check(lib().sair_compute_reward_batch(
         x.ctypes.data_as(C.POINTER(_lib.RewardInputsC)), d.ctypes.data_as(C.POINTER(C.c_int32)),
         S, T, frontier._h, C.byref(c), out))
+    return np.array([[o.latency, o.cost, o.sla, o.proactive, o.pareto, o.total, o.clipped]
+                     for o in out[:T]], dtype=np.float64).reshape(T, 7)
+
+
+def compute_reward_replay(inputs, deltas, update, frontier: ParetoFrontier, cfg: RewardConfig):
+    """The replay loop (scalelab_cli.cpp:118-147, harness.cpp:250-251) in one
+    call: row t's compute_reward against the frontier as updated by the earlier
+    rows with update[s], then frontier.update(l_after_t, c_after_t) if
+    update[t].  Returns T x 7 (latency, cost, sla, proactive, pareto, total,
+    clipped); `frontier` ends in the final state."""
+    x = _f64(inputs).reshape(-1, 4)
+    T = len(x)
+    d = np.ascontiguousarray(deltas, dtype=np.int32).reshape(T, -1, 4)
+    S = d.shape[1]
+    u = np.ascontiguousarray(update, dtype=np.uint8).reshape(T)
+    out = (_lib.RewardBreakdownC * max(T, 1))()
+    c = cfg._c()
+    _check(lib().sair_compute_reward_replay(
+        x.ctypes.data_as(C.POINTER(_lib.RewardInputsC)), d.ctypes.data_as(C.POINTER(C.c_int32)),
+        S, T, u.ctypes.data_as(C.POINTER(C.c_uint8)), frontier._h, C.byref(c), out))
     return np.array([[o.latency, o.cost, o.sla, o.proactive, o.pareto, o.total, o.clipped]
                      for o in out[:T]], dtype=np.float64).reshape(T, 7)

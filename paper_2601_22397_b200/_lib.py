@@ -128,6 +128,10 @@ SIGNATURES = {
     "sair_compute_reward_batch": (C.c_int, [C.POINTER(RewardInputsC), _i32p, C.c_size_t,
                                             C.c_size_t, _vp, C.POINTER(RewardConfigC),
                                             C.POINTER(RewardBreakdownC)]),
+    "sair_compute_reward_replay": (C.c_int, [C.POINTER(RewardInputsC), _i32p, C.c_size_t,
+                                             C.c_size_t, C.POINTER(C.c_uint8), _vp,
+                                             C.POINTER(RewardConfigC),
+                                             C.POINTER(RewardBreakdownC)]),
 }
 
 

@@ -542,4 +542,13 @@ sair_status sair_compute_reward_batch(const sair_reward_inputs* in, const int32_
     return guard([&] { sair::compute_reward_batch(in, deltas, stages, T, f, cfg, out); });
 }
 
+sair_status sair_compute_reward_replay(const sair_reward_inputs* in, const int32_t* deltas,
+                                       size_t stages, size_t T, const uint8_t* update,
+                                       sair_frontier_t f, const sair_reward_config* cfg,
+                                       sair_reward_breakdown* out) {
+    if (!f || !cfg || (T && (!in || !out || !update)) || (T && stages && !deltas))
+        return bad("null input");
+    return guard([&] { sair::compute_reward_replay(in, deltas, stages, T, update, f, cfg, out); });
+}
+
 }  // extern "C"

@@ -177,6 +177,9 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
 void compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas, size_t S, size_t T,
                           sair_frontier_s* f, const sair_reward_config* cfg,
                           sair_reward_breakdown* out);
+void compute_reward_replay(const sair_reward_inputs* in, const int32_t* deltas, size_t S,
+                           size_t T, const uint8_t* update, sair_frontier_s* f,
+                           const sair_reward_config* cfg, sair_reward_breakdown* out);
 double action_magnitude(const int32_t* deltas, size_t S, int device);
 double similarity(const double* a, const double* b, int d, double sigma, int device);
 

@@ -482,6 +482,180 @@ __global__ void reward_kernel(const double* __restrict__ in, const int32_t* __re
     }
 }
 
+// ---- prefix-sequential replay ----------------------
+//
+// Round t's reward is scored against the frontier of the rows s < t flagged
+// for update (scalelab_cli.cpp:118-147 cmd_replay; harness.cpp:250-251), then
+// row t is inserted when flagged.  The rounds are cut into R blocks, one
+// replayer thread each:
+//   replay_local_kernel   block b's own frontier L_b (its flagged rows only);
+//   replay_prefix_kernel  G_0 = the frontier before the replay, G_{b+1} =
+//                         G_b (+) L_b -- the frontier of a union is the
+//                         frontier of the union of frontiers, and the batch
+//                         result is order-independent -- stored as the start
+//                         state S_b of every block;
+//   replay_block_kernel   replayer b walks its rounds from S_b exactly as the
+//                         sequential loop does: the five-term reward against
+//                         the current frontier, then insert_normalized.
+// Frontiers live in per-replayer global scratch of `cap` points; a replayer
+// that would exceed it raises a flag and the host re-runs with one replayer.
+
+// insert_normalized, pareto.cpp:43-54, on a sorted array (sequential)
+__device__ bool fr_insert(double* l, double* c, size_t& F, size_t cap, double pl, double pc,
+                          int* overflow) {
+    size_t u = 0, hi = F;  // upper_bound(pl)
+    while (u < hi) {
+        const size_t mid = (u + hi) >> 1;
+        if (l[mid] > pl) hi = mid; else u = mid + 1;
+    }
+    if (u > 0 && (dom2(l[u - 1], c[u - 1], pl, pc) || (l[u - 1] == pl && c[u - 1] == pc)))
+        return false;  // equal to or dominated by a member
+    size_t a = u;      // members with l == pl sit before u; with c > pc they are dominated
+    while (a > 0 && l[a - 1] == pl) --a;
+    size_t e = a;      // members p dominates: l >= pl and c >= pc, a contiguous run
+    while (e < F && c[e] >= pc) ++e;
+    const size_t nF = F - (e - a) + 1;
+    if (nF > cap) {
+        atomicExch(overflow, 1);
+        return false;
+    }
+    if (e - a != 1) {  // shift the tail [e, F) to a + 1
+        if (e > a + 1) {
+            for (size_t i = e; i < F; ++i) {
+                l[i - (e - a) + 1] = l[i];
+                c[i - (e - a) + 1] = c[i];
+            }
+        } else {
+            for (size_t i = F; i-- > e;) {
+                l[i + 1] = l[i];
+                c[i + 1] = c[i];
+            }
+        }
+    }
+    l[a] = pl;
+    c[a] = pc;
+    F = nF;
+    return true;
+}
+
+__device__ double fr_hv(const double* l, const double* c, size_t F) {  // pareto.cpp:56-65
+    double hv = 0.0;
+    for (size_t i = 0; i < F; ++i) {
+        const double nl = i + 1 < F ? l[i + 1] : 1.0;
+        hv = dadd(hv, dmul(dsub(nl, l[i]), dsub(1.0, c[i])));
+    }
+    return hv;
+}
+
+struct ReplayArgs {
+    const double* in;        // [T][4] l_before, l_after, c_before, c_after
+    const int32_t* deltas;   // [T][S][4]
+    const uint8_t* update;   // [T]
+    size_t T, S, B, R, cap;
+    double l_max, c_max;
+    RewardCfg cfg;
+    double* fl;              // [R][cap] working frontiers
+    double* fc;
+    size_t* fn;              // [R]
+    double* sl;              // [R][cap] block start states
+    double* sc;
+    size_t* sn;              // [R]
+    const double* f0l;       // the frontier before the replay
+    const double* f0c;
+    size_t f0n;
+    double* gl;              // [gcap] running prefix frontier (its final state is the result)
+    double* gc;
+    size_t* gn;
+    size_t gcap;
+    double* out;             // [T][7]
+    int* overflow;
+};
+
+__global__ void replay_local_kernel(const ReplayArgs a) {
+    const size_t b = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (b >= a.R) return;
+    double* l = a.fl + b * a.cap;
+    double* c = a.fc + b * a.cap;
+    size_t F = 0;
+    const size_t t1 = min(a.T, (b + 1) * a.B);
+    for (size_t t = b * a.B; t < t1; ++t) {
+        if (!a.update[t]) continue;
+        double pl, pc;
+        f_normalize(a.l_max, a.c_max, a.in[4 * t + 1], a.in[4 * t + 3], &pl, &pc, nullptr);
+        fr_insert(l, c, F, a.cap, pl, pc, a.overflow);
+    }
+    a.fn[b] = F;
+}
+
+__global__ void replay_prefix_kernel(const ReplayArgs a) {
+    if (threadIdx.x || blockIdx.x) return;
+    size_t G = a.f0n;
+    for (size_t i = 0; i < G; ++i) {
+        a.gl[i] = a.f0l[i];
+        a.gc[i] = a.f0c[i];
+    }
+    for (size_t b = 0; b < a.R; ++b) {
+        if (G > a.cap) {
+            atomicExch(a.overflow, 1);
+            return;
+        }
+        for (size_t i = 0; i < G; ++i) {
+            a.sl[b * a.cap + i] = a.gl[i];
+            a.sc[b * a.cap + i] = a.gc[i];
+        }
+        a.sn[b] = G;
+        for (size_t i = 0; i < a.fn[b]; ++i)
+            fr_insert(a.gl, a.gc, G, a.gcap, a.fl[b * a.cap + i], a.fc[b * a.cap + i], a.overflow);
+    }
+    *a.gn = G;
+}
+
+__global__ void replay_block_kernel(const ReplayArgs a) {
+    const size_t b = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (b >= a.R) return;
+    double* l = a.fl + b * a.cap;
+    double* c = a.fc + b * a.cap;
+    size_t F = a.sn[b];
+    for (size_t i = 0; i < F; ++i) {
+        l[i] = a.sl[b * a.cap + i];
+        c[i] = a.sc[b * a.cap + i];
+    }
+    double hv = fr_hv(l, c, F);
+    const RewardCfg& cfg = a.cfg;
+    const size_t t1 = min(a.T, (b + 1) * a.B);
+    for (size_t t = b * a.B; t < t1; ++t) {
+        // compute_reward, reward.cpp:21-44, against the current frontier
+        const double lb = a.in[4 * t], la = a.in[4 * t + 1], cb = a.in[4 * t + 2],
+                     ca = a.in[4 * t + 3];
+        double latency = ddiv(dmul(cfg.w_l, dsub(lb, la)), cfg.l_base);
+        double cost = ddiv(dmul(-cfg.w_c, dsub(ca, cb)), cfg.c_budget);
+        double sla = 0.0;
+        if (la > cfg.t_sla) {
+            double ratio = ddiv(la, cfg.t_sla);
+            sla = dadd(-dmul(ratio, ratio), 1.0);
+        }
+        double sg = dsub(ddiv(lb, cfg.t_sla), 1.0);
+        if (sg < 0.0) sg = 0.0;
+        double proactive = dmul(dmul(sg, action_mu(a.deltas + t * a.S * 4, a.S)), cfg.w_p);
+        double pl, pc;
+        f_normalize(a.l_max, a.c_max, la, ca, &pl, &pc, nullptr);
+        const FrontierView v{l, c, F, hv};
+        double pareto = f_reward(v, pl, pc, nullptr);
+        double sum = dadd(dadd(dadd(dadd(latency, cost), sla), proactive), pareto);
+        double total = sum < -cfg.r_max ? -cfg.r_max : (cfg.r_max < sum ? cfg.r_max : sum);
+        double* o = a.out + 7 * t;
+        o[0] = latency;
+        o[1] = cost;
+        o[2] = sla;
+        o[3] = proactive;
+        o[4] = pareto;
+        o[5] = total;
+        o[6] = total != sum ? 1.0 : 0.0;
+        // update(l_after, c_after), pareto.cpp:36-41: normalize, then insert
+        if (a.update[t] && fr_insert(l, c, F, a.cap, pl, pc, a.overflow)) hv = fr_hv(l, c, F);
+    }
+}
+
 // ------------------------------------------------------------------- host --
 
 static int grid_for(size_t n, int threads = 256) {
@@ -825,6 +999,99 @@ void compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas, s
         const double* o = h.data() + 7 * t;
         out[t] = sair_reward_breakdown{o[0], o[1], o[2], o[3], o[4], o[5], o[6] != 0.0};
     }
+}
+
+void compute_reward_replay(const sair_reward_inputs* in, const int32_t* deltas, size_t S,
+                           size_t T, const uint8_t* update, sair_frontier_s* f,
+                           const sair_reward_config* cfg, sair_reward_breakdown* out) {
+    RewardCfg rc = check_cfg(cfg);
+    if (T == 0) return;
+    DeviceGuard g(f->device);
+    size_t nupd = 0;
+    for (size_t t = 0; t < T; ++t) nupd += update[t] != 0;
+    // replayers: >= 32 rounds each, <= 4096; frontier scratch of `cap` points
+    size_t R = std::max<size_t>(1, std::min<size_t>(4096, T / 32));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const size_t B = (T + R - 1) / R;
+        R = (T + B - 1) / B;
+        const size_t cap = R == 1 ? f->F + nupd + 1 : std::min<size_t>(f->F + nupd + 1, 1024);
+        const size_t gcap = f->F + nupd + 1;
+        const size_t dbytes = T * S * 16;
+        const size_t bytes = T * 32 + dbytes + T + T * 56 + 4 * R * cap * 8 + 2 * R * 8 +
+                             2 * gcap * 8 + 64 + 16 * 256;
+        char* base = static_cast<char*>(f->b_in.get(bytes));
+        size_t off = 0;
+        auto take = [&](size_t n) {
+            char* ptr = base + off;
+            off += (n + 255) / 256 * 256;
+            return ptr;
+        };
+        ReplayArgs a{};
+        double* din = reinterpret_cast<double*>(take(T * 32));
+        int32_t* dd = reinterpret_cast<int32_t*>(take(dbytes + 16));
+        uint8_t* du = reinterpret_cast<uint8_t*>(take(T));
+        a.in = din;
+        a.deltas = dd;
+        a.update = du;
+        a.T = T;
+        a.S = S;
+        a.B = B;
+        a.R = R;
+        a.cap = cap;
+        a.l_max = f->l_max;
+        a.c_max = f->c_max;
+        a.cfg = rc;
+        a.out = reinterpret_cast<double*>(take(T * 56));
+        a.fl = reinterpret_cast<double*>(take(R * cap * 8));
+        a.fc = reinterpret_cast<double*>(take(R * cap * 8));
+        a.sl = reinterpret_cast<double*>(take(R * cap * 8));
+        a.sc = reinterpret_cast<double*>(take(R * cap * 8));
+        a.fn = reinterpret_cast<size_t*>(take(R * 8));
+        a.sn = reinterpret_cast<size_t*>(take(R * 8));
+        a.gl = reinterpret_cast<double*>(take(gcap * 8));
+        a.gc = reinterpret_cast<double*>(take(gcap * 8));
+        a.gn = reinterpret_cast<size_t*>(take(8));
+        a.overflow = reinterpret_cast<int*>(take(8));
+        a.gcap = gcap;
+        a.f0l = f->fl;
+        a.f0c = f->fc;
+        a.f0n = f->F;
+        SAIR_CUDA(cudaMemcpyAsync(din, in, T * 32, cudaMemcpyHostToDevice, f->st));
+        if (dbytes) SAIR_CUDA(cudaMemcpyAsync(dd, deltas, dbytes, cudaMemcpyHostToDevice, f->st));
+        SAIR_CUDA(cudaMemcpyAsync(du, update, T, cudaMemcpyHostToDevice, f->st));
+        SAIR_CUDA(cudaMemsetAsync(a.overflow, 0, 4, f->st));
+        const int blocks = (int)((R + 127) / 128);
+        replay_local_kernel<<<blocks, 128, 0, f->st>>>(a);
+        replay_prefix_kernel<<<1, 32, 0, f->st>>>(a);
+        replay_block_kernel<<<blocks, 128, 0, f->st>>>(a);
+        SAIR_LAUNCH("replay kernels");
+        int ovf = 0;
+        size_t G = 0;
+        SAIR_CUDA(cudaMemcpyAsync(&ovf, a.overflow, 4, cudaMemcpyDeviceToHost, f->st));
+        SAIR_CUDA(cudaMemcpyAsync(&G, a.gn, 8, cudaMemcpyDeviceToHost, f->st));
+        SAIR_CUDA(cudaStreamSynchronize(f->st));
+        if (ovf) {  // a frontier outgrew its scratch: one replayer, full capacity
+            R = 1;
+            continue;
+        }
+        std::vector<double> h(7 * T);
+        SAIR_CUDA(cudaMemcpyAsync(h.data(), a.out, T * 56, cudaMemcpyDeviceToHost, f->st));
+        // the frontier after every flagged row (the prefix kernel's final state)
+        reserve(f, std::max<size_t>(G, 1));
+        if (G) {
+            SAIR_CUDA(cudaMemcpyAsync(f->fl, a.gl, G * 8, cudaMemcpyDeviceToDevice, f->st));
+            SAIR_CUDA(cudaMemcpyAsync(f->fc, a.gc, G * 8, cudaMemcpyDeviceToDevice, f->st));
+        }
+        SAIR_CUDA(cudaStreamSynchronize(f->st));
+        f->F = G;
+        sync_mirror(f);
+        for (size_t t = 0; t < T; ++t) {
+            const double* o = h.data() + 7 * t;
+            out[t] = sair_reward_breakdown{o[0], o[1], o[2], o[3], o[4], o[5], o[6] != 0.0};
+        }
+        return;
+    }
+    throw Error(SAIR_EINVAL, "replay: frontier scratch overflow");
 }
 
 double action_magnitude(const int32_t* deltas, size_t S, int device) {
