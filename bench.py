@@ -275,6 +275,7 @@ def run_ours(a, rank, world, local_rank):
     }
     if rank == 0 and world == 1 and not a.no_pareto:
         out["config2"] = bench_config2(dev, a.steps)
+        out["config5_step"] = bench_decision_step(buf, dev)
     if rank == 0 and not a.no_pareto:
         out["pareto"] = bench_pareto(dev)
     if rank == 0:
@@ -284,6 +285,41 @@ def run_ours(a, rank, world, local_rank):
     if dist:
         dist.destroy_process_group()
     return out
+
+
+def bench_decision_step(buf, dev, P=30000, steps=3):
+    """configs[4] on one GPU's shard: the device side of one batched decision
+    step for P = 10k pipelines x 3 workload patterns over the 16M-record store
+    (128M / 8 GPUs): select + veto scan (wide pass), per-pipeline frontier
+    reward + update, bulk append of the P new experiences."""
+    import paper_2601_22397_b200 as sair
+    from paper_2601_22397_b200 import decision, synth
+    rng = np.random.default_rng(SEED)
+    fs = sair.FrontierSet(P, 2000.0, 10.0, device=dev)
+    scfg = sair.SelectionConfig(m=K_SEL, lambda_div=0.0)
+    rcfg = sair.RewardConfig()
+    times = {"retrieve": 0.0, "reward_store": 0.0}
+    for s in range(steps + 1):
+        ctx = synth.queries(SEED + 100 + s, P, DIM)
+        inputs = np.stack([rng.uniform(100, 2500, P), rng.uniform(50, 2600, P),
+                           rng.uniform(0.5, 10, P), rng.uniform(0.5, 11, P)], 1)
+        deltas = rng.integers(-2, 3, size=(P, 3, 4)).astype(np.int32)
+        upd = np.ones(P, np.uint8)
+        rounds = np.full(P, 1000 + s, np.int32)
+        t0 = time.perf_counter()
+        decision.retrieve(buf, ctx, scfg)
+        t1 = time.perf_counter()
+        decision.score_and_store(buf, fs, ctx, inputs, deltas, upd, rounds, rcfg)
+        t2 = time.perf_counter()
+        if s:  # the first step warms up
+            times["retrieve"] += t1 - t0
+            times["reward_store"] += t2 - t1
+    tot = sum(times.values())
+    return {"workload": f"configs[4] per GPU: {P} pipelines, store {buf.size()} records x d={DIM}, "
+                        f"k={K_SEL}, lambda_div=0",
+            "decisions_per_s": round(P * steps / tot, 1), "ms_per_step": round(tot / steps * 1e3, 3),
+            "retrieve_ms": round(times["retrieve"] / steps * 1e3, 3),
+            "reward_and_store_ms": round(times["reward_store"] / steps * 1e3, 3)}
 
 
 def bench_config2(dev, steps):

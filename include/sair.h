@@ -55,6 +55,7 @@ typedef enum {
 
 typedef struct sair_store_s* sair_store_t;       /* ExperienceBuffer state */
 typedef struct sair_frontier_s* sair_frontier_t; /* ParetoFrontier state */
+typedef struct sair_frontier_set_s* sair_frontier_set_t; /* P independent ParetoFrontiers */
 
 /* SelectionConfig, experience.hpp:27-32 (+ this library's knobs). */
 typedef struct {
@@ -80,6 +81,7 @@ typedef struct {
     float prepass_ms;       /* device time of the threshold sample pre-pass (tensor-core path) */
     int tensor_core;        /* 1: tcgen05 8-query stream pass; 2: tcgen05 wide (32-128 query) pass */
     int small;              /* 1: the whole call ran as the one-launch exact small-store select */
+    size_t retried;         /* queries given a second wide pass with raised thresholds */
 } sair_select_stats;
 
 SAIR_API const char* sair_last_error(void);
@@ -342,6 +344,25 @@ SAIR_API sair_status sair_compute_reward_replay(const sair_reward_inputs* in,
                                                 const uint8_t* update, sair_frontier_t f,
                                                 const sair_reward_config* cfg,
                                                 sair_reward_breakdown* out);
+
+/* ------------------------------------------------------------------------
+ * A set of P independent frontiers (one
+ * ParetoFrontier per simulated pipeline, harness.cpp:150) stepped together.
+ * ------------------------------------------------------------------------ */
+SAIR_API sair_status sair_frontier_set_create(size_t P, double l_max_ms, double c_max, int device,
+                                              sair_frontier_set_t* out);
+SAIR_API sair_status sair_frontier_set_destroy(sair_frontier_set_t s);
+/* One decision step of every pipeline p (harness.cpp:250-251): out[p] =
+ * compute_reward(in[p], deltas[p], frontier_p, cfg), then frontier_p.update(
+ * l_after, c_after) when update[p] != 0.  deltas is P x stages x 4. */
+SAIR_API sair_status sair_frontier_set_step(sair_frontier_set_t s, const sair_reward_inputs* in,
+                                            const int32_t* deltas, size_t stages,
+                                            const uint8_t* update, const sair_reward_config* cfg,
+                                            sair_reward_breakdown* out);
+/* points() / hypervolume() of pipeline p (up to cap points copied). */
+SAIR_API sair_status sair_frontier_set_points(sair_frontier_set_t s, size_t p, double* l,
+                                              double* c, size_t cap, size_t* F,
+                                              double* hypervolume);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,7 @@ __all__ = [
     "StageDelta", "ParetoFrontier", "ObjectivePoint", "dominates", "RewardConfig",
     "RewardInputs", "RewardBreakdown", "compute_reward", "compute_reward_batch",
     "action_magnitude", "context_features", "dominance_counts", "SairError", "InvalidArgument",
-    "compute_reward_replay",
+    "compute_reward_replay", "FrontierSet",
     "LogicError", "OutOfRange", "SELECT_AUTO", "SELECT_EXACT",
 ]
 
@@ -632,3 +632,51 @@ def compute_reward_replay(inputs, deltas, update, frontier: ParetoFrontier, cfg:
         S, T, u.ctypes.data_as(C.POINTER(C.c_uint8)), frontier._h, C.byref(c), out))
     return np.array([[o.latency, o.cost, o.sla, o.proactive, o.pareto, o.total, o.clipped]
                      for o in out[:T]], dtype=np.float64).reshape(T, 7)
+
+
+class FrontierSet:
+    """P independent ParetoFrontiers stepped together (config 5: one frontier
+    per simulated pipeline, harness.cpp:150, :250-251)."""
+
+    def __init__(self, P: int, latency_max_ms: float, cost_max: float, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().sair_frontier_set_create(P, latency_max_ms, cost_max, device, C.byref(h)))
+        self._h = h
+        self.P = P
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().sair_frontier_set_destroy(h)
+            self._h = None
+
+    def step(self, inputs, deltas, update, cfg: RewardConfig):
+        """compute_reward of every pipeline's row against its own frontier, then
+        its update() where update[p]; returns P x 7 (as compute_reward_batch)."""
+        x = _f64(inputs).reshape(self.P, 4)
+        d = np.ascontiguousarray(deltas, dtype=np.int32).reshape(self.P, -1, 4)
+        u = np.ascontiguousarray(update, dtype=np.uint8).reshape(self.P)
+        out = (_lib.RewardBreakdownC * max(self.P, 1))()
+        c = cfg._c()
+        _check(lib().sair_frontier_set_step(
+            self._h, x.ctypes.data_as(C.POINTER(_lib.RewardInputsC)),
+            d.ctypes.data_as(C.POINTER(C.c_int32)), d.shape[1],
+            u.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(c), out))
+        return np.array([[o.latency, o.cost, o.sla, o.proactive, o.pareto, o.total, o.clipped]
+                         for o in out[:self.P]], dtype=np.float64).reshape(self.P, 7)
+
+    def points_array(self, p: int):
+        F = C.c_size_t()
+        hv = C.c_double()
+        _check(lib().sair_frontier_set_points(self._h, p, None, None, 0, C.byref(F), C.byref(hv)))
+        n = max(F.value, 1)
+        l, c = np.zeros(n), np.zeros(n)
+        _check(lib().sair_frontier_set_points(self._h, p, _dp(l), _dp(c), n, C.byref(F),
+                                              C.byref(hv)))
+        return l[:F.value], c[:F.value]
+
+    def hypervolume(self, p: int) -> float:
+        F = C.c_size_t()
+        hv = C.c_double()
+        _check(lib().sair_frontier_set_points(self._h, p, None, None, 0, C.byref(F), C.byref(hv)))
+        return hv.value

@@ -33,7 +33,8 @@ class SelectStatsC(C.Structure):
     _fields_ = [("queries", C.c_size_t), ("certified", C.c_size_t),
                 ("exact_fallbacks", C.c_size_t), ("candidates", C.c_size_t), ("qb", C.c_int),
                 ("stream_launches", C.c_int), ("stream_ms", C.c_float), ("total_ms", C.c_float),
-                ("prepass_ms", C.c_float), ("tensor_core", C.c_int), ("small", C.c_int)]
+                ("prepass_ms", C.c_float), ("tensor_core", C.c_int), ("small", C.c_int),
+                ("retried", C.c_size_t)]
 
 
 class RewardConfigC(C.Structure):
@@ -128,6 +129,14 @@ SIGNATURES = {
     "sair_compute_reward_batch": (C.c_int, [C.POINTER(RewardInputsC), _i32p, C.c_size_t,
                                             C.c_size_t, _vp, C.POINTER(RewardConfigC),
                                             C.POINTER(RewardBreakdownC)]),
+    "sair_frontier_set_create": (C.c_int, [C.c_size_t, C.c_double, C.c_double, C.c_int,
+                                           C.POINTER(_vp)]),
+    "sair_frontier_set_destroy": (C.c_int, [_vp]),
+    "sair_frontier_set_step": (C.c_int, [_vp, C.POINTER(RewardInputsC), _i32p, C.c_size_t,
+                                         C.POINTER(C.c_uint8), C.POINTER(RewardConfigC),
+                                         C.POINTER(RewardBreakdownC)]),
+    "sair_frontier_set_points": (C.c_int, [_vp, C.c_size_t, _dp, _dp, C.c_size_t,
+                                           C.POINTER(C.c_size_t), _dp]),
     "sair_compute_reward_replay": (C.c_int, [C.POINTER(RewardInputsC), _i32p, C.c_size_t,
                                              C.c_size_t, C.POINTER(C.c_uint8), _vp,
                                              C.POINTER(RewardConfigC),

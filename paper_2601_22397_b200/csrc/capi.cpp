@@ -551,4 +551,41 @@ sair_status sair_compute_reward_replay(const sair_reward_inputs* in, const int32
     return guard([&] { sair::compute_reward_replay(in, deltas, stages, T, update, f, cfg, out); });
 }
 
+// ---------------------------------------------------------- frontier set --
+
+sair_status sair_frontier_set_create(size_t P, double l_max_ms, double c_max, int device,
+                                     sair_frontier_set_t* out) {
+    if (!out) return bad("null out");
+    auto* s = new (std::nothrow) sair_frontier_set_s();
+    if (!s) return SAIR_ENOMEM;
+    sair_status st = guard([&] { sair::frontier_set_init(s, P, l_max_ms, c_max, device); });
+    if (st != SAIR_OK) {
+        delete s;
+        return st;
+    }
+    *out = s;
+    return SAIR_OK;
+}
+
+sair_status sair_frontier_set_destroy(sair_frontier_set_t s) {
+    if (!s) return SAIR_OK;
+    sair_status st = guard([&] { sair::frontier_set_free(s); });
+    delete s;
+    return st;
+}
+
+sair_status sair_frontier_set_step(sair_frontier_set_t s, const sair_reward_inputs* in,
+                                   const int32_t* deltas, size_t stages, const uint8_t* update,
+                                   const sair_reward_config* cfg, sair_reward_breakdown* out) {
+    if (!s || !cfg || (s->P && (!in || !out || !update)) || (s->P && stages && !deltas))
+        return bad("null input");
+    return guard([&] { sair::frontier_set_step(s, in, deltas, stages, update, cfg, out); });
+}
+
+sair_status sair_frontier_set_points(sair_frontier_set_t s, size_t p, double* l, double* c,
+                                     size_t cap, size_t* F, double* hypervolume) {
+    if (!s || !F) return bad("null input");
+    return guard([&] { *F = sair::frontier_set_points(s, p, l, c, cap, hypervolume); });
+}
+
 }  // extern "C"

@@ -127,6 +127,19 @@ struct sair_frontier_s {
     sair::HBuf h_io;
 };
 
+// ----------------------------------------------------------- frontier set --
+struct sair_frontier_set_s {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    size_t P = 0, cap = 0, maxf = 0;
+    double l_max = 1.0, c_max = 1.0;
+    double* fl = nullptr;  // [P][cap]
+    double* fc = nullptr;
+    size_t* fn = nullptr;  // [P]
+    double* hv = nullptr;  // [P]
+    sair::DBuf b_in;
+};
+
 namespace sair {
 
 // statistics the reference's formulas see: the whole buffer's (experience.cpp:159-166, :229-231)
@@ -181,6 +194,13 @@ void compute_reward_replay(const sair_reward_inputs* in, const int32_t* deltas, 
                            size_t T, const uint8_t* update, sair_frontier_s* f,
                            const sair_reward_config* cfg, sair_reward_breakdown* out);
 double action_magnitude(const int32_t* deltas, size_t S, int device);
+void frontier_set_init(sair_frontier_set_s* s, size_t P, double l_max, double c_max, int device);
+void frontier_set_free(sair_frontier_set_s* s);
+void frontier_set_step(sair_frontier_set_s* s, const sair_reward_inputs* in, const int32_t* deltas,
+                       size_t S, const uint8_t* update, const sair_reward_config* cfg,
+                       sair_reward_breakdown* out);
+size_t frontier_set_points(sair_frontier_set_s* s, size_t p, double* l, double* c, size_t cap,
+                           double* hv);
 double similarity(const double* a, const double* b, int d, double sigma, int device);
 
 }  // namespace sair

@@ -571,6 +571,35 @@ struct ReplayArgs {
     int* overflow;
 };
 
+// compute_reward, reward.cpp:21-44, of one row against a frontier view;
+// returns the normalized (l_after, c_after) for the caller's update()
+__device__ void reward_row(const double* in, const int32_t* deltas, size_t S, const FrontierView& v,
+                           double l_max, double c_max, const RewardCfg& cfg, double* o, double* pl,
+                           double* pc) {
+    const double lb = in[0], la = in[1], cb = in[2], ca = in[3];
+    double latency = ddiv(dmul(cfg.w_l, dsub(lb, la)), cfg.l_base);
+    double cost = ddiv(dmul(-cfg.w_c, dsub(ca, cb)), cfg.c_budget);
+    double sla = 0.0;
+    if (la > cfg.t_sla) {
+        double ratio = ddiv(la, cfg.t_sla);
+        sla = dadd(-dmul(ratio, ratio), 1.0);
+    }
+    double sg = dsub(ddiv(lb, cfg.t_sla), 1.0);
+    if (sg < 0.0) sg = 0.0;
+    double proactive = dmul(dmul(sg, action_mu(deltas, S)), cfg.w_p);
+    f_normalize(l_max, c_max, la, ca, pl, pc, nullptr);
+    double pareto = f_reward(v, *pl, *pc, nullptr);
+    double sum = dadd(dadd(dadd(dadd(latency, cost), sla), proactive), pareto);
+    double total = sum < -cfg.r_max ? -cfg.r_max : (cfg.r_max < sum ? cfg.r_max : sum);
+    o[0] = latency;
+    o[1] = cost;
+    o[2] = sla;
+    o[3] = proactive;
+    o[4] = pareto;
+    o[5] = total;
+    o[6] = total != sum ? 1.0 : 0.0;
+}
+
 __global__ void replay_local_kernel(const ReplayArgs a) {
     const size_t b = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (b >= a.R) return;
@@ -621,38 +650,53 @@ __global__ void replay_block_kernel(const ReplayArgs a) {
         c[i] = a.sc[b * a.cap + i];
     }
     double hv = fr_hv(l, c, F);
-    const RewardCfg& cfg = a.cfg;
     const size_t t1 = min(a.T, (b + 1) * a.B);
     for (size_t t = b * a.B; t < t1; ++t) {
-        // compute_reward, reward.cpp:21-44, against the current frontier
-        const double lb = a.in[4 * t], la = a.in[4 * t + 1], cb = a.in[4 * t + 2],
-                     ca = a.in[4 * t + 3];
-        double latency = ddiv(dmul(cfg.w_l, dsub(lb, la)), cfg.l_base);
-        double cost = ddiv(dmul(-cfg.w_c, dsub(ca, cb)), cfg.c_budget);
-        double sla = 0.0;
-        if (la > cfg.t_sla) {
-            double ratio = ddiv(la, cfg.t_sla);
-            sla = dadd(-dmul(ratio, ratio), 1.0);
-        }
-        double sg = dsub(ddiv(lb, cfg.t_sla), 1.0);
-        if (sg < 0.0) sg = 0.0;
-        double proactive = dmul(dmul(sg, action_mu(a.deltas + t * a.S * 4, a.S)), cfg.w_p);
         double pl, pc;
-        f_normalize(a.l_max, a.c_max, la, ca, &pl, &pc, nullptr);
-        const FrontierView v{l, c, F, hv};
-        double pareto = f_reward(v, pl, pc, nullptr);
-        double sum = dadd(dadd(dadd(dadd(latency, cost), sla), proactive), pareto);
-        double total = sum < -cfg.r_max ? -cfg.r_max : (cfg.r_max < sum ? cfg.r_max : sum);
-        double* o = a.out + 7 * t;
-        o[0] = latency;
-        o[1] = cost;
-        o[2] = sla;
-        o[3] = proactive;
-        o[4] = pareto;
-        o[5] = total;
-        o[6] = total != sum ? 1.0 : 0.0;
+        reward_row(a.in + 4 * t, a.deltas + t * a.S * 4, a.S, FrontierView{l, c, F, hv}, a.l_max,
+                   a.c_max, a.cfg, a.out + 7 * t, &pl, &pc);
         // update(l_after, c_after), pareto.cpp:36-41: normalize, then insert
         if (a.update[t] && fr_insert(l, c, F, a.cap, pl, pc, a.overflow)) hv = fr_hv(l, c, F);
+    }
+}
+
+// ---- a set of independent frontiers (config 5: one per pipeline) ----------
+//
+// P small frontiers in one allocation ([P][cap] latencies / costs, sizes,
+// cached hypervolumes).  One decision step scores every pipeline's outcome
+// against its own frontier and applies its update() (harness.cpp:250-251),
+// one thread per pipeline (frontiers stay small: tens of points).
+
+struct SetArgs {
+    const double* in;       // [P][4]
+    const int32_t* deltas;  // [P][S][4]
+    const uint8_t* update;  // [P]
+    size_t P, S, cap;
+    double l_max, c_max;
+    RewardCfg cfg;
+    double* fl;
+    double* fc;
+    size_t* fn;
+    double* hv;
+    double* out;            // [P][7]
+    unsigned long long* maxf;
+    int* overflow;
+};
+
+__global__ void frontier_set_step_kernel(const SetArgs a) {
+    for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < a.P;
+         p += (size_t)gridDim.x * blockDim.x) {
+        double* l = a.fl + p * a.cap;
+        double* c = a.fc + p * a.cap;
+        size_t F = a.fn[p];
+        double pl, pc;
+        reward_row(a.in + 4 * p, a.deltas + p * a.S * 4, a.S, FrontierView{l, c, F, a.hv[p]},
+                   a.l_max, a.c_max, a.cfg, a.out + 7 * p, &pl, &pc);
+        if (a.update[p] && fr_insert(l, c, F, a.cap, pl, pc, a.overflow)) {
+            a.fn[p] = F;
+            a.hv[p] = fr_hv(l, c, F);
+        }
+        atomicMax(a.maxf, (unsigned long long)F);
     }
 }
 
@@ -1092,6 +1136,128 @@ void compute_reward_replay(const sair_reward_inputs* in, const int32_t* deltas, 
         return;
     }
     throw Error(SAIR_EINVAL, "replay: frontier scratch overflow");
+}
+
+void frontier_set_init(sair_frontier_set_s* s, size_t P, double l_max, double c_max, int device) {
+    if (l_max <= 0.0 || c_max <= 0.0)
+        throw Error(SAIR_EINVAL, "ParetoFrontier: normalizers must be positive");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw Error(SAIR_ECUDA, "no CUDA device (libsair has no CPU fallback)");
+    if (device < 0 || device >= ndev) throw Error(SAIR_EINVAL, "device ordinal out of range");
+    s->device = device;
+    s->P = P;
+    s->l_max = l_max;
+    s->c_max = c_max;
+    DeviceGuard g(device);
+    SAIR_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    s->cap = 16;
+    SAIR_CUDA(cudaMalloc(&s->fl, std::max<size_t>(P, 1) * s->cap * 8));
+    SAIR_CUDA(cudaMalloc(&s->fc, std::max<size_t>(P, 1) * s->cap * 8));
+    SAIR_CUDA(cudaMalloc(&s->fn, std::max<size_t>(P, 1) * 8));
+    SAIR_CUDA(cudaMalloc(&s->hv, std::max<size_t>(P, 1) * 8));
+    SAIR_CUDA(cudaMemsetAsync(s->fn, 0, std::max<size_t>(P, 1) * 8, s->st));
+    SAIR_CUDA(cudaMemsetAsync(s->hv, 0, std::max<size_t>(P, 1) * 8, s->st));
+    SAIR_CUDA(cudaStreamSynchronize(s->st));
+}
+
+void frontier_set_free(sair_frontier_set_s* s) {
+    DeviceGuard g(s->device);
+    if (s->st) cudaStreamSynchronize(s->st);
+    cudaFree(s->fl);
+    cudaFree(s->fc);
+    cudaFree(s->fn);
+    cudaFree(s->hv);
+    s->b_in.release();
+    if (s->st) cudaStreamDestroy(s->st);
+    s->st = nullptr;
+}
+
+// grow every frontier's capacity (strided copy: [P][cap] -> [P][ncap])
+static void set_grow(sair_frontier_set_s* s, size_t ncap) {
+    double *l, *c;
+    SAIR_CUDA(cudaMalloc(&l, s->P * ncap * 8));
+    SAIR_CUDA(cudaMalloc(&c, s->P * ncap * 8));
+    SAIR_CUDA(cudaMemcpy2DAsync(l, ncap * 8, s->fl, s->cap * 8, s->cap * 8, s->P,
+                                cudaMemcpyDeviceToDevice, s->st));
+    SAIR_CUDA(cudaMemcpy2DAsync(c, ncap * 8, s->fc, s->cap * 8, s->cap * 8, s->P,
+                                cudaMemcpyDeviceToDevice, s->st));
+    SAIR_CUDA(cudaStreamSynchronize(s->st));
+    cudaFree(s->fl);
+    cudaFree(s->fc);
+    s->fl = l;
+    s->fc = c;
+    s->cap = ncap;
+}
+
+void frontier_set_step(sair_frontier_set_s* s, const sair_reward_inputs* in, const int32_t* deltas,
+                       size_t S, const uint8_t* update, const sair_reward_config* cfg,
+                       sair_reward_breakdown* out) {
+    RewardCfg rc = check_cfg(cfg);
+    const size_t P = s->P;
+    if (P == 0) return;
+    DeviceGuard g(s->device);
+    if (s->maxf + 1 > s->cap) set_grow(s, std::max(2 * s->cap, s->maxf + 1));
+    const size_t dbytes = P * S * 16;
+    char* base = static_cast<char*>(s->b_in.get(P * 32 + dbytes + P + P * 56 + 64 + 5 * 256));
+    size_t off = 0;
+    auto take = [&](size_t n) {
+        char* ptr = base + off;
+        off += (n + 255) / 256 * 256;
+        return ptr;
+    };
+    SetArgs a{};
+    double* din = reinterpret_cast<double*>(take(P * 32));
+    int32_t* dd = reinterpret_cast<int32_t*>(take(dbytes + 16));
+    uint8_t* du = reinterpret_cast<uint8_t*>(take(P));
+    a.out = reinterpret_cast<double*>(take(P * 56));
+    a.maxf = reinterpret_cast<unsigned long long*>(take(16));
+    a.overflow = reinterpret_cast<int*>(a.maxf + 1);
+    a.in = din;
+    a.deltas = dd;
+    a.update = du;
+    a.P = P;
+    a.S = S;
+    a.cap = s->cap;
+    a.l_max = s->l_max;
+    a.c_max = s->c_max;
+    a.cfg = rc;
+    a.fl = s->fl;
+    a.fc = s->fc;
+    a.fn = s->fn;
+    a.hv = s->hv;
+    SAIR_CUDA(cudaMemcpyAsync(din, in, P * 32, cudaMemcpyHostToDevice, s->st));
+    if (dbytes) SAIR_CUDA(cudaMemcpyAsync(dd, deltas, dbytes, cudaMemcpyHostToDevice, s->st));
+    SAIR_CUDA(cudaMemcpyAsync(du, update, P, cudaMemcpyHostToDevice, s->st));
+    SAIR_CUDA(cudaMemsetAsync(a.maxf, 0, 16, s->st));
+    frontier_set_step_kernel<<<grid_for(P, 128), 128, 0, s->st>>>(a);
+    SAIR_LAUNCH("frontier_set_step_kernel");
+    std::vector<double> h(7 * P);
+    unsigned long long mf[2] = {0, 0};
+    SAIR_CUDA(cudaMemcpyAsync(h.data(), a.out, P * 56, cudaMemcpyDeviceToHost, s->st));
+    SAIR_CUDA(cudaMemcpyAsync(mf, a.maxf, 16, cudaMemcpyDeviceToHost, s->st));
+    SAIR_CUDA(cudaStreamSynchronize(s->st));
+    // capacity was ensured up front (>= max F + 1), so an insert never overflows
+    if (mf[1] & 0xFFFFFFFFull) throw Error(SAIR_ECUDA, "frontier set: capacity overflow");
+    s->maxf = (size_t)mf[0];
+    for (size_t p = 0; p < P; ++p) {
+        const double* o = h.data() + 7 * p;
+        out[p] = sair_reward_breakdown{o[0], o[1], o[2], o[3], o[4], o[5], o[6] != 0.0};
+    }
+}
+
+size_t frontier_set_points(sair_frontier_set_s* s, size_t p, double* l, double* c, size_t cap,
+                           double* hv) {
+    if (p >= s->P) throw Error(SAIR_ERANGE, "frontier set: pipeline index out of range");
+    DeviceGuard g(s->device);
+    size_t F = 0;
+    SAIR_CUDA(cudaMemcpyAsync(&F, s->fn + p, 8, cudaMemcpyDeviceToHost, s->st));
+    if (hv) SAIR_CUDA(cudaMemcpyAsync(hv, s->hv + p, 8, cudaMemcpyDeviceToHost, s->st));
+    SAIR_CUDA(cudaStreamSynchronize(s->st));
+    const size_t k = std::min(F, cap);
+    if (k && l) SAIR_CUDA(cudaMemcpy(l, s->fl + p * s->cap, k * 8, cudaMemcpyDeviceToHost));
+    if (k && c) SAIR_CUDA(cudaMemcpy(c, s->fc + p * s->cap, k * 8, cudaMemcpyDeviceToHost));
+    return F;
 }
 
 double action_magnitude(const int32_t* deltas, size_t S, int device) {

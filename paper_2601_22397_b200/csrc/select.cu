@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
 // because the keys of one list share their leading digits.
 __global__ void __launch_bounds__(1024)
     merge_kernel(const float* __restrict__ in_key, const uint32_t* __restrict__ in_idx, int G,
-                 int lists_stride, int kmax, int QB, int kp, int knn, float* __restrict__ out_key,
+                 int lists_stride, int kmax, int kout, int QB, int kp, int knn, float* __restrict__ out_key,
                  uint32_t* __restrict__ out_idx, float* __restrict__ out_thr) {
     const int L = blockIdx.x;
     const int K = L < QB ? kp : knn;
@@ -462,8 +462,8 @@ __global__ void __launch_bounds__(1024)
     }
     for (int j = tid; j < K; j += blockDim.x) {
         const unsigned long long u = skey[j];
-        out_key[(size_t)L * kmax + j] = ord2f((uint32_t)(u >> 32));
-        out_idx[(size_t)L * kmax + j] = ~(uint32_t)(u & 0xffffffffu);
+        out_key[(size_t)L * kout + j] = ord2f((uint32_t)(u >> 32));
+        out_idx[(size_t)L * kout + j] = ~(uint32_t)(u & 0xffffffffu);
     }
     if (tid == 0) out_thr[L] = ord2f((uint32_t)(skey[K - 1] >> 32));
 }
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(1024)
 template <int ITEMS>
 __global__ void __launch_bounds__(1024)
     merge_reg_kernel(const float* __restrict__ in_key, const uint32_t* __restrict__ in_idx, int G,
-                     int lists_stride, int kmax, int QB, int kp, int knn,
+                     int lists_stride, int kmax, int kout, int QB, int kp, int knn,
                      float* __restrict__ out_key, uint32_t* __restrict__ out_idx,
                      float* __restrict__ out_thr) {
     const int L = blockIdx.x;
@@ -483,21 +483,26 @@ __global__ void __launch_bounds__(1024)
         idx = in_idx[off];
         return true;
     };
-    block_topk<ITEMS>(load, G * K, K, out_key + (size_t)L * kmax, out_idx + (size_t)L * kmax,
+    block_topk<ITEMS>(load, G * K, K, out_key + (size_t)L * kout, out_idx + (size_t)L * kout,
                       out_thr + L);
 }
 
-// one merge launch: the register kernel when every list fits, else the global one
+// one merge launch: the register kernel when every list fits, else the global
+// one.  Inputs [G][lists][kmax] with K entries per CTA list; outputs
+// [2 qb][kout] (kout = kmax unless the caller's input stride is larger).
 void launch_merge(cudaStream_t st, const float* ck, const uint32_t* ci, int G, int lists, int kmax,
-                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr) {
+                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr, int kout) {
+    if (kout <= 0) kout = kmax;
     const int nb = knn ? 2 * qb : qb;
     const size_t total = (size_t)G * std::max(kp, knn);
     if (total <= 4 * 1024)
-        merge_reg_kernel<4><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, qb, kp, knn, mk, mi, mthr);
+        merge_reg_kernel<4><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, kout, qb, kp, knn, mk, mi,
+                                                 mthr);
     else if (total <= 16 * 1024)
-        merge_reg_kernel<16><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, qb, kp, knn, mk, mi, mthr);
+        merge_reg_kernel<16><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, kout, qb, kp, knn, mk, mi,
+                                                  mthr);
     else
-        merge_kernel<<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, qb, kp, knn, mk, mi, mthr);
+        merge_kernel<<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, kout, qb, kp, knn, mk, mi, mthr);
     SAIR_LAUNCH("merge_kernel");
 }
 
@@ -533,6 +538,7 @@ struct RefineArgs {
     int64_t* out_nn;
     double* out_nn_sim;
     int* out_nn_cert;
+    float* out_thr;     // [4][QB]: merged K'-th key (sel, veto), start threshold (sel, veto)
     double* out_rew;    // [QB][m] reward of each pick (shard merge)
     int32_t* out_round; // [QB][m]
 };
@@ -756,6 +762,12 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
     if (tid == 0) {
         a.out_count[q] = want;
         a.out_cert[q] = s_cert;
+        if (a.out_thr) {
+            a.out_thr[q] = s_thr[0];
+            a.out_thr[a.QB + q] = a.knn ? s_thr[1] : -INFINITY;
+            a.out_thr[2 * a.QB + q] = a.t0 ? a.t0[q] : -INFINITY;
+            a.out_thr[3 * a.QB + q] = a.t0 && a.knn ? a.t0[a.QB + q] : -INFINITY;
+        }
     }
     if (a.knn == 0) return;
     // nearest record by exact similarity; first index wins ties (policy.cpp:146-153)
@@ -1009,13 +1021,22 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         unsigned int* dpmax = reinterpret_cast<unsigned int*>(mthr + 2 * qb);
         double* zs = s->b_z.as<double>((size_t)qb * kp * d);
         double* dc = s->b_consts.as<double>(2 * (size_t)d + (size_t)qb * d + qb);
-        const size_t ngroups = (nq + qb - 1) / qb;
+        // One batch: the queries ql (indices into the call's queries), in groups
+        // of qb; t0o (wide pass only) overrides the sampled start thresholds,
+        // 2 qb floats per group (selection lists, then veto lists).
+        std::vector<float> thr_of(nq * 4, -INFINITY);
+        auto run_batch = [&](const std::vector<size_t>& ql, const std::vector<float>* t0o) {
+        const size_t nbq = ql.size();
+        const size_t ngroups = (nbq + qb - 1) / qb;
+        std::vector<double> zc(nbq * d);
+        for (size_t i = 0; i < nbq; ++i)
+            std::copy(p.z.begin() + ql[i] * d, p.z.begin() + (ql[i] + 1) * d, zc.begin() + i * d);
         // Every group's kernels are enqueued back to back on the store's stream
         // (device scratch is reused in stream order); each group has its own
         // pinned staging, output slice and events, and the host synchronises
         // once, after one device-to-host copy of all outputs.
         const size_t ob = ((size_t)qb * m * 8 * 4 + (size_t)qb * m * 4 + (size_t)qb * 8 * 2 +
-                           (size_t)qb * 4 * 4 + 64 + 255) & ~(size_t)255;
+                           (size_t)qb * 4 * 4 + (size_t)qb * 4 * 4 + 64 + 255) & ~(size_t)255;
         char* dout = static_cast<char*>(s->b_out.get(ob * ngroups));
         char* hout = static_cast<char*>(s->h_out.get(ob * ngroups));
         struct O {
@@ -1029,6 +1050,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             int* nn_cert;
             double* rew;
             int32_t* round;
+            float* thr;  // [4][qb]: K'-th merged key (sel, veto), start threshold (sel, veto)
         };
         auto carve = [&](char* b) {
             O o;
@@ -1042,6 +1064,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             o.nn_cert = o.cert + qb;
             o.rew = reinterpret_cast<double*>(o.nn_cert + qb + (qb & 1));
             o.round = reinterpret_cast<int32_t*>(o.rew + qb * m);
+            o.thr = reinterpret_cast<float*>(o.round + qb * m);
             return o;
         };
         // pinned, so the copies never stage through pageable memory
@@ -1064,8 +1087,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         s->last.tensor_core = use_wide ? 2 : (use_mma ? 1 : 0);
         for (size_t g = 0; g < ngroups; ++g) {
             const size_t g0 = g * qb;
-            const int nqg = (int)std::min<size_t>(qb, nq - g0);
-            const double* zgrp = p.z.data() + g0 * d;
+            const int nqg = (int)std::min<size_t>(qb, nbq - g0);
+            const double* zgrp = zc.data() + g0 * d;
             double* hc = hc_all + g * nhc;
             std::copy(p.mean.begin(), p.mean.end(), hc);
             std::copy(p.sd.begin(), p.sd.end(), hc + d);
@@ -1074,7 +1097,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                 for (int k = 0; k < d; ++k) hc[2 * (size_t)d + (size_t)qq * d + k] = z[k];
             }
             const GroupIo io{hstage_all ? hstage_all + g * hstride : nullptr, s->gev[3 * g + 1],
-                             s->gev[3 * g + 2]};
+                             s->gev[3 * g + 2], t0o ? t0o->data() + g * 2 * qb : nullptr};
             const O D = carve(dout + g * ob);
             SAIR_CUDA(cudaMemsetAsync(dpmax, 0, 4, s->st));
             SAIR_CUDA(cudaEventRecord(s->gev[3 * g], s->st));
@@ -1136,6 +1159,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.out_nn_cert = D.nn_cert;
             ra.out_rew = D.rew;
             ra.out_round = D.round;
+            ra.out_thr = D.thr;
             refine_kernel<<<nqg, 256, refine_smem, s->st>>>(ra);
             SAIR_LAUNCH("refine_kernel");
         }
@@ -1143,7 +1167,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         SAIR_CUDA(cudaStreamSynchronize(s->st));
         for (size_t g = 0; g < ngroups; ++g) {
             const size_t g0 = g * qb;
-            const int nqg = (int)std::min<size_t>(qb, nq - g0);
+            const int nqg = (int)std::min<size_t>(qb, nbq - g0);
             const O H = carve(hout + g * ob);
             float ms = 0.f;
             if (use_mma || use_wide) {
@@ -1156,7 +1180,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             }
             stream_ms += ms;
             for (int qq = 0; qq < nqg; ++qq) {
-                const size_t gq = g0 + qq;
+                const size_t gq = ql[g0 + qq];
+                for (int k = 0; k < 4; ++k) thr_of[gq * 4 + k] = H.thr[k * qb + qq];
                 if (!(H.cert[qq] && (!out_nn || H.nn_cert[qq]))) continue;
                 done[gq] = 1;
                 out_count[gq] = (size_t)H.cnt[qq];
@@ -1172,6 +1197,31 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                     out_nn_sim[gq] = H.nn_sim[qq];
                 }
                 s->last.certified++;
+            }
+        }
+        };
+        std::vector<size_t> all_q(nq);
+        for (size_t i = 0; i < nq; ++i) all_q[i] = i;
+        run_batch(all_q, nullptr);
+        if (use_wide && cfg.lambda_div == 0.0) {
+            // Second chance before the exact pass: a list that overflowed its
+            // per-CTA capacity (records with high keys concentrated in a few
+            // pages: a freshly appended batch) still kept >= K' keys above the
+            // start threshold, so its K'-th kept key is a valid, higher start
+            // threshold.  One more wide pass with it usually certifies.
+            std::vector<size_t> rest;
+            for (size_t i = 0; i < nq; ++i)
+                if (!done[i]) rest.push_back(i);
+            if (!rest.empty()) {
+                const size_t ng = (rest.size() + qb - 1) / qb;
+                std::vector<float> t0r(ng * 2 * qb, -FLT_MAX);
+                for (size_t j = 0; j < rest.size(); ++j) {
+                    const size_t i = rest[j], g = j / qb, qq = j % qb;
+                    t0r[g * 2 * qb + qq] = std::max(thr_of[i * 4 + 2], thr_of[i * 4 + 0]);
+                    t0r[g * 2 * qb + qb + qq] = std::max(thr_of[i * 4 + 3], thr_of[i * 4 + 1]);
+                }
+                run_batch(rest, &t0r);
+                s->last.retried = rest.size();
             }
         }
     }

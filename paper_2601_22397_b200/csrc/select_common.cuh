@@ -65,6 +65,7 @@ inline QueryPrep prep_queries(const sair_store_s* s, const double* q, size_t nq,
 struct GroupIo {
     float* hstage;
     cudaEvent_t e_mid, e_end;
+    const float* t0_override;  // wide pass: [2 QW] start thresholds (skip the sample pass)
 };
 
 // select_mma.cu: the tcgen05 streaming kernel (plan + launcher)
@@ -102,6 +103,10 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
                   double lambda, bool want_nn, int64_t* out_idx, double* out_sim,
                   double* out_score, size_t* out_count, int64_t* out_nn, double* out_nn_sim,
                   double* out_reward, int32_t* out_round);
+
+// select.cu: global top-K' of every list across per-CTA lists [G][lists][kmax]
+void launch_merge(cudaStream_t st, const float* ck, const uint32_t* ci, int G, int lists, int kmax,
+                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr, int kout = 0);
 
 // select_exact.cu: one query through the full fp64 pass.
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,

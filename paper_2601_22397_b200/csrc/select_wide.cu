@@ -24,11 +24,12 @@
 //           so the K'-th largest of those maxima is <= the store's K'-th key
 //           (they belong to distinct records) -> the start threshold t0.
 //   stream  every page; a record whose key beats t0 is appended to its
-//           query's global candidate list (atomic slot; a full list only
-//           records the largest key it dropped, which the certification
-//           bound then covers).
-// list_topk_kernel selects each list's top-K' and the refine kernel
-// (select.cu) finishes exactly as for the 8-query path.
+//           query's list of this CTA (shared-memory slot counter, global
+//           store; a full list only records the largest key it dropped,
+//           which the certification bound then covers).
+// At the end each CTA list keeps its K' best; the cross-CTA merge
+// (launch_merge, select.cu) and the refine kernel finish exactly as for the
+// 8-query path.
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -40,6 +41,7 @@
 #include "select_common.cuh"
 #include "topk_select.cuh"
 #include "umma.cuh"
+#include "warp_topk.cuh"
 
 namespace sair {
 
@@ -69,9 +71,9 @@ struct WideArgs {
     float* smax;              // sample out [2QW][4 * spages]
     float* lkey;              // stream out: per-CTA lists [grid][2QW][cap]
     uint32_t* lidx;
-    uint32_t* lcnt;           // [grid][2QW] entries in each CTA list
     unsigned int* dropped;    // [2QW] max ordinal of a key dropped on a full list
     uint32_t cap;             // per-CTA list capacity
+    int kp, kv;               // K' of the selection / veto lists
     unsigned int* pmax;       // max P over records (float bits)
     uint32_t tcols;           // TMEM columns allocated (power of two >= nst * QW)
     int probe;                // diagnostics (SAIR_PROBE_WIDE=1): skip the epilogue math
@@ -129,7 +131,8 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     float* sM = sB + 2 * QW;     // [2] max |B| per list kind
     uint32_t* scnt = reinterpret_cast<uint32_t*>(sM + 4);  // [2QW] CTA list fill
     uint32_t* sdrop = scnt + 2 * QW;                       // [2QW] dropped max ordinal
-    uint64_t* full = reinterpret_cast<uint64_t*>(sdrop + 2 * QW);
+    uint32_t* whist = sdrop + 2 * QW;                      // [WE][256] compaction histograms
+    uint64_t* full = reinterpret_cast<uint64_t*>(whist + WE * 256);
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 8;
@@ -406,9 +409,23 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         }
         if (a.mode == 1) {
             asm volatile("bar.sync 1, %0;" ::"n"(WE * 32) : "memory");
-            for (int L = tid; L < 2 * QW; L += WE * 32) {
-                a.lcnt[(size_t)blockIdx.x * 2 * QW + L] = min(scnt[L], a.cap);
-                if (sdrop[L]) atomicMax(&a.dropped[L], sdrop[L]);
+            // Each CTA list keeps its K' best (the CTA's K'-th key is <= the
+            // store's K'-th key, so nothing that can reach the pool is lost),
+            // padded to exactly K' entries (-inf keys) for the cross-CTA merge.
+            for (int L = warp; L < 2 * QW; L += WE) {
+                const int K = L < QW ? a.kp : a.kv;
+                if (K == 0) continue;
+                const size_t o = ((size_t)blockIdx.x * 2 * QW + L) * a.cap;
+                int c = (int)min(scnt[L], a.cap);
+                if (c > K) {
+                    warp_keep_topk(a.lkey + o, a.lidx + o, c, K, whist + warp * 256, lane);
+                    c = K;
+                }
+                for (int j = c + lane; j < K; j += 32) {
+                    a.lkey[o + j] = -INFINITY;
+                    a.lidx[o + j] = 0xFFFFFFFFu - (uint32_t)j;
+                }
+                if (lane == 0 && sdrop[L]) atomicMax(&a.dropped[L], sdrop[L]);
             }
         }
     }
@@ -502,27 +519,6 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
-// top-K' of one global candidate list (one block per list)
-template <int ITEMS>
-__global__ void __launch_bounds__(1024)
-    list_topk_kernel(const float* __restrict__ lkey, const uint32_t* __restrict__ lidx,
-                     const uint32_t* __restrict__ lcnt, uint32_t cap, int G, int QW, int kp,
-                     int knn, int kmax, float* __restrict__ out_key,
-                     uint32_t* __restrict__ out_idx, float* __restrict__ out_thr) {
-    const int L = blockIdx.x;
-    const int K = L < QW ? kp : knn;
-    auto load = [&](int e, float& key, uint32_t& idx) {
-        const int g = e / (int)cap, j = e - g * (int)cap;
-        const size_t row = (size_t)g * 2 * QW + L;
-        if ((uint32_t)j >= lcnt[row]) return false;
-        key = lkey[row * cap + j];
-        idx = lidx[row * cap + j];
-        return true;
-    };
-    block_topk<ITEMS>(load, G * (int)cap, K, out_key + (size_t)L * kmax, out_idx + (size_t)L * kmax,
-                      out_thr + L);
-}
-
 inline float tf32_trunc(double v) {
     float f = (float)v;
     uint32_t u;
@@ -588,11 +584,15 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     unsigned int* ddrop = dcnt + L;
     float* dsmax = reinterpret_cast<float*>(ddrop + L);
     const size_t lent = (size_t)pl.grid * L * pl.cap;
-    char* lists = static_cast<char*>(s->b_sample.get(lent * 8 + (size_t)pl.grid * L * 4 + 256));
+    char* lists = static_cast<char*>(s->b_sample.get(lent * 8 + 256));
     float* lkey = reinterpret_cast<float*>(lists);
     uint32_t* lidx = reinterpret_cast<uint32_t*>(lists + lent * 4);
-    uint32_t* gcnt = lidx + lent;
-    SAIR_CUDA(cudaMemcpyAsync(dc, hb, (nc - L) * sizeof(float), cudaMemcpyHostToDevice, s->st));
+    if (io.t0_override) {  // a retry: start thresholds given, no sample pass
+        std::copy(io.t0_override, io.t0_override + L, hb + (nc - L));
+        SAIR_CUDA(cudaMemcpyAsync(dc, hb, nc * sizeof(float), cudaMemcpyHostToDevice, s->st));
+    } else {
+        SAIR_CUDA(cudaMemcpyAsync(dc, hb, (nc - L) * sizeof(float), cudaMemcpyHostToDevice, s->st));
+    }
     SAIR_CUDA(cudaMemsetAsync(dcnt, 0, 2 * L * sizeof(uint32_t), s->st));
 
     WideArgs a{};
@@ -611,53 +611,43 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.smax = dsmax;
     a.lkey = lkey;
     a.lidx = lidx;
-    a.lcnt = gcnt;
     a.dropped = ddrop;
     a.cap = pl.cap;
+    a.kp = pl.kp;
+    a.kv = pl.knn;
     a.pmax = pmax;
     a.probe = std::getenv("SAIR_PROBE_WIDE") ? std::atoi(std::getenv("SAIR_PROBE_WIDE")) : 0;
     a.tcols = 32;
     while (a.tcols < (uint32_t)(pl.nst * QW)) a.tcols <<= 1;
     SAIR_CUDA(cudaFuncSetAttribute(stream_wide_kernel<DP, QW>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    // sample pass -> t0 (written into the consts the stream pass reads)
-    a.mode = 0;
-    stream_wide_kernel<DP, QW><<<(int)std::min<uint32_t>(pl.spages, (uint32_t)pl.grid),
-                                 WIDE_THREADS, pl.smem, s->st>>>(a);
-    SAIR_LAUNCH("stream_wide_kernel(sample)");
-    wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(dsmax, (uint32_t)S4, QW, pl.kp,
-                                                             pl.knn, dt0);
-    SAIR_LAUNCH("wide_kth_kernel");
+    if (!io.t0_override) {
+        // sample pass -> t0 (written into the consts the stream pass reads)
+        a.mode = 0;
+        stream_wide_kernel<DP, QW><<<(int)std::min<uint32_t>(pl.spages, (uint32_t)pl.grid),
+                                     WIDE_THREADS, pl.smem, s->st>>>(a);
+        SAIR_LAUNCH("stream_wide_kernel(sample)");
+        wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(dsmax, (uint32_t)S4, QW, pl.kp,
+                                                                 pl.knn, dt0);
+        SAIR_LAUNCH("wide_kth_kernel");
+    }
     SAIR_CUDA(cudaEventRecord(io.e_mid, s->st));
     a.mode = 1;
     stream_wide_kernel<DP, QW><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
     SAIR_LAUNCH("stream_wide_kernel(stream)");
     SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
-    const int nl = pl.knn ? 2 * QW : QW;
-    if ((size_t)pl.grid * pl.cap <= 4096)
-        list_topk_kernel<4><<<nl, 1024, 0, s->st>>>(lkey, lidx, gcnt, pl.cap, pl.grid, QW, pl.kp,
-                                                     pl.knn, pl.kmax, mk, mi, mthr);
-    else
-        list_topk_kernel<16><<<nl, 1024, 0, s->st>>>(lkey, lidx, gcnt, pl.cap, pl.grid, QW,
-                                                      pl.kp, pl.knn, pl.kmax, mk, mi, mthr);
-    SAIR_LAUNCH("list_topk_kernel");
-    if (std::getenv("SAIR_WIDE_DEBUG")) {  // diagnostics: list fill and thresholds
-        std::vector<uint32_t> hc((size_t)pl.grid * L), hd(L);
+    // per-query top-K' across the CTAs' compacted lists ([G][2QW][cap], K' each)
+    launch_merge(s->st, lkey, lidx, pl.grid, 2 * QW, (int)pl.cap, QW, pl.kp, pl.knn, mk, mi, mthr,
+                 pl.kmax);
+    if (std::getenv("SAIR_WIDE_DEBUG")) {  // diagnostics: overflowing lists, thresholds
+        std::vector<uint32_t> hd(L);
         std::vector<float> ht(L);
-        SAIR_CUDA(cudaMemcpyAsync(hc.data(), gcnt, hc.size() * 4, cudaMemcpyDeviceToHost, s->st));
         SAIR_CUDA(cudaMemcpyAsync(hd.data(), ddrop, L * 4, cudaMemcpyDeviceToHost, s->st));
         SAIR_CUDA(cudaMemcpyAsync(ht.data(), dt0, L * 4, cudaMemcpyDeviceToHost, s->st));
         SAIR_CUDA(cudaStreamSynchronize(s->st));
-        uint64_t tot = 0, mx = 0, nd = 0;
-        for (int i = 0; i < QW; ++i) {
-            uint64_t c = 0;
-            for (int g = 0; g < pl.grid; ++g) c += hc[(size_t)g * L + i];
-            tot += c;
-            mx = std::max<uint64_t>(mx, c);
-            nd += hd[i] != 0;
-        }
-        fprintf(stderr, "[wide] QW=%d spages=%u lists: mean %.1f max %llu dropped-lists %llu t0[0]=%g\n",
-                QW, pl.spages, (double)tot / QW, (unsigned long long)mx, (unsigned long long)nd,
+        size_t nd = 0;
+        for (int i = 0; i < QW; ++i) nd += hd[i] != 0;
+        fprintf(stderr, "[wide] QW=%d spages=%u dropped-lists %zu t0[0]=%g\n", QW, pl.spages, nd,
                 (double)ht[0]);
     }
     s->mma_t0 = dt0;
@@ -676,7 +666,7 @@ WideFn wide_pick_qw(int qw) {
 size_t wide_smem(int dp, int qw, int nst) {
     return 1024 + (size_t)nst * 4 * 32 * dp * 4 + WB * (size_t)(dp / 8) * qw * 32 +
            (size_t)2 * nst * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 +
-           48 * 8 + 16;
+           WE * 256 * 4 + 48 * 8 + 16;
 }
 
 }  // namespace
@@ -714,7 +704,9 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
     pl->spages = (uint32_t)std::min<size_t>(
         npages, std::min<size_t>(
                     16384, std::max<size_t>(64, (size_t)std::sqrt(10.0 * pl->kp * npages))));
-    pl->cap = 96;  // per CTA and list: ~16 K' / 148 expected (148 x 96 <= 16384)
+    // per CTA and list (global memory): ~7 candidates expected at 148 CTAs;
+    // 512 absorbs a few pages of concentrated high keys (a freshly appended batch)
+    pl->cap = 512;
     const size_t limit = 227 * 1024;
     // TMEM: nst stages x QW columns <= 512
     pl->nst = std::min(8, 512 / pl->qw);

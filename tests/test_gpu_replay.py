@@ -71,3 +71,25 @@ def test_replay_matches_sequential_reference(ref, kind, T):
         # > 64 points: the local exclusive area instead of HV(F u p) - HV(F)
         assert np.all(np.abs(got[:, 4] - want[:, 4]) <= 1e-12)
         assert np.all(np.abs(got[:, 5] - want[:, 5]) <= 1e-12)
+
+
+def test_frontier_set_matches_independent_reference_frontiers(ref):
+    """config 5's per-pipeline frontiers: P frontiers stepped together for
+    several decision rounds against P reference frontiers stepped one by one."""
+    rng = np.random.default_rng(11)
+    P, rounds = 300, 12
+    fs = sair.FrontierSet(P, L_MAX, C_MAX)
+    rfs = [RefFrontier(ref, L_MAX, C_MAX) for _ in range(P)]
+    for r in range(rounds):
+        inputs, deltas, update = _rounds(rng, P, "grid" if r % 3 == 0 else "uniform")
+        got = fs.step(inputs, deltas, update, CFG)
+        for p in range(P):
+            want = ref_compute_reward(ref, inputs[p], deltas[p], rfs[p], CFGV)
+            assert np.array_equal(got[p], want), (r, p)
+            if update[p]:
+                rfs[p].update(inputs[p, 1], inputs[p, 3])
+    for p in range(0, P, 7):
+        gl, gc = fs.points_array(p)
+        wl, wc = rfs[p].points()
+        assert np.array_equal(gl, wl) and np.array_equal(gc, wc)
+        assert fs.hypervolume(p) == rfs[p].hypervolume()
