@@ -597,6 +597,19 @@ def compute_reward(inp: RewardInputs, action: ScalingAction, frontier: ParetoFro
                            bool(out.clipped))
 
 
+def _breakdowns(out, T: int) -> np.ndarray:
+    """T sair_reward_breakdown structs -> T x 7 float64 (latency, cost, sla,
+    proactive, pareto, total, clipped), without a Python loop."""
+    if T == 0:
+        return np.zeros((0, 7))
+    rec = np.ctypeslib.as_array(out, shape=(len(out),))[:T]
+    res = np.empty((T, 7))
+    for j, name in enumerate(("latency", "cost", "sla", "proactive", "pareto", "total")):
+        res[:, j] = rec[name]
+    res[:, 6] = rec["clipped"]
+    return res
+
+
 def compute_reward_batch(inputs, deltas, frontier: ParetoFrontier, cfg: RewardConfig):
     """compute_reward for T rows: inputs T x 4 (l_before, l_after, c_before,
     c_after), deltas T x S x 4.  Returns a T x 7 array (latency, cost, sla,
@@ -610,8 +623,7 @@ def compute_reward_batch(inputs, deltas, frontier: ParetoFrontier, cfg: RewardCo
     _check(lib().sair_compute_reward_batch(
         x.ctypes.data_as(C.POINTER(_lib.RewardInputsC)), d.ctypes.data_as(C.POINTER(C.c_int32)),
         S, T, frontier._h, C.byref(c), out))
-    return np.array([[o.latency, o.cost, o.sla, o.proactive, o.pareto, o.total, o.clipped]
-                     for o in out[:T]], dtype=np.float64).reshape(T, 7)
+    return _breakdowns(out, T)
 
 
 def compute_reward_replay(inputs, deltas, update, frontier: ParetoFrontier, cfg: RewardConfig):
@@ -630,8 +642,7 @@ def compute_reward_replay(inputs, deltas, update, frontier: ParetoFrontier, cfg:
     _check(lib().sair_compute_reward_replay(
         x.ctypes.data_as(C.POINTER(_lib.RewardInputsC)), d.ctypes.data_as(C.POINTER(C.c_int32)),
         S, T, u.ctypes.data_as(C.POINTER(C.c_uint8)), frontier._h, C.byref(c), out))
-    return np.array([[o.latency, o.cost, o.sla, o.proactive, o.pareto, o.total, o.clipped]
-                     for o in out[:T]], dtype=np.float64).reshape(T, 7)
+    return _breakdowns(out, T)
 
 
 class FrontierSet:
@@ -662,8 +673,7 @@ class FrontierSet:
             self._h, x.ctypes.data_as(C.POINTER(_lib.RewardInputsC)),
             d.ctypes.data_as(C.POINTER(C.c_int32)), d.shape[1],
             u.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(c), out))
-        return np.array([[o.latency, o.cost, o.sla, o.proactive, o.pareto, o.total, o.clipped]
-                         for o in out[:self.P]], dtype=np.float64).reshape(self.P, 7)
+        return _breakdowns(out, self.P)
 
     def points_array(self, p: int):
         F = C.c_size_t()
