@@ -107,6 +107,7 @@ struct sair_store_s {
     sair::HBuf h_stage, h_out, h_mmab, h_consts;
     sair::DBuf b_mmab;    // tensor-core B operand constants, t0, dropped
     sair::DBuf b_sample;  // sample pre-pass keys
+    sair::DBuf b_loo;     // standardized rows + locally weighted LOO means (per call)
     std::vector<cudaEvent_t> gev;  // per query group: start, end of pre-pass, end of stream
     const float* mma_t0 = nullptr;
     const unsigned int* mma_dropped = nullptr;

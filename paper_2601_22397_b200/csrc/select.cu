@@ -945,12 +945,14 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     // (the greedy's diversity penalties defeat a fixed candidate pool), the
     // exact mode, or a store small enough that one exact pass is the cheaper
     // launch sequence.
-    const bool small_ok = !cfg.locally_weighted_mean && small_select_fits(s, m) &&
+    const bool small_ok = small_select_fits(s, m) &&
                           std::getenv("SAIR_NO_SMALL") == nullptr;
-    if (small_ok && (cfg.lambda_div != 0.0 || cfg.mode == SAIR_SELECT_EXACT || n <= SMALL_DIRECT_N)) {
+    if (small_ok && (cfg.lambda_div != 0.0 || cfg.mode == SAIR_SELECT_EXACT ||
+                     cfg.locally_weighted_mean || n <= SMALL_DIRECT_N)) {
         std::vector<size_t> all(nq);
         for (size_t i = 0; i < nq; ++i) all[i] = i;
-        small_select(s, p, all, m, cfg.lambda_div, out_nn != nullptr, out_idx, out_sim, out_score,
+        small_select(s, p, all, m, cfg.lambda_div, cfg.locally_weighted_mean != 0, out_nn != nullptr,
+                     out_idx, out_sim, out_score,
                      out_count, out_nn, out_nn_sim, out_reward, out_round);
         s->last.exact_fallbacks = 0;
         s->last.small = 1;
@@ -1229,17 +1231,22 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         std::vector<size_t> rest;
         for (size_t i = 0; i < nq; ++i)
             if (!done[i]) rest.push_back(i);
-        small_select(s, p, rest, m, cfg.lambda_div, out_nn != nullptr, out_idx, out_sim,
+        small_select(s, p, rest, m, cfg.lambda_div, cfg.locally_weighted_mean != 0,
+                     out_nn != nullptr, out_idx, out_sim,
                      out_score, out_count, out_nn, out_nn_sim, out_reward, out_round);
         s->last.exact_fallbacks += rest.size();
         for (size_t i : rest) done[i] = 1;
     }
+    const double* loo_pre = nullptr;
+    for (size_t i = 0; i < nq && cfg.locally_weighted_mean && !loo_pre; ++i)
+        if (!done[i]) loo_pre = local_loo_all(s, p);  // once for every remaining query
     for (size_t i = 0; i < nq; ++i) {
         if (done[i]) continue;
         exact_one(s, p, p.z.data() + i * d, m, cfg.lambda_div, cfg.locally_weighted_mean != 0,
                   out_idx + i * m, out_sim + i * m, out_score + i * m, &out_count[i],
                   out_nn ? out_nn + i : nullptr, out_nn ? out_nn_sim + i : nullptr,
-                  out_reward ? out_reward + i * m : nullptr, out_round ? out_round + i * m : nullptr);
+                  out_reward ? out_reward + i * m : nullptr, out_round ? out_round + i * m : nullptr,
+                  loo_pre);
         s->last.exact_fallbacks++;
     }
     SAIR_CUDA(cudaEventRecord(s->ev[3], s->st));

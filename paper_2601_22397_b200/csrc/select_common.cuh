@@ -100,7 +100,7 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
 constexpr size_t SMALL_DIRECT_N = 4096;  // lambda == 0: below this, skip the filter
 bool small_select_fits(const sair_store_s* s, size_t m);
 void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>& qidx, size_t m,
-                  double lambda, bool want_nn, int64_t* out_idx, double* out_sim,
+                  double lambda, bool local, bool want_nn, int64_t* out_idx, double* out_sim,
                   double* out_score, size_t* out_count, int64_t* out_nn, double* out_nn_sim,
                   double* out_reward, int32_t* out_round);
 
@@ -112,6 +112,9 @@ void launch_merge(cudaStream_t st, const float* ck, const uint32_t* ci, int G, i
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,
                size_t* o_cnt, int64_t* o_nn, double* o_nn_sim, double* o_rew = nullptr,
-               int32_t* o_round = nullptr);
+               int32_t* o_round = nullptr, const double* loo_pre = nullptr);
+// select_small.cu: the locally weighted LOO means of every record (exact,
+// once per call) into a scratch buffer owned by the store
+const double* local_loo_all(sair_store_s* s, const QueryPrep& p);
 
 }  // namespace sair

@@ -206,7 +206,7 @@ __global__ void surprisal_kernel(const ExactArgs a, size_t index, double* out) {
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,
                size_t* o_cnt, int64_t* o_nn, double* o_nn_sim, double* o_rew,
-               int32_t* o_round) {
+               int32_t* o_round, const double* loo_pre) {
     const size_t n = s->n;
     const int d = s->d;
     char* base = static_cast<char*>(
@@ -251,7 +251,9 @@ void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_
     SAIR_CUDA(cudaMemcpyAsync(dm, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s->st));
     const int threads = 256;
     const int blocks = (int)std::min<size_t>((n + threads - 1) / threads, 4096);
-    if (local) {
+    if (local && loo_pre) {
+        a.loo = loo_pre;  // computed once for the whole call (query-independent)
+    } else if (local) {
         a.loo = nullptr;
         local_loo_kernel<<<blocks, threads, 0, s->st>>>(a, loo);
         SAIR_LAUNCH("local_loo_kernel");

@@ -46,6 +46,7 @@ struct SmallArgs {
     size_t n, per;       // records, records per CTA
     size_t n_loo;        // loo_mean's n (the whole buffer's)
     double total, two_s2, lambda;
+    const double* loo;   // [n] locally weighted LOO means (nullable: the global mean)
     int64_t gbase;
     int64_t* out_idx;    // [nq][m]
     double* out_sim;
@@ -66,6 +67,54 @@ __global__ void zrows_kernel(const double* __restrict__ x64, const double* __res
         const int k = (int)(e % d);
         z[(size_t)k * n + e / d] = ddiv(dsub(x64[e], mean[k]), sd[k]);
     }
+}
+
+// locally_weighted_mean LOO, experience.cpp:216-228 (loo_mean with
+// cfg.locally_weighted_mean): for record i, sum_{j != i} w_ij r_j / sum w_ij
+// with w_ij = similarity(z_j, z_i) (the reference calls similarity(
+// standardize(items_[j].context), zi) -- z_j first), sequential in j; the
+// global mean when the weights vanish (<= 1e-12).  Query-independent: once
+// per call.  One thread per record i; j tiles of the standardized rows are
+// staged in shared memory and shared by the block.
+constexpr int LOO_TILE = 64;
+__global__ void __launch_bounds__(256) local_loo_z_kernel(const double* __restrict__ z,
+                                                           const double* __restrict__ r64, size_t n,
+                                                           int d, double two_s2, double total,
+                                                           size_t n_loo, double* __restrict__ loo) {
+    extern __shared__ double zt[];  // [d][LOO_TILE] + r[LOO_TILE]
+    double* rt = zt + (size_t)d * LOO_TILE;
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const bool valid = i < n;
+    double wsum = 0.0, acc = 0.0;
+    for (size_t j0 = 0; j0 < n; j0 += LOO_TILE) {
+        const int cnt = (int)min((size_t)LOO_TILE, n - j0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < d * LOO_TILE; e += blockDim.x) {
+            const int k = e / LOO_TILE, jj = e % LOO_TILE;
+            zt[e] = jj < cnt ? z[(size_t)k * n + j0 + jj] : 0.0;
+        }
+        for (int jj = threadIdx.x; jj < LOO_TILE; jj += blockDim.x)
+            rt[jj] = jj < cnt ? r64[j0 + jj] : 0.0;
+        __syncthreads();
+        if (!valid) continue;
+        for (int jj = 0; jj < cnt; ++jj) {
+            if (j0 + jj == i) continue;
+            double d2 = 0.0;
+            for (int k = 0; k < d; ++k) {
+                const double t = dsub(zt[k * LOO_TILE + jj], z[(size_t)k * n + i]);
+                d2 = dadd(d2, dmul(t, t));
+            }
+            const double w = sim_from_d2(d2, two_s2);
+            wsum = dadd(wsum, w);
+            acc = dadd(acc, dmul(w, rt[jj]));
+        }
+    }
+    if (!valid) return;
+    if (n_loo <= 1) {
+        loo[i] = 0.0;
+        return;
+    }
+    loo[i] = wsum > 1e-12 ? ddiv(acc, wsum) : ddiv(dsub(total, r64[i]), (double)(n_loo - 1));
 }
 
 __device__ __forceinline__ Best block_best(Best b, Best* wb) {
@@ -120,7 +169,8 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_select_kernel(const __gri
         }
         const double s = sim_from_d2(d2, a.two_s2);
         const double r = a.r64[lo + j];
-        const double loo = a.n_loo <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n_loo - 1));
+        const double loo = a.loo ? a.loo[lo + j]
+                                 : (a.n_loo <= 1 ? 0.0 : ddiv(dsub(a.total, r), (double)(a.n_loo - 1)));
         sim[j] = s;
         score[j] = dmul(s, fabs(dsub(r, loo)));
         pen[j] = 0.0;
@@ -234,13 +284,35 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_select_kernel(const __gri
 
 }  // namespace
 
+const double* local_loo_all(sair_store_s* s, const QueryPrep& p) {
+    const size_t n = s->n;
+    const int d = s->d;
+    char* base = static_cast<char*>(s->b_loo.get(n * d * 8 + 2 * (size_t)d * 8 + n * 8 + 3 * 256));
+    double* z = reinterpret_cast<double*>(base);
+    double* msd = reinterpret_cast<double*>(base + ((n * d * 8 + 255) & ~(size_t)255));
+    double* loo = msd + 2 * (size_t)d + 32;
+    double* hin = s->h_consts.as<double>(2 * (size_t)d);
+    std::copy(p.mean.begin(), p.mean.end(), hin);
+    std::copy(p.sd.begin(), p.sd.end(), hin + d);
+    SAIR_CUDA(cudaMemcpyAsync(msd, hin, 2 * (size_t)d * 8, cudaMemcpyHostToDevice, s->st));
+    zrows_kernel<<<(int)std::min<size_t>((n * d + 255) / 256, 2048), 256, 0, s->st>>>(
+        s->x64, msd, msd + d, n, d, z);
+    const size_t lsm = ((size_t)d * LOO_TILE + LOO_TILE) * 8;
+    SAIR_CUDA(cudaFuncSetAttribute(local_loo_z_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)lsm));
+    local_loo_z_kernel<<<(int)((n + 255) / 256), 256, lsm, s->st>>>(
+        z, s->r64, n, d, p.two_s2, eff_stats(s).total, eff_n(s), loo);
+    SAIR_LAUNCH("local_loo_z_kernel");
+    return loo;
+}
+
 bool small_select_fits(const sair_store_s* s, size_t m) {
     return s->n > 0 && s->n <= SMALL_CS_MAX * SMALL_PER_MAX && m <= 256 && s->d <= 1024;
 }
 
 // Exact select() of the queries `qidx` (standardized rows of p.z) in one launch.
 void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>& qidx, size_t m,
-                  double lambda, bool want_nn, int64_t* out_idx, double* out_sim,
+                  double lambda, bool local, bool want_nn, int64_t* out_idx, double* out_sim,
                   double* out_score, size_t* out_count, int64_t* out_nn, double* out_nn_sim,
                   double* out_reward, int32_t* out_round) {
     const size_t nq = qidx.size();
@@ -252,7 +324,7 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
     // device scratch: z rows | mean sd | zq | outputs
     const size_t ob = nq * m * (8 * 4 + 4) + nq * (4 + 8 + 8) + 256;
     char* base = static_cast<char*>(s->b_exact.get(n * d * 8 + 2 * (size_t)d * 8 +
-                                                    nq * d * 8 + ob + 4 * 256));
+                                                    nq * d * 8 + ob + n * 8 + 5 * 256));
     size_t off = 0;
     auto take = [&](size_t bytes) {
         char* ptr = base + off;
@@ -273,6 +345,16 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
     zrows_kernel<<<(int)std::min<size_t>((n * d + 255) / 256, 2048), 256, 0, s->st>>>(
         s->x64, msd, msd + d, n, d, z);
     SAIR_LAUNCH("zrows_kernel");
+    double* dloo = nullptr;
+    if (local) {
+        dloo = reinterpret_cast<double*>(take(n * 8));
+        const size_t lsm = ((size_t)d * LOO_TILE + LOO_TILE) * 8;
+        SAIR_CUDA(cudaFuncSetAttribute(local_loo_z_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+        local_loo_z_kernel<<<(int)((n + 255) / 256), 256, lsm, s->st>>>(
+            z, s->r64, n, d, p.two_s2, eff_stats(s).total, eff_n(s), dloo);
+        SAIR_LAUNCH("local_loo_z_kernel");
+    }
 
     SmallArgs a{};
     a.z = z;
@@ -289,6 +371,7 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
     a.total = eff_stats(s).total;
     a.two_s2 = p.two_s2;
     a.lambda = lambda;
+    a.loo = dloo;
     a.gbase = s->gbase;
     a.out_idx = reinterpret_cast<int64_t*>(dout);
     a.out_sim = reinterpret_cast<double*>(a.out_idx + nq * m);
