@@ -83,7 +83,7 @@ bool make_mma_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bo
 // select_wide.cu: the tcgen05 large-batch streaming filter (QW = 32/64/128
 // queries per pass) -> merged per-query top-K' lists for the refine kernel
 struct WidePlan {
-    int dp, qw, kp, knn, kmax, nst, grid;
+    int dp, qw, kp, knn, kmax, nst, ntm, grid;
     size_t smem;
     uint32_t cap, spages;
 };

@@ -65,7 +65,7 @@ struct WideArgs {
     const float* r32;
     uint32_t n, npages;
     float c1, c0, rdelta, alpha;
-    int nst, knn, mode;       // mode 0 = sample, 1 = stream
+    int nst, ntm, knn, mode;  // smem page stages, TMEM stages; mode 0 = sample, 1 = stream
     uint32_t spages;          // sample mode: sampled pages (page = i * npages / spages)
     const float* consts;      // B tiles (hi, lo; smem image) | s [DP] | cc [QW] | t0 [2QW]
     float* smax;              // sample out [2QW][4 * spages]
@@ -75,7 +75,7 @@ struct WideArgs {
     uint32_t cap;             // per-CTA list capacity
     int kp, kv;               // K' of the selection / veto lists
     unsigned int* pmax;       // max P over records (float bits)
-    uint32_t tcols;           // TMEM columns allocated (power of two >= nst * QW)
+    uint32_t tcols;           // TMEM columns allocated (power of two >= ntm * QW)
     int probe;                // diagnostics (SAIR_PROBE_WIDE=1): skip the epilogue math
 };
 
@@ -120,7 +120,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nst = a.nst, PR = 2 * a.nst;  // smem/TMEM stages, record-constant slots
+    // smem page stages, TMEM accumulator stages (decoupled: a page's shared
+    // stage is released once the MMA has read it and P is done, its TMEM stage
+    // once the epilogue is done), record-constant slots (>= ntm + 1 apart)
+    const int nst = a.nst, ntm = a.ntm, PR = a.nst + a.ntm;
     unsigned char* stage = smem;
     float* btile = reinterpret_cast<float*>(stage + (size_t)nst * PAGE_BYTES);  // [2][KSTEPS]
     float* prec = btile + WB * KSTEPS * BT_BYTES / 4;  // [PR][4][PAGE]: Asel, Ann, P, lg
@@ -184,6 +187,8 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         for (int s = 0; s < nst; ++s) {
             bar_init(&full[s], 1);
             bar_init(&empty[s], 2);   // the record-constant warp pair of the page
+        }
+        for (int s = 0; s < ntm; ++s) {
             bar_init(&tfull[s], 1);
             bar_init(&tempty[s], 4);  // the four epilogue warps of the page's group
         }
@@ -230,11 +235,12 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             const uint32_t bbase = su32(btile);
             for (uint32_t it = 0; it < mine; ++it) {
                 const uint32_t s = it % nst, ph = (it / nst) & 1u;
+                const uint32_t ts = it % ntm, tph = (it / ntm) & 1u;
                 bar_wait(&full[s], ph);
-                if (it >= (uint32_t)nst) bar_wait(&tempty[s], ph ^ 1u);
+                if (it >= (uint32_t)ntm) bar_wait(&tempty[ts], tph ^ 1u);
                 tc_fence_after();
                 const uint32_t abase = su32(stage + (size_t)s * PAGE_BYTES);
-                const uint32_t dcol = tmem + (uint32_t)(s * QW);
+                const uint32_t dcol = tmem + (uint32_t)(ts * QW);
 #pragma unroll
                 for (int ks = 0; ks < KSTEPS; ++ks) {
                     const uint64_t ad = umma_desc(abase + ks * 1024, BOX_BYTES, 512, 1);
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                         umma_tf32(dcol, ad, bd, IDESC, ks > 0 || h > 0 ? 1u : 0u);
                     }
                 }
-                umma_commit(&tfull[s]);
+                umma_commit(&tfull[ts]);
             }
         }
     } else if (warp >= W_REC) {
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             *reinterpret_cast<float2*>(pr + 3 * PAGE + rloc) = ol;
             __syncwarp();
             if (lane == 0) bar_arrive(&pready[it % PR]);
-            bar_wait(&tfull[s], ph);  // the MMA is done reading the stage
+            bar_wait(&tfull[it % ntm], (it / ntm) & 1u);  // the MMA is done reading the stage
             __syncwarp();
             if (lane == 0) bar_arrive(&empty[s]);
         }
@@ -316,7 +322,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         const int par = warp >> 2, quarter = warp & 3;
         const int rloc = quarter * 32 + lane;
         for (uint32_t it = par; it < mine; it += 2) {
-            const uint32_t s = it % nst, ph = (it / nst) & 1u;
+            const uint32_t s = it % ntm, ph = (it / ntm) & 1u;  // TMEM stage
             const uint32_t rec = page_of(it) * PAGE + rloc;
             bar_wait(&pready[it % PR], (it / PR) & 1u);
             const float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
@@ -605,6 +611,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.rdelta = rdelta;
     a.alpha = alpha;
     a.nst = pl.nst;
+    a.ntm = pl.ntm;
     a.knn = pl.knn ? 1 : 0;
     a.spages = pl.spages;
     a.consts = dc;
@@ -618,7 +625,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.pmax = pmax;
     a.probe = std::getenv("SAIR_PROBE_WIDE") ? std::atoi(std::getenv("SAIR_PROBE_WIDE")) : 0;
     a.tcols = 32;
-    while (a.tcols < (uint32_t)(pl.nst * QW)) a.tcols <<= 1;
+    while (a.tcols < (uint32_t)(pl.ntm * QW)) a.tcols <<= 1;
     SAIR_CUDA(cudaFuncSetAttribute(stream_wide_kernel<DP, QW>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (!io.t0_override) {
@@ -663,9 +670,9 @@ WideFn wide_pick_qw(int qw) {
     }
 }
 
-size_t wide_smem(int dp, int qw, int nst) {
+size_t wide_smem(int dp, int qw, int nst, int ntm) {
     return 1024 + (size_t)nst * 4 * 32 * dp * 4 + WB * (size_t)(dp / 8) * qw * 32 +
-           (size_t)2 * nst * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 +
+           (size_t)(nst + ntm) * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 +
            WE * 256 * 4 + 48 * 8 + 16;
 }
 
@@ -708,11 +715,12 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
     // 512 absorbs a few pages of concentrated high keys (a freshly appended batch)
     pl->cap = 512;
     const size_t limit = 227 * 1024;
-    // TMEM: nst stages x QW columns <= 512
-    pl->nst = std::min(8, 512 / pl->qw);
-    while (pl->nst > 2 && wide_smem(pl->dp, pl->qw, pl->nst) > limit) --pl->nst;
-    if (wide_smem(pl->dp, pl->qw, pl->nst) > limit) return false;
-    pl->smem = wide_smem(pl->dp, pl->qw, pl->nst);
+    // TMEM: ntm stages x QW columns <= 512; as many shared page stages as fit
+    pl->ntm = std::min(8, 512 / pl->qw);
+    pl->nst = 8;
+    while (pl->nst > 2 && wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm) > limit) --pl->nst;
+    if (wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm) > limit) return false;
+    pl->smem = wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
     pl->grid = (int)std::max<size_t>(1, std::min<size_t>(npages, (size_t)nsm));
