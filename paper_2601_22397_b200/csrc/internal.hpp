@@ -108,6 +108,7 @@ struct sair_store_s {
     sair::DBuf b_mmab;    // tensor-core B operand constants, t0, dropped
     sair::DBuf b_sample;  // sample pre-pass keys
     sair::DBuf b_loo;     // standardized rows + locally weighted LOO means (per call)
+    sair::DBuf b_greedy;  // batched exact greedy: rows + per-(query, record) state
     std::vector<cudaEvent_t> gev;  // per query group: start, end of pre-pass, end of stream
     const float* mma_t0 = nullptr;
     const unsigned int* mma_dropped = nullptr;

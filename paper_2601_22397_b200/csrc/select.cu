@@ -1240,6 +1240,20 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     const double* loo_pre = nullptr;
     for (size_t i = 0; i < nq && cfg.locally_weighted_mean && !loo_pre; ++i)
         if (!done[i]) loo_pre = local_loo_all(s, p);  // once for every remaining query
+    if (m <= 256 && std::getenv("SAIR_NO_GREEDY") == nullptr) {
+        // the remaining queries (lambda > 0 on a large store, the exact mode,
+        // uncertified ones): the batched exact greedy, G queries per pass
+        std::vector<size_t> rest;
+        for (size_t i = 0; i < nq; ++i)
+            if (!done[i]) rest.push_back(i);
+        if (!rest.empty()) {
+            greedy_select(s, p, rest, m, cfg.lambda_div, loo_pre, out_nn != nullptr, out_idx,
+                          out_sim, out_score, out_count, out_nn, out_nn_sim, out_reward,
+                          out_round);
+            s->last.exact_fallbacks += rest.size();
+            for (size_t i : rest) done[i] = 1;
+        }
+    }
     for (size_t i = 0; i < nq; ++i) {
         if (done[i]) continue;
         exact_one(s, p, p.z.data() + i * d, m, cfg.lambda_div, cfg.locally_weighted_mean != 0,

@@ -108,6 +108,17 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
 void launch_merge(cudaStream_t st, const float* ck, const uint32_t* ci, int G, int lists, int kmax,
                   int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr, int kout = 0);
 
+// standardize() of every stored row into z [d][n] (select_small.cu)
+void zrows_launch(const double* x64, const double* mean, const double* sd, size_t n, int d,
+                  double* z, cudaStream_t st);
+
+// select_greedy.cu: exact select() of many queries over a large store, G
+// queries per pass, every greedy step enqueued without a host round trip
+void greedy_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>& qidx, size_t m,
+                   double lambda, const double* loo, bool want_nn, int64_t* out_idx,
+                   double* out_sim, double* out_score, size_t* out_count, int64_t* out_nn,
+                   double* out_nn_sim, double* out_reward, int32_t* out_round);
+
 // select_exact.cu: one query through the full fp64 pass.
 void exact_one(sair_store_s* s, const QueryPrep& p, const double* zq_host, size_t m,
                double lambda, bool local, int64_t* o_idx, double* o_sim, double* o_score,

@@ -284,6 +284,13 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_select_kernel(const __gri
 
 }  // namespace
 
+void zrows_launch(const double* x64, const double* mean, const double* sd, size_t n, int d,
+                  double* z, cudaStream_t st) {
+    zrows_kernel<<<(int)std::min<size_t>((n * d + 255) / 256, 2048), 256, 0, st>>>(x64, mean, sd, n,
+                                                                                 d, z);
+    SAIR_LAUNCH("zrows_kernel");
+}
+
 const double* local_loo_all(sair_store_s* s, const QueryPrep& p) {
     const size_t n = s->n;
     const int d = s->d;

@@ -1,0 +1,59 @@
+"""The batched exact greedy for large stores (select_greedy.cu): lambda_div > 0
+above the small-store size, the exact mode and every uncertified query.  It
+must equal the C oracle (the reference's select restated, pinned bit for bit)
+and the per-query multi-launch pass it replaces (SAIR_NO_GREEDY)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2601_22397_b200 as sair  # noqa: E402
+from paper_2601_22397_b200 import ExperienceBuffer, SelectionConfig, synth  # noqa: E402
+
+
+def near(got, want, rel):
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    return np.all(np.abs(got - want) <= rel * np.maximum(1.0, np.abs(want)))
+
+
+@pytest.mark.parametrize("n,d,nq,m,lam", [(100000, 23, 6, 8, 0.1), (80000, 64, 9, 32, 0.1),
+                                          (70000, 16, 5, 15, 0.5), (90000, 8, 4, 12, 0.0)])
+def test_greedy_matches_oracle(orc, n, d, nq, m, lam):
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(n + 3, n, d, clustered=(d == 16))
+    ctx = synth.contexts(n + 3, 0, n, d, clustered=(d == 16))
+    rew, rnd = synth.rewards(n + 3, 0, n), synth.rounds(0, n)
+    xq = synth.queries(n + 4, nq, d, clustered=(d == 16))
+    sigma = db.effective_sigma()
+    cfg = SelectionConfig(m=m, lambda_div=lam, mode=sair.SELECT_EXACT)
+    idx, sim, sc, cnt, nn_i, nn_s = db.select_batch(xq, cfg, nearest=True)
+    oi, osim, osc, ocnt = orc.select_batch(ctx, rew, rnd, xq, m, lam, sigma)
+    assert np.array_equal(cnt, ocnt) and np.array_equal(idx, oi)
+    assert near(sc, osc, 1e-12) and near(sim, osim, 1e-12)
+    for q in range(nq):
+        j, s = orc.nearest(ctx, xq[q], sigma)
+        assert nn_i[q] == j and abs(nn_s[q] - s) <= 1e-12
+
+
+def test_greedy_equals_per_query_pass_and_lambda_default_path():
+    n, d = 120000, 32
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(8, n, d)
+    xq = synth.queries(9, 40, d)
+    cfg = SelectionConfig(m=16, lambda_div=0.1)   # the reference's default lambda
+    got = db.select_batch(xq, cfg, nearest=True)
+    st = db.last_stats()
+    assert st["exact_fallbacks"] + st["certified"] == 40
+    os.environ["SAIR_NO_GREEDY"] = "1"
+    try:
+        want = db.select_batch(xq[:5], cfg, nearest=True)
+    finally:
+        os.environ.pop("SAIR_NO_GREEDY")
+    for a, b in zip(got, want):
+        assert np.array_equal(np.asarray(a)[:5], b)
