@@ -216,6 +216,20 @@ SAIR_API sair_status sair_store_select_shard(sair_store_t h, const double* queri
                                              int64_t* out_idx, double* out_sim,
                                              double* out_score, double* out_reward,
                                              int32_t* out_round, size_t* out_count);
+/* The shard's side of select() for lambda_div > 0 on a buffer spread over
+ * ranks (experience.cpp:261-285 with the arg-max taken across shards by the
+ * caller between steps; sharded.py).  greedy_begin scores this shard for nq
+ * queries (global statistics, exact fp64) and writes per query the shard's
+ * best untaken record as nq x (6 + dim) doubles: gain, round, global index
+ * (-1 and gain -inf when none), similarity, score, reward, standardized row.
+ * greedy_next takes the step's global picks (global indices, nq) and their
+ * rows (nq x dim): local picks become taken, every penalty adds its pick's
+ * similarity, and the new bests are written the same way. */
+SAIR_API sair_status sair_store_greedy_begin(sair_store_t h, const double* queries, size_t nq,
+                                             int dim, const sair_select_config* cfg,
+                                             double* out_best);
+SAIR_API sair_status sair_store_greedy_next(sair_store_t h, const int64_t* picks,
+                                            const double* rows, double* out_best);
 /* Merge per-shard top-m lists (shard-major arrays [nshards][nq][m], counts
  * [nshards][nq]) into the buffer's select() result for lambda_div == 0:
  * (score desc, round asc, index asc), then curriculum order. */

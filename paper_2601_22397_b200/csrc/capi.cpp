@@ -321,6 +321,18 @@ sair_status sair_store_select_shard(sair_store_t h, const double* queries, size_
     });
 }
 
+sair_status sair_store_greedy_begin(sair_store_t h, const double* queries, size_t nq, int dim,
+                                    const sair_select_config* cfg, double* out_best) {
+    if (!h || !queries || !out_best) return bad("null input");
+    return guard([&] { sair::greedy_begin(h, queries, nq, dim, defaults(cfg), out_best); });
+}
+
+sair_status sair_store_greedy_next(sair_store_t h, const int64_t* picks, const double* rows,
+                                   double* out_best) {
+    if (!h || !picks || !rows || !out_best) return bad("null input");
+    return guard([&] { sair::greedy_next(h, picks, rows, out_best); });
+}
+
 sair_status sair_merge_topk(const double* score, const double* sim, const double* reward,
                             const int32_t* round, const int64_t* gidx, const size_t* count,
                             size_t nshards, size_t nq, size_t m, int device, int64_t* out_idx,

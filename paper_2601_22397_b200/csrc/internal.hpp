@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -59,6 +60,8 @@ struct HBuf {
 // Host-maintained fp64 statistics (bit-identical to the reference's
 // ExperienceBuffer members sum_, sum_sq_, the reward total of loo_mean, and the
 // sigma cache; experience.hpp:82-88).
+struct GreedySession;  // select_greedy.cu: a distributed greedy in progress
+
 struct StoreStats {
     std::vector<double> sum, sum_sq, xabs;  // per dim; xabs = max |x| (filter bound)
     double total = 0.0;                     // sum of rewards in index order
@@ -109,6 +112,7 @@ struct sair_store_s {
     sair::DBuf b_sample;  // sample pre-pass keys
     sair::DBuf b_loo;     // standardized rows + locally weighted LOO means (per call)
     sair::DBuf b_greedy;  // batched exact greedy: rows + per-(query, record) state
+    std::shared_ptr<sair::GreedySession> greedy;  // sharded lambda > 0 select in progress
     std::vector<cudaEvent_t> gev;  // per query group: start, end of pre-pass, end of stream
     const float* mma_t0 = nullptr;
     const unsigned int* mma_dropped = nullptr;
@@ -204,5 +208,10 @@ void frontier_set_step(sair_frontier_set_s* s, const sair_reward_inputs* in, con
 size_t frontier_set_points(sair_frontier_set_s* s, size_t p, double* l, double* c, size_t cap,
                            double* hv);
 double similarity(const double* a, const double* b, int d, double sigma, int device);
+
+// select_greedy.cu: a shard's side of the distributed exact greedy
+void greedy_begin(sair_store_s* s, const double* q, size_t nq, int dim,
+                  const sair_select_config& cfg, double* out);
+void greedy_next(sair_store_s* s, const int64_t* gpick, const double* rows, double* out);
 
 }  // namespace sair

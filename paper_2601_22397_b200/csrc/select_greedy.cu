@@ -22,6 +22,7 @@
 // rows.
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <vector>
 
 #include "select_common.cuh"
@@ -329,6 +330,181 @@ void greedy_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t
             }
         }
     }
+}
+
+
+// ------------------------------------------------- distributed sessions ----
+//
+// A shard of a buffer spread over ranks runs the same greedy with the global
+// pick decided by the caller between steps (sharded.py): greedy_begin scores
+// the shard for G queries; greedy_next applies the previous global picks
+// (taken where local, their rows added to every penalty) and returns the
+// shard's best per query.  A rank's best carries everything the others need:
+// gain, round, global index, the pick's similarity, score, reward and row.
+
+namespace {
+
+// the caller's global picks: mark local ones taken, stage every pick's row
+__global__ void greedy_apply_kernel(const GreedyArgs a, const int64_t* __restrict__ gpick,
+                                    const double* __restrict__ zrows, int64_t gbase) {
+    const int g = blockIdx.x;
+    const int64_t p = gpick[g] - gbase;
+    if (threadIdx.x == 0 && p >= 0 && (size_t)p < a.n) a.taken[(size_t)g * a.n + p] = 1;
+    for (int k = threadIdx.x; k < a.d; k += blockDim.x)
+        a.zpick[(size_t)g * a.d + k] = zrows[(size_t)g * a.d + k];
+}
+
+// per query: the shard's best -> [gain, round, gidx, sim, score, reward, row[d]]
+__global__ void greedy_local_best_kernel(const GreedyArgs a, int64_t gbase, double* __restrict__ out) {
+    const int g = blockIdx.x;
+    __shared__ Best wb[32];
+    Best b{0.0, 0, 0, -1};
+    for (int t = threadIdx.x; t < a.nblk; t += blockDim.x) {
+        const Best c = a.part[(size_t)g * a.nblk + t];
+        if (better(c, b)) b = c;
+    }
+    b = warp_best(b);
+    if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = b;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        Best c = threadIdx.x < (blockDim.x >> 5) ? wb[threadIdx.x] : Best{0.0, 0, 0, -1};
+        c = warp_best(c);
+        if (threadIdx.x == 0) wb[0] = c;
+    }
+    __syncthreads();
+    const Best w = wb[0];
+    double* o = out + (size_t)g * (6 + a.d);
+    if (w.j < 0) {  // no untaken record on this shard
+        if (threadIdx.x == 0) {
+            o[0] = -INFINITY;
+            o[1] = 0.0;
+            o[2] = -1.0;
+        }
+        return;
+    }
+    const size_t p = (size_t)w.i;
+    if (threadIdx.x == 0) {
+        const double* zq = a.zq + (size_t)g * a.d;
+        double d2 = 0.0;
+        for (int k = 0; k < a.d; ++k) {
+            const double t = dsub(a.z[(size_t)k * a.n + p], zq[k]);
+            d2 = dadd(d2, dmul(t, t));
+        }
+        o[0] = w.g;
+        o[1] = (double)w.r;
+        o[2] = (double)(gbase + (int64_t)p);
+        o[3] = sim_from_d2(d2, a.two_s2);
+        o[4] = a.score[(size_t)g * a.n + p];
+        o[5] = a.r64[p];
+    }
+    for (int k = threadIdx.x; k < a.d; k += blockDim.x) o[6 + k] = a.z[(size_t)k * a.n + p];
+}
+
+}  // namespace
+
+struct GreedySession {
+    GreedyArgs a{};
+    int nctas = 0;
+    size_t smem = 0;
+    int step = 0;
+    double* dout = nullptr;  // [G][6 + d]
+    int64_t* dpick = nullptr;
+    double* drows = nullptr;
+};
+
+static GreedySession& session(sair_store_s* s) {
+    if (!s->greedy) s->greedy = std::make_shared<GreedySession>();
+    return *s->greedy;
+}
+
+void greedy_begin(sair_store_s* s, const double* q, size_t G, int dim,
+                  const sair_select_config& cfg, double* out) {
+    if (G == 0 || G > 1024) throw Error(SAIR_EINVAL, "greedy session: 1..1024 queries");
+    if (s->n == 0) throw Error(SAIR_EINVAL, "greedy session: empty store");
+    if (cfg.locally_weighted_mean)
+        throw Error(SAIR_EINVAL, "locally_weighted_mean is not supported on a sharded store");
+    DeviceGuard dg(s->device);
+    const double sigma = store_effective_sigma(s, cfg.sigma_sim);
+    if (dim != s->d) throw Error(SAIR_EINVAL, "experience store: feature dimension mismatch");
+    const QueryPrep p = prep_queries(s, q, G, sigma);
+    const double lambda = cfg.lambda_div;
+    GreedySession& ss = session(s);
+    const size_t n = s->n;
+    const int d = s->d;
+    const int nctas = (int)((n + GT - 1) / GT);
+    const int nblk = nctas * GW;
+    char* base = static_cast<char*>(s->b_greedy.get(
+        n * d * 8 + 2 * (size_t)d * 8 + G * d * 8 * 3 + G * n * 17 + G * nblk * sizeof(Best) +
+        G * (6 + d) * 8 + G * 8 + 12 * 256));
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char* ptr = base + off;
+        off += (bytes + 255) / 256 * 256;
+        return ptr;
+    };
+    double* z = reinterpret_cast<double*>(take(n * d * 8));
+    double* msd = reinterpret_cast<double*>(take((2 * (size_t)d + G * d) * 8));
+    GreedyArgs& a = ss.a;
+    a = GreedyArgs{};
+    a.z = z;
+    a.r64 = s->r64;
+    a.rnd = s->rnd;
+    a.zq = msd + 2 * (size_t)d;
+    a.n = n;
+    a.n_loo = eff_n(s);
+    a.d = d;
+    a.G = (int)G;
+    a.want = 1;
+    a.total = eff_stats(s).total;
+    a.two_s2 = p.two_s2;
+    a.lambda = lambda;
+    a.score = reinterpret_cast<double*>(take(G * n * 8));
+    a.pen = reinterpret_cast<double*>(take(G * n * 8));
+    a.taken = reinterpret_cast<unsigned char*>(take(G * n));
+    a.part = reinterpret_cast<Best*>(take(G * nblk * sizeof(Best)));
+    a.zpick = reinterpret_cast<double*>(take(G * d * 8));
+    a.nblk = nblk;
+    ss.dout = reinterpret_cast<double*>(take(G * (6 + d) * 8));
+    ss.dpick = reinterpret_cast<int64_t*>(take(G * 8));
+    ss.drows = reinterpret_cast<double*>(take(G * d * 8));
+    ss.nctas = nctas;
+    ss.smem = ((size_t)d * GT + (size_t)GQ * d) * 8;
+    ss.step = 0;
+    double* hin = s->h_consts.as<double>(2 * (size_t)d + G * d);
+    std::copy(p.mean.begin(), p.mean.end(), hin);
+    std::copy(p.sd.begin(), p.sd.end(), hin + d);
+    std::copy(p.z.begin(), p.z.begin() + G * d, hin + 2 * d);
+    SAIR_CUDA(cudaMemcpyAsync(msd, hin, (2 * (size_t)d + G * d) * 8, cudaMemcpyHostToDevice, s->st));
+    zrows_launch(s->x64, msd, msd + d, n, d, z, s->st);
+    SAIR_CUDA(cudaFuncSetAttribute(greedy_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)ss.smem));
+    greedy_step_kernel<<<nctas, GT, ss.smem, s->st>>>(a, 0);
+    greedy_local_best_kernel<<<(int)G, 256, 0, s->st>>>(a, s->gbase, ss.dout);
+    SAIR_LAUNCH("greedy_begin");
+    SAIR_CUDA(cudaMemcpyAsync(out, ss.dout, G * (6 + d) * 8, cudaMemcpyDeviceToHost, s->st));
+    SAIR_CUDA(cudaStreamSynchronize(s->st));
+}
+
+void greedy_next(sair_store_s* s, const int64_t* gpick, const double* rows, double* out) {
+    if (!s->greedy || !s->greedy->a.score) throw Error(SAIR_ELOGIC, "greedy session not begun");
+    DeviceGuard dg(s->device);
+    GreedySession& ss = *s->greedy;
+    GreedyArgs& a = ss.a;
+    const size_t G = (size_t)a.G;
+    const int d = a.d;
+    int64_t* hp = reinterpret_cast<int64_t*>(s->h_consts.as<double>(G * (1 + d)));
+    double* hr = reinterpret_cast<double*>(hp + G);
+    std::copy(gpick, gpick + G, hp);
+    std::copy(rows, rows + G * d, hr);
+    SAIR_CUDA(cudaMemcpyAsync(ss.dpick, hp, G * 8, cudaMemcpyHostToDevice, s->st));
+    SAIR_CUDA(cudaMemcpyAsync(ss.drows, hr, G * d * 8, cudaMemcpyHostToDevice, s->st));
+    greedy_apply_kernel<<<(int)G, 64, 0, s->st>>>(a, ss.dpick, ss.drows, s->gbase);
+    ++ss.step;
+    greedy_step_kernel<<<ss.nctas, GT, ss.smem, s->st>>>(a, ss.step);
+    greedy_local_best_kernel<<<(int)G, 256, 0, s->st>>>(a, s->gbase, ss.dout);
+    SAIR_LAUNCH("greedy_next");
+    SAIR_CUDA(cudaMemcpyAsync(out, ss.dout, G * (6 + d) * 8, cudaMemcpyDeviceToHost, s->st));
+    SAIR_CUDA(cudaStreamSynchronize(s->st));
 }
 
 }  // namespace sair

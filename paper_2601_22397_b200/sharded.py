@@ -17,9 +17,13 @@ exchanges, each deterministic (rank order):
    curriculum order).  With lambda_div == 0 the buffer's top-m is a subset of
    the union of the shards' top-m, so the merge is exact.
 
-lambda_div > 0 (the greedy with diversity penalties) needs every shard's
-candidate pool and the pool vectors on one device; it is not sharded yet
-(DESIGN.md "Multi-GPU").
+lambda_div > 0 (the greedy with diversity penalties): every step's arg-max is
+taken across shards -- each rank scores its shard exactly (device, fp64, the
+reference's rounding order) and reports its best untaken record per query
+with everything the others need (gain, round, global index, similarity,
+score, reward, standardized row); one all-gather per step, the global winner
+by (gain desc, round asc, index asc), and every rank adds the winner's
+similarity to its penalties (sair_store_greedy_begin / _next).
 
 Pareto: outcome tuples are sharded the same way.  The
 frontier of a union is the frontier of the union of the shards' frontiers, so
@@ -161,13 +165,66 @@ class ShardedExperienceBuffer:
     def select_batch(self, queries, cfg: SelectionConfig):
         """The buffer's select() for every query: (idx, sim, score, count)."""
         if cfg.lambda_div != 0.0:
-            raise NotImplementedError("sharded select supports lambda_div == 0 (DESIGN.md)")
+            return self._select_greedy(queries, cfg)
         idx, sim, sc, rw, rd, cnt = self.select_local(queries, cfg)
         nq, m = idx.shape
         pack = np.concatenate([sc, sim, rw, idx.astype(np.float64), rd.astype(np.float64),
                                cnt.astype(np.float64)[:, None]], axis=1)
         parts = _all_gather(self.dist, pack, f"cuda:{self.device}")
         return merge_parts(parts, nq, m, self.device)
+
+
+    def _select_greedy(self, queries, cfg: SelectionConfig):
+        q = _f64(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        nq, d = q.shape
+        m = max(cfg.m, 1)
+        want = min(cfg.m, self.n_global)
+        idx = np.full((nq, m), -1, np.int64)
+        sim, sc = np.zeros((nq, m)), np.zeros((nq, m))
+        cnt = np.full(nq, want, np.int64)
+        if want == 0:
+            return idx, sim, sc, np.zeros(nq, np.int64)
+        best = np.zeros((nq, 6 + d))
+        c = cfg._c()
+        _check(lib().sair_store_greedy_begin(self.local._h, _dp(q), nq, d, C.byref(c), _dp(best)))
+        picks = np.zeros((want, nq, 6), np.float64)
+        dev = f"cuda:{self.device}"
+        for step in range(want):
+            parts = np.stack(_all_gather(self.dist, best, dev))      # [ranks][nq][6 + d]
+            win = global_winner(parts)                                # [nq] rank of the winner
+            w = parts[win, np.arange(nq)]
+            picks[step] = w[:, :6]
+            if step + 1 < want:
+                g = np.ascontiguousarray(w[:, 2].astype(np.int64))
+                rows = np.ascontiguousarray(w[:, 6:])
+                _check(lib().sair_store_greedy_next(
+                    self.local._h, g.ctypes.data_as(C.POINTER(C.c_int64)), _dp(rows), _dp(best)))
+        order = curriculum_order(picks[:, :, 5], picks[:, :, 1])      # [nq][want]
+        for qq in range(nq):
+            p = picks[order[qq], qq]
+            idx[qq, :want] = p[:, 2].astype(np.int64)
+            sim[qq, :want] = p[:, 3]
+            sc[qq, :want] = p[:, 4]
+        return idx, sim, sc, cnt
+
+
+def global_winner(parts: np.ndarray) -> np.ndarray:
+    """Per query the rank whose best wins: gain desc, round asc, global index
+    asc (experience.cpp:268-278); parts = [ranks][nq][>= 3] (gain, round, gidx)."""
+    gain, rnd, gi = parts[:, :, 0], parts[:, :, 1], parts[:, :, 2]
+    # lexsort: last key primary; -inf gains (no candidate) sort last
+    keys = np.lexsort((gi, rnd, -gain), axis=0)
+    return keys[0]
+
+
+def curriculum_order(reward: np.ndarray, rnd: np.ndarray) -> np.ndarray:
+    """Stable order by (reward asc, round asc) over pick order (:290-294);
+    reward / rnd are [want][nq]; returns [nq][want] pick positions."""
+    want, nq = reward.shape
+    pos = np.arange(want)
+    return np.stack([np.lexsort((pos, rnd[:, q], reward[:, q])) for q in range(nq)])
 
 
 def merge_parts(parts: List[np.ndarray], nq: int, m: int, device: int):

@@ -122,22 +122,46 @@ def test_sharded_protocol_matches_single_buffer_cpu(orc):
         assert np.array_equal([v for _, v in got], sc)
 
 
-def _gpu_worker(rank, world, port, q, nq=10):
+def test_sharded_greedy_rules_cpu():
+    """The host side of the sharded lambda > 0 select: the global winner rule
+    (gain desc, round asc, global index asc; -inf = shard exhausted) and the
+    curriculum order (reward asc, round asc, pick order), against a direct
+    restatement on random parts with many ties."""
+    from paper_2601_22397_b200.sharded import curriculum_order, global_winner
+    rng = np.random.default_rng(4)
+    R, nq = 5, 200
+    parts = np.zeros((R, nq, 3))
+    parts[:, :, 0] = rng.integers(0, 3, (R, nq)) / 4.0
+    parts[rng.uniform(size=(R, nq)) < 0.1, 0] = -np.inf
+    parts[:, :, 1] = rng.integers(0, 3, (R, nq))
+    parts[:, :, 2] = rng.permutation(R * nq).reshape(R, nq)
+    win = global_winner(parts)
+    for q in range(nq):
+        want = min(range(R), key=lambda r: (-parts[r, q, 0], parts[r, q, 1], parts[r, q, 2]))
+        assert win[q] == want
+    rew = rng.integers(0, 3, (12, nq)) / 2.0
+    rnd = rng.integers(0, 3, (12, nq))
+    order = curriculum_order(rew, rnd)
+    for q in range(nq):
+        assert list(order[q]) == sorted(range(12), key=lambda i: (rew[i, q], rnd[i, q], i))
+
+
+def _gpu_worker(rank, world, port, q, nq=10, lam=0.0):
     from paper_2601_22397_b200 import SelectionConfig
     from paper_2601_22397_b200.sharded import ShardedExperienceBuffer
     _init(rank, world, port)
     buf = ShardedExperienceBuffer(dist, device=0)
     buf.store_synthetic(SEED, 200000, 32)
     xq = synth.queries(SEED, nq, 32)
-    out = buf.select_batch(xq, SelectionConfig(m=32, lambda_div=0.0))
+    out = buf.select_batch(xq, SelectionConfig(m=32 if lam == 0.0 else 12, lambda_div=lam))
     if rank == 0:
         q.put((buf.sigma,) + tuple(out))
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("nq", [10, 160])  # the 8-query pass / the wide tensor-core pass
-def test_sharded_select_on_device_matches_single_store(nq):
+@pytest.mark.parametrize("nq,lam", [(10, 0.0), (160, 0.0), (6, 0.1)])  # 8-query / wide / greedy
+def test_sharded_select_on_device_matches_single_store(nq, lam):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2601_22397_b200 as sair
@@ -145,7 +169,8 @@ def test_sharded_select_on_device_matches_single_store(nq):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, nq)) for r in range(world)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q, nq, lam))
+             for r in range(world)]
     for p in procs:
         p.start()
     sigma, idx, sim, sc, cnt = q.get(timeout=300)
@@ -156,7 +181,8 @@ def test_sharded_select_on_device_matches_single_store(nq):
     one.store_synthetic(SEED, 200000, 32)
     assert sigma == one.effective_sigma()
     i1, s1, c1, n1 = one.select_batch(synth.queries(SEED, nq, 32),
-                                      sair.SelectionConfig(m=32, lambda_div=0.0))
+                                      sair.SelectionConfig(m=32 if lam == 0.0 else 12,
+                                                           lambda_div=lam))
     assert np.array_equal(cnt, n1)
     assert np.array_equal(idx, i1)
     assert np.array_equal(sc, c1) and np.array_equal(sim, s1)
