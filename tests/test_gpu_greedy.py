@@ -57,3 +57,36 @@ def test_greedy_equals_per_query_pass_and_lambda_default_path():
         os.environ.pop("SAIR_NO_GREEDY")
     for a, b in zip(got, want):
         assert np.array_equal(np.asarray(a)[:5], b)
+
+
+@pytest.mark.parametrize("n,d,lam", [(20000, 100, 0.0), (20000, 100, 0.1), (70000, 200, 0.0),
+                                     (6000, 130, 0.1)])
+def test_wide_dimensions_match_oracle(orc, n, d, lam):
+    """d > 64 (the CUDA-core stream kernel up to 128, the exact passes above)."""
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(d, n, d)
+    ctx, rew, rnd = synth.contexts(d, 0, n, d), synth.rewards(d, 0, n), synth.rounds(0, n)
+    xq = synth.queries(d + 1, 5, d)
+    sigma = db.effective_sigma()
+    idx, sim, sc, cnt = db.select_batch(xq, SelectionConfig(m=10, lambda_div=lam))
+    oi, osim, osc, ocnt = orc.select_batch(ctx, rew, rnd, xq, 10, lam, sigma)
+    assert np.array_equal(idx, oi) and near(sc, osc, 1e-12)
+
+
+def test_negative_rewards_and_gate(orc):
+    """r_min < 0: negative rewards stored; |r - loo| of both signs."""
+    n, d = 30000, 12
+    rng = np.random.default_rng(5)
+    ctx = rng.normal(size=(n, d))
+    rew = rng.uniform(-2.0, 1.0, n)
+    rnd = np.arange(n, dtype=np.int32)
+    db = ExperienceBuffer(-1.5)
+    db.store_many(ctx, rew, rnd)
+    keep = rew > -1.5
+    assert db.size() == int(keep.sum()) and db.rejected() == int((~keep).sum())
+    sigma = db.effective_sigma()
+    xq = rng.normal(size=(40, d))
+    for lam in (0.0, 0.1):
+        idx, sim, sc, cnt = db.select_batch(xq, SelectionConfig(m=8, lambda_div=lam))
+        oi, osim, osc, _ = orc.select_batch(ctx[keep], rew[keep], rnd[keep], xq, 8, lam, sigma)
+        assert np.array_equal(idx, oi) and near(sc, osc, 1e-12)
