@@ -29,9 +29,16 @@ for r in rows[2:]:
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 srows = list(csv.reader(src.splitlines()))
-h = srows[1]
+hi = next(i for i, r in enumerate(srows) if "Source" in r and "Warp Stall Sampling (All Samples)" in r)
+h = srows[hi]
 isrc, ist = h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
-data = [(r[isrc], int(r[ist] or 0)) for r in srows[2:] if len(r) > ist]
+data = []
+for r in srows[hi + 1:]:
+    if len(r) > ist:
+        try:
+            data.append((r[isrc], int(r[ist] or 0)))
+        except ValueError:
+            pass
 tot = sum(n for _, n in data) or 1
 c = Counter()
 for s, n in data:
