@@ -406,6 +406,15 @@ def bench_pareto(dev):
     dt = time.perf_counter() - t0
     res["replay"] = {"rounds": T, "s_e2e": round(dt, 4), "rounds_per_s": round(T / dt, 1),
                      "final_frontier": fr.size()}
+    # configs[2] at full size for two objectives: O(T log T) counting
+    t2 = synth.tuples(SEED + 2, PARETO_T, 2, "uniform")
+    sair.dominance_counts(t2[:4096])
+    t0 = time.perf_counter()
+    _, mem2 = sair.dominance_counts(t2)
+    dt2 = time.perf_counter() - t0
+    res["dominance_counts_K2_4M"] = {"tuples": PARETO_T, "s_e2e": round(dt2, 4),
+                                     "tuples_per_s": round(PARETO_T / dt2, 1),
+                                     "frontier": int(mem2.sum())}
     for K in (2, 3, 4):
         T = 262144
         t = synth.tuples(SEED + K, T, K, "uniform")

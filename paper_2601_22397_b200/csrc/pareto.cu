@@ -17,6 +17,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <vector>
 
@@ -421,6 +423,78 @@ __global__ void __launch_bounds__(256)
     if (valid) {
         if (counts) counts[pi] = cnt;
         if (member) member[pi] = (cnt == 0 && !dup) ? 1 : 0;
+    }
+}
+
+
+// ---- K7 for two objectives: O(T log T) counting ----------------------------
+//
+// Sort by (rank_l, rank_c, arrival): j dominates i iff j sits before i with
+// rank_c(j) <= rank_c(i), except exact duplicates (equal pair), which form a
+// contiguous run.  #{earlier, c <= c_i} is counted by a bottom-up merge sort
+// of the c-ranks in that order: at the level where j (left block) and i (right
+// block) separate, i's upper_bound in the sorted left block counts every such
+// j exactly once.  count_i = that total - (duplicates before i); member_i =
+// count 0 and first of its duplicate run (pareto.cpp:36-54 keeps the first).
+
+__global__ void pair_key_kernel(const uint32_t* __restrict__ ranks, size_t T, int K,
+                                uint64_t* __restrict__ key, uint32_t* __restrict__ pos) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint64_t rl = ranks[i * K], rc = K > 1 ? ranks[i * K + 1] : 0u;
+        key[i] = (rl << 32) | rc;
+        pos[i] = (uint32_t)i;
+    }
+}
+
+// v[p] = c-rank in sorted order, id[p] = p, first[p] = start of p's run of equal keys
+__global__ void pair_init_kernel(const uint64_t* __restrict__ skey, size_t T,
+                                 uint32_t* __restrict__ v, uint32_t* __restrict__ id,
+                                 uint32_t* __restrict__ first, uint32_t* __restrict__ acc) {
+    for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < T;
+         p += (size_t)gridDim.x * blockDim.x) {
+        v[p] = (uint32_t)(skey[p] & 0xFFFFFFFFull);
+        id[p] = (uint32_t)p;
+        acc[p] = 0;
+        first[p] = (p == 0 || skey[p] != skey[p - 1]) ? (uint32_t)p : 0u;
+    }
+}
+
+// one merge level: blocks of w sorted values; right-block elements count the
+// left block's values <= theirs; both write their merged position (left first
+// on ties)
+__global__ void merge_count_kernel(const uint32_t* __restrict__ v, const uint32_t* __restrict__ id,
+                                   size_t T, size_t w, uint32_t* __restrict__ v2,
+                                   uint32_t* __restrict__ id2, uint32_t* __restrict__ acc) {
+    for (size_t x = blockIdx.x * (size_t)blockDim.x + threadIdx.x; x < T;
+         x += (size_t)gridDim.x * blockDim.x) {
+        const size_t blk = x / w, base = (blk & ~(size_t)1) * w;
+        const bool right = blk & 1;
+        const size_t lo = right ? base : base + w;  // the sibling block
+        const size_t hi = min(lo + w, T);
+        const uint32_t val = v[x];
+        size_t a = lo, b = hi;  // right: upper_bound (<= val); left: lower_bound (< val)
+        while (a < b) {
+            const size_t mid = (a + b) >> 1;
+            if (right ? v[mid] <= val : v[mid] < val) a = mid + 1; else b = mid;
+        }
+        const size_t in_sib = a - lo, own = x - (right ? base + w : base);
+        if (right) acc[id[x]] += (uint32_t)in_sib;
+        const size_t out = base + own + in_sib;
+        v2[out] = val;
+        id2[out] = id[x];
+    }
+}
+
+__global__ void pair_finish_kernel(const uint32_t* __restrict__ acc, const uint32_t* __restrict__ first,
+                                   const uint32_t* __restrict__ perm, size_t T,
+                                   uint32_t* __restrict__ counts, uint8_t* __restrict__ member) {
+    for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < T;
+         p += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t f = first[p];
+        const uint32_t c = acc[p] - (uint32_t)(p - f);
+        counts[perm[p]] = c;
+        member[perm[p]] = (c == 0 && f == p) ? 1 : 0;
     }
 }
 
@@ -974,6 +1048,40 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
         scatter_rank_kernel<<<gr, 256, 0, st>>>(rk, perm, T, K, k, ranks, rsum);
     }
     SAIR_LAUNCH("rank kernels");
+    if (K <= 2 && std::getenv("SAIR_DOM_TILES") == nullptr) {
+        // two objectives: O(T log T) merge counting (the pairwise tiles are for K >= 3)
+        if (part == 0) {
+            pair_key_kernel<<<gr, 256, 0, st>>>(ranks, T, K, key, pos);
+            size_t tb = b_tmp.bytes;
+            SAIR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, pos, perm, (int)T, 0, 64,
+                                                      st));
+            uint32_t* first = flag;    // reuse: run starts (max-scan below)
+            uint32_t* va = rk;
+            uint32_t* ida = rsum;
+            uint32_t* vb = ssum;
+            uint32_t* idb = sranks;   // >= T entries
+            pair_init_kernel<<<gr, 256, 0, st>>>(skey, T, va, ida, first, dcnt);
+            tb = b_tmp.bytes;
+            SAIR_CUDA(cub::DeviceScan::InclusiveScan(tmp, tb, first, first, cub::Max(), (int)T, st));
+            for (size_t w = 1; w < T; w <<= 1) {
+                merge_count_kernel<<<gr, 256, 0, st>>>(va, ida, T, w, vb, idb, dcnt);
+                std::swap(va, vb);
+                std::swap(ida, idb);
+            }
+            pair_finish_kernel<<<gr, 256, 0, st>>>(dcnt, first, perm, T, reinterpret_cast<uint32_t*>(ranks),
+                                                   dmem);
+            SAIR_LAUNCH("pair counting");
+            if (counts)
+                SAIR_CUDA(cudaMemcpyAsync(counts, ranks, T * 4, cudaMemcpyDeviceToHost, st));
+        } else {
+            SAIR_CUDA(cudaMemsetAsync(dmem, 0, T, st));
+            if (counts) std::memset(counts, 0, T * 4);
+        }
+        if (member) SAIR_CUDA(cudaMemcpyAsync(member, dmem, T, cudaMemcpyDeviceToHost, st));
+        SAIR_CUDA(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+        return;
+    }
     // order by rank sum
     {
         batch_keys_kernel<<<gr, 256, 0, st>>>(dt, dt, T, key, skey, pos);  // pos = iota

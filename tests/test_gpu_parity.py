@@ -369,3 +369,30 @@ def test_dominance_counts_match_oracle(orc, K):
         assert np.array_equal(cnt, ocnt) and np.array_equal(mem, omem)
         _, mem2 = sair.dominance_counts(t, counts=False)
         assert np.array_equal(mem2, omem)
+
+
+@pytest.mark.parametrize("K", [1, 2])
+@pytest.mark.parametrize("dist", ["uniform", "grid", "anti"])
+def test_two_objective_counting_equals_pairwise_tiles(K, dist):
+    """K <= 2 counts by the O(T log T) merge counting equal the pairwise tile
+    kernel (the K >= 3 path, forced with SAIR_DOM_TILES) at 150k tuples."""
+    import os
+    T = 150000
+    if dist == "anti":
+        l = np.random.default_rng(K).uniform(size=T)
+        t = np.stack([l, 1.0 - l + np.random.default_rng(K + 1).uniform(-1e-3, 1e-3, T)], 1)[:, :K]
+    else:
+        t = synth.tuples(31 + K, T, K, "grid" if dist == "grid" else "uniform")
+        if dist == "grid":
+            t = np.floor(t * 32) / 32
+    cnt, mem = sair.dominance_counts(t)
+    os.environ["SAIR_DOM_TILES"] = "1"
+    try:
+        c2, m2 = sair.dominance_counts(t)
+    finally:
+        os.environ.pop("SAIR_DOM_TILES")
+    assert np.array_equal(cnt, c2) and np.array_equal(mem, m2)
+    # and the parts combine by a sum (only part 0 does the work for K <= 2)
+    p0 = sair.dominance_counts(t, part=0, nparts=2)
+    p1 = sair.dominance_counts(t, part=1, nparts=2)
+    assert np.array_equal(p0[0] + p1[0], cnt) and np.array_equal(p0[1] | p1[1], mem)
