@@ -705,12 +705,13 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
     // could not hold a threshold-less sample
     if (npages < 512) return false;
     // Sample size: a sample of S pages leaves ~K' npages / S candidates per
-    // list, and each costs the stream pass a slow chunk (~1/8 page of work
-    // for 128 lists); S = sqrt(10 K' npages) balances the two (28% of the
-    // pages at 1M records, 7% at 16M).
+    // list, and each costs the stream pass a slow chunk; S = sqrt(5 K' npages)
+    // balances the two (measured optimum of c in sqrt(c K' npages) at 1M and
+    // 16M records: 20% / 5% of the pages).
+    const double sc = std::getenv("SAIR_SAMPLE_C") ? std::atof(std::getenv("SAIR_SAMPLE_C")) : 5.0;
     pl->spages = (uint32_t)std::min<size_t>(
         npages, std::min<size_t>(
-                    16384, std::max<size_t>(64, (size_t)std::sqrt(10.0 * pl->kp * npages))));
+                    16384, std::max<size_t>(64, (size_t)std::sqrt(sc * pl->kp * npages))));
     // per CTA and list (global memory): ~7 candidates expected at 148 CTAs;
     // 512 absorbs a few pages of concentrated high keys (a freshly appended batch)
     pl->cap = 512;
