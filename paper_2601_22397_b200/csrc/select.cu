@@ -523,6 +523,7 @@ struct RefineArgs {
     double total, two_s2, lambda, beta, gamma, key_slack_abs;
     double bq_rel;  // relative rounding of the MMA's query operand (wide pass), else 0
     int has_excl, has_excl_nn;
+    int nq;                // queries of this group (<= QB)
     const float* ckey;
     const uint32_t* cidx;  // merged, sorted [2QB][kmax]
     const float* cthr;     // [2QB]
@@ -553,8 +554,15 @@ __device__ __forceinline__ double excl_bound(const RefineArgs& a, int L, float k
     return U;
 }
 
-__global__ void __launch_bounds__(256) refine_kernel(const RefineArgs a) {
+// One launch refines every query group of a call: blockIdx.y = group (its
+// own argument block), blockIdx.x = query within the group.
+__global__ void __launch_bounds__(256) refine_kernel(const RefineArgs* __restrict__ args) {
+    __shared__ RefineArgs sa;
+    if (threadIdx.x == 0) sa = args[blockIdx.y];
+    __syncthreads();
+    const RefineArgs& a = sa;
     const int q = blockIdx.x;
+    if (q >= a.nq) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     extern __shared__ __align__(16) unsigned char sm[];
     double* score = reinterpret_cast<double*>(sm);
@@ -1017,12 +1025,6 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         const size_t lists = use_wide ? 1 : (size_t)pl.grid * 2 * qb * kmax;
         float* ck = s->b_cand.as<float>(lists * 2);
         uint32_t* ci = reinterpret_cast<uint32_t*>(ck + lists);
-        float* mk = s->b_merged.as<float>((size_t)2 * qb * kmax * 2 + 2 * qb + 4);
-        uint32_t* mi = reinterpret_cast<uint32_t*>(mk + (size_t)2 * qb * kmax);
-        float* mthr = reinterpret_cast<float*>(mi + (size_t)2 * qb * kmax);
-        unsigned int* dpmax = reinterpret_cast<unsigned int*>(mthr + 2 * qb);
-        double* zs = s->b_z.as<double>((size_t)qb * kp * d);
-        double* dc = s->b_consts.as<double>(2 * (size_t)d + (size_t)qb * d + qb);
         // One batch: the queries ql (indices into the call's queries), in groups
         // of qb; t0o (wide pass only) overrides the sampled start thresholds,
         // 2 qb floats per group (selection lists, then veto lists).
@@ -1079,6 +1081,32 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             SAIR_CUDA(cudaEventCreate(&e));
             s->gev.push_back(e);
         }
+        // per-group device state read by the one refine launch at the end:
+        // merged lists, start thresholds, dropped keys, Pmax, refine constants,
+        // the refine's standardized-row scratch
+        const size_t mstride = (size_t)2 * qb * kmax;
+        const size_t zstride = (size_t)qb * kp * d;
+        char* gbase_p = static_cast<char*>(s->b_grp.get(
+            ngroups * (mstride * 8 + 2 * qb * 4 + 2 * qb * 8 + 8 + nhc * 8 + zstride * 8) +
+            8 * 256 + ngroups * sizeof(RefineArgs)));
+        size_t goff = 0;
+        auto gtake = [&](size_t bytes) {
+            char* ptr = gbase_p + goff;
+            goff += (bytes + 255) / 256 * 256;
+            return ptr;
+        };
+        float* mk_g = reinterpret_cast<float*>(gtake(ngroups * mstride * 4));
+        uint32_t* mi_g = reinterpret_cast<uint32_t*>(gtake(ngroups * mstride * 4));
+        float* mthr_g = reinterpret_cast<float*>(gtake(ngroups * 2 * qb * 4));
+        float* t0_g = reinterpret_cast<float*>(gtake(ngroups * 2 * qb * 4));
+        unsigned int* drop_g = reinterpret_cast<unsigned int*>(gtake(ngroups * 2 * qb * 4));
+        unsigned int* pmax_g = reinterpret_cast<unsigned int*>(gtake(ngroups * 4));
+        double* dc_g = reinterpret_cast<double*>(gtake(ngroups * nhc * 8));
+        double* zs_g = reinterpret_cast<double*>(gtake(ngroups * zstride * 8));
+        RefineArgs* ra_dev = reinterpret_cast<RefineArgs*>(gtake(ngroups * sizeof(RefineArgs)));
+        RefineArgs* ra_host = reinterpret_cast<RefineArgs*>(
+            s->h_ra.get(ngroups * sizeof(RefineArgs) + 64));
+        SAIR_CUDA(cudaMemsetAsync(pmax_g, 0, ngroups * 4, s->st));
         std::vector<double> cc;
         const size_t refine_smem = (size_t)kp * (8 * 4 + 4 * 4) + 16 + (size_t)knn * 8 +
                                    (size_t)8 * 8 * (d + 1) * 8 + (size_t)(kp + knn) * 4 + 64;
@@ -1101,7 +1129,11 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             const GroupIo io{hstage_all ? hstage_all + g * hstride : nullptr, s->gev[3 * g + 1],
                              s->gev[3 * g + 2], t0o ? t0o->data() + g * 2 * qb : nullptr};
             const O D = carve(dout + g * ob);
-            SAIR_CUDA(cudaMemsetAsync(dpmax, 0, 4, s->st));
+            float* mk = mk_g + g * mstride;
+            uint32_t* mi = mi_g + g * mstride;
+            float* mthr = mthr_g + g * 2 * qb;
+            unsigned int* dpmax = pmax_g + g;
+            double* dc = dc_g + g * nhc;
             SAIR_CUDA(cudaEventRecord(s->gev[3 * g], s->st));
             if (use_wide)  // sample + stream + per-list top-K' (records e_mid, e_end)
                 wfill(s, wp, p, zgrp, nqg, c1, c0, rdelta, alpha, mk, mi, mthr, dpmax, cc, io);
@@ -1115,7 +1147,14 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             SAIR_CUDA(cudaMemcpyAsync(dc, hc, nhc * 8, cudaMemcpyHostToDevice, s->st));
             if (!use_wide)
                 launch_merge(s->st, ck, ci, pl.grid, 2 * qb, kmax, qb, kp, knn, mk, mi, mthr);
+            if (use_mma || use_wide) {  // keep this group's thresholds past the next group
+                SAIR_CUDA(cudaMemcpyAsync(t0_g + g * 2 * qb, s->mma_t0, 2 * qb * 4,
+                                          cudaMemcpyDeviceToDevice, s->st));
+                SAIR_CUDA(cudaMemcpyAsync(drop_g + g * 2 * qb, s->mma_dropped, 2 * qb * 4,
+                                          cudaMemcpyDeviceToDevice, s->st));
+            }
             RefineArgs ra{};
+            ra.nq = nqg;
             ra.x64 = s->x64;
             ra.r64 = s->r64;
             ra.rnd = s->rnd;
@@ -1147,9 +1186,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.ckey = mk;
             ra.cidx = mi;
             ra.cthr = mthr;
-            ra.t0 = use_mma || use_wide ? s->mma_t0 : nullptr;
-            ra.dropped = use_mma || use_wide ? s->mma_dropped : nullptr;
-            ra.zs = zs;
+            ra.t0 = use_mma || use_wide ? t0_g + g * 2 * qb : nullptr;
+            ra.dropped = use_mma || use_wide ? drop_g + g * 2 * qb : nullptr;
+            ra.zs = zs_g + g * zstride;
             ra.gbase = s->gbase;
             ra.out_idx = D.idx;
             ra.out_sim = D.sim;
@@ -1162,9 +1201,13 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.out_rew = D.rew;
             ra.out_round = D.round;
             ra.out_thr = D.thr;
-            refine_kernel<<<nqg, 256, refine_smem, s->st>>>(ra);
-            SAIR_LAUNCH("refine_kernel");
+            ra_host[g] = ra;
         }
+        // every group's refine in one launch
+        SAIR_CUDA(cudaMemcpyAsync(ra_dev, ra_host, ngroups * sizeof(RefineArgs),
+                                  cudaMemcpyHostToDevice, s->st));
+        refine_kernel<<<dim3((unsigned)qb, (unsigned)ngroups), 256, refine_smem, s->st>>>(ra_dev);
+        SAIR_LAUNCH("refine_kernel");
         SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob * ngroups, cudaMemcpyDeviceToHost, s->st));
         SAIR_CUDA(cudaStreamSynchronize(s->st));
         for (size_t g = 0; g < ngroups; ++g) {
