@@ -13,7 +13,7 @@
 //                      TF32, both halves accumulating into the same TMEM
 //                      columns (fp32).  The records are TF32-exact (stored
 //                      rounded), so the split keeps the fp32 filter tolerance.
-//   warps 0-7          two groups of four lane quarters take alternate pages:
+//   epilogue warps     three groups of four lane quarters take every third page:
 //                      P = ||y||^2 from the shared tile, then 32 TMEM columns
 //                      at a time (tcgen05.ld 32x32b.x32): key = log2 residual
 //                      - alpha d2 per (record, query).
@@ -49,12 +49,13 @@ using namespace umma;
 
 namespace {
 
-// warp roles: 0-7 epilogue (two groups of four TMEM lane quarters), 8-11
-// record constants (two pairs taking alternate pages; they own the shared
-// page stage), 12 producer, 13 MMA
-constexpr int WE = 8;
-constexpr int W_REC = 8, W_PROD = 12, W_MMA = 13;
-constexpr int WIDE_THREADS = 14 * 32;
+// warp roles: 0-11 epilogue (three groups of four TMEM lane quarters taking
+// every third page), 12-15 record constants (two pairs taking alternate
+// pages; they own the shared page stage), 16 producer, 17 MMA
+constexpr int WE = 12;                 // three groups of four epilogue warps
+constexpr int NEG = WE / 4;
+constexpr int W_REC = WE, W_PROD = WE + 4, W_MMA = WE + 5;
+constexpr int WIDE_THREADS = (WE + 6) * 32;
 // B operand parts: 1 = the query constants rounded to nearest TF32 (the
 // perturbation is a bounded query error the certification carries, DESIGN.md
 // "K4"); 2 = hi + lo split, two MMAs per K-step
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         // ---------------- epilogue: two groups of four lane quarters ----------------
         const int par = warp >> 2, quarter = warp & 3;
         const int rloc = quarter * 32 + lane;
-        for (uint32_t it = par; it < mine; it += 2) {
+        for (uint32_t it = par; it < mine; it += NEG) {
             const uint32_t s = it % ntm, ph = (it / ntm) & 1u;  // TMEM stage
             const uint32_t rec = page_of(it) * PAGE + rloc;
             bar_wait(&pready[it % PR], (it / PR) & 1u);
