@@ -274,6 +274,7 @@ def run_ours(a, rank, world, local_rank):
         "hbm_target": hbm_target,
     }
     if rank == 0 and world == 1 and not a.no_pareto:
+        out["config1"] = bench_config1(dev)
         out["config2"] = bench_config2(dev, a.steps)
         out["config5_step"] = bench_decision_step(buf, dev)
     if rank == 0 and not a.no_pareto:
@@ -285,6 +286,40 @@ def run_ours(a, rank, world, local_rank):
     if dist:
         dist.destroy_process_group()
     return out
+
+
+def bench_config1(dev, steps=50):
+    """configs[0]: one decision step at a time over a 10k-record buffer
+    (d = 32; the bundled scenarios' contexts are zero-padded 23 -> 32, so a
+    synthetic stand-in of that shape): select m = 8 with lambda_div = 0.1 (the
+    reference's default) and the fused veto scan, compute_reward + update
+    against the frontier, store() of the new experience -- latency per
+    decision through the public API (wall clock; each call synchronises)."""
+    import paper_2601_22397_b200 as sair
+    from paper_2601_22397_b200 import synth
+    db = sair.ExperienceBuffer(0.0, device=dev)
+    db.store_synthetic(SEED + 3, 10000, 32)
+    fr = sair.ParetoFrontier(2000.0, 10.0, device=dev)
+    rng = np.random.default_rng(SEED)
+    cfg = sair.SelectionConfig(m=8, lambda_div=0.1)
+    rc = sair.RewardConfig()
+    act = sair.ScalingAction.noop(3)
+    lat = []
+    for s in range(steps + 5):
+        x = synth.queries(SEED + 200 + s, 1, 32)
+        inp = sair.RewardInputs(rng.uniform(300, 900), rng.uniform(300, 900), rng.uniform(1, 5),
+                                rng.uniform(1, 5))
+        t0 = time.perf_counter()
+        db.select_batch(x, cfg, nearest=True)
+        r = sair.compute_reward(inp, act, fr, rc)
+        fr.update(inp.l_after_ms, inp.c_after)
+        db.store(sair.Experience(list(x[0]), act, r.total, 10000 + s))
+        if s >= 5:
+            lat.append(time.perf_counter() - t0)
+    return {"workload": "configs[0]: 10k records x d=32, k=8, lambda_div=0.1, veto scan, "
+                        "compute_reward + update + store per decision (synthetic stand-in)",
+            "us_per_decision_median": round(float(np.median(lat)) * 1e6, 1),
+            "decisions_per_s": round(1.0 / float(np.median(lat)), 1)}
 
 
 def bench_decision_step(buf, dev, P=30000, steps=3):

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -12,6 +13,13 @@
 
 namespace sair {
 
+// growth policy of the scratch buffers: sizes that creep up call by call (a
+// store growing one record per decision step) must not reallocate every call
+inline size_t grow_to(size_t need, size_t have) {
+    size_t n = std::max(need, have + have / 2);
+    return (n + 65535) & ~(size_t)65535;
+}
+
 // Grow-only device scratch buffer.
 struct DBuf {
     void* p = nullptr;
@@ -20,9 +28,10 @@ struct DBuf {
         if (need > bytes) {
             if (p) cudaFree(p);
             p = nullptr;
+            const size_t nb = grow_to(need, bytes);
             bytes = 0;
-            SAIR_CUDA(cudaMalloc(&p, need));
-            bytes = need;
+            SAIR_CUDA(cudaMalloc(&p, nb));
+            bytes = nb;
         }
         return p;
     }
@@ -44,9 +53,10 @@ struct HBuf {
         if (need > bytes) {
             if (p) cudaFreeHost(p);
             p = nullptr;
+            const size_t nb = grow_to(need, bytes);
             bytes = 0;
-            SAIR_CUDA(cudaMallocHost(&p, need));
-            bytes = need;
+            SAIR_CUDA(cudaMallocHost(&p, nb));
+            bytes = nb;
         }
         return p;
     }

@@ -1134,21 +1134,26 @@ void compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas, s
     RewardCfg rc = check_cfg(cfg);
     if (T == 0) return;
     DeviceGuard g(f->device);
-    size_t dbytes = T * S * 4 * 4;
-    char* base = static_cast<char*>(f->b_in.get(T * 32 + dbytes + T * 56 + 1024));
+    // one pinned staging buffer: inputs | deltas in, breakdowns out (a decision
+    // step scores one row: one copy each way, no pageable staging)
+    const size_t dbytes = T * S * 4 * 4;
+    const size_t inb = T * 32 + ((dbytes + 255) & ~(size_t)255);
+    char* base = static_cast<char*>(f->b_in.get(inb + T * 56 + 1024));
+    char* hb = static_cast<char*>(f->h_io.get(inb + T * 56 + 1024));
+    std::memcpy(hb, in, T * 32);
+    if (dbytes) std::memcpy(hb + T * 32, deltas, dbytes);
     double* din = reinterpret_cast<double*>(base);
-    int32_t* dd = reinterpret_cast<int32_t*>(din + 4 * T);
-    double* dout = reinterpret_cast<double*>(base + T * 32 + (dbytes + 255) / 256 * 256);
-    SAIR_CUDA(cudaMemcpyAsync(din, in, T * 32, cudaMemcpyHostToDevice, f->st));
-    if (dbytes) SAIR_CUDA(cudaMemcpyAsync(dd, deltas, dbytes, cudaMemcpyHostToDevice, f->st));
+    int32_t* dd = reinterpret_cast<int32_t*>(base + T * 32);
+    double* dout = reinterpret_cast<double*>(base + inb);
+    SAIR_CUDA(cudaMemcpyAsync(base, hb, T * 32 + dbytes, cudaMemcpyHostToDevice, f->st));
     reward_kernel<<<grid_for(T), 256, 0, f->st>>>(din, dd, S, T, view(f), f->l_max, f->c_max, rc,
                                                   dout);
     SAIR_LAUNCH("reward_kernel");
-    std::vector<double> h(7 * T);
-    SAIR_CUDA(cudaMemcpyAsync(h.data(), dout, T * 56, cudaMemcpyDeviceToHost, f->st));
+    const double* h = reinterpret_cast<const double*>(hb + inb);
+    SAIR_CUDA(cudaMemcpyAsync(hb + inb, dout, T * 56, cudaMemcpyDeviceToHost, f->st));
     SAIR_CUDA(cudaStreamSynchronize(f->st));
     for (size_t t = 0; t < T; ++t) {
-        const double* o = h.data() + 7 * t;
+        const double* o = h + 7 * t;
         out[t] = sair_reward_breakdown{o[0], o[1], o[2], o[3], o[4], o[5], o[6] != 0.0};
     }
 }
