@@ -149,7 +149,10 @@ def run_ours(a, rank, world, local_rank):
     import paper_2601_22397_b200 as sair
     from paper_2601_22397_b200 import synth
 
-    dev = local_rank
+    # one GPU per rank; SAIR_BENCH_BACKEND=gloo (with ranks sharing the
+    # visible GPUs) only exercises the multi-rank code path on a smaller box
+    backend = os.environ.get("SAIR_BENCH_BACKEND", "nccl")
+    dev = local_rank % max(1, torch.cuda.device_count()) if backend != "nccl" else local_rank
     torch.cuda.set_device(dev)
     dist = None
     n_total = a.records
@@ -158,7 +161,10 @@ def run_ours(a, rank, world, local_rank):
     if world > 1:
         import torch.distributed as dist
         from paper_2601_22397_b200.sharded import ShardedExperienceBuffer, shard_range
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
         lo, hi = shard_range(n_total, rank, world)
         sharded = ShardedExperienceBuffer(dist, dev)
         sharded.store_synthetic(SEED, n_total, DIM)
@@ -196,7 +202,7 @@ def run_ours(a, rank, world, local_rank):
             dist.barrier()
         ms = e0.elapsed_time(e1)
         if dist:
-            t = torch.tensor([ms], device=f"cuda:{dev}")
+            t = torch.tensor([ms], device=f"cuda:{dev}" if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, stats
@@ -216,7 +222,8 @@ def run_ours(a, rank, world, local_rank):
         dist.barrier()
     e2e_s = time.perf_counter() - t0
     if dist:
-        t = torch.tensor([e2e_s], device=f"cuda:{dev}", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device=f"cuda:{dev}" if backend == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e = a.steps * a.queries / e2e_s
@@ -232,8 +239,12 @@ def run_ours(a, rank, world, local_rank):
     roof["traffic"] = None
     if tp.exists():
         tj = json.loads(tp.read_text()).get(roof["kernel"].split(" ")[0], {})
-        roof["traffic"] = tj.get("dram_bytes_per_launch")
-        roof["traffic_source"] = tj.get("source")
+        if tj.get("dram_bytes_per_launch"):
+            # ncu capture of a 16M-record launch; a shard's launch reads its share
+            scale = (hi - lo) / float(tj.get("records", N_RECORDS))
+            roof["traffic"] = round(tj["dram_bytes_per_launch"] * scale)
+            roof["traffic_source"] = tj.get("source") + (
+                f", scaled x{scale:.3f} to this rank's records" if scale != 1.0 else "")
     gpu_launches = _launches(stats) + (a.steps if dist else 0)
 
     # the north star's HBM target: Q = 8 queries per step, one memory-bound pass
