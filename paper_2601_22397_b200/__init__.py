@@ -160,7 +160,10 @@ class ExperienceBuffer:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().sair_store_destroy(h)
+            try:
+                lib().sair_store_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     # value semantics (experience.hpp:45)
@@ -388,7 +391,10 @@ class ParetoFrontier:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().sair_frontier_destroy(h)
+            try:
+                lib().sair_frontier_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def copy(self) -> "ParetoFrontier":
@@ -658,7 +664,10 @@ class FrontierSet:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().sair_frontier_set_destroy(h)
+            try:
+                lib().sair_frontier_set_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def step(self, inputs, deltas, update, cfg: RewardConfig):

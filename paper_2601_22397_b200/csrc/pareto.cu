@@ -161,12 +161,29 @@ __device__ __forceinline__ void f_normalize(double l_max, double c_max, double l
 
 // ----------------------------------------------------------------- kernels --
 
+// K8: one tuple per thread; a frontier of up to SCORE_SMEM_F points is staged
+// in shared memory (every tuple's binary search and scans hit it), tuples are
+// read as one 16-byte load
+constexpr size_t SCORE_SMEM_F = 4096;
 __global__ void score_batch_kernel(FrontierView f, const double* __restrict__ pts, size_t T,
                                    double* __restrict__ out, uint8_t* __restrict__ dom_out) {
+    extern __shared__ double fs[];  // [F] l | [F] c  (when staged)
+    FrontierView v = f;
+    if (f.F <= SCORE_SMEM_F) {
+        for (size_t i = threadIdx.x; i < f.F; i += blockDim.x) {
+            fs[i] = f.l[i];
+            fs[f.F + i] = f.c[i];
+        }
+        __syncthreads();
+        v.l = fs;
+        v.c = fs + f.F;
+    }
+    const double2* p2 = reinterpret_cast<const double2*>(pts);
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < T;
          t += (size_t)gridDim.x * blockDim.x) {
+        const double2 q = p2[t];
         bool dm;
-        out[t] = f_reward(f, pts[2 * t], pts[2 * t + 1], &dm);
+        out[t] = f_reward(v, q.x, q.y, &dm);
         if (dom_out) dom_out[t] = dm;
     }
 }
@@ -782,6 +799,14 @@ static int grid_for(size_t n, int threads = 256) {
 
 static FrontierView view(const sair_frontier_s* f) { return FrontierView{f->fl, f->fc, f->F, f->hv}; }
 
+static size_t score_smem(size_t F) {
+    if (F > SCORE_SMEM_F) return 0;
+    const size_t b = F * 16;
+    if (b > 48 * 1024) cudaFuncSetAttribute(score_batch_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
+    return b;
+}
+
 void frontier_init(sair_frontier_s* f, double l_max, double c_max, int device) {
     // pareto.cpp:14-18
     if (l_max <= 0.0 || c_max <= 0.0)
@@ -979,7 +1004,7 @@ void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
     double* dout = dp + 2 * T;
     uint8_t* ddom = reinterpret_cast<uint8_t*>(dout + T);
     SAIR_CUDA(cudaMemcpyAsync(dp, pts, T * 16, cudaMemcpyHostToDevice, f->st));
-    score_batch_kernel<<<grid_for(T), 256, 0, f->st>>>(view(f), dp, T, dout, ddom);
+    score_batch_kernel<<<grid_for(T), 256, score_smem(f->F), f->st>>>(view(f), dp, T, dout, ddom);
     SAIR_LAUNCH("score_batch_kernel");
     SAIR_CUDA(cudaMemcpyAsync(out, dout, T * 8, cudaMemcpyDeviceToHost, f->st));
     if (dom) SAIR_CUDA(cudaMemcpyAsync(dom, ddom, T, cudaMemcpyDeviceToHost, f->st));
@@ -989,7 +1014,7 @@ void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
 // device-pointer variant (bench: tuples resident in HBM)
 void frontier_score_batch_device(sair_frontier_s* f, const double* dpts, size_t T, double* dout,
                                  uint8_t* ddom, cudaStream_t st) {
-    score_batch_kernel<<<grid_for(T), 256, 0, st>>>(view(f), dpts, T, dout, ddom);
+    score_batch_kernel<<<grid_for(T), 256, score_smem(f->F), st>>>(view(f), dpts, T, dout, ddom);
     SAIR_LAUNCH("score_batch_kernel");
 }
 
