@@ -7,7 +7,7 @@
 // queries, then `want` greedy steps.  State per (query, record): score, penalty
 // (fp64) and a taken flag, so a step is one pass:
 //   greedy_step_kernel   a CTA holds 128 records' standardized rows in shared
-//                        memory (dimension-major) and, two queries at a time
+//                        memory (dimension-major) and, four queries at a time
 //                        (independent fp64 chains), adds sim(z_i, z_pick) of
 //                        the previous step's pick to the penalty (:283-284, in
 //                        pick order), forms the gain score - lambda pen (:270)
@@ -54,22 +54,6 @@ struct GreedyArgs {
     int nblk;             // warps over the store (nwarp)
 };
 
-// d2 of this thread's record (dimension-major tile) to two rows at once: two
-// independent chains, each summed in k order (similarity(), :125-130)
-__device__ __forceinline__ void d2_pair(const double* zt, const double* za, const double* zb, int d,
-                                        double& d2a, double& d2b) {
-    double x = 0.0, y = 0.0;
-#pragma unroll 4
-    for (int k = 0; k < d; ++k) {
-        const double v = zt[k * GT];
-        const double ta = dsub(v, za[k]), tb = dsub(v, zb[k]);
-        x = dadd(x, dmul(ta, ta));
-        y = dadd(y, dmul(tb, tb));
-    }
-    d2a = x;
-    d2b = y;
-}
-
 // step 0 (score = exact surprisal score, pen = 0) or step t > 0 (penalty update
 // with the pick of step t - 1), then each warp's best gain per query
 __global__ void __launch_bounds__(GT) greedy_step_kernel(const GreedyArgs a, int step) {
@@ -93,25 +77,50 @@ __global__ void __launch_bounds__(GT) greedy_step_kernel(const GreedyArgs a, int
         if (step == 0 || pen_step)
             for (int e = threadIdx.x; e < gn * d; e += GT) rows[e] = src[(size_t)g0 * d + e];
         __syncthreads();
-        for (int gg = 0; gg < gn; gg += 2) {
-            const int g1 = g0 + gg, g2 = min(g1 + 1, g0 + gn - 1);
-            double d2a = 0.0, d2b = 0.0;
-            const size_t o1 = (size_t)g1 * a.n + i, o2 = (size_t)g2 * a.n + i;
-            const bool live1 = valid && (step == 0 || !a.taken[o1]);
-            const bool live2 = valid && (step == 0 || !a.taken[o2]);
-            if ((step == 0 || pen_step) && (live1 || live2))
-                d2_pair(mine, rows + (size_t)gg * d, rows + (size_t)(g2 - g0) * d, d, d2a, d2b);
-            for (int h = 0; h < 2; ++h) {
-                const int g = h ? g2 : g1;
-                if (h && g2 == g1) break;
-                const size_t o = h ? o2 : o1;
-                const bool live = h ? live2 : live1;
-                const double d2 = h ? d2b : d2a;
+        for (int gg = 0; gg < gn; gg += 4) {
+            // four queries at a time: four independent fp64 chains per record,
+            // their state loaded before the chains so the loads overlap them
+            int gq[4];
+            size_t oq[4];
+            bool live[4];
+            double scq[4] = {0.0, 0.0, 0.0, 0.0}, pnq[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                gq[h] = g0 + min(gg + h, gn - 1);
+                oq[h] = (size_t)gq[h] * a.n + i;
+                live[h] = valid && gg + h < gn && (step == 0 || !a.taken[oq[h]]);
+                if (step > 0 && live[h]) {
+                    scq[h] = a.score[oq[h]];
+                    if (pen_step) pnq[h] = a.pen[oq[h]];
+                }
+            }
+            double x[4] = {0.0, 0.0, 0.0, 0.0};
+            if ((step == 0 || pen_step) && (live[0] || live[1] || live[2] || live[3])) {
+                const double* r0 = rows + (size_t)(gq[0] - g0) * d;
+                const double* r1 = rows + (size_t)(gq[1] - g0) * d;
+                const double* r2 = rows + (size_t)(gq[2] - g0) * d;
+                const double* r3 = rows + (size_t)(gq[3] - g0) * d;
+#pragma unroll 2
+                for (int k = 0; k < d; ++k) {  // similarity(), :125-130, each in k order
+                    const double v = mine[k * GT];
+                    const double t0 = dsub(v, r0[k]), t1 = dsub(v, r1[k]);
+                    const double t2 = dsub(v, r2[k]), t3 = dsub(v, r3[k]);
+                    x[0] = dadd(x[0], dmul(t0, t0));
+                    x[1] = dadd(x[1], dmul(t1, t1));
+                    x[2] = dadd(x[2], dmul(t2, t2));
+                    x[3] = dadd(x[3], dmul(t3, t3));
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                if (gg + h >= gn) break;
+                const int g = gq[h];
+                const size_t o = oq[h];
                 Best b{0.0, 0, 0, -1};
                 if (step == 0) {
                     Best nb{0.0, 0, 0, -1};
                     if (valid) {
-                        const double s = sim_from_d2(d2, a.two_s2);
+                        const double s = sim_from_d2(x[h], a.two_s2);
                         const double r = a.r64[i];
                         const double loo = a.loo ? a.loo[i]
                                                  : (a.n_loo <= 1 ? 0.0
@@ -128,13 +137,13 @@ __global__ void __launch_bounds__(GT) greedy_step_kernel(const GreedyArgs a, int
                         nb = warp_best(nb);
                         if (lane == 0) a.part_nn[(size_t)g * a.nblk + wslot] = nb;
                     }
-                } else if (live) {
+                } else if (live[h]) {
                     double pn = 0.0;
                     if (pen_step) {
-                        pn = dadd(a.pen[o], sim_from_d2(d2, a.two_s2));  // :283-284
+                        pn = dadd(pnq[h], sim_from_d2(x[h], a.two_s2));  // :283-284
                         a.pen[o] = pn;
                     }
-                    b = Best{dsub(a.score[o], dmul(a.lambda, pn)), a.rnd[i], (int64_t)i, 1};
+                    b = Best{dsub(scq[h], dmul(a.lambda, pn)), a.rnd[i], (int64_t)i, 1};
                 }
                 b = warp_best(b);
                 if (lane == 0) a.part[(size_t)g * a.nblk + wslot] = b;
