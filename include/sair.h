@@ -216,6 +216,12 @@ SAIR_API sair_status sair_store_select_shard(sair_store_t h, const double* queri
                                              int64_t* out_idx, double* out_sim,
                                              double* out_score, double* out_reward,
                                              int32_t* out_round, size_t* out_count);
+/* sair_merge_topk on an all-gathered DEVICE buffer (NCCL): d_parts is
+ * [nshards][nq][5m + 1] doubles (per rank: score[m], sim[m], reward[m],
+ * global index[m], round[m], count), d_out [nq][3m + 1] (index[m], sim[m],
+ * score[m], count), ordered on `stream` (a cudaStream_t, 0 = default). */
+SAIR_API sair_status sair_merge_topk_packed(const double* d_parts, size_t nshards, size_t nq,
+                                            size_t m, int device, void* stream, double* d_out);
 /* The shard's side of select() for lambda_div > 0 on a buffer spread over
  * ranks (experience.cpp:261-285 with the arg-max taken across shards by the
  * caller between steps; sharded.py).  greedy_begin scores this shard for nq

@@ -88,6 +88,8 @@ SIGNATURES = {
     "sair_store_greedy_begin": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int,
                                           C.POINTER(SelectConfigC), _dp]),
     "sair_store_greedy_next": (C.c_int, [_vp, C.POINTER(C.c_int64), _dp, _dp]),
+    "sair_merge_topk_packed": (C.c_int, [_vp, C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, _vp,
+                                         _vp]),
     "sair_store_last_stats": (C.c_int, [_vp, C.POINTER(SelectStatsC)]),
     "sair_store_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
     "sair_store_set_shard": (C.c_int, [_vp, C.c_int64]),

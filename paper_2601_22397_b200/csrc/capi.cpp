@@ -345,6 +345,15 @@ sair_status sair_merge_topk(const double* score, const double* sim, const double
     });
 }
 
+sair_status sair_merge_topk_packed(const double* d_parts, size_t nshards, size_t nq, size_t m,
+                                   int device, void* stream, double* d_out) {
+    if (nq && (!d_parts || !d_out)) return bad("null input");
+    if (m > 4096) return bad("merge: m too large");
+    return guard([&] {
+        sair::merge_packed(d_parts, nshards, nq, m, device, static_cast<cudaStream_t>(stream), d_out);
+    });
+}
+
 sair_status sair_store_stream(sair_store_t h, void** stream) {
     if (!h || !stream) return bad("null handle");
     *stream = h->st;

@@ -188,6 +188,8 @@ void merge_topk(const double* score, const double* sim, const double* reward,
                 const int32_t* round, const int64_t* gidx, const size_t* count, size_t nshards,
                 size_t nq, size_t m, int device, int64_t* out_idx, double* out_sim,
                 double* out_score, size_t* out_count);
+void merge_packed(const double* parts, size_t nshards, size_t nq, size_t m, int device,
+                  cudaStream_t st, double* out);
 double store_surprisal(sair_store_s* s, size_t index, const double* x,
                        const sair_select_config& cfg);
 

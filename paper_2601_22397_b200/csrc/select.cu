@@ -1370,6 +1370,72 @@ __global__ void merge_topk_kernel(const double* __restrict__ score, const double
     if (threadIdx.x == 0) o_cnt[q] = want;
 }
 
+// The same merge on an all-gathered device buffer (sharded.py, NCCL):
+// parts [nshards][nq][5m + 1] doubles per rank -- score[m], sim[m], reward[m],
+// global index[m], round[m], count -- into out [nq][3m + 1]: index[m], sim[m],
+// score[m], count.
+__global__ void merge_packed_kernel(const double* __restrict__ parts, int nshards, int nq, int m,
+                                    double* __restrict__ out) {
+    extern __shared__ int picks_sh[];  // [m] pick order, then [m] curriculum order
+    int* order = picks_sh + m;
+    const int q = blockIdx.x;
+    const int W = 5 * m + 1, total = nshards * m;
+    auto row = [&](int sh) { return parts + ((size_t)sh * nq + q) * W; };
+    auto cnt = [&](int sh) { return (int)row(sh)[5 * m]; };
+    auto valid = [&](int e) { return e % m < cnt(e / m); };
+    auto best_of = [&](int e) {
+        const double* r = row(e / m);
+        const int j = e % m;
+        return Best{r[j], (int32_t)r[4 * m + j], (int64_t)r[3 * m + j], 1};
+    };
+    int want = 0;
+    for (int sh = 0; sh < nshards; ++sh) want += cnt(sh);
+    want = min(want, m);
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        if (!valid(e)) continue;
+        const Best be = best_of(e);
+        int rank = 0;
+        for (int f = 0; f < total; ++f) {
+            if (f == e || !valid(f)) continue;
+            rank += better(best_of(f), be);
+        }
+        if (rank < want) picks_sh[rank] = e;
+    }
+    __syncthreads();
+    auto rw = [&](int e) { return row(e / m)[2 * m + e % m]; };
+    auto rd = [&](int e) { return row(e / m)[4 * m + e % m]; };
+    for (int x = threadIdx.x; x < want; x += blockDim.x) {
+        const int v = picks_sh[x];
+        int pos = 0;
+        for (int y = 0; y < want; ++y) {
+            const int u = picks_sh[y];
+            const bool less = rw(u) != rw(v) ? rw(u) < rw(v) : rd(u) < rd(v);
+            const bool same = rw(u) == rw(v) && rd(u) == rd(v);
+            pos += less || (same && y < x);
+        }
+        order[pos] = v;
+    }
+    __syncthreads();
+    double* o = out + (size_t)q * (3 * m + 1);
+    for (int x = threadIdx.x; x < want; x += blockDim.x) {
+        const double* r = row(order[x] / m);
+        const int j = order[x] % m;
+        o[x] = r[3 * m + j];
+        o[m + x] = r[m + j];
+        o[2 * m + x] = r[j];
+    }
+    if (threadIdx.x == 0) o[3 * m] = (double)want;
+}
+
+void merge_packed(const double* parts, size_t nshards, size_t nq, size_t m, int device,
+                  cudaStream_t st, double* out) {
+    if (nq == 0 || m == 0) return;
+    DeviceGuard g(device);
+    merge_packed_kernel<<<(int)nq, 256, 2 * m * sizeof(int), st>>>(parts, (int)nshards, (int)nq,
+                                                                  (int)m, out);
+    SAIR_LAUNCH("merge_packed_kernel");
+}
+
 void merge_topk(const double* score, const double* sim, const double* reward,
                 const int32_t* round, const int64_t* gidx, const size_t* count, size_t nshards,
                 size_t nq, size_t m, int device, int64_t* out_idx, double* out_sim,

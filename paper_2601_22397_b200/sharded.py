@@ -170,8 +170,7 @@ class ShardedExperienceBuffer:
         nq, m = idx.shape
         pack = np.concatenate([sc, sim, rw, idx.astype(np.float64), rd.astype(np.float64),
                                cnt.astype(np.float64)[:, None]], axis=1)
-        parts = _all_gather(self.dist, pack, f"cuda:{self.device}")
-        return merge_parts(parts, nq, m, self.device)
+        return merge_gathered(self.dist, pack, nq, m, self.device)
 
 
     def _select_greedy(self, queries, cfg: SelectionConfig):
@@ -225,6 +224,35 @@ def curriculum_order(reward: np.ndarray, rnd: np.ndarray) -> np.ndarray:
     want, nq = reward.shape
     pos = np.arange(want)
     return np.stack([np.lexsort((pos, rnd[:, q], reward[:, q])) for q in range(nq)])
+
+
+def merge_gathered(dist, pack: np.ndarray, nq: int, m: int, device: int):
+    """All-gather every rank's packed top-m ([nq][5m + 1]) into one device
+    tensor and merge it there (sair_merge_topk_packed): one host->device copy
+    of this rank's part, the collective, the merge kernel, and one
+    device->host copy of the [nq][3m + 1] result."""
+    import torch
+    R = dist.get_world_size()
+    dev = torch.device("cuda", device)
+    t = torch.from_numpy(np.ascontiguousarray(pack))
+    if dist.get_backend() == "nccl":
+        t = t.to(dev)
+        gathered = torch.empty((R,) + tuple(t.shape), dtype=t.dtype, device=dev)
+        dist.all_gather_into_tensor(gathered, t)
+    else:  # gloo: gather on the host, merge on the device
+        parts = [torch.empty_like(t) for _ in range(R)]
+        dist.all_gather(parts, t)
+        gathered = torch.stack(parts).to(dev)
+    out = torch.empty((nq, 3 * m + 1), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _check(lib().sair_merge_topk_packed(gathered.data_ptr(), R, nq, m, device, stream,
+                                        out.data_ptr()))
+    o = out.cpu().numpy()
+    cnt = o[:, 3 * m].astype(np.int64)
+    idx = o[:, :m].astype(np.int64)
+    for q in range(nq):
+        idx[q, cnt[q]:] = -1
+    return idx, o[:, m:2 * m].copy(), o[:, 2 * m:3 * m].copy(), cnt
 
 
 def merge_parts(parts: List[np.ndarray], nq: int, m: int, device: int):
