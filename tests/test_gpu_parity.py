@@ -396,3 +396,34 @@ def test_two_objective_counting_equals_pairwise_tiles(K, dist):
     p0 = sair.dominance_counts(t, part=0, nparts=2)
     p1 = sair.dominance_counts(t, part=1, nparts=2)
     assert np.array_equal(p0[0] + p1[0], cnt) and np.array_equal(p0[1] | p1[1], mem)
+
+
+def test_shard_merges_agree():
+    """The two cross-shard merges (host arrays: sair_merge_topk; the
+    all-gathered device buffer: sair_merge_topk_packed) on random per-shard
+    top-m with ties in score and round and ragged counts."""
+    import ctypes as C
+    from paper_2601_22397_b200 import _lib
+    from paper_2601_22397_b200.sharded import merge_parts
+    rng = np.random.default_rng(8)
+    R, nq, m = 3, 60, 8
+    parts = []
+    gid = rng.permutation(R * nq * m).reshape(R, nq, m)
+    for r in range(R):
+        sc = np.sort(rng.integers(0, 6, (nq, m)) / 8.0, axis=1)[:, ::-1]
+        cnt = rng.integers(0, m + 1, nq)
+        parts.append(np.concatenate([sc, rng.uniform(size=(nq, m)), rng.integers(0, 3, (nq, m)) / 2.0,
+                                     gid[r].astype(np.float64), rng.integers(0, 4, (nq, m)).astype(np.float64),
+                                     cnt[:, None].astype(np.float64)], axis=1))
+    i1, s1, c1, n1 = merge_parts(parts, nq, m, 0)
+    dev = torch.from_numpy(np.stack(parts)).cuda()
+    out = torch.empty((nq, 3 * m + 1), dtype=torch.float64, device="cuda")
+    assert sair.lib().sair_merge_topk_packed(dev.data_ptr(), R, nq, m, 0, None, out.data_ptr()) == 0
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    n2 = o[:, 3 * m].astype(np.int64)
+    assert np.array_equal(n1, n2)
+    for q in range(nq):
+        k = n1[q]
+        assert np.array_equal(i1[q, :k], o[q, :k].astype(np.int64))
+        assert np.array_equal(s1[q, :k], o[q, m:m + k]) and np.array_equal(c1[q, :k], o[q, 2 * m:2 * m + k])
