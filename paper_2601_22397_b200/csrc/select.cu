@@ -349,7 +349,14 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
 __global__ void __launch_bounds__(1024)
     merge_kernel(const float* __restrict__ in_key, const uint32_t* __restrict__ in_idx, int G,
                  int lists_stride, int kmax, int kout, int QB, int kp, int knn, float* __restrict__ out_key,
-                 uint32_t* __restrict__ out_idx, float* __restrict__ out_thr) {
+                 uint32_t* __restrict__ out_idx, float* __restrict__ out_thr, size_t in_g,
+                 size_t out_g) {
+    // blockIdx.y: a query group (in_g / out_g: its input / output strides)
+    in_key += blockIdx.y * in_g;
+    in_idx += blockIdx.y * in_g;
+    out_key += blockIdx.y * out_g;
+    out_idx += blockIdx.y * out_g;
+    out_thr += blockIdx.y * (size_t)lists_stride;
     const int L = blockIdx.x;
     const int K = L < QB ? kp : knn;
     const int total = G * K;
@@ -473,7 +480,12 @@ __global__ void __launch_bounds__(1024)
     merge_reg_kernel(const float* __restrict__ in_key, const uint32_t* __restrict__ in_idx, int G,
                      int lists_stride, int kmax, int kout, int QB, int kp, int knn,
                      float* __restrict__ out_key, uint32_t* __restrict__ out_idx,
-                     float* __restrict__ out_thr) {
+                     float* __restrict__ out_thr, size_t in_g, size_t out_g) {
+    in_key += blockIdx.y * in_g;
+    in_idx += blockIdx.y * in_g;
+    out_key += blockIdx.y * out_g;
+    out_idx += blockIdx.y * out_g;
+    out_thr += blockIdx.y * (size_t)lists_stride;
     const int L = blockIdx.x;
     const int K = L < QB ? kp : knn;
     auto load = [&](int e, float& key, uint32_t& idx) {
@@ -491,18 +503,20 @@ __global__ void __launch_bounds__(1024)
 // one.  Inputs [G][lists][kmax] with K entries per CTA list; outputs
 // [2 qb][kout] (kout = kmax unless the caller's input stride is larger).
 void launch_merge(cudaStream_t st, const float* ck, const uint32_t* ci, int G, int lists, int kmax,
-                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr, int kout) {
+                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr, int kout,
+                  int ngroups, size_t in_g, size_t out_g) {
     if (kout <= 0) kout = kmax;
-    const int nb = knn ? 2 * qb : qb;
+    const dim3 nb((unsigned)(knn ? 2 * qb : qb), (unsigned)ngroups);
     const size_t total = (size_t)G * std::max(kp, knn);
     if (total <= 4 * 1024)
         merge_reg_kernel<4><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, kout, qb, kp, knn, mk, mi,
-                                                 mthr);
+                                                 mthr, in_g, out_g);
     else if (total <= 16 * 1024)
         merge_reg_kernel<16><<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, kout, qb, kp, knn, mk, mi,
-                                                  mthr);
+                                                  mthr, in_g, out_g);
     else
-        merge_kernel<<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, kout, qb, kp, knn, mk, mi, mthr);
+        merge_kernel<<<nb, 1024, 0, st>>>(ck, ci, G, lists, kmax, kout, qb, kp, knn, mk, mi, mthr,
+                                          in_g, out_g);
     SAIR_LAUNCH("merge_kernel");
 }
 
@@ -1104,6 +1118,10 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         double* dc_g = reinterpret_cast<double*>(gtake(ngroups * nhc * 8));
         double* zs_g = reinterpret_cast<double*>(gtake(ngroups * zstride * 8));
         RefineArgs* ra_dev = reinterpret_cast<RefineArgs*>(gtake(ngroups * sizeof(RefineArgs)));
+        // the wide pass's compacted CTA lists of every group (merged in one launch)
+        const size_t lstride = use_wide ? (size_t)wp.grid * 2 * qb * kmax : 0;
+        float* lk_g = use_wide ? s->b_wlists.as<float>(ngroups * lstride * 2) : nullptr;
+        uint32_t* li_g = use_wide ? reinterpret_cast<uint32_t*>(lk_g + ngroups * lstride) : nullptr;
         RefineArgs* ra_host = reinterpret_cast<RefineArgs*>(
             s->h_ra.get(ngroups * sizeof(RefineArgs) + 64));
         SAIR_CUDA(cudaMemsetAsync(pmax_g, 0, ngroups * 4, s->st));
@@ -1127,7 +1145,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                 for (int k = 0; k < d; ++k) hc[2 * (size_t)d + (size_t)qq * d + k] = z[k];
             }
             const GroupIo io{hstage_all ? hstage_all + g * hstride : nullptr, s->gev[3 * g + 1],
-                             s->gev[3 * g + 2], t0o ? t0o->data() + g * 2 * qb : nullptr};
+                             s->gev[3 * g + 2], t0o ? t0o->data() + g * 2 * qb : nullptr,
+                             use_wide ? lk_g + g * lstride : nullptr,
+                             use_wide ? li_g + g * lstride : nullptr};
             const O D = carve(dout + g * ob);
             float* mk = mk_g + g * mstride;
             uint32_t* mi = mi_g + g * mstride;
@@ -1203,6 +1223,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.out_thr = D.thr;
             ra_host[g] = ra;
         }
+        if (use_wide)  // every group's per-query top-K' across its CTA lists, one launch
+            launch_merge(s->st, lk_g, li_g, wp.grid, 2 * qb, kmax, qb, kp, knn, mk_g, mi_g, mthr_g,
+                         kmax, (int)ngroups, lstride, mstride);
         // every group's refine in one launch
         SAIR_CUDA(cudaMemcpyAsync(ra_dev, ra_host, ngroups * sizeof(RefineArgs),
                                   cudaMemcpyHostToDevice, s->st));

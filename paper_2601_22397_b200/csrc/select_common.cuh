@@ -66,6 +66,8 @@ struct GroupIo {
     float* hstage;
     cudaEvent_t e_mid, e_end;
     const float* t0_override;  // wide pass: [2 QW] start thresholds (skip the sample pass)
+    float* lists_key;          // wide pass: compacted CTA lists out, [grid][2 QW][kmax]
+    uint32_t* lists_idx;
 };
 
 // select_mma.cu: the tcgen05 streaming kernel (plan + launcher)
@@ -106,7 +108,8 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
 
 // select.cu: global top-K' of every list across per-CTA lists [G][lists][kmax]
 void launch_merge(cudaStream_t st, const float* ck, const uint32_t* ci, int G, int lists, int kmax,
-                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr, int kout = 0);
+                  int qb, int kp, int knn, float* mk, uint32_t* mi, float* mthr, int kout = 0,
+                  int ngroups = 1, size_t in_gstride = 0, size_t out_gstride = 0);
 
 // standardize() of every stored row into z [d][n] (select_small.cu)
 void zrows_launch(const double* x64, const double* mean, const double* sd, size_t n, int d,

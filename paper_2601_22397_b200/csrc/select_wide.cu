@@ -75,6 +75,9 @@ struct WideArgs {
     unsigned int* dropped;    // [2QW] max ordinal of a key dropped on a full list
     uint32_t cap;             // per-CTA list capacity
     int kp, kv;               // K' of the selection / veto lists
+    float* okey;              // compacted lists out: [grid][2QW][kout] (the merge's input)
+    uint32_t* oidx;
+    int kout;
     unsigned int* pmax;       // max P over records (float bits)
     uint32_t tcols;           // TMEM columns allocated (power of two >= ntm * QW)
     int probe;                // diagnostics (SAIR_PROBE_WIDE=1): skip the epilogue math
@@ -428,9 +431,11 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                     warp_keep_topk(a.lkey + o, a.lidx + o, c, K, whist + warp * 256, lane);
                     c = K;
                 }
-                for (int j = c + lane; j < K; j += 32) {
-                    a.lkey[o + j] = -INFINITY;
-                    a.lidx[o + j] = 0xFFFFFFFFu - (uint32_t)j;
+                const size_t oo = ((size_t)blockIdx.x * 2 * QW + L) * a.kout;
+                for (int j = lane; j < K; j += 32) {
+                    const bool have = j < c;
+                    a.okey[oo + j] = have ? a.lkey[o + j] : -INFINITY;
+                    a.oidx[oo + j] = have ? a.lidx[o + j] : 0xFFFFFFFFu - (uint32_t)j;
                 }
                 if (lane == 0 && sdrop[L]) atomicMax(&a.dropped[L], sdrop[L]);
             }
@@ -623,6 +628,9 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.cap = pl.cap;
     a.kp = pl.kp;
     a.kv = pl.knn;
+    a.okey = io.lists_key;
+    a.oidx = io.lists_idx;
+    a.kout = pl.kmax;
     a.pmax = pmax;
     a.probe = std::getenv("SAIR_PROBE_WIDE") ? std::atoi(std::getenv("SAIR_PROBE_WIDE")) : 0;
     a.tcols = 32;
@@ -644,9 +652,11 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     stream_wide_kernel<DP, QW><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
     SAIR_LAUNCH("stream_wide_kernel(stream)");
     SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
-    // per-query top-K' across the CTAs' compacted lists ([G][2QW][cap], K' each)
-    launch_merge(s->st, lkey, lidx, pl.grid, 2 * QW, (int)pl.cap, QW, pl.kp, pl.knn, mk, mi, mthr,
-                 pl.kmax);
+    // the per-query top-K' across the CTAs' compacted lists (io.lists_key:
+    // [G][2QW][kmax], K' each) is merged by the caller, all groups at once
+    (void)mk;
+    (void)mi;
+    (void)mthr;
     if (std::getenv("SAIR_WIDE_DEBUG")) {  // diagnostics: overflowing lists, thresholds
         std::vector<uint32_t> hd(L);
         std::vector<float> ht(L);
