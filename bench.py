@@ -124,11 +124,13 @@ def _launches(stats):
 
 def _stream_roofline(stats, n_local, hbm_peak, peak_kind, bf16_peak, qw):
     """Roofline of the dominant kernel (the stream pass): algorithmic bytes =
-    records x (4 d_pad + 4) per launch / its CUDA-event time."""
+    records x (4 d_pad + 4) per launch (the fp32 page row + the fp32 reward)
+    / its CUDA-event time; the wide pass (qw > 0) reads the call's cached
+    (P, log residual) pair instead of the reward: 4 d_pad + 8."""
     launches = sum(s["stream_launches"] for s in stats)
     stream_ms = sum(s["stream_ms"] for s in stats)
     dp = 64 if DIM > 32 else 32
-    alg_bytes = n_local * (4 * dp + 4)
+    alg_bytes = n_local * (4 * dp + (8 if qw else 4))
     per_launch_s = stream_ms / 1e3 / max(launches, 1)
     achieved = alg_bytes / per_launch_s / 1e9
     out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",

@@ -124,6 +124,7 @@ struct sair_store_s {
     sair::DBuf b_greedy;  // batched exact greedy: rows + per-(query, record) state
     sair::DBuf b_grp;     // per query group of one select call: merged lists, thresholds, ...
     sair::DBuf b_wlists;  // the wide pass's compacted CTA lists of every group of a call
+    sair::DBuf b_pl;      // per record (P, log residual) of the current call (wide pass)
     sair::HBuf h_ra;      // pinned refine argument blocks
     std::shared_ptr<sair::GreedySession> greedy;  // sharded lambda > 0 select in progress
     std::vector<cudaEvent_t> gev;  // per query group: start, end of pre-pass, end of stream

@@ -1043,6 +1043,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         // of qb; t0o (wide pass only) overrides the sampled start thresholds,
         // 2 qb floats per group (selection lists, then veto lists).
         std::vector<float> thr_of(nq * 4, -INFINITY);
+        bool pl_ready = false;  // the (P, lg) cache holds this call's values
         auto run_batch = [&](const std::vector<size_t>& ql, const std::vector<float>* t0o) {
         const size_t nbq = ql.size();
         const size_t ngroups = (nbq + qb - 1) / qb;
@@ -1121,6 +1122,10 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         // the wide pass's compacted CTA lists of every group (merged in one launch)
         const size_t lstride = use_wide ? (size_t)wp.grid * 2 * qb * kmax : 0;
         float* lk_g = use_wide ? s->b_wlists.as<float>(ngroups * lstride * 2) : nullptr;
+        // (P, log residual) per record: the same for every group of the call
+        // (one standardization, one set of reward constants) -- computed by the
+        // first stream pass, read by every later launch
+        float* pl_cache = use_wide ? s->b_pl.as<float>(((n + PAGE - 1) / PAGE) * PAGE * 2) : nullptr;
         uint32_t* li_g = use_wide ? reinterpret_cast<uint32_t*>(lk_g + ngroups * lstride) : nullptr;
         RefineArgs* ra_host = reinterpret_cast<RefineArgs*>(
             s->h_ra.get(ngroups * sizeof(RefineArgs) + 64));
@@ -1147,7 +1152,10 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             const GroupIo io{hstage_all ? hstage_all + g * hstride : nullptr, s->gev[3 * g + 1],
                              s->gev[3 * g + 2], t0o ? t0o->data() + g * 2 * qb : nullptr,
                              use_wide ? lk_g + g * lstride : nullptr,
-                             use_wide ? li_g + g * lstride : nullptr};
+                             use_wide ? li_g + g * lstride : nullptr,
+                             use_wide && pl_ready ? pl_cache : nullptr,
+                             use_wide && !pl_ready ? pl_cache : nullptr};
+            if (use_wide) pl_ready = true;
             const O D = carve(dout + g * ob);
             float* mk = mk_g + g * mstride;
             uint32_t* mi = mi_g + g * mstride;

@@ -68,6 +68,8 @@ struct GroupIo {
     const float* t0_override;  // wide pass: [2 QW] start thresholds (skip the sample pass)
     float* lists_key;          // wide pass: compacted CTA lists out, [grid][2 QW][kmax]
     uint32_t* lists_idx;
+    const float* pl_in;        // wide pass: this call's per-record (P, lg) cache, or null
+    float* pl_out;             // wide pass: fill the cache in this group's stream pass
 };
 
 // select_mma.cu: the tcgen05 streaming kernel (plan + launcher)

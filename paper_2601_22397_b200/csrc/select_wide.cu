@@ -75,6 +75,8 @@ struct WideArgs {
     unsigned int* dropped;    // [2QW] max ordinal of a key dropped on a full list
     uint32_t cap;             // per-CTA list capacity
     int kp, kv;               // K' of the selection / veto lists
+    const float* pl_in;       // per-record (P, log residual) of this call, [n][2], or null
+    float* pl_out;            // written by the call's first stream pass, or null
     float* okey;              // compacted lists out: [grid][2QW][kout] (the merge's input)
     uint32_t* oidx;
     int kout;
@@ -272,32 +274,45 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             const uint32_t s = it % nst, ph = (it / nst) & 1u;
             const uint32_t rec = page_of(it) * PAGE + rloc;
             const bool v0 = rec < a.n, v1 = rec + 1 < a.n;
-            float2 r2 = make_float2(0.f, 0.f);
-            if (v1) r2 = __ldg(reinterpret_cast<const float2*>(a.r32 + rec));
-            else if (v0) r2.x = __ldg(a.r32 + rec);
-            bar_wait(&full[s], ph);
-            const unsigned char* box = stage + (size_t)s * PAGE_BYTES + box_i * BOX_BYTES;
-            float2 Pa = make_float2(0.f, 0.f), Pb = Pa;
+            float2 P2, L2;  // P = ||y||^2 and the log residual of the two records
+            if (a.pl_in) {
+                // computed by an earlier launch of this call (same statistics)
+                const float4 v = __ldg(reinterpret_cast<const float4*>(a.pl_in) + rec / 2);
+                P2 = make_float2(v.x, v.z);
+                L2 = make_float2(v.y, v.w);
+                bar_wait(&full[s], ph);
+            } else {
+                float2 r2 = make_float2(0.f, 0.f);
+                if (v1) r2 = __ldg(reinterpret_cast<const float2*>(a.r32 + rec));
+                else if (v0) r2.x = __ldg(a.r32 + rec);
+                bar_wait(&full[s], ph);
+                const unsigned char* box = stage + (size_t)s * PAGE_BYTES + box_i * BOX_BYTES;
+                float2 Pa = make_float2(0.f, 0.f), Pb = Pa;
 #pragma unroll
-            for (int k = 0; k < DP; k += 2) {
-                const float2 xa = *reinterpret_cast<const float2*>(
-                    box + k * 128 + ((((l16 >> 2) ^ (k & 3)) << 5) | ((l16 & 3) << 3)));
-                const float2 xb = *reinterpret_cast<const float2*>(
-                    box + (k + 1) * 128 + ((((l16 >> 2) ^ ((k + 1) & 3)) << 5) | ((l16 & 3) << 3)));
-                const float2 ya = __fmul2_rn(xa, make_float2(ss[k], ss[k]));
-                const float2 yb = __fmul2_rn(xb, make_float2(ss[k + 1], ss[k + 1]));
-                Pa = __ffma2_rn(ya, ya, Pa);
-                Pb = __ffma2_rn(yb, yb, Pb);
+                for (int k = 0; k < DP; k += 2) {
+                    const float2 xa = *reinterpret_cast<const float2*>(
+                        box + k * 128 + ((((l16 >> 2) ^ (k & 3)) << 5) | ((l16 & 3) << 3)));
+                    const float2 xb = *reinterpret_cast<const float2*>(
+                        box + (k + 1) * 128 +
+                        ((((l16 >> 2) ^ ((k + 1) & 3)) << 5) | ((l16 & 3) << 3)));
+                    const float2 ya = __fmul2_rn(xa, make_float2(ss[k], ss[k]));
+                    const float2 yb = __fmul2_rn(xb, make_float2(ss[k + 1], ss[k + 1]));
+                    Pa = __ffma2_rn(ya, ya, Pa);
+                    Pb = __ffma2_rn(yb, yb, Pb);
+                }
+                P2 = __fadd2_rn(Pa, Pb);
+                L2 = make_float2(log2f(fabsf(fmaf(r2.x, a.c1, -a.c0)) + a.rdelta),
+                                 log2f(fabsf(fmaf(r2.y, a.c1, -a.c0)) + a.rdelta));
+                if (a.pl_out && v0)
+                    reinterpret_cast<float4*>(a.pl_out)[rec / 2] = make_float4(P2.x, L2.x, P2.y, L2.y);
             }
-            const float2 P2 = __fadd2_rn(Pa, Pb);
             float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
             float2 oa, on, op, ol;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const bool valid = e ? v1 : v0;
-                const float P = e ? P2.y : P2.x, r = e ? r2.y : r2.x;
+                const float P = e ? P2.y : P2.x, lg = e ? L2.y : L2.x;
                 if (valid) pmax = fmaxf(pmax, P);
-                const float lg = log2f(fabsf(fmaf(r, a.c1, -a.c0)) + a.rdelta);
                 const float A = lg / a.alpha - P;
                 // an invalid record never passes a pre-test
                 const float as = valid ? A + 0x1p-19f * (fabsf(A) + P + sM[0]) : -INFINITY;
@@ -628,6 +643,8 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.cap = pl.cap;
     a.kp = pl.kp;
     a.kv = pl.knn;
+    a.pl_in = io.pl_in;
+    a.pl_out = nullptr;
     a.okey = io.lists_key;
     a.oidx = io.lists_idx;
     a.kout = pl.kmax;
@@ -649,6 +666,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     }
     SAIR_CUDA(cudaEventRecord(io.e_mid, s->st));
     a.mode = 1;
+    a.pl_out = io.pl_out;  // the first stream pass of a call caches (P, lg) per record
     stream_wide_kernel<DP, QW><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
     SAIR_LAUNCH("stream_wide_kernel(stream)");
     SAIR_CUDA(cudaEventRecord(io.e_end, s->st));

@@ -6,7 +6,7 @@ db = sair.ExperienceBuffer(0.0)
 db.store_synthetic(2026, 1 << 24, 64)
 xq = synth.queries(7, 128, 64)
 cfg = sair.SelectionConfig(m=4, lambda_div=0.0)
-for p in ["0", "1", "0", "1"]:
+for p in ["0", "2", "0", "2"]:
     os.environ["SAIR_PROBE_WIDE"] = p
     db.select_batch(xq, cfg)
     st = db.last_stats()
