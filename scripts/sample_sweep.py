@@ -7,7 +7,7 @@ for n in (1 << 24, 1 << 20):
     db.store_synthetic(2026, n, 64)
     xq = synth.queries(7, 1024, 64)
     cfg = sair.SelectionConfig(m=32, lambda_div=0.0)
-    for c in ("10", "5", "2.5", "1.2", "20"):
+    for c in ("5", "2.5", "3.5", "7"):
         os.environ["SAIR_SAMPLE_C"] = c
         db.select_batch(xq, cfg)
         t0 = time.perf_counter()
