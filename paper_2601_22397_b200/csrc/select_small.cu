@@ -117,22 +117,6 @@ __global__ void __launch_bounds__(256) local_loo_z_kernel(const double* __restri
     loo[i] = wsum > 1e-12 ? ddiv(acc, wsum) : ddiv(dsub(total, r64[i]), (double)(n_loo - 1));
 }
 
-__device__ __forceinline__ Best block_best(Best b, Best* wb) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    b = warp_best(b);
-    if (lane == 0) wb[warp] = b;
-    __syncthreads();
-    if (warp == 0) {
-        Best c = lane < (int)(blockDim.x >> 5) ? wb[lane] : Best{0.0, 0, 0, -1};
-        c = warp_best(c);
-        if (lane == 0) wb[32] = c;
-    }
-    __syncthreads();
-    const Best r = wb[32];
-    __syncthreads();
-    return r;
-}
-
 __global__ void __launch_bounds__(SMALL_THREADS) small_select_kernel(const __grid_constant__ SmallArgs a) {
     cg::cluster_group cl = cg::this_cluster();
     const int crank = (int)cl.block_rank();
@@ -178,17 +162,28 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_select_kernel(const __gri
     }
     __syncthreads();
     int par = 0;
+    const int lane = tid & 31, warp = tid >> 5;
     auto cluster_best = [&](Best b) {
-        // every CTA contributes its best; all reduce the same set in rank order
-        b = block_best(b, wb);
-        if (tid == 0) cbest[par] = b;
-        cl.sync();
-        Best g{0.0, 0, 0, -1};
-        for (int r = 0; r < a.cs; ++r) {
-            const Best* rb = cl.map_shared_rank(cbest + par, r);
-            const Best c = *rb;
-            if (better(c, g)) g = c;
+        // the CTA's best (warp shuffles, one barrier), published in shared
+        // memory; after the cluster barrier warp 0 reads the CTAs' bests from
+        // distributed shared memory (lane r <- rank r) and every CTA reduces
+        // the same set to the same winner
+        b = warp_best(b);
+        if (lane == 0) wb[warp] = b;
+        __syncthreads();
+        if (warp == 0) {
+            Best c = lane < (int)(blockDim.x >> 5) ? wb[lane] : Best{0.0, 0, 0, -1};
+            c = warp_best(c);
+            if (lane == 0) cbest[par] = c;
         }
+        cl.sync();
+        if (warp == 0) {
+            Best c = lane < a.cs ? *cl.map_shared_rank(cbest + par, lane) : Best{0.0, 0, 0, -1};
+            c = warp_best(c);
+            if (lane == 0) wb[32] = c;
+        }
+        __syncthreads();
+        const Best g = wb[32];
         par ^= 1;
         return g;
     };
