@@ -125,6 +125,10 @@ struct sair_store_s {
     sair::DBuf b_grp;     // per query group of one select call: merged lists, thresholds, ...
     sair::DBuf b_wlists;  // the wide pass's compacted CTA lists of every group of a call
     sair::DBuf b_pl;      // per record (P, log residual) of the current call (wide pass)
+    sair::DBuf b_hot;     // the wide sample's highest-residual pages ...
+    size_t hot_n = 0;     // ... valid while the store holds hot_n records (append-only)
+    float hot_c1 = 0.f, hot_c0 = 0.f;  // and the call's reward constants match
+    uint32_t hot_sp = 0;  // and the uniform sample's page count
     sair::HBuf h_ra;      // pinned refine argument blocks
     std::shared_ptr<sair::GreedySession> greedy;  // sharded lambda > 0 select in progress
     std::vector<cudaEvent_t> gev;  // per query group: start, end of pre-pass, end of stream

@@ -1044,6 +1044,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         // 2 qb floats per group (selection lists, then veto lists).
         std::vector<float> thr_of(nq * 4, -INFINITY);
         bool pl_ready = false;  // the (P, lg) cache holds this call's values
+        uint32_t nhot = 0;
+        const uint32_t* hot = use_wide ? wide_hot_pages(s, wp, c1, c0, &nhot) : nullptr;
         auto run_batch = [&](const std::vector<size_t>& ql, const std::vector<float>* t0o) {
         const size_t nbq = ql.size();
         const size_t ngroups = (nbq + qb - 1) / qb;
@@ -1154,7 +1156,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                              use_wide ? lk_g + g * lstride : nullptr,
                              use_wide ? li_g + g * lstride : nullptr,
                              use_wide && pl_ready ? pl_cache : nullptr,
-                             use_wide && !pl_ready ? pl_cache : nullptr};
+                             use_wide && !pl_ready ? pl_cache : nullptr, hot, nhot};
             if (use_wide) pl_ready = true;
             const O D = carve(dout + g * ob);
             float* mk = mk_g + g * mstride;
@@ -1290,7 +1292,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                 if (!done[i]) rest.push_back(i);
             if (!rest.empty()) {
                 const size_t ng = (rest.size() + qb - 1) / qb;
-                std::vector<float> t0r(ng * 2 * qb, -FLT_MAX);
+                // padding slots of the last group never admit a record (a -inf
+                // start there would send every record down the slow path)
+                std::vector<float> t0r(ng * 2 * qb, FLT_MAX);
                 for (size_t j = 0; j < rest.size(); ++j) {
                     const size_t i = rest[j], g = j / qb, qq = j % qb;
                     t0r[g * 2 * qb + qq] = std::max(thr_of[i * 4 + 2], thr_of[i * 4 + 0]);

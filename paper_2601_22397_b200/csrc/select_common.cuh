@@ -70,6 +70,8 @@ struct GroupIo {
     uint32_t* lists_idx;
     const float* pl_in;        // wide pass: this call's per-record (P, lg) cache, or null
     float* pl_out;             // wide pass: fill the cache in this group's stream pass
+    const uint32_t* hot;       // wide sample: extra pages (highest reward residual), or null
+    uint32_t nhot;             // slots in `hot` (entries >= npages are empty)
 };
 
 // select_mma.cu: the tcgen05 streaming kernel (plan + launcher)
@@ -95,6 +97,10 @@ using WideFn = void (*)(sair_store_s*, const WidePlan&, const QueryPrep&, const 
                         float, float, float, float*, uint32_t*, float*, unsigned int*,
                         std::vector<double>&, const GroupIo&);
 WideFn pick_wide(int dp, int qw);
+// the wide sample's highest-residual pages of this call (nhot slots, empty
+// ones >= npages), or null
+const uint32_t* wide_hot_pages(sair_store_s* s, const WidePlan& pl, float c1, float c0,
+                               uint32_t* nhot);
 double wide_bq_rel();  // relative error bound of the wide pass's query operand
 bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                     WidePlan* pl);

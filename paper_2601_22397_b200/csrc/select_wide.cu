@@ -38,6 +38,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "select_common.cuh"
 #include "topk_select.cuh"
 #include "umma.cuh"
@@ -67,9 +69,11 @@ struct WideArgs {
     uint32_t n, npages;
     float c1, c0, rdelta, alpha;
     int nst, ntm, knn, mode;  // smem page stages, TMEM stages; mode 0 = sample, 1 = stream
-    uint32_t spages;          // sample mode: sampled pages (page = i * npages / spages)
+    uint32_t spages;          // sample mode: sampled pages (page = i * npages / spages) ...
+    const uint32_t* hot;      // ... then these (distinct from the above; >= npages: empty)
+    uint32_t nhot;
     const float* consts;      // B tiles (hi, lo; smem image) | s [DP] | cc [QW] | t0 [2QW]
-    float* smax;              // sample out [2QW][4 * spages]
+    float* smax;              // sample out [2QW][4 * (spages + nhot)]
     float* lkey;              // stream out: per-CTA lists [grid][2QW][cap]
     uint32_t* lidx;
     unsigned int* dropped;    // [2QW] max ordinal of a key dropped on a full list
@@ -213,12 +217,19 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    const uint32_t units = a.mode == 0 ? a.spages : a.npages;
+    const uint32_t units = a.mode == 0 ? a.spages + a.nhot : a.npages;
     const uint32_t G = gridDim.x, r0 = blockIdx.x;
     const uint32_t mine = r0 < units ? (units - 1 - r0) / G + 1 : 0;
     auto page_of = [&](uint32_t it) -> uint32_t {
         const uint32_t u = r0 + it * G;
-        return a.mode == 0 ? (uint32_t)((uint64_t)u * a.npages / a.spages) : u;
+        if (a.mode != 0) return u;
+        if (u < a.spages) return (uint32_t)((uint64_t)u * a.npages / a.spages);
+        const uint32_t h = a.hot[u - a.spages];
+        return h < a.npages ? h : 0u;  // an empty slot reads page 0, all its records invalid
+    };
+    auto empty_unit = [&](uint32_t it) -> bool {
+        const uint32_t u = r0 + it * G;
+        return a.mode == 0 && u >= a.spages && a.hot[u - a.spages] >= a.npages;
     };
 
     if (warp == W_PROD) {
@@ -273,7 +284,8 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         for (uint32_t it = (uint32_t)(w >> 1); it < mine; it += 2) {
             const uint32_t s = it % nst, ph = (it / nst) & 1u;
             const uint32_t rec = page_of(it) * PAGE + rloc;
-            const bool v0 = rec < a.n, v1 = rec + 1 < a.n;
+            const bool live = !empty_unit(it);
+            const bool v0 = live && rec < a.n, v1 = live && rec + 1 < a.n;
             float2 P2, L2;  // P = ||y||^2 and the log residual of the two records
             if (a.pl_in) {
                 // computed by an earlier launch of this call (same statistics)
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                             acc[j] = valid ? fmaf(-d2, a.alpha, lg) : -INFINITY;
                             kn[j] = valid ? -d2 : -INFINITY;
                         }
-                        const uint32_t S4 = 4 * a.spages, col = r0 + it * G;
+                        const uint32_t S4 = 4 * (a.spages + a.nhot), col = r0 + it * G;
                         const float mk = transpose_max(acc, lane);
                         a.smax[(size_t)(c0 + lane) * S4 + 4 * col + quarter] = mk;
                         if (a.knn) {
@@ -603,7 +615,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     }
     // device: consts | lists | counters
     const size_t L = 2 * (size_t)QW;
-    const size_t S4 = 4 * (size_t)pl.spages;
+    const size_t S4 = 4 * ((size_t)pl.spages + (io.hot ? io.nhot : 0));
     char* base = static_cast<char*>(s->b_mmab.get(nc * 4 + 256 + L * 8 + S4 * L * 4 + 256));
     float* dc = reinterpret_cast<float*>(base);
     float* dt0 = dc + WB * (size_t)DP * QW + DP + QW;  // the t0 slot of consts
@@ -635,6 +647,8 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.ntm = pl.ntm;
     a.knn = pl.knn ? 1 : 0;
     a.spages = pl.spages;
+    a.hot = io.hot;
+    a.nhot = io.hot ? io.nhot : 0;
     a.consts = dc;
     a.smax = dsmax;
     a.lkey = lkey;
@@ -657,7 +671,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     if (!io.t0_override) {
         // sample pass -> t0 (written into the consts the stream pass reads)
         a.mode = 0;
-        stream_wide_kernel<DP, QW><<<(int)std::min<uint32_t>(pl.spages, (uint32_t)pl.grid),
+        stream_wide_kernel<DP, QW><<<(int)std::min<uint32_t>(pl.spages + a.nhot, (uint32_t)pl.grid),
                                      WIDE_THREADS, pl.smem, s->st>>>(a);
         SAIR_LAUNCH("stream_wide_kernel(sample)");
         wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(dsmax, (uint32_t)S4, QW, pl.kp,
@@ -690,6 +704,39 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     s->mma_dropped = ddrop;
 }
 
+// per page: the largest record-constant residual |r c1 - c0| (the reward
+// factor of the key, |r - loo mean| scaled, experience.cpp:139-140,148)
+__global__ void page_resid_kernel(const float* __restrict__ r32, uint32_t n, uint32_t npages,
+                                  float c1, float c0, float* __restrict__ out,
+                                  uint32_t* __restrict__ ids) {
+    const uint32_t page = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (page >= npages) return;
+    float v = 0.f;
+#pragma unroll
+    for (int i = 0; i < PAGE / 32; ++i) {
+        const uint32_t rec = page * PAGE + i * 32 + lane;
+        if (rec < n) v = fmaxf(v, fabsf(fmaf(__ldg(r32 + rec), c1, -c0)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) {
+        out[page] = v;
+        ids[page] = page;
+    }
+}
+
+// the H highest pages (sorted order) that the uniform sample (page =
+// floor(u npages / spages)) does not already hold; the others leave an
+// empty slot
+__global__ void hot_mark_kernel(const uint32_t* __restrict__ sorted, uint32_t npages,
+                                uint32_t spages, uint32_t H, uint32_t* __restrict__ hot) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= H) return;
+    const uint32_t p = sorted[i];
+    const uint64_t u = ((uint64_t)p * spages + npages - 1) / npages;
+    hot[i] = u < spages && u * npages / spages == p ? 0xFFFFFFFFu : p;
+}
+
 template <int DP>
 WideFn wide_pick_qw(int qw) {
     switch (qw) {
@@ -706,6 +753,49 @@ size_t wide_smem(int dp, int qw, int nst, int ntm) {
 }
 
 }  // namespace
+
+// The wide sample's second part: the pages with the largest reward residual.
+// A page whose records carry a much larger |r - loo mean| than the rest (a
+// freshly appended batch of outcomes far from the store's mean) holds most
+// queries' best keys, and a uniform sample would miss it: the start
+// threshold would sit far below the K'-th key and the stream pass would
+// admit that page's records for every query.  Any set of distinct pages
+// gives a valid start threshold, so adding these only tightens it.
+const uint32_t* wide_hot_pages(sair_store_s* s, const WidePlan& pl, float c1, float c0,
+                               uint32_t* nhot) {
+    const uint32_t npages = (uint32_t)((s->n + PAGE - 1) / PAGE);
+    const uint32_t H = std::min<uint32_t>(256u, npages / 32);
+    *nhot = H;
+    if (H == 0) return nullptr;
+    const size_t pb = ((size_t)npages * 4 + 255) & ~(size_t)255;
+    if (s->b_hot.p && s->hot_n == s->n && s->hot_c1 == c1 && s->hot_c0 == c0 &&
+        s->hot_sp == pl.spages)
+        return reinterpret_cast<const uint32_t*>(static_cast<char*>(s->b_hot.p) + 4 * pb);
+    size_t tmp = 0;
+    SAIR_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, (const float*)nullptr,
+                                                        (float*)nullptr, (const uint32_t*)nullptr,
+                                                        (uint32_t*)nullptr, (int)npages));
+    char* base = static_cast<char*>(s->b_hot.get(4 * pb + (((size_t)H * 4 + 255) & ~(size_t)255) +
+                                                 tmp + 256));
+    float* vals = reinterpret_cast<float*>(base);
+    uint32_t* ids = reinterpret_cast<uint32_t*>(base + pb);
+    float* vals_s = reinterpret_cast<float*>(base + 2 * pb);
+    uint32_t* ids_s = reinterpret_cast<uint32_t*>(base + 3 * pb);
+    uint32_t* hot = reinterpret_cast<uint32_t*>(base + 4 * pb);
+    void* tbuf = base + 4 * pb + (((size_t)H * 4 + 255) & ~(size_t)255);
+    page_resid_kernel<<<(npages + 7) / 8, 256, 0, s->st>>>(s->r32, (uint32_t)s->n, npages, c1, c0,
+                                                          vals, ids);
+    SAIR_LAUNCH("page_resid_kernel");
+    SAIR_CUDA(cub::DeviceRadixSort::SortPairsDescending(tbuf, tmp, vals, vals_s, ids, ids_s,
+                                                        (int)npages, 0, 32, s->st));
+    hot_mark_kernel<<<(H + 255) / 256, 256, 0, s->st>>>(ids_s, npages, pl.spages, H, hot);
+    SAIR_LAUNCH("hot_mark_kernel");
+    s->hot_n = s->n;  // reused by later calls until the store grows
+    s->hot_c1 = c1;
+    s->hot_c0 = c0;
+    s->hot_sp = pl.spages;
+    return hot;
+}
 
 WideFn pick_wide(int dp, int qw) {
     switch (dp) {

@@ -121,3 +121,32 @@ def test_config2_1m_256_queries_against_exact():
                                                       mode=sair.SELECT_EXACT), nearest=True)
     for a, b in zip(fast, exact):
         assert np.array_equal(np.asarray(a)[pick], b)
+
+
+def test_wide_after_high_residual_append(orc):
+    """Config 5's store after a decision step: a batch of outcomes far from the
+    store's mean appended at the end.  The sample's highest-residual pages
+    put the start threshold next to the K'-th key, so every query certifies in
+    the first pass (no retry); results equal the oracle's, before and after a
+    second append (the hot-page list is rebuilt when the store grows)."""
+    n, d, nq, m = 90000, 32, 128, 16
+    db, ctx, rew, rnd = synth_store(31, n, d)
+    rng = np.random.default_rng(3)
+    cfg = SelectionConfig(m=m, lambda_div=0.0)
+    for step in range(2):
+        k = 1500
+        c = synth.queries(40 + step, k, d)
+        r = rng.uniform(3, 6, k)  # above the r_min gate, far above the mean
+        db.store_many(c, r, np.full(k, 7 + step, np.int32))
+        ctx = np.concatenate([ctx, c])
+        rew = np.concatenate([rew, r])
+        rnd = np.concatenate([rnd, np.full(k, 7 + step, np.int32)])
+        xq = synth.queries(50 + step, nq, d)
+        for _ in range(2):  # the second call reuses the hot-page list
+            idx, sim, sc, cnt, _, _ = db.select_batch(xq, cfg, nearest=True)
+            st = db.last_stats()
+            assert st["tensor_core"] == 2 and st["certified"] == nq, st
+            assert st["retried"] == 0 and st["exact_fallbacks"] == 0, st
+        oi, osim, osc, ocnt = orc.select_batch(ctx, rew, rnd, xq, m, 0.0, db.effective_sigma())
+        assert np.array_equal(cnt, ocnt) and np.array_equal(idx, oi)
+        assert near(sc, osc, 1e-12) and near(sim, osim, 1e-12)
