@@ -8,11 +8,13 @@ CUDA device fails with ``SairError(SAIR_ECUDA)``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import re
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libsair.so"
+# SAIR_LIB_PATH: a side build for A/B timing (scripts/); unset, the in-tree library
+LIB_PATH = Path(os.environ.get("SAIR_LIB_PATH") or PKG / "libsair.so")
 HEADER = PKG.parent / "include" / "sair.h"
 
 SAIR_OK, SAIR_EINVAL, SAIR_ELOGIC, SAIR_ERANGE, SAIR_EIO, SAIR_ECUDA, SAIR_ENOMEM, SAIR_ENCCL = range(8)
