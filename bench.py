@@ -259,6 +259,16 @@ def run_ours(a, rank, world, local_rank):
     hbm_target = {"queries_per_step": Q_HBM, "value": round(a.steps * Q_HBM / (ms_h / 1e3), 2),
                   "unit": "queries/s", "ms_per_step": round(ms_h / a.steps, 4), "roofline": roof_h,
                   "certified_queries": sum(s["certified"] for s in st_h)}
+    # the rest of the north star's Q in {1, 2, 4, 8}: the same pass, fewer queries
+    hbm_target["sweep"] = {}
+    for qn in (1, 2, 4):
+        for i in range(3):
+            select(qh[i][:qn])
+        ms_q, st_q = timed([q[:qn] for q in qh[3:]], a.steps)
+        rq = _stream_roofline(st_q, hi - lo, hbm_peak, peak_kind, bf16_peak, 0)
+        hbm_target["sweep"][str(qn)] = {
+            "value": round(a.steps * qn / (ms_q / 1e3), 2), "unit": "queries/s",
+            "ms_per_step": round(ms_q / a.steps, 4), "frac": rq["frac"]}
 
     out = {
         "metric": "retrieval queries/s @16M exps k=32",
@@ -463,6 +473,33 @@ def bench_pareto(dev):
     res["dominance_counts_K2_4M"] = {"tuples": PARETO_T, "s_e2e": round(dt2, 4),
                                      "tuples_per_s": round(PARETO_T / dt2, 1),
                                      "frontier": int(mem2.sum())}
+    # the other configs[2] distributions at full size, two objectives: batch
+    # insert (e2e), device scoring against the resulting frontier, counts
+    res["distributions"] = {}
+    for dist in ("anti", "corr", "grid"):
+        pd = synth.tuples(SEED + 5, PARETO_T, 2, dist)
+        fd = sair.ParetoFrontier(1.0, 1.0, device=dev)
+        t0 = time.perf_counter()
+        Fd = fd.insert_batch(pd)
+        ins = time.perf_counter() - t0
+        dp_ = torch.from_numpy(pd).to(f"cuda:{dev}")
+        fd.score_batch_device(dp_.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
+                              s.cuda_stream)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(3):
+            fd.score_batch_device(dp_.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
+                                  s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        sms = e0.elapsed_time(e1) / 3
+        t0 = time.perf_counter()
+        _, md = sair.dominance_counts(pd)
+        dc = time.perf_counter() - t0
+        res["distributions"][dist] = {
+            "frontier": Fd, "insert_s_e2e": round(ins, 4), "score_ms": round(sms, 4),
+            "scored_tuples_per_s": round(PARETO_T / (sms / 1e3), 1),
+            "dominance_counts_K2_s_e2e": round(dc, 4), "count_frontier": int(md.sum())}
     for K in (2, 3, 4):
         T = 262144
         t = synth.tuples(SEED + K, T, K, "uniform")

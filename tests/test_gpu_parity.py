@@ -295,7 +295,7 @@ def test_frontier_sequences_match_reference(ref):
 
 
 def test_batch_insert_and_scoring_at_scale(orc):
-    for dist in ("uniform", "anti", "grid"):
+    for dist in ("uniform", "anti", "grid", "corr"):
         pts = synth.tuples(17, 200000, 2, dist)
         df = ParetoFrontier(1.0, 1.0)
         F = df.insert_batch(pts[:120000])
@@ -360,7 +360,7 @@ def test_reward_golden_and_batch():
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4])
 def test_dominance_counts_match_oracle(orc, K):
-    for dist in ("uniform", "grid"):
+    for dist in ("uniform", "grid", "anti", "corr"):
         t = synth.tuples(23 + K, 3000, K, dist)
         if dist == "grid":
             t = np.floor(t * 8) / 8  # many duplicates and ties
