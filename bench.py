@@ -317,32 +317,45 @@ def bench_config1(dev, steps=50):
     synthetic stand-in of that shape): select m = 8 with lambda_div = 0.1 (the
     reference's default) and the fused veto scan, compute_reward + update
     against the frontier, store() of the new experience -- latency per
-    decision through the public API (wall clock; each call synchronises)."""
+    decision through the public API (wall clock): `decision.replay_step` (one
+    device call, one host synchronisation), and the same four calls made
+    separately (each synchronises) for comparison."""
     import paper_2601_22397_b200 as sair
-    from paper_2601_22397_b200 import synth
-    db = sair.ExperienceBuffer(0.0, device=dev)
-    db.store_synthetic(SEED + 3, 10000, 32)
-    fr = sair.ParetoFrontier(2000.0, 10.0, device=dev)
-    rng = np.random.default_rng(SEED)
+    from paper_2601_22397_b200 import decision, synth
     cfg = sair.SelectionConfig(m=8, lambda_div=0.1)
     rc = sair.RewardConfig()
     act = sair.ScalingAction.noop(3)
-    lat = []
-    for s in range(steps + 5):
-        x = synth.queries(SEED + 200 + s, 1, 32)
-        inp = sair.RewardInputs(rng.uniform(300, 900), rng.uniform(300, 900), rng.uniform(1, 5),
-                                rng.uniform(1, 5))
-        t0 = time.perf_counter()
-        db.select_batch(x, cfg, nearest=True)
-        r = sair.compute_reward(inp, act, fr, rc)
-        fr.update(inp.l_after_ms, inp.c_after)
-        db.store(sair.Experience(list(x[0]), act, r.total, 10000 + s))
-        if s >= 5:
-            lat.append(time.perf_counter() - t0)
+
+    def run(fused):
+        db = sair.ExperienceBuffer(0.0, device=dev)
+        db.store_synthetic(SEED + 3, 10000, 32)
+        fr = sair.ParetoFrontier(2000.0, 10.0, device=dev)
+        rng = np.random.default_rng(SEED)
+        lat = []
+        for s in range(steps + 5):
+            x = synth.queries(SEED + 200 + s, 1, 32)
+            inp = sair.RewardInputs(rng.uniform(300, 900), rng.uniform(300, 900),
+                                    rng.uniform(1, 5), rng.uniform(1, 5))
+            t0 = time.perf_counter()
+            if fused:
+                decision.replay_step(db, fr, x[0], cfg, inp, act, rc, update=True,
+                                     round=10000 + s)
+            else:
+                db.select_batch(x, cfg, nearest=True)
+                r = sair.compute_reward(inp, act, fr, rc)
+                fr.update(inp.l_after_ms, inp.c_after)
+                db.store(sair.Experience(list(x[0]), act, r.total, 10000 + s))
+            if s >= 5:
+                lat.append(time.perf_counter() - t0)
+        return float(np.median(lat))
+
+    fused, four = run(True), run(False)
     return {"workload": "configs[0]: 10k records x d=32, k=8, lambda_div=0.1, veto scan, "
                         "compute_reward + update + store per decision (synthetic stand-in)",
-            "us_per_decision_median": round(float(np.median(lat)) * 1e6, 1),
-            "decisions_per_s": round(1.0 / float(np.median(lat)), 1)}
+            "us_per_decision_median": round(fused * 1e6, 1),
+            "decisions_per_s": round(1.0 / fused, 1),
+            "api": "decision.replay_step (sair_decision_step: one host synchronisation)",
+            "four_calls_us_per_decision_median": round(four * 1e6, 1)}
 
 
 def bench_decision_step(buf, dev, P=30000, steps=3):

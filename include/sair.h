@@ -334,6 +334,29 @@ typedef struct { /* RewardBreakdown, reward.hpp:30-38 */
     int clipped;
 } sair_reward_breakdown;
 
+/* ------------------------------------------------------------------------
+ * Decision step: one iteration of the reference's loop,
+ * harness.cpp:197-261, replayed with the step's outcome known (config 1's
+ * trace replay): select(x) with the veto scan (:205; policy.cpp:140-157),
+ * compute_reward of `in` / `deltas` against the frontier before the update
+ * (:250; reward.hpp:44-46), frontier.update(in->l_after_ms, in->c_after) when
+ * `update` (:251), store() of (x, reward total, round) through the r_min
+ * gate (:253-261).  Same results as sair_store_select + sair_compute_reward +
+ * sair_frontier_update + sair_store_append in that order, enqueued on the
+ * store's stream with one host synchronisation.  out_count is the select's
+ * count (<= cfg->m entries in out_idx / out_sim / out_score); out_nn_* the
+ * veto scan; out_inserted / out_stored the update's and store()'s results.
+ * ------------------------------------------------------------------------ */
+SAIR_API sair_status sair_decision_step(sair_store_t h, sair_frontier_t f, const double* x,
+                                        int dim, const sair_select_config* cfg,
+                                        const sair_reward_inputs* in, const int32_t* deltas,
+                                        size_t stages, const sair_reward_config* rcfg,
+                                        int update, int32_t round, int64_t* out_idx,
+                                        double* out_sim, double* out_score, size_t* out_count,
+                                        int64_t* out_nn_idx, double* out_nn_sim,
+                                        sair_reward_breakdown* out_reward, int* out_inserted,
+                                        int* out_stored);
+
 /* action_magnitude, reward.cpp:9-19; deltas = stages x {replicas,
  * cpu_millicores, memory_mb, rate_ratio_tenths}. */
 SAIR_API sair_status sair_action_magnitude(const int32_t* deltas, size_t stages, double* out);

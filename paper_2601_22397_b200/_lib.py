@@ -133,6 +133,11 @@ SIGNATURES = {
     "sair_action_magnitude": (C.c_int, [_i32p, C.c_size_t, _dp]),
     "sair_compute_reward": (C.c_int, [C.POINTER(RewardInputsC), _i32p, C.c_size_t, _vp,
                                       C.POINTER(RewardConfigC), C.POINTER(RewardBreakdownC)]),
+    "sair_decision_step": (C.c_int, [_vp, _vp, _dp, C.c_int, C.POINTER(SelectConfigC),
+                                     C.POINTER(RewardInputsC), _i32p, C.c_size_t,
+                                     C.POINTER(RewardConfigC), C.c_int, C.c_int32, _i64p, _dp,
+                                     _dp, _szp, _i64p, _dp, C.POINTER(RewardBreakdownC),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "sair_compute_reward_batch": (C.c_int, [C.POINTER(RewardInputsC), _i32p, C.c_size_t,
                                             C.c_size_t, _vp, C.POINTER(RewardConfigC),
                                             C.POINTER(RewardBreakdownC)]),

@@ -556,6 +556,28 @@ sair_status sair_compute_reward(const sair_reward_inputs* in, const int32_t* del
     return guard([&] { sair::compute_reward_batch(in, deltas, stages, 1, f, cfg, out); });
 }
 
+sair_status sair_decision_step(sair_store_t h, sair_frontier_t f, const double* x, int dim,
+                               const sair_select_config* cfg, const sair_reward_inputs* in,
+                               const int32_t* deltas, size_t stages,
+                               const sair_reward_config* rcfg, int update, int32_t round,
+                               int64_t* out_idx, double* out_sim, double* out_score,
+                               size_t* out_count, int64_t* out_nn_idx, double* out_nn_sim,
+                               sair_reward_breakdown* out_reward, int* out_inserted,
+                               int* out_stored) {
+    if (!h || !f) return bad("null handle");
+    if (!x || !in || !rcfg || !out_count || !out_reward || !out_inserted || !out_stored ||
+        (stages && !deltas))
+        return bad("null input");
+    if ((out_nn_idx == nullptr) != (out_nn_sim == nullptr)) return bad("nn outputs come in pairs");
+    return guard([&] {
+        double pl = 0.0, pc = 0.0;
+        normalize_host(f, in->l_after_ms, in->c_after, &pl, &pc, nullptr);
+        sair::decision_step(h, f, x, dim, defaults(cfg), in, deltas, stages, rcfg, update != 0,
+                            pl, pc, round, out_idx, out_sim, out_score, out_count, out_nn_idx,
+                            out_nn_sim, out_reward, out_inserted, out_stored);
+    });
+}
+
 sair_status sair_compute_reward_batch(const sair_reward_inputs* in, const int32_t* deltas,
                                       size_t stages, size_t T, sair_frontier_t f,
                                       const sair_reward_config* cfg, sair_reward_breakdown* out) {

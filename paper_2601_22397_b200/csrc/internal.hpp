@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -125,6 +126,8 @@ struct sair_store_s {
     sair::DBuf b_grp;     // per query group of one select call: merged lists, thresholds, ...
     sair::DBuf b_wlists;  // the wide pass's compacted CTA lists of every group of a call
     sair::DBuf b_pl;      // per record (P, log residual) of the current call (wide pass)
+    bool defer_sync = false;         // decision step: the small select leaves its copy-out
+    std::function<void()> pending;   // pending, and its host unpack here
     sair::DBuf b_hot;     // the wide sample's highest-residual pages ...
     size_t hot_n = 0;     // ... valid while the store holds hot_n records (append-only)
     float hot_c1 = 0.f, hot_c0 = 0.f;  // and the call's reward constants match
@@ -178,6 +181,12 @@ void store_reserve(sair_store_s* s, size_t need);
 size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
                     const double* reward, const int32_t* round, uint8_t* accepted);
 void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int dim, int clustered);
+// decision step (pareto.cu): store() of one experience whose reward a kernel
+// earlier on the store's stream wrote to d_reward -- the row is written behind
+// it, gated on the device; the commit applies the same gate and the host sums
+void store_append_one_async(sair_store_s* s, const double* x, const double* d_reward,
+                            int32_t round);
+bool store_append_one_commit(sair_store_s* s, const double* x, double reward);
 void store_standardize(const sair_store_s* s, const double* x, double* z);
 double store_effective_sigma(sair_store_s* s, double sigma_sim);
 void store_mean_sd(const sair_store_s* s, double* mean, double* sd);
@@ -205,6 +214,13 @@ void frontier_init(sair_frontier_s* f, double l_max, double c_max, int device);
 void frontier_free(sair_frontier_s* f);
 void frontier_clone(const sair_frontier_s* f, sair_frontier_s* o);
 bool frontier_insert_one(sair_frontier_s* f, double pl, double pc);
+// one decision step: select + veto, reward, frontier update, store, one sync
+void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim,
+                   const sair_select_config& cfg, const sair_reward_inputs* in,
+                   const int32_t* deltas, size_t S, const sair_reward_config* rcfg, bool update,
+                   double pl, double pc, int32_t round, int64_t* o_idx, double* o_sim,
+                   double* o_score, size_t* o_count, int64_t* o_nn, double* o_nn_sim,
+                   sair_reward_breakdown* o_rw, int* o_inserted, int* o_stored);
 size_t frontier_insert_batch(sair_frontier_s* f, const double* pts, size_t T);
 double frontier_point_query(sair_frontier_s* f, double pl, double pc, int op, double* aux);
 void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, double* out,

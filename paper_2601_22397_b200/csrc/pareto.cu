@@ -1398,6 +1398,138 @@ size_t frontier_set_points(sair_frontier_set_s* s, size_t p, double* l, double* 
     return F;
 }
 
+// ---------------------------------------------------------- decision step --
+// insert_one_kernel's result committed on the device: the survivors (and the
+// point) copied back when it was inserted
+__global__ void insert_commit_kernel(double* __restrict__ fl, double* __restrict__ fc,
+                                     const double* __restrict__ ol, const double* __restrict__ oc,
+                                     const unsigned long long* __restrict__ res) {
+    if (!res[0]) return;
+    const size_t nF = (size_t)res[1];
+    for (size_t i = threadIdx.x; i < nF; i += blockDim.x) {
+        fl[i] = ol[i];
+        fc[i] = oc[i];
+    }
+}
+
+// hypervolume() after the update (pareto.cpp:56-65, point_query_kernel's Q_HV
+// loop), the size read from the insert's result
+__global__ void hv_after_insert_kernel(const double* __restrict__ fl, const double* __restrict__ fc,
+                                       const unsigned long long* __restrict__ res, size_t F0,
+                                       double* __restrict__ out) {
+    if (threadIdx.x || blockIdx.x) return;
+    const size_t F = res[0] ? (size_t)res[1] : F0;
+    double hv = 0.0;
+    for (size_t i = 0; i < F; ++i) {
+        double nl = i + 1 < F ? fl[i + 1] : 1.0;
+        hv = dadd(hv, dmul(dsub(nl, fl[i]), dsub(1.0, fc[i])));
+    }
+    out[0] = hv;
+}
+
+// One decision of the reference's loop (harness.cpp:197-261), replayed with the
+// step's outcome known: select(x) + veto scan
+// (:205, policy.cpp:140-157), compute_reward against the pre-update frontier
+// (:250), update (:251), store() (:253-261) -- enqueued on the store's stream
+// back to back with one host synchronisation; results identical to the four
+// calls in that order.  A store that is empty or of another dimension (store()
+// would fix or reject the dimension) takes the four calls.
+void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim,
+                   const sair_select_config& cfg, const sair_reward_inputs* in,
+                   const int32_t* deltas, size_t S, const sair_reward_config* rcfg, bool update,
+                   double pl, double pc, int32_t round, int64_t* o_idx, double* o_sim,
+                   double* o_score, size_t* o_count, int64_t* o_nn, double* o_nn_sim,
+                   sair_reward_breakdown* o_rw, int* o_inserted, int* o_stored) {
+    const RewardCfg rc = check_cfg(rcfg);
+    if (s->device != f->device)
+        throw Error(SAIR_EINVAL, "decision step: store and frontier on different devices");
+    if (s->n == 0 || dim != s->d) {
+        store_select(s, x, 1, dim, cfg, o_idx, o_sim, o_score, o_count, o_nn, o_nn_sim, nullptr,
+                     nullptr);
+        compute_reward_batch(in, deltas, S, 1, f, rcfg, o_rw);
+        *o_inserted = update ? frontier_insert_one(f, pl, pc) : 0;
+        uint8_t acc = 0;
+        store_append(s, x, 1, dim, &o_rw->total, &round, &acc);
+        *o_stored = acc;
+        return;
+    }
+    DeviceGuard g(s->device);
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    // capacity first: a reallocation synchronises, and must not move arrays
+    // under work already enqueued
+    store_reserve(s, s->n + 1);
+    if (update) reserve(f, f->F + 1);
+    const size_t F0 = f->F;
+    s->defer_sync = true;
+    try {
+        store_select(s, x, 1, dim, cfg, o_idx, o_sim, o_score, o_count, o_nn, o_nn_sim, nullptr,
+                     nullptr);
+    } catch (...) {
+        s->defer_sync = false;
+        s->pending = nullptr;
+        throw;
+    }
+    s->defer_sync = false;
+    cudaStream_t st = s->st;
+    // reward of the outcome against the frontier before the update
+    const size_t dbytes = S * 4 * 4;
+    const size_t inb = (32 + dbytes + 255) & ~(size_t)255;
+    const size_t fb = (F0 + 1) * 8;
+    char* dbase = static_cast<char*>(f->b_in.get(inb + 256 + 64));
+    char* hb = static_cast<char*>(f->h_io.get(inb + 256 + 2 * fb + 64));
+    std::memcpy(hb, in, 32);
+    if (dbytes) std::memcpy(hb + 32, deltas, dbytes);
+    double* din = reinterpret_cast<double*>(dbase);
+    int32_t* dd = reinterpret_cast<int32_t*>(dbase + 32);
+    double* dout = reinterpret_cast<double*>(dbase + inb);  // 7 breakdown values
+    SAIR_CUDA(cudaMemcpyAsync(dbase, hb, 32 + dbytes, cudaMemcpyHostToDevice, st));
+    reward_kernel<<<1, 32, 0, st>>>(din, dd, S, 1, view(f), f->l_max, f->c_max, rc, dout);
+    SAIR_LAUNCH("reward_kernel");
+    double* h_rw = reinterpret_cast<double*>(hb + inb);                     // [7]
+    auto* h_res = reinterpret_cast<unsigned long long*>(hb + inb + 64);    // [2]
+    double* h_hv = reinterpret_cast<double*>(hb + inb + 80);                // [1]
+    double* h_fl = reinterpret_cast<double*>(hb + inb + 256);               // [F0 + 1]
+    double* h_fc = h_fl + F0 + 1;
+    if (update) {  // frontier.update on the device, committed there
+        double* ol = f->b_out.as<double>(2 * (F0 + 1) + 4);
+        double* oc = ol + (F0 + 1);
+        double* tmp = f->b_tmp.as<double>(4);
+        auto* res = reinterpret_cast<unsigned long long*>(tmp);
+        insert_one_kernel<<<1, 1024, 0, st>>>(f->fl, f->fc, F0, pl, pc, ol, oc, res);
+        SAIR_LAUNCH("insert_one_kernel");
+        insert_commit_kernel<<<1, 256, 0, st>>>(f->fl, f->fc, ol, oc, res);
+        SAIR_LAUNCH("insert_commit_kernel");
+        hv_after_insert_kernel<<<1, 32, 0, st>>>(f->fl, f->fc, res, F0, tmp + 2);
+        SAIR_LAUNCH("hv_after_insert_kernel");
+        SAIR_CUDA(cudaMemcpyAsync(h_res, res, 24, cudaMemcpyDeviceToHost, st));  // res, hv
+        SAIR_CUDA(cudaMemcpyAsync(h_fl, f->fl, fb, cudaMemcpyDeviceToHost, st));
+        SAIR_CUDA(cudaMemcpyAsync(h_fc, f->fc, fb, cudaMemcpyDeviceToHost, st));
+    }
+    // store(): the row behind them, gated on the reward total on the device
+    store_append_one_async(s, x, dout + 5, round);
+    SAIR_CUDA(cudaMemcpyAsync(h_rw, dout, 56, cudaMemcpyDeviceToHost, st));
+    SAIR_CUDA(cudaStreamSynchronize(st));
+    if (s->pending) {  // the select's outputs
+        auto unpack = std::move(s->pending);
+        s->pending = nullptr;
+        unpack();
+        float tot = 0.f;
+        cudaEventElapsedTime(&tot, s->ev[0], s->ev[3]);
+        s->last.total_ms = tot;
+    }
+    *o_rw = sair_reward_breakdown{h_rw[0], h_rw[1], h_rw[2], h_rw[3], h_rw[4], h_rw[5],
+                                  h_rw[6] != 0.0};
+    *o_inserted = 0;
+    if (update && h_res[0]) {
+        f->F = (size_t)h_res[1];
+        f->hl.assign(h_fl, h_fl + f->F);
+        f->hc.assign(h_fc, h_fc + f->F);
+        f->hv = *h_hv;
+        *o_inserted = 1;
+    }
+    *o_stored = store_append_one_commit(s, x, h_rw[5]);
+}
+
 double action_magnitude(const int32_t* deltas, size_t S, int device) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)

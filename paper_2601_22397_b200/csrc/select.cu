@@ -979,6 +979,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         s->last.exact_fallbacks = 0;
         s->last.small = 1;
         SAIR_CUDA(cudaEventRecord(s->ev[3], s->st));
+        if (s->defer_sync) return;  // the decision step synchronises (and times) later
         SAIR_CUDA(cudaEventSynchronize(s->ev[3]));
         float tot = 0.f;
         cudaEventElapsedTime(&tot, s->ev[0], s->ev[3]);

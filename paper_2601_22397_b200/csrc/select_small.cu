@@ -402,7 +402,7 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
     SAIR_LAUNCH("small_select_kernel");
     char* hout = static_cast<char*>(s->h_out.get(ob));
     SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob, cudaMemcpyDeviceToHost, s->st));
-    SAIR_CUDA(cudaStreamSynchronize(s->st));
+    auto unpack = [=]() {
     const int64_t* hidx = reinterpret_cast<const int64_t*>(hout);
     const double* hsim = reinterpret_cast<const double*>(hidx + nq * m);
     const double* hsc = hsim + nq * m;
@@ -424,6 +424,13 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
             out_nn_sim[g] = hnns[i];
         }
     }
+    };
+    if (s->defer_sync) {  // a decision step: the caller synchronises once, then unpacks
+        s->pending = unpack;
+        return;
+    }
+    SAIR_CUDA(cudaStreamSynchronize(s->st));
+    unpack();
 }
 
 }  // namespace sair

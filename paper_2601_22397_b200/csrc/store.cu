@@ -315,6 +315,62 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
     return n_acc;
 }
 
+// one row appended at `rec` when the reward a previous kernel on the stream
+// computed passes the gate (experience.cpp:136-139); scatter_rows_kernel's layout
+__global__ void scatter_one_gated_kernel(const double* __restrict__ sx,
+                                         const double* __restrict__ reward, double r_min,
+                                         int32_t round, size_t rec, int d, int dp,
+                                         float* __restrict__ pages, float* __restrict__ r32,
+                                         double* __restrict__ r64, int32_t* __restrict__ rnd,
+                                         double* __restrict__ x64,
+                                         const double* __restrict__ shift) {
+    const double r = *reward;
+    if (!(r > r_min)) return;
+    for (int k = threadIdx.x; k < dp; k += blockDim.x) {
+        const double v = k < d ? sx[k] : 0.0;
+        pages[page_index(rec, k, dp)] = k < d ? to_tf32(v - shift[k]) : 0.f;
+        if (k < d) x64[rec * d + k] = v;
+    }
+    if (threadIdx.x == 0) {
+        r64[rec] = r;
+        r32[rec] = (float)r;
+        rnd[rec] = round;
+    }
+}
+
+void store_append_one_async(sair_store_s* s, const double* x, const double* d_reward,
+                            int32_t round) {
+    // callers: a non-empty store of this dimension, capacity reserved
+    const int d = s->d;
+    double* hx = s->h_stage.as<double>((size_t)d + 2);
+    std::memcpy(hx, x, (size_t)d * sizeof(double));
+    double* dx = s->b_stage.as<double>((size_t)d + 2);
+    SAIR_CUDA(cudaMemcpyAsync(dx, hx, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, s->st));
+    scatter_one_gated_kernel<<<1, 64, 0, s->st>>>(dx, d_reward, s->r_min, round, s->n, d, s->dp,
+                                                  s->pages, s->r32, s->r64, s->rnd, s->x64,
+                                                  s->d_shift);
+    SAIR_LAUNCH("scatter_one_gated_kernel");
+}
+
+bool store_append_one_commit(sair_store_s* s, const double* x, double reward) {
+    // the host half of store_append for the row the device just wrote (or not)
+    if (!(reward > s->r_min)) {
+        ++s->rejected;
+        return false;
+    }
+    auto& st = s->stats;
+    for (int j = 0; j < s->d; ++j) {  // experience.cpp:146-149
+        st.sum[j] += x[j];
+        st.sum_sq[j] += x[j] * x[j];
+        st.xabs[j] = std::max(st.xabs[j], std::fabs(x[j]));
+    }
+    st.total += reward;
+    st.rabs = std::max(st.rabs, std::fabs(reward));
+    s->n += 1;
+    ++s->stale;  // experience.cpp:151
+    return true;
+}
+
 void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int dim,
                             int clustered) {
     if (count == 0) return;
