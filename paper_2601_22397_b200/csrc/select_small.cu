@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "select_common.cuh"
@@ -312,6 +313,47 @@ bool small_select_fits(const sair_store_s* s, size_t m) {
     return s->n > 0 && s->n <= SMALL_CS_MAX * SMALL_PER_MAX && m <= 256 && s->d <= 1024;
 }
 
+static size_t small_smem_bytes(size_t n, int d, size_t m, int cs) {
+    // per CTA: score, penalty, similarity, taken per record of its slice; the
+    // query and pick rows; the picks; the bests
+    const size_t per = (n + cs - 1) / cs;
+    return per * 25 + 2 * (size_t)d * 8 + m * 24 + 35 * sizeof(Best) + 64;
+}
+
+// CTAs per query: one record per thread where a cluster of up to 16 CTAs (a
+// non-portable size: it needs a GPC with 16 free SMs) is schedulable, so a
+// step's critical path is one record (10k x 32, m = 8: 73 -> 59 us); else the
+// portable 8.
+static int small_cluster_size(size_t n, int d, size_t m) {
+    const int want = (int)std::min<size_t>(std::getenv("SAIR_SMALL_CS8") ? 8 : 16,
+                                           std::max<size_t>(1, (n + SMALL_THREADS - 1) /
+                                                                   SMALL_THREADS));
+    if (want <= 8) return want;
+    SAIR_CUDA(cudaFuncSetAttribute(small_select_kernel,
+                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const size_t smem = small_smem_bytes(n, d, m, want);
+    SAIR_CUDA(cudaFuncSetAttribute(small_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    cudaLaunchConfig_t oc{};
+    oc.gridDim = dim3((unsigned)want);
+    oc.blockDim = dim3(SMALL_THREADS);
+    oc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute ca[1];
+    ca[0].id = cudaLaunchAttributeClusterDimension;
+    ca[0].val.clusterDim.x = (unsigned)want;
+    ca[0].val.clusterDim.y = 1;
+    ca[0].val.clusterDim.z = 1;
+    oc.attrs = ca;
+    oc.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, small_select_kernel, &oc) != cudaSuccess ||
+        nclusters < 1) {
+        cudaGetLastError();
+        return 8;
+    }
+    return want;
+}
+
 // Exact select() of the queries `qidx` (standardized rows of p.z) in one launch.
 void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>& qidx, size_t m,
                   double lambda, bool local, bool want_nn, int64_t* out_idx, double* out_sim,
@@ -321,7 +363,7 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
     if (nq == 0) return;
     const size_t n = s->n;
     const int d = s->d;
-    const int cs = (int)std::min<size_t>(SMALL_CS_MAX, std::max<size_t>(1, (n + 1023) / 1024));
+    const int cs = small_cluster_size(n, d, m);
     const size_t per = (n + cs - 1) / cs;
     // device scratch: z rows | mean sd | zq | outputs
     const size_t ob = nq * m * (8 * 4 + 4) + nq * (4 + 8 + 8) + 256;
@@ -383,7 +425,7 @@ void small_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>
     a.out_nn_sim = reinterpret_cast<double*>(a.out_nn + nq);
     a.out_round = reinterpret_cast<int32_t*>(a.out_nn_sim + nq);
     a.out_cnt = a.out_round + nq * m;
-    const size_t smem = per * 25 + 2 * (size_t)d * 8 + m * 24 + 35 * sizeof(Best) + 64;
+    const size_t smem = small_smem_bytes(n, d, m, cs);
     SAIR_CUDA(cudaFuncSetAttribute(small_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     cudaLaunchConfig_t lc{};
