@@ -62,6 +62,16 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
 // TF32 operand block, so one contiguous bulk copy of a page lands a ready UMMA
 // operand in shared memory (select_mma.cu), and a warp reading one dimension
 // of 32 records still touches 32 distinct banks.
+#ifdef __CUDACC__
+// the fp32 page copy holds TF32-rounded values (round to nearest): the
+// tensor-core filter then reads the stored values exactly (select_mma.cu)
+__device__ __forceinline__ float to_tf32(double v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"((float)v));
+    return __uint_as_float(r);
+}
+#endif
+
 __host__ __device__ __forceinline__ size_t page_index(size_t rec, int k, int dp) {
     const size_t page = rec / PAGE;
     const uint32_t slot = (uint32_t)(rec % PAGE), b = slot >> 5, t = slot & 31u;

@@ -181,11 +181,8 @@ void store_reserve(sair_store_s* s, size_t need);
 size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
                     const double* reward, const int32_t* round, uint8_t* accepted);
 void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int dim, int clustered);
-// decision step (pareto.cu): store() of one experience whose reward a kernel
-// earlier on the store's stream wrote to d_reward -- the row is written behind
-// it, gated on the device; the commit applies the same gate and the host sums
-void store_append_one_async(sair_store_s* s, const double* x, const double* d_reward,
-                            int32_t round);
+// decision step (pareto.cu): the host half of store() for the row its tail
+// kernel wrote behind the device-side gate -- the same gate, the host sums
 bool store_append_one_commit(sair_store_s* s, const double* x, double reward);
 void store_standardize(const sair_store_s* s, const double* x, double* z);
 double store_effective_sigma(sair_store_s* s, double sigma_sim);

@@ -17,6 +17,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
@@ -215,10 +217,10 @@ __global__ void point_query_kernel(FrontierView f, double pl, double pc, int op,
 
 // insert_normalized, pareto.cpp:43-54, one point, one CTA: reject test, then
 // survivors (not dominated by p) compacted around p's lower_bound slot.
-__global__ void __launch_bounds__(1024)
-    insert_one_kernel(const double* __restrict__ fl, const double* __restrict__ fc, size_t F,
-                      double pl, double pc, double* __restrict__ ol, double* __restrict__ oc,
-                      unsigned long long* __restrict__ res /* [0]=inserted, [1]=newF */) {
+__device__ void insert_one_block(const double* __restrict__ fl, const double* __restrict__ fc,
+                                 size_t F, double pl, double pc, double* __restrict__ ol,
+                                 double* __restrict__ oc,
+                                 unsigned long long* __restrict__ res /* [0]=inserted, [1]=newF */) {
     __shared__ int s_reject;
     __shared__ unsigned s_wsum[32];
     __shared__ size_t s_base;
@@ -279,6 +281,13 @@ __global__ void __launch_bounds__(1024)
         res[0] = 1;
         res[1] = s_base + 1;
     }
+}
+
+__global__ void __launch_bounds__(1024)
+    insert_one_kernel(const double* __restrict__ fl, const double* __restrict__ fc, size_t F,
+                      double pl, double pc, double* __restrict__ ol, double* __restrict__ oc,
+                      unsigned long long* __restrict__ res) {
+    insert_one_block(fl, fc, F, pl, pc, ol, oc, res);
 }
 
 // ---- K6 batch insert --------------------------------------------------------
@@ -1399,32 +1408,90 @@ size_t frontier_set_points(sair_frontier_set_s* s, size_t p, double* l, double* 
 }
 
 // ---------------------------------------------------------- decision step --
-// insert_one_kernel's result committed on the device: the survivors (and the
-// point) copied back when it was inserted
-__global__ void insert_commit_kernel(double* __restrict__ fl, double* __restrict__ fc,
-                                     const double* __restrict__ ol, const double* __restrict__ oc,
-                                     const unsigned long long* __restrict__ res) {
-    if (!res[0]) return;
-    const size_t nF = (size_t)res[1];
-    for (size_t i = threadIdx.x; i < nF; i += blockDim.x) {
-        fl[i] = ol[i];
-        fc[i] = oc[i];
-    }
-}
+struct DecisionTail {
+    const double* in;      // [4] RewardInputs | deltas [S][4] int32 | x [d]
+    const int32_t* deltas;
+    const double* x;
+    size_t S;
+    double* fl;            // the frontier (device), F0 points, capacity >= F0 + 1
+    double* fc;
+    size_t F0;
+    double hv, l_max, c_max;
+    RewardCfg rc;
+    int update;
+    double pl, pc;         // the outcome, normalized (host normalize(), pareto.cpp:20-29)
+    double* ol;            // [F0 + 1] insert scratch
+    double* oc;
+    // the store row
+    double r_min;
+    int32_t round;
+    size_t rec;
+    int d, dp;
+    float* pages;
+    float* r32;
+    double* r64;
+    int32_t* rnd;
+    double* x64;
+    const double* shift;
+    double* out;           // [7] breakdown | [2] insert result | hv | pad | fl [F0+1] | fc [F0+1]
+};
 
-// hypervolume() after the update (pareto.cpp:56-65, point_query_kernel's Q_HV
-// loop), the size read from the insert's result
-__global__ void hv_after_insert_kernel(const double* __restrict__ fl, const double* __restrict__ fc,
-                                       const unsigned long long* __restrict__ res, size_t F0,
-                                       double* __restrict__ out) {
-    if (threadIdx.x || blockIdx.x) return;
-    const size_t F = res[0] ? (size_t)res[1] : F0;
-    double hv = 0.0;
-    for (size_t i = 0; i < F; ++i) {
-        double nl = i + 1 < F ? fl[i + 1] : 1.0;
-        hv = dadd(hv, dmul(dsub(nl, fl[i]), dsub(1.0, fc[i])));
+// Everything after the select, one CTA: compute_reward against the frontier
+// before the update (reward.cpp:21-44), insert_normalized (pareto.cpp:43-54)
+// and its commit, hypervolume() (pareto.cpp:56-65), and the store() row
+// behind the r_min gate on the reward total (experience.cpp:136-139).
+__global__ void __launch_bounds__(1024) decision_tail_kernel(const DecisionTail a) {
+    __shared__ double srw[7];
+    __shared__ unsigned long long sres[2];
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        double pl, pc;
+        reward_row(a.in, a.deltas, a.S, FrontierView{a.fl, a.fc, a.F0, a.hv}, a.l_max, a.c_max,
+                   a.rc, srw, &pl, &pc);
+        sres[0] = 0;
+        sres[1] = a.F0;
     }
-    out[0] = hv;
+    __syncthreads();
+    if (tid < 7) a.out[tid] = srw[tid];
+    if (a.update) {
+        insert_one_block(a.fl, a.fc, a.F0, a.pl, a.pc, a.ol, a.oc, sres);
+        __syncthreads();
+        const size_t F = (size_t)sres[1];
+        if (sres[0])
+            for (size_t i = tid; i < F; i += blockDim.x) {
+                a.fl[i] = a.ol[i];
+                a.fc[i] = a.oc[i];
+            }
+        __syncthreads();
+        double* ml = a.out + 10;
+        double* mc = ml + a.F0 + 1;
+        for (size_t i = tid; i < F; i += blockDim.x) {
+            ml[i] = a.fl[i];
+            mc[i] = a.fc[i];
+        }
+        if (tid == 0) {
+            double hv = 0.0;
+            for (size_t i = 0; i < F; ++i) {
+                double nl = i + 1 < F ? a.fl[i + 1] : 1.0;
+                hv = dadd(hv, dmul(dsub(nl, a.fl[i]), dsub(1.0, a.fc[i])));
+            }
+            a.out[9] = hv;
+            reinterpret_cast<unsigned long long*>(a.out)[7] = sres[0];
+            reinterpret_cast<unsigned long long*>(a.out)[8] = sres[1];
+        }
+    }
+    const double r = srw[5];
+    if (!(r > a.r_min)) return;
+    for (int k = tid; k < a.dp; k += blockDim.x) {
+        const double v = k < a.d ? a.x[k] : 0.0;
+        a.pages[page_index(a.rec, k, a.dp)] = k < a.d ? to_tf32(v - a.shift[k]) : 0.f;
+        if (k < a.d) a.x64[a.rec * a.d + k] = v;
+    }
+    if (tid == 0) {
+        a.r64[a.rec] = r;
+        a.r32[a.rec] = (float)r;
+        a.rnd[a.rec] = a.round;
+    }
 }
 
 // One decision of the reference's loop (harness.cpp:197-261), replayed with the
@@ -1453,6 +1520,9 @@ void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim
         *o_stored = acc;
         return;
     }
+    static const bool trace = std::getenv("SAIR_TRACE_DECISION") != nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     DeviceGuard g(s->device);
     SAIR_CUDA(cudaStreamSynchronize(f->st));
     // capacity first: a reallocation synchronises, and must not move arrays
@@ -1470,45 +1540,58 @@ void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim
         throw;
     }
     s->defer_sync = false;
+    const auto t1 = clk::now();
     cudaStream_t st = s->st;
-    // reward of the outcome against the frontier before the update
+    // one input copy, one kernel, one output copy after the select
+    const int d = s->d;
     const size_t dbytes = S * 4 * 4;
-    const size_t inb = (32 + dbytes + 255) & ~(size_t)255;
-    const size_t fb = (F0 + 1) * 8;
-    char* dbase = static_cast<char*>(f->b_in.get(inb + 256 + 64));
-    char* hb = static_cast<char*>(f->h_io.get(inb + 256 + 2 * fb + 64));
+    const size_t xo = (32 + dbytes + 7) & ~(size_t)7;
+    const size_t inb = xo + (size_t)d * 8;
+    const size_t outn = 10 + 2 * (F0 + 1);
+    char* dbase = static_cast<char*>(f->b_in.get(((inb + 255) & ~(size_t)255) + outn * 8 + 64));
+    char* hb = static_cast<char*>(f->h_io.get(((inb + 255) & ~(size_t)255) + outn * 8 + 64));
     std::memcpy(hb, in, 32);
     if (dbytes) std::memcpy(hb + 32, deltas, dbytes);
-    double* din = reinterpret_cast<double*>(dbase);
-    int32_t* dd = reinterpret_cast<int32_t*>(dbase + 32);
-    double* dout = reinterpret_cast<double*>(dbase + inb);  // 7 breakdown values
-    SAIR_CUDA(cudaMemcpyAsync(dbase, hb, 32 + dbytes, cudaMemcpyHostToDevice, st));
-    reward_kernel<<<1, 32, 0, st>>>(din, dd, S, 1, view(f), f->l_max, f->c_max, rc, dout);
-    SAIR_LAUNCH("reward_kernel");
-    double* h_rw = reinterpret_cast<double*>(hb + inb);                     // [7]
-    auto* h_res = reinterpret_cast<unsigned long long*>(hb + inb + 64);    // [2]
-    double* h_hv = reinterpret_cast<double*>(hb + inb + 80);                // [1]
-    double* h_fl = reinterpret_cast<double*>(hb + inb + 256);               // [F0 + 1]
-    double* h_fc = h_fl + F0 + 1;
-    if (update) {  // frontier.update on the device, committed there
-        double* ol = f->b_out.as<double>(2 * (F0 + 1) + 4);
-        double* oc = ol + (F0 + 1);
-        double* tmp = f->b_tmp.as<double>(4);
-        auto* res = reinterpret_cast<unsigned long long*>(tmp);
-        insert_one_kernel<<<1, 1024, 0, st>>>(f->fl, f->fc, F0, pl, pc, ol, oc, res);
-        SAIR_LAUNCH("insert_one_kernel");
-        insert_commit_kernel<<<1, 256, 0, st>>>(f->fl, f->fc, ol, oc, res);
-        SAIR_LAUNCH("insert_commit_kernel");
-        hv_after_insert_kernel<<<1, 32, 0, st>>>(f->fl, f->fc, res, F0, tmp + 2);
-        SAIR_LAUNCH("hv_after_insert_kernel");
-        SAIR_CUDA(cudaMemcpyAsync(h_res, res, 24, cudaMemcpyDeviceToHost, st));  // res, hv
-        SAIR_CUDA(cudaMemcpyAsync(h_fl, f->fl, fb, cudaMemcpyDeviceToHost, st));
-        SAIR_CUDA(cudaMemcpyAsync(h_fc, f->fc, fb, cudaMemcpyDeviceToHost, st));
-    }
-    // store(): the row behind them, gated on the reward total on the device
-    store_append_one_async(s, x, dout + 5, round);
-    SAIR_CUDA(cudaMemcpyAsync(h_rw, dout, 56, cudaMemcpyDeviceToHost, st));
+    std::memcpy(hb + xo, x, (size_t)d * 8);
+    double* dout = reinterpret_cast<double*>(dbase + ((inb + 255) & ~(size_t)255));
+    double* hout = reinterpret_cast<double*>(hb + ((inb + 255) & ~(size_t)255));
+    SAIR_CUDA(cudaMemcpyAsync(dbase, hb, inb, cudaMemcpyHostToDevice, st));
+    DecisionTail t{};
+    t.in = reinterpret_cast<const double*>(dbase);
+    t.deltas = reinterpret_cast<const int32_t*>(dbase + 32);
+    t.x = reinterpret_cast<const double*>(dbase + xo);
+    t.S = S;
+    t.fl = f->fl;
+    t.fc = f->fc;
+    t.F0 = F0;
+    t.hv = f->hv;
+    t.l_max = f->l_max;
+    t.c_max = f->c_max;
+    t.rc = rc;
+    t.update = update ? 1 : 0;
+    t.pl = pl;
+    t.pc = pc;
+    double* ol = update ? f->b_out.as<double>(2 * (F0 + 1) + 4) : nullptr;
+    t.ol = ol;
+    t.oc = ol ? ol + (F0 + 1) : nullptr;
+    t.r_min = s->r_min;
+    t.round = round;
+    t.rec = s->n;
+    t.d = d;
+    t.dp = s->dp;
+    t.pages = s->pages;
+    t.r32 = s->r32;
+    t.r64 = s->r64;
+    t.rnd = s->rnd;
+    t.x64 = s->x64;
+    t.shift = s->d_shift;
+    t.out = dout;
+    decision_tail_kernel<<<1, 1024, 0, st>>>(t);
+    SAIR_LAUNCH("decision_tail_kernel");
+    SAIR_CUDA(cudaMemcpyAsync(hout, dout, (update ? outn : 7) * 8, cudaMemcpyDeviceToHost, st));
+    const auto t2 = clk::now();
     SAIR_CUDA(cudaStreamSynchronize(st));
+    const auto t3 = clk::now();
     if (s->pending) {  // the select's outputs
         auto unpack = std::move(s->pending);
         s->pending = nullptr;
@@ -1517,17 +1600,27 @@ void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim
         cudaEventElapsedTime(&tot, s->ev[0], s->ev[3]);
         s->last.total_ms = tot;
     }
+    const double* h_rw = hout;
     *o_rw = sair_reward_breakdown{h_rw[0], h_rw[1], h_rw[2], h_rw[3], h_rw[4], h_rw[5],
                                   h_rw[6] != 0.0};
     *o_inserted = 0;
-    if (update && h_res[0]) {
-        f->F = (size_t)h_res[1];
-        f->hl.assign(h_fl, h_fl + f->F);
-        f->hc.assign(h_fc, h_fc + f->F);
-        f->hv = *h_hv;
-        *o_inserted = 1;
+    if (update) {
+        unsigned long long res[2];
+        std::memcpy(res, hout + 7, 16);
+        if (res[0]) {
+            f->F = (size_t)res[1];
+            f->hl.assign(hout + 10, hout + 10 + f->F);
+            f->hc.assign(hout + 10 + F0 + 1, hout + 10 + F0 + 1 + f->F);
+            f->hv = hout[9];
+            *o_inserted = 1;
+        }
     }
     *o_stored = store_append_one_commit(s, x, h_rw[5]);
+    if (trace) {
+        auto us = [](clk::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
+        fprintf(stderr, "[decision] select enqueue %.1f  rest enqueue %.1f  sync wait %.1f  after %.1f us\n",
+                us(t1 - t0), us(t2 - t1), us(t3 - t2), us(clk::now() - t3));
+    }
 }
 
 double action_magnitude(const int32_t* deltas, size_t S, int device) {

@@ -23,6 +23,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <mutex>
 #include <cstdlib>
 #include <vector>
 
@@ -329,9 +332,19 @@ static int small_cluster_size(size_t n, int d, size_t m) {
                                            std::max<size_t>(1, (n + SMALL_THREADS - 1) /
                                                                    SMALL_THREADS));
     if (want <= 8) return want;
+    // the answer only changes with the shared-memory size: remembered (per
+    // process; the pool's GPUs are identical) so a decision step does not pay
+    // the occupancy query
+    static std::mutex mu;
+    static size_t ok_smem = 0, bad_smem = SIZE_MAX;
+    const size_t smem = small_smem_bytes(n, d, m, want);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (smem <= ok_smem) return want;
+        if (smem >= bad_smem) return 8;
+    }
     SAIR_CUDA(cudaFuncSetAttribute(small_select_kernel,
                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    const size_t smem = small_smem_bytes(n, d, m, want);
     SAIR_CUDA(cudaFuncSetAttribute(small_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     cudaLaunchConfig_t oc{};
@@ -349,8 +362,12 @@ static int small_cluster_size(size_t n, int d, size_t m) {
     if (cudaOccupancyMaxActiveClusters(&nclusters, small_select_kernel, &oc) != cudaSuccess ||
         nclusters < 1) {
         cudaGetLastError();
+        std::lock_guard<std::mutex> lk(mu);
+        bad_smem = std::min(bad_smem, smem);
         return 8;
     }
+    std::lock_guard<std::mutex> lk(mu);
+    ok_smem = std::max(ok_smem, smem);
     return want;
 }
 

@@ -16,14 +16,6 @@ namespace sair {
 
 // ---------------------------------------------------------------- kernels --
 
-// the fp32 page copy holds TF32-rounded values (round to nearest): the
-// tensor-core filter then reads the stored values exactly (select_mma.cu)
-__device__ __forceinline__ float to_tf32(double v) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"((float)v));
-    return __uint_as_float(r);
-}
-
 // Scatter `cnt` staged rows (fp64, record-major) into the store at [n0, n0+cnt).
 __global__ void scatter_rows_kernel(const double* __restrict__ sx, const double* __restrict__ sr,
                                     const int32_t* __restrict__ sround, size_t n0, size_t cnt,
@@ -313,43 +305,6 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
     }
     if (!err.empty()) throw Error(SAIR_EINVAL, err);
     return n_acc;
-}
-
-// one row appended at `rec` when the reward a previous kernel on the stream
-// computed passes the gate (experience.cpp:136-139); scatter_rows_kernel's layout
-__global__ void scatter_one_gated_kernel(const double* __restrict__ sx,
-                                         const double* __restrict__ reward, double r_min,
-                                         int32_t round, size_t rec, int d, int dp,
-                                         float* __restrict__ pages, float* __restrict__ r32,
-                                         double* __restrict__ r64, int32_t* __restrict__ rnd,
-                                         double* __restrict__ x64,
-                                         const double* __restrict__ shift) {
-    const double r = *reward;
-    if (!(r > r_min)) return;
-    for (int k = threadIdx.x; k < dp; k += blockDim.x) {
-        const double v = k < d ? sx[k] : 0.0;
-        pages[page_index(rec, k, dp)] = k < d ? to_tf32(v - shift[k]) : 0.f;
-        if (k < d) x64[rec * d + k] = v;
-    }
-    if (threadIdx.x == 0) {
-        r64[rec] = r;
-        r32[rec] = (float)r;
-        rnd[rec] = round;
-    }
-}
-
-void store_append_one_async(sair_store_s* s, const double* x, const double* d_reward,
-                            int32_t round) {
-    // callers: a non-empty store of this dimension, capacity reserved
-    const int d = s->d;
-    double* hx = s->h_stage.as<double>((size_t)d + 2);
-    std::memcpy(hx, x, (size_t)d * sizeof(double));
-    double* dx = s->b_stage.as<double>((size_t)d + 2);
-    SAIR_CUDA(cudaMemcpyAsync(dx, hx, (size_t)d * sizeof(double), cudaMemcpyHostToDevice, s->st));
-    scatter_one_gated_kernel<<<1, 64, 0, s->st>>>(dx, d_reward, s->r_min, round, s->n, d, s->dp,
-                                                  s->pages, s->r32, s->r64, s->rnd, s->x64,
-                                                  s->d_shift);
-    SAIR_LAUNCH("scatter_one_gated_kernel");
 }
 
 bool store_append_one_commit(sair_store_s* s, const double* x, double reward) {
