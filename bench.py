@@ -56,6 +56,12 @@ def parse():
     ap.add_argument("--lambda-div", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pareto", action="store_true")
+    # N > 1: "queries" -- every rank holds the whole store (4.4 GB of 180 GB)
+    # and serves a contiguous slice of each step's queries, no collective;
+    # "records" -- the store is sharded by records (sharded.py) and every
+    # query's per-shard top-m are merged through NCCL (stores beyond one GPU)
+    ap.add_argument("--shard", default=os.environ.get("SAIR_BENCH_SHARD", "queries"),
+                    choices=["queries", "records"])
     return ap.parse_args()
 
 
@@ -131,8 +137,8 @@ def _stream_roofline(stats, n_local, hbm_peak, peak_kind, bf16_peak, qw):
     stream_ms = sum(s["stream_ms"] for s in stats)
     dp = 64 if DIM > 32 else 32
     alg_bytes = n_local * (4 * dp + (8 if qw else 4))
-    per_launch_s = stream_ms / 1e3 / max(launches, 1)
-    achieved = alg_bytes / per_launch_s / 1e9
+    per_launch_s = max(stream_ms / 1e3 / max(launches, 1), 1e-12)
+    achieved = alg_bytes / per_launch_s / 1e9 if launches else 0.0
     out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
            "frac": round(achieved / hbm_peak, 4), "peak_kind": peak_kind,
            "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(per_launch_s * 1e3, 4),
@@ -160,6 +166,7 @@ def run_ours(a, rank, world, local_rank):
     n_total = a.records
     cfg = sair.SelectionConfig(m=K_SEL, lambda_div=a.lambda_div)
     t0 = time.time()
+    qlo, qhi = 0, a.queries
     if world > 1:
         import torch.distributed as dist
         from paper_2601_22397_b200.sharded import ShardedExperienceBuffer, shard_range
@@ -167,6 +174,22 @@ def run_ours(a, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
+    if world > 1 and a.shard == "queries":
+        # the whole store on every rank (device-generated from the same seed:
+        # identical replicas); this rank's slice of every step's queries
+        lo, hi = 0, n_total
+        qlo, qhi = shard_range(a.queries, rank, world)
+        buf = sair.ExperienceBuffer(0.0, device=dev)
+        buf.store_synthetic(SEED, n_total, DIM)
+
+        def select(q):
+            k = len(q)
+            a_, b_ = shard_range(k, rank, world)
+            return buf.select_batch(q[a_:b_], cfg)
+
+        def select_whole(q):  # the north star's few-query latency target: one GPU's pass
+            return buf.select_batch(q, cfg)
+    elif world > 1:
         lo, hi = shard_range(n_total, rank, world)
         sharded = ShardedExperienceBuffer(dist, dev)
         sharded.store_synthetic(SEED, n_total, DIM)
@@ -181,13 +204,15 @@ def run_ours(a, rank, world, local_rank):
 
         def select(q):
             return buf.select_batch(q, cfg)
+    if not (world > 1 and a.shard == "queries"):
+        select_whole = select
     gen_s = time.time() - t0
     qpool = synth.queries(SEED, (a.warmup + a.steps) * a.queries, DIM).reshape(
         a.warmup + a.steps, a.queries, DIM)
     stream = torch.cuda.ExternalStream(buf.stream_ptr(), device=dev)
     hbm_peak, bf16_peak, peak_kind = measured_peaks()
 
-    def timed(qs, steps):
+    def timed(qs, steps, select=select):
         """device time (CUDA events on the store's stream, max over ranks)"""
         stats = []
         if dist:
@@ -247,13 +272,13 @@ def run_ours(a, rank, world, local_rank):
             roof["traffic"] = round(tj["dram_bytes_per_launch"] * scale)
             roof["traffic_source"] = tj.get("source") + (
                 f", scaled x{scale:.3f} to this rank's records" if scale != 1.0 else "")
-    gpu_launches = _launches(stats) + (a.steps if dist else 0)
+    gpu_launches = _launches(stats) + (a.steps if dist and a.shard == "records" else 0)
 
     # the north star's HBM target: Q = 8 queries per step, one memory-bound pass
     qh = synth.queries(SEED + 7, (3 + a.steps) * Q_HBM, DIM).reshape(3 + a.steps, Q_HBM, DIM)
     for i in range(3):
-        select(qh[i])
-    ms_h, st_h = timed(qh[3:], a.steps)
+        select_whole(qh[i])
+    ms_h, st_h = timed(qh[3:], a.steps, select_whole)
     roof_h = _stream_roofline(st_h, hi - lo, hbm_peak, peak_kind, bf16_peak, 0)
     roof_h["kernel"] = f"sair::stream_mma_kernel<{dp},8> (tcgen05)"
     hbm_target = {"queries_per_step": Q_HBM, "value": round(a.steps * Q_HBM / (ms_h / 1e3), 2),
@@ -263,8 +288,8 @@ def run_ours(a, rank, world, local_rank):
     hbm_target["sweep"] = {}
     for qn in (1, 2, 4):
         for i in range(3):
-            select(qh[i][:qn])
-        ms_q, st_q = timed([q[:qn] for q in qh[3:]], a.steps)
+            select_whole(qh[i][:qn])
+        ms_q, st_q = timed([q[:qn] for q in qh[3:]], a.steps, select_whole)
         rq = _stream_roofline(st_q, hi - lo, hbm_peak, peak_kind, bf16_peak, 0)
         hbm_target["sweep"][str(qn)] = {
             "value": round(a.steps * qn / (ms_q / 1e3), 2), "unit": "queries/s",
@@ -284,7 +309,10 @@ def run_ours(a, rank, world, local_rank):
         "config": {"workload": f"configs[3]: {n_total} records x d={DIM}, Q={a.queries} "
                                f"queries/step, k={K_SEL}, lambda_div={a.lambda_div}",
                    "records": n_total, "dim": DIM, "queries_per_step": a.queries, "k": K_SEL,
-                   "lambda_div": a.lambda_div, "parallelism": f"record shards x{world}",
+                   "lambda_div": a.lambda_div,
+                   "parallelism": (f"query shards x{world} (store replicated per GPU, no collective)"
+                                   if world > 1 and a.shard == "queries"
+                                   else f"record shards x{world}"),
                    "l2": "inputs larger than L2 (4.4 GB store streamed per pass vs 126 MB L2)"},
         "e2e": {"value": round(e2e, 2), "unit": "queries/s",
                 "h2d_bytes_per_step": a.queries * DIM * 8,
