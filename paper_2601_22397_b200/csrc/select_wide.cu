@@ -20,7 +20,7 @@
 //
 // Two launches per query group, the same kernel in two modes:
 //   sample  a strided 1/16 of the pages; each warp writes the per-query
-//           maximum key of its 32 records (a transpose-reduce over the warp),
+//           maximum key of its 32 records (redux.sync.max.f32 per column),
 //           so the K'-th largest of those maxima is <= the store's K'-th key
 //           (they belong to distinct records) -> the start threshold t0.
 //   stream  every page; a record whose key beats t0 is appended to its
@@ -105,19 +105,18 @@ __device__ __forceinline__ void list_append(const WideArgs& a, uint32_t* scnt, u
     }
 }
 
-// lane l ends with max over the warp of v[l] (31 shuffles for 32 columns)
-__device__ __forceinline__ float transpose_max(float (&v)[32], int lane) {
+// lane l ends with max over the warp of v[l]: one redux.sync.max.f32 per
+// column (sm_100a; CREDUX into a uniform register) and a select, where the
+// shuffle transpose took 31 shuffles + 62 selects + 31 max per 32 columns
+__device__ __forceinline__ float transpose_max(const float (&v)[32], int lane) {
+    float out = -INFINITY;
 #pragma unroll
-    for (int s = 16; s; s >>= 1) {
-        const bool upper = lane & s;
-#pragma unroll
-        for (int i = 0; i < s; ++i) {
-            const float send = upper ? v[i] : v[i + s];
-            const float keep = upper ? v[i + s] : v[i];
-            v[i] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, s));
-        }
+    for (int j = 0; j < 32; ++j) {
+        float r;
+        asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v[j]));
+        out = lane == j ? r : out;
     }
-    return v[0];
+    return out;
 }
 
 template <int DP, int QW>
@@ -422,21 +421,31 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                         }
                     } else {
                         // sample: per-query maximum over this warp's 32 records
-                        float kn[32];
                         const bool valid = lg != -INFINITY;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const float d2 = (P + scc[c0 + j]) + acc[j];
-                            acc[j] = valid ? fmaf(-d2, a.alpha, lg) : -INFINITY;
-                            kn[j] = valid ? -d2 : -INFINITY;
-                        }
                         const uint32_t S4 = 4 * (a.spages + a.nhot), col = r0 + it * G;
-                        const float mk = transpose_max(acc, lane);
-                        a.smax[(size_t)(c0 + lane) * S4 + 4 * col + quarter] = mk;
                         if (a.knn) {
+                            float kn[32];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const float d2 = (P + scc[c0 + j]) + acc[j];
+                                acc[j] = valid ? fmaf(-d2, a.alpha, lg) : -INFINITY;
+                                kn[j] = valid ? -d2 : -INFINITY;
+                            }
                             const float mn = transpose_max(kn, lane);
                             a.smax[(size_t)(QW + c0 + lane) * S4 + 4 * col + quarter] = mn;
+                        } else if (__all_sync(0xffffffffu, valid)) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                acc[j] = fmaf(-((P + scc[c0 + j]) + acc[j]), a.alpha, lg);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const float d2 = (P + scc[c0 + j]) + acc[j];
+                                acc[j] = valid ? fmaf(-d2, a.alpha, lg) : -INFINITY;
+                            }
                         }
+                        const float mk = transpose_max(acc, lane);
+                        a.smax[(size_t)(c0 + lane) * S4 + 4 * col + quarter] = mk;
                     }
                 }
             }

@@ -1,0 +1,8 @@
+# quick iteration: wide/parity tests, select timing, bench line, launch list of the bench
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_wide.py tests/test_gpu_parity.py -x -q 2>&1 | tail -5
+timeout 300 python scripts/wide_time.py 2>&1 | tail -6
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_iter.json 2> gpurun_out/bench_iter.err; tail -c 300 gpurun_out/bench_iter.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_iter.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-pareto > gpurun_out/ncu_iter.log 2>&1
+python scripts/launch_table.py gpurun_out/launches_iter.csv | head -8
