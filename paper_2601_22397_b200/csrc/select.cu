@@ -1175,7 +1175,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             if (!use_wide) SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
             s->last.stream_launches++;
             for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
-            SAIR_CUDA(cudaMemcpyAsync(dc, hc, nhc * 8, cudaMemcpyHostToDevice, s->st));
+            // (the refine constants of every group go up in one copy after the loop)
             if (!use_wide)
                 launch_merge(s->st, ck, ci, pl.grid, 2 * qb, kmax, qb, kp, knn, mk, mi, mthr);
             if (use_mma || use_wide) {  // keep this group's thresholds past the next group
@@ -1238,6 +1238,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             launch_merge(s->st, lk_g, li_g, wp.grid, 2 * qb, kmax, qb, kp, knn, mk_g, mi_g, mthr_g,
                          kmax, (int)ngroups, lstride, mstride);
         // every group's refine in one launch
+        SAIR_CUDA(cudaMemcpyAsync(dc_g, hc_all, ngroups * nhc * 8, cudaMemcpyHostToDevice, s->st));
         SAIR_CUDA(cudaMemcpyAsync(ra_dev, ra_host, ngroups * sizeof(RefineArgs),
                                   cudaMemcpyHostToDevice, s->st));
         refine_kernel<<<dim3((unsigned)qb, (unsigned)ngroups), 256, refine_smem, s->st>>>(ra_dev);
