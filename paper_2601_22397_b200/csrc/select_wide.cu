@@ -195,7 +195,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < nst; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&empty[s], 2);   // the record-constant warp pair of the page
+            // the MMAs' commit + the record-constant warp pair of the page (they
+            // read it for P; and their arrival keeps their parity waits on
+            // full[] from falling two phases behind)
+            bar_init(&empty[s], 3);
         }
         for (int s = 0; s < ntm; ++s) {
             bar_init(&tfull[s], 1);
@@ -268,12 +271,14 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                     }
                 }
                 umma_commit(&tfull[ts]);
+                umma_commit(&empty[s]);  // the stage is free once these MMAs are done
             }
         }
     } else if (warp >= W_REC) {
         // ---------------- record constants: P, lg, pre-test bounds ----------------
-        // These warps own the shared page stage: P = ||y||^2 needs the page, the
-        // epilogue only TMEM, so the stage is released as soon as the MMA is done.
+        // P = ||y||^2 needs the page (the first pass of a call; later passes read
+        // the (P, lg) cache), the epilogue only TMEM: the stage is released by the
+        // MMAs' commit and these warps, never by the epilogue.
         // A pair of warps per page (the pairs take alternate pages); a thread owns
         // two row-adjacent records: one LDS.64 and one FMUL2 + FFMA2 per dimension.
         const int w = warp - W_REC, half = w & 1;
@@ -337,10 +342,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             *reinterpret_cast<float2*>(pr + 2 * PAGE + rloc) = op;
             *reinterpret_cast<float2*>(pr + 3 * PAGE + rloc) = ol;
             __syncwarp();
-            if (lane == 0) bar_arrive(&pready[it % PR]);
-            bar_wait(&tfull[it % ntm], (it / ntm) & 1u);  // the MMA is done reading the stage
-            __syncwarp();
-            if (lane == 0) bar_arrive(&empty[s]);
+            if (lane == 0) {
+                bar_arrive(&pready[it % PR]);
+                bar_arrive(&empty[s]);  // no wait for the MMA: its commit also arrives
+            }
         }
         if (a.mode == 1) {
 #pragma unroll
