@@ -1106,7 +1106,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         const size_t zstride = (size_t)qb * kp * d;
         char* gbase_p = static_cast<char*>(s->b_grp.get(
             ngroups * (mstride * 8 + 2 * qb * 4 + 2 * qb * 8 + 8 + nhc * 8 + zstride * 8) +
-            8 * 256 + ngroups * sizeof(RefineArgs)));
+            8 * 256 + ngroups * sizeof(RefineArgs) +
+            (use_wide ? ngroups * (hstride * 4 + 4 * (size_t)qb * 4) + 2 * 256 : 0)));
         size_t goff = 0;
         auto gtake = [&](size_t bytes) {
             char* ptr = gbase_p + goff;
@@ -1122,6 +1123,11 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         double* dc_g = reinterpret_cast<double*>(gtake(ngroups * nhc * 8));
         double* zs_g = reinterpret_cast<double*>(gtake(ngroups * zstride * 8));
         RefineArgs* ra_dev = reinterpret_cast<RefineArgs*>(gtake(ngroups * sizeof(RefineArgs)));
+        // wide pass: every group's constants (hstride floats each, the host
+        // staging's image) and list counters [2][2 qb], uploaded / zeroed once
+        float* wc_g = use_wide ? reinterpret_cast<float*>(gtake(ngroups * hstride * 4)) : nullptr;
+        uint32_t* wcnt_g =
+            use_wide ? reinterpret_cast<uint32_t*>(gtake(ngroups * 4 * (size_t)qb * 4)) : nullptr;
         // the wide pass's compacted CTA lists of every group (merged in one launch)
         const size_t lstride = use_wide ? (size_t)wp.grid * 2 * qb * kmax : 0;
         float* lk_g = use_wide ? s->b_wlists.as<float>(ngroups * lstride * 2) : nullptr;
@@ -1141,6 +1147,26 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         s->last.candidates = kp;
         s->last.qb = qb;
         s->last.tensor_core = use_wide ? 2 : (use_mma ? 1 : 0);
+        // wide pass: a group's constants on the host (phase 1 of wfill) and the
+        // refine's cc; they go up in two copies per call -- group 0's, then,
+        // computed while the device runs group 0, every later group's -- not
+        // one copy per group between the passes
+        auto wide_prep = [&](size_t g) {
+            const size_t g0 = g * qb;
+            GroupIo io{};
+            io.hstage = hstage_all + g * hstride;
+            io.t0_override = t0o ? t0o->data() + g * 2 * qb : nullptr;
+            io.phase = 1;
+            wfill(s, wp, p, zc.data() + g0 * d, (int)std::min<size_t>(qb, nbq - g0), c1, c0,
+                  rdelta, alpha, nullptr, nullptr, nullptr, nullptr, cc, io);
+            double* hc = hc_all + g * nhc;
+            for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
+        };
+        if (use_wide) {
+            wide_prep(0);
+            SAIR_CUDA(cudaMemcpyAsync(wc_g, hstage_all, hstride * 4, cudaMemcpyHostToDevice, s->st));
+            SAIR_CUDA(cudaMemsetAsync(wcnt_g, 0, ngroups * 4 * (size_t)qb * 4, s->st));
+        }
         for (size_t g = 0; g < ngroups; ++g) {
             const size_t g0 = g * qb;
             const int nqg = (int)std::min<size_t>(qb, nbq - g0);
@@ -1157,7 +1183,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                              use_wide ? lk_g + g * lstride : nullptr,
                              use_wide ? li_g + g * lstride : nullptr,
                              use_wide && pl_ready ? pl_cache : nullptr,
-                             use_wide && !pl_ready ? pl_cache : nullptr, hot, nhot};
+                             use_wide && !pl_ready ? pl_cache : nullptr, hot, nhot,
+                             use_wide ? 2 : 0, use_wide ? wc_g + g * hstride : nullptr,
+                             use_wide ? wcnt_g + g * 4 * (size_t)qb : nullptr};
             if (use_wide) pl_ready = true;
             const O D = carve(dout + g * ob);
             float* mk = mk_g + g * mstride;
@@ -1173,12 +1201,20 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             else
                 fill(s, pl, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
             if (!use_wide) SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
+            if (use_wide && g == 0 && ngroups > 1) {
+                for (size_t g2 = 1; g2 < ngroups; ++g2) wide_prep(g2);
+                SAIR_CUDA(cudaMemcpyAsync(wc_g + hstride, hstage_all + hstride,
+                                          (ngroups - 1) * hstride * 4, cudaMemcpyHostToDevice,
+                                          s->st));
+            }
             s->last.stream_launches++;
-            for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
+            if (!use_wide)  // (the wide pass's were written by its first loop)
+                for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
             // (the refine constants of every group go up in one copy after the loop)
             if (!use_wide)
                 launch_merge(s->st, ck, ci, pl.grid, 2 * qb, kmax, qb, kp, knn, mk, mi, mthr);
-            if (use_mma || use_wide) {  // keep this group's thresholds past the next group
+            if (use_mma) {  // keep this group's thresholds past the next group (the wide
+                            // pass's stay in the group's own constants / counters)
                 SAIR_CUDA(cudaMemcpyAsync(t0_g + g * 2 * qb, s->mma_t0, 2 * qb * 4,
                                           cudaMemcpyDeviceToDevice, s->st));
                 SAIR_CUDA(cudaMemcpyAsync(drop_g + g * 2 * qb, s->mma_dropped, 2 * qb * 4,
@@ -1217,8 +1253,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.ckey = mk;
             ra.cidx = mi;
             ra.cthr = mthr;
-            ra.t0 = use_mma || use_wide ? t0_g + g * 2 * qb : nullptr;
-            ra.dropped = use_mma || use_wide ? drop_g + g * 2 * qb : nullptr;
+            ra.t0 = use_wide ? s->mma_t0 : (use_mma ? t0_g + g * 2 * qb : nullptr);
+            ra.dropped = use_wide ? s->mma_dropped : (use_mma ? drop_g + g * 2 * qb : nullptr);
             ra.zs = zs_g + g * zstride;
             ra.gbase = s->gbase;
             ra.out_idx = D.idx;

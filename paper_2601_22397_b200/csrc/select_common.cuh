@@ -72,6 +72,13 @@ struct GroupIo {
     float* pl_out;             // wide pass: fill the cache in this group's stream pass
     const uint32_t* hot;       // wide sample: extra pages (highest reward residual), or null
     uint32_t nhot;             // slots in `hot` (entries >= npages are empty)
+    // wide pass, batched call: 0 = compute + upload + launch; 1 = only compute
+    // this group's constants into hstage (and cc); 2 = only launch, the
+    // constants already at dconsts (every group's went up in one copy) and
+    // the list counters at dcnt [2 * 2 QW] already zeroed
+    int phase;
+    float* dconsts;
+    uint32_t* dcnt;
 };
 
 // select_mma.cu: the tcgen05 streaming kernel (plan + launcher)

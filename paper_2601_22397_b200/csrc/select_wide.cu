@@ -601,52 +601,60 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     float* hb = io.hstage;  // nc floats
     float* sv = hb + WB * (size_t)DP * QW;
     float* ccv = sv + DP;
-    for (int k = 0; k < DP; ++k) sv[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
-    cc_out.assign(QW, 0.0);
-    for (int q = 0; q < QW; ++q) {
-        // padded query slots repeat query 0 (their lists are never read)
-        const double* z = zgrp + (size_t)(q < nqg ? q : 0) * d;
-        double cc = 0.0;
-        for (int k = 0; k < DP; ++k) {
-            float c = 0.f;
-            if (k < d) c = (float)((p.mean[k] - s->shift[k]) / p.sd[k] + z[k]);
-            cc += (double)c * (double)c;
-            const double bk = k < d ? -2.0 * (double)c * (double)sv[k] : 0.0;
-            // smem image of the K-major B tiles: (q % 8) * 16 + (q / 8) * 256 +
-            // (k % 4) * 4 + (k / 4) * 128 bytes within K-step k / 8
-            const size_t off = (size_t)(k / 8) * QW * 8 + (q % 8) * 4 + (q / 8) * 64 +
-                               (k % 4) + ((k % 8) / 4) * 32;
-            if (WB == 1) {
-                hb[off] = tf32_rn(bk);
-            } else {
-                const float hi = tf32_trunc(bk);
-                hb[off] = hi;
-                hb[(size_t)DP * QW + off] = tf32_trunc(bk - (double)hi);
-            }
-        }
-        ccv[q] = (float)cc;
-        cc_out[q] = cc;
-    }
-    // device: consts | lists | counters
     const size_t L = 2 * (size_t)QW;
+    if (io.phase != 2) {
+        for (int k = 0; k < DP; ++k) sv[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
+        cc_out.assign(QW, 0.0);
+        for (int q = 0; q < QW; ++q) {
+            // padded query slots repeat query 0 (their lists are never read)
+            const double* z = zgrp + (size_t)(q < nqg ? q : 0) * d;
+            double cc = 0.0;
+            for (int k = 0; k < DP; ++k) {
+                float c = 0.f;
+                if (k < d) c = (float)((p.mean[k] - s->shift[k]) / p.sd[k] + z[k]);
+                cc += (double)c * (double)c;
+                const double bk = k < d ? -2.0 * (double)c * (double)sv[k] : 0.0;
+                // smem image of the K-major B tiles: (q % 8) * 16 + (q / 8) * 256 +
+                // (k % 4) * 4 + (k / 4) * 128 bytes within K-step k / 8
+                const size_t off = (size_t)(k / 8) * QW * 8 + (q % 8) * 4 + (q / 8) * 64 +
+                                   (k % 4) + ((k % 8) / 4) * 32;
+                if (WB == 1) {
+                    hb[off] = tf32_rn(bk);
+                } else {
+                    const float hi = tf32_trunc(bk);
+                    hb[off] = hi;
+                    hb[(size_t)DP * QW + off] = tf32_trunc(bk - (double)hi);
+                }
+            }
+            ccv[q] = (float)cc;
+            cc_out[q] = cc;
+        }
+        if (io.t0_override) std::copy(io.t0_override, io.t0_override + L, hb + (nc - L));
+    }
+    if (io.phase == 1) return;
+    // device: consts | lists | counters
     const size_t S4 = 4 * ((size_t)pl.spages + (io.hot ? io.nhot : 0));
     char* base = static_cast<char*>(s->b_mmab.get(nc * 4 + 256 + L * 8 + S4 * L * 4 + 256));
     float* dc = reinterpret_cast<float*>(base);
     float* dt0 = dc + WB * (size_t)DP * QW + DP + QW;  // the t0 slot of consts
     uint32_t* dcnt = reinterpret_cast<uint32_t*>(base + ((nc * 4 + 255) & ~(size_t)255));
     unsigned int* ddrop = dcnt + L;
-    float* dsmax = reinterpret_cast<float*>(ddrop + L);
+    float* const dsmax = reinterpret_cast<float*>(ddrop + L);
     const size_t lent = (size_t)pl.grid * L * pl.cap;
     char* lists = static_cast<char*>(s->b_sample.get(lent * 8 + 256));
     float* lkey = reinterpret_cast<float*>(lists);
     uint32_t* lidx = reinterpret_cast<uint32_t*>(lists + lent * 4);
-    if (io.t0_override) {  // a retry: start thresholds given, no sample pass
-        std::copy(io.t0_override, io.t0_override + L, hb + (nc - L));
-        SAIR_CUDA(cudaMemcpyAsync(dc, hb, nc * sizeof(float), cudaMemcpyHostToDevice, s->st));
+    if (io.phase == 2) {  // constants and zeroed counters already on the device
+        dc = io.dconsts;
+        dt0 = dc + WB * (size_t)DP * QW + DP + QW;
+        dcnt = io.dcnt;
+        ddrop = dcnt + L;
     } else {
-        SAIR_CUDA(cudaMemcpyAsync(dc, hb, (nc - L) * sizeof(float), cudaMemcpyHostToDevice, s->st));
+        // a retry (start thresholds given, no sample pass) uploads them too
+        SAIR_CUDA(cudaMemcpyAsync(dc, hb, (io.t0_override ? nc : nc - L) * sizeof(float),
+                                  cudaMemcpyHostToDevice, s->st));
+        SAIR_CUDA(cudaMemsetAsync(dcnt, 0, 2 * L * sizeof(uint32_t), s->st));
     }
-    SAIR_CUDA(cudaMemsetAsync(dcnt, 0, 2 * L * sizeof(uint32_t), s->st));
 
     WideArgs a{};
     a.pages = s->pages;
