@@ -856,6 +856,9 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
     // per CTA and list (global memory): ~7 candidates expected at 148 CTAs;
     // 512 absorbs a few pages of concentrated high keys (a freshly appended batch)
     pl->cap = 512;
+    // tests: a tiny capacity forces full lists (the dropped-key bound, the
+    // threshold retry and the exact fallback)
+    if (const char* e = std::getenv("SAIR_WIDE_CAP")) pl->cap = (uint32_t)std::max(1, std::atoi(e));
     const size_t limit = 227 * 1024;
     // TMEM: ntm stages x QW columns <= 512; as many shared page stages as fit
     pl->ntm = std::min(8, 512 / pl->qw);

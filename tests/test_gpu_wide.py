@@ -150,3 +150,30 @@ def test_wide_after_high_residual_append(orc):
         oi, osim, osc, ocnt = orc.select_batch(ctx, rew, rnd, xq, m, 0.0, db.effective_sigma())
         assert np.array_equal(cnt, ocnt) and np.array_equal(idx, oi)
         assert near(sc, osc, 1e-12) and near(sim, osim, 1e-12)
+
+
+@pytest.mark.parametrize("cap", [1, 4])
+def test_wide_full_lists_retry_and_fallback(orc, cap):
+    """Per-CTA lists far too small (SAIR_WIDE_CAP): lists overflow, the
+    dropped-key bound leaves queries uncertified, the threshold retry pass
+    (start thresholds uploaded with the group constants) and the exact
+    fallback finish them -- the answer is still the oracle's."""
+    n, d, nq, m = 70000, 32, 160, 16
+    db, ctx, rew, rnd = synth_store(n + 7, n, d)
+    sigma = db.effective_sigma()
+    xq = synth.queries(n + 8, nq, d)
+    os.environ["SAIR_WIDE_CAP"] = str(cap)
+    try:
+        idx, sim, sc, cnt = db.select_batch(xq, SelectionConfig(m=m, lambda_div=0.0))
+        st = db.last_stats()
+    finally:
+        os.environ.pop("SAIR_WIDE_CAP", None)
+    assert st["tensor_core"] == 2 and st["retried"] > 0, st
+    oi, osim, osc, ocnt = orc.select_batch(ctx, rew, rnd, xq, m, 0.0, sigma)
+    assert np.array_equal(cnt, ocnt)
+    assert np.array_equal(idx, oi)
+    assert near(sc, osc, 1e-12) and near(sim, osim, 1e-12)
+    # and the next call (default capacity) is unaffected
+    idx2, _, sc2, _ = db.select_batch(xq, SelectionConfig(m=m, lambda_div=0.0))
+    assert db.last_stats()["retried"] == 0
+    assert np.array_equal(idx2, oi) and near(sc2, osc, 1e-12)
