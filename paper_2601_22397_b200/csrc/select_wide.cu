@@ -4,25 +4,28 @@
 // (SURVEY.md 8(a) A9 "K4", configs 2/4/5), so one pass over the store serves
 // QW = 32/64/128 queries at once instead of one pass per 8 (select_mma.cu):
 //
-//   warp 8 (producer)  one bulk copy (TMA engine) per page into an NST-deep
+//   warp 16 (producer) one bulk copy (TMA engine) per page into an NST-deep
 //                      shared-memory ring; pages are stored as ready MN-major
 //                      SWIZZLE_128B_BASE32B TF32 operand blocks (common.cuh).
-//   warp 9 (MMA)       per page 2 x DP/8 tcgen05.mma kind::tf32, M = 128
-//                      records x N = QW queries x K = 8: A = the page tile,
-//                      B = the query constants -2 c_qk / sd_k split hi + lo in
-//                      TF32, both halves accumulating into the same TMEM
-//                      columns (fp32).  The records are TF32-exact (stored
-//                      rounded), so the split keeps the fp32 filter tolerance.
-//   epilogue warps     three groups of four lane quarters take every third page:
-//                      P = ||y||^2 from the shared tile, then 32 TMEM columns
-//                      at a time (tcgen05.ld 32x32b.x32): key = log2 residual
-//                      - alpha d2 per (record, query).
+//   warp 17 (MMA)      per page DP/8 tcgen05.mma kind::tf32, M = 128 records x
+//                      N = QW queries x K = 8: A = the page tile, B = the query
+//                      constants -2 c_qk / sd_k rounded to nearest TF32 (WB = 1;
+//                      the bounded perturbation is carried by the
+//                      certification), accumulating into TMEM (fp32); its
+//                      commit also releases the page's shared stage.
+//   warps 12-15        record constants: P = ||y||^2 (or the per-call cache),
+//                      the log residual and the pre-test bounds per record.
+//   warps 0-11         epilogue, three groups of four lane quarters taking every
+//                      third page: 32 TMEM columns at a time (tcgen05.ld
+//                      32x32b.x32), a loose pre-test per (record, query) pair,
+//                      the exact key = log2 residual - alpha d2 on the rare hit.
 //
 // Two launches per query group, the same kernel in two modes:
-//   sample  a strided 1/16 of the pages; each warp writes the per-query
-//           maximum key of its 32 records (redux.sync.max.f32 per column),
-//           so the K'-th largest of those maxima is <= the store's K'-th key
-//           (they belong to distinct records) -> the start threshold t0.
+//   sample  sqrt(5 K' npages) strided pages plus the highest-residual pages;
+//           each warp writes the per-query maximum key of its 32 records
+//           (redux.sync.max.f32 per column), so the K'-th largest of those
+//           maxima is <= the store's K'-th key (distinct records) -> the
+//           start threshold t0 (wide_kth_kernel).
 //   stream  every page; a record whose key beats t0 is appended to its
 //           query's list of this CTA (shared-memory slot counter, global
 //           store; a full list only records the largest key it dropped,
