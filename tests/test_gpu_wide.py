@@ -177,3 +177,23 @@ def test_wide_full_lists_retry_and_fallback(orc, cap):
     idx2, _, sc2, _ = db.select_batch(xq, SelectionConfig(m=m, lambda_div=0.0))
     assert db.last_stats()["retried"] == 0
     assert np.array_equal(idx2, oi) and near(sc2, osc, 1e-12)
+
+
+def test_wide_32_and_64_query_kernels_many_pages_per_cta():
+    """The 32- and 64-query wide kernels (5 shared page stages, 8 TMEM stages)
+    over 4M records (~220 pages per CTA: the rings wrap many times) certify
+    every query and give the 8-query pass's answer."""
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(4242, 1 << 22, 64)
+    cfg = SelectionConfig(m=32, lambda_div=0.0)
+    for nq, qb in ((40, 32), (100, 64)):
+        xq = synth.queries(4243 + nq, nq, 64)
+        idx, sim, sc, cnt = db.select_batch(xq, cfg)
+        st = db.last_stats()
+        assert st["qb"] == qb and st["tensor_core"] == 2, st
+        assert st["certified"] == nq and st["exact_fallbacks"] == 0, st
+        with no_wide():
+            idx8, sim8, sc8, cnt8 = db.select_batch(xq, cfg)
+        assert db.last_stats()["tensor_core"] == 1
+        assert np.array_equal(cnt, cnt8) and np.array_equal(idx, idx8)
+        assert near(sc, sc8, 1e-12) and near(sim, sim8, 1e-12)
