@@ -191,9 +191,28 @@ class ExperienceBuffer:
         o._mirror = False
         return o, bad.value
 
-    def persist(self, path: str):
-        """ExperienceBuffer::persist (experience.cpp:232-241) from the device store
-        (source / action are not held on the device and are written empty)."""
+    def persist(self, path: str, lossy: bool = False):
+        """ExperienceBuffer::persist (experience.cpp:232-241).  With the AoS mirror
+        (rows stored one by one) every record is written from it, source and
+        action included, in nlohmann's compact dump format (sorted keys) -- what
+        the reference itself writes.  Without it (bulk / synthetic / loaded rows)
+        the device store holds no source or action: that export writes them
+        empty and must be asked for with ``lossy=True``."""
+        if self._mirror:
+            import json
+            with open(path, "w", encoding="utf-8") as out:
+                for e in self._items:
+                    act = [{"cpu_millicores": int(st.cpu_millicores), "memory_mb": int(st.memory_mb),
+                            "rate_ratio_tenths": int(st.rate_ratio_tenths),
+                            "replicas": int(st.replicas)} for st in e.action.stages]
+                    j = {"action": act, "context": [float(v) for v in e.context],
+                         "reward": float(e.reward), "round": int(e.round), "source": e.source}
+                    out.write(json.dumps(j, separators=(",", ":"), ensure_ascii=False) + "\n")
+            return
+        if not lossy:
+            raise LogicError(_lib.SAIR_ELOGIC,
+                             "persist(): no host mirror of source/action for bulk rows; "
+                             "pass lossy=True to write them empty")
         _check(lib().sair_store_persist_jsonl(self._h, str(path).encode()))
 
     def export(self, offset: int = 0, count: Optional[int] = None):

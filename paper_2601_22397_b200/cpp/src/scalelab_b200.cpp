@@ -145,6 +145,8 @@ double ExperienceBuffer::surprisal(std::size_t index, const std::vector<double>&
 std::vector<std::vector<SelectedExperience>> ExperienceBuffer::select_batch(
     const std::vector<std::vector<double>>& queries, const SelectionConfig& cfg,
     std::vector<std::int64_t>* nearest, std::vector<double>* nearest_sim) const {
+    if ((nearest == nullptr) != (nearest_sim == nullptr))
+        throw std::invalid_argument("select_batch: nearest and nearest_sim come in pairs");
     const std::size_t nq = queries.size();
     std::vector<std::vector<SelectedExperience>> out(nq);
     if (nq == 0) return out;
@@ -165,7 +167,7 @@ std::vector<std::vector<SelectedExperience>> ExperienceBuffer::select_batch(
     const sair_select_config c = to_c(cfg);
     check(sair_store_select(h_, q.data(), nq, d, &c, idx.data(), sim.data(), score.data(),
                             cnt.data(), nearest ? nearest->data() : nullptr,
-                            nearest ? nearest_sim->data() : nullptr));
+                            nearest_sim ? nearest_sim->data() : nullptr));
     for (std::size_t i = 0; i < nq; ++i)
         for (std::size_t j = 0; j < cnt[i]; ++j)
             out[i].push_back({items_.at(static_cast<std::size_t>(idx[i * m + j])),

@@ -1482,9 +1482,10 @@ __global__ void __launch_bounds__(1024) decision_tail_kernel(const DecisionTail 
     }
     const double r = srw[5];
     if (!(r > a.r_min)) return;
-    for (int k = tid; k < a.dp; k += blockDim.x) {
+    const int w = a.d > a.dp ? a.d : a.dp;  // x64 takes all d columns, the page dp
+    for (int k = tid; k < w; k += blockDim.x) {
         const double v = k < a.d ? a.x[k] : 0.0;
-        a.pages[page_index(a.rec, k, a.dp)] = k < a.d ? to_tf32(v - a.shift[k]) : 0.f;
+        if (k < a.dp) a.pages[page_index(a.rec, k, a.dp)] = k < a.d ? to_tf32(v - a.shift[k]) : 0.f;
         if (k < a.d) a.x64[a.rec * a.d + k] = v;
     }
     if (tid == 0) {

@@ -986,8 +986,11 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         s->last.total_ms = tot;
         return;
     }
+    // the filter's certification bounds an outside record's gain by its score,
+    // which needs lambda_div >= 0 (a negative lambda rewards similarity; the
+    // reference accepts it, scenario.cpp:197): those queries take the exact paths
     const bool fast = cfg.mode != SAIR_SELECT_EXACT && !cfg.locally_weighted_mean && d <= 128 &&
-                      n < (size_t)1 << 31 && m <= 256;
+                      n < (size_t)1 << 31 && m <= 256 && cfg.lambda_div >= 0.0;
     float stream_ms = 0.f, prepass_ms = 0.f;
     if (fast) {
         // tensor-core streaming kernel when the shape fits,

@@ -23,15 +23,17 @@ __global__ void scatter_rows_kernel(const double* __restrict__ sx, const double*
                                     float* __restrict__ r32, double* __restrict__ r64,
                                     int32_t* __restrict__ rnd, double* __restrict__ x64,
                                     const double* __restrict__ shift) {
-    size_t total = cnt * (size_t)dp;
+    // w covers both layouts: the page row holds dp >= min(d, 256) columns
+    // (d > 256 never takes the fp32 filter paths), x64 every one of the d
+    const int w = d > dp ? d : dp;
+    size_t total = cnt * (size_t)w;
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
          t += (size_t)gridDim.x * blockDim.x) {
-        size_t i = t / dp;
-        int k = (int)(t % dp);
+        size_t i = t / w;
+        int k = (int)(t % w);
         size_t rec = n0 + i;
         double v = k < d ? sx[i * d + k] : 0.0;
-        pages[page_index(rec, k, dp)] =
-            k < d ? to_tf32(v - shift[k]) : 0.f;
+        if (k < dp) pages[page_index(rec, k, dp)] = k < d ? to_tf32(v - shift[k]) : 0.f;
         if (k < d) x64[rec * d + k] = v;
         if (k == 0) {
             r64[rec] = sr[i];
@@ -291,7 +293,7 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
             SAIR_CUDA(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, s->st));
             SAIR_CUDA(cudaMemcpyAsync(dr, hr, k * 8, cudaMemcpyHostToDevice, s->st));
             SAIR_CUDA(cudaMemcpyAsync(dround, hround, k * 4, cudaMemcpyHostToDevice, s->st));
-            size_t work = k * (size_t)s->dp;
+            size_t work = k * (size_t)std::max(s->dp, s->d);
             int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
             scatter_rows_kernel<<<blocks, 256, 0, s->st>>>(dx, dr, dround, s->n, k, s->d, s->dp,
                                                            s->pages, s->r32, s->r64, s->rnd,

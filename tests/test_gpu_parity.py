@@ -138,6 +138,49 @@ def test_select_matches_reference(ref, lam, n, d, m):
         assert nn_i[q] == best and abs(nn_s[q] - sims[best]) <= 1e-12
 
 
+@pytest.mark.parametrize("n,d", [(600, 300), (70000, 300)])
+def test_wide_contexts_beyond_the_page_width(ref, orc, n, d):
+    """d > 256 (37+ stages): the page rows hold 256 columns, the fp64 rows all
+    d -- sigma, get, select (one-launch small path below 64k records, the exact
+    passes above) against the reference / its pinned restatement."""
+    rng = np.random.default_rng(d + n)
+    ctx = rng.normal(size=(n, d)) * rng.uniform(0.5, 5, d)
+    rew = rng.uniform(0.01, 1.01, n)
+    rounds = np.arange(n, dtype=np.int32)
+    db = ExperienceBuffer(0.0)
+    db.store_many(ctx, rew, rounds)
+    c, r, _ = db.get(n - 1)
+    assert np.array_equal(c, ctx[n - 1]) and r == rew[n - 1]
+    sigma = db.effective_sigma()
+    assert sigma == orc.sigma_median(ctx)
+    xq = rng.normal(size=(3, d))
+    for lam in (0.0, 0.1):
+        idx, sim, sc, cnt = db.select_batch(xq, SelectionConfig(m=8, lambda_div=lam))
+        oi, osim, osc, _ = orc.select_batch(ctx, rew, rounds, xq, 8, lam, sigma)
+        assert np.array_equal(idx, oi)
+        assert near(sc, osc, 1e-12)
+    if n <= 1000:
+        rb = RefBuffer(ref, 0.0)
+        rb.store_many(ctx, rew, rounds)
+        r_round, _, r_score = rb.select(xq[0], 8, 0.1, 0.0)
+        assert np.array_equal(rounds[idx[0, :len(r_round)]], r_round)
+
+
+@pytest.mark.parametrize("n", [3000, 100000])
+def test_negative_lambda_takes_the_exact_path(orc, n):
+    """lambda_div < 0 (accepted by the reference, scenario.cpp:197) rewards
+    similarity: the score bound cannot certify it, the answer is the exact one."""
+    d = 16
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(21, n, d)
+    ctx, rew, rnd = synth.contexts(21, 0, n, d), synth.rewards(21, 0, n), synth.rounds(0, n)
+    xq = synth.queries(22, 40, d)
+    idx, sim, sc, cnt = db.select_batch(xq, SelectionConfig(m=8, lambda_div=-0.3))
+    oi, osim, osc, _ = orc.select_batch(ctx, rew, rnd, xq, 8, -0.3, db.effective_sigma())
+    assert np.array_equal(idx, oi)
+    assert near(sc, osc, 1e-12)
+
+
 def test_exact_mode_and_fast_path_agree(orc):
     n, d = 50000, 64
     ctx = synth.contexts(11, 0, n, d)

@@ -74,7 +74,9 @@ def test_persist_round_trip_through_the_reference(ref, tmp_path):
     db = ExperienceBuffer(0.0)
     db.store_synthetic(5, n, d)
     p = tmp_path / "out.jsonl"
-    db.persist(p)
+    with pytest.raises(sair.LogicError):   # bulk rows: no source/action to write
+        db.persist(p)
+    db.persist(p, lossy=True)
     rb, bad = RefBuffer.load(ref, p, 0.0)
     assert bad == 0 and rb.size() == n
     q = tmp_path / "ref.jsonl"
@@ -84,3 +86,25 @@ def test_persist_round_trip_through_the_reference(ref, tmp_path):
     a, b = db.export(), back.export()
     assert bad == 0 and all(np.array_equal(u, v) for u, v in zip(a, b))
     assert np.array_equal(a[0][123], synth.contexts(5, 123, 1, d)[0])
+
+
+def test_persist_from_the_mirror_keeps_source_and_action(ref, tmp_path):
+    """Rows stored one by one keep the host mirror: persist() writes their
+    source and action, byte-identical to the reference's own persist()."""
+    rng = np.random.default_rng(9)
+    db = ExperienceBuffer(0.0)
+    for i in range(40):
+        act = sair.ScalingAction([sair.StageDelta(int(rng.integers(-2, 3)), int(rng.integers(-500, 500)),
+                                                  int(rng.integers(-64, 64)), int(rng.integers(-3, 4)))
+                                  for _ in range(3)])
+        db.store(sair.Experience(list(rng.normal(size=23) * rng.uniform(0.1, 1e3)), act,
+                                 float(rng.normal()), i, ["llm", "mock", "explore"][i % 3]))
+    p = tmp_path / "mirror.jsonl"
+    db.persist(p)
+    lines = p.read_text().splitlines()
+    assert len(lines) == db.size() and all(json.loads(x)["action"] for x in lines)
+    rb, bad = RefBuffer.load(ref, p, 0.0)
+    assert bad == 0 and rb.size() == db.size()
+    q = tmp_path / "ref.jsonl"
+    rb.persist(q)
+    assert p.read_bytes() == q.read_bytes()
