@@ -597,7 +597,7 @@ def _cpu_model():
 def run_reference(a):
     """The reference's own select (oracle/_ref: proj/src/experience.cpp compiled
     unmodified, -O3 -DNDEBUG) on the host cores.  The literal select is O(N^2)
-    (experience.cpp:229-231 inside :255-258), so each step is a bounded sample:
+    (experience.cpp:138-140 inside :163-167), so each step is a bounded sample:
     Q queries over an n_s-record buffer on Q threads; the 16M-equivalent rate
     is extrapolated from a quadratic fit through two sample sizes."""
     from oracle.oracle import REF_SO, Ref, RefBuffer

@@ -4,8 +4,8 @@
  * This is the drop-in boundary.  The reference exposes the path as a C++
  * class API (namespace scalelab); it has no FFI of its own.  Each entry point
  * below replaces one reference member, cited as file:line relative to
- * /root/reference/proj.  The host-side mirrors (paper_2601_22397_b200/
- * scalelab_api.hpp for C++, paper_2601_22397_b200/__init__.py for Python)
+ * /root/reference/proj.  The host-side mirrors (paper_2601_22397_b200/cpp/: the scalelab
+ * classes for C++; paper_2601_22397_b200/__init__.py for Python)
  * call only these functions.  See INTEGRATION.md for the bindings.
  *
  * Conventions
@@ -93,14 +93,14 @@ SAIR_API sair_status sair_device_count(int* out);
  * Experience store -- ExperienceBuffer (experience.hpp:45-89)
  * ------------------------------------------------------------------------ */
 
-/* ExperienceBuffer(double r_min), experience.cpp:133. Device-resident SoA. */
+/* ExperienceBuffer(double r_min), experience.cpp:42. Device-resident SoA. */
 SAIR_API sair_status sair_store_create(double r_min, int device, size_t capacity_hint,
                                        sair_store_t* out);
 SAIR_API sair_status sair_store_destroy(sair_store_t h);
 /* Deep copy (the reference's value semantics, experience.hpp:45). */
 SAIR_API sair_status sair_store_clone(sair_store_t h, sair_store_t* out);
 
-/* ExperienceBuffer::store for `count` rows, experience.cpp:135-153: each row is
+/* ExperienceBuffer::store for `count` rows, experience.cpp:44-62: each row is
  * gated (reward > r_min, else counted as rejected); the dimension is fixed by
  * the first accepted row and a change is SAIR_EINVAL (rows before the bad one
  * stay stored, as with sequential store() calls).  ctx is count x dim fp64
@@ -125,7 +125,7 @@ SAIR_API sair_status sair_store_r_min(sair_store_t h, double* out);      /* r_mi
 SAIR_API sair_status sair_store_get(sair_store_t h, size_t index, double* ctx, double* reward,
                                     int32_t* round);
 
-/* ExperienceBuffer::standardize, experience.cpp:155-169 (fp64, host-kept sums). */
+/* ExperienceBuffer::standardize, experience.cpp:64-78 (fp64, host-kept sums). */
 /* Bulk device->host copy of records [offset, offset + count) (each pointer
  * nullable): ctx [count][dim], reward [count], round [count]. */
 SAIR_API sair_status sair_store_export(sair_store_t h, size_t offset, size_t count, double* ctx,
@@ -147,21 +147,21 @@ SAIR_API sair_status sair_store_persist_jsonl(sair_store_t h, const char* path);
 
 SAIR_API sair_status sair_store_standardize(sair_store_t h, const double* x, int dim, double* z);
 
-/* ExperienceBuffer::effective_sigma, experience.cpp:207-212, including the
- * stale-after-50-insertions cache; a refresh (experience.cpp:171-205) runs the
+/* ExperienceBuffer::effective_sigma, experience.cpp:116-121, including the
+ * stale-after-50-insertions cache; a refresh (experience.cpp:80-114) runs the
  * 512-subsample pairwise median on the device. */
 SAIR_API sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double* out);
 
-/* similarity(a, b, sigma), experience.cpp:121-131: SAIR_EINVAL when the
+/* similarity(a, b, sigma), experience.cpp:30-40: SAIR_EINVAL when the
  * lengths differ or sigma <= 0. */
 SAIR_API sair_status sair_similarity(const double* a, size_t len_a, const double* b, size_t len_b,
                                      double sigma, double* out);
 
-/* ExperienceBuffer::surprisal, experience.cpp:234-240 (SAIR_ERANGE on a bad index). */
+/* ExperienceBuffer::surprisal, experience.cpp:143-149 (SAIR_ERANGE on a bad index). */
 SAIR_API sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, int dim,
                                           const sair_select_config* cfg, double* out);
 
-/* ExperienceBuffer::select for nq queries, experience.cpp:242-296.
+/* ExperienceBuffer::select for nq queries, experience.cpp:151-205.
  * queries: nq x dim fp64.  For query q, out_count[q] = min(m, n) picks are
  * written at out_idx/out_sim/out_score[q*m ...] in the reference's curriculum
  * order (stable by reward asc, round asc).  out_idx are store indices
@@ -189,7 +189,7 @@ SAIR_API sair_status sair_store_last_stats(sair_store_t h, sair_select_stats* ou
 
 /* Global index of this store's first record (call before the first append). */
 SAIR_API sair_status sair_store_set_shard(sair_store_t h, int64_t global_offset);
-/* This store's own sums (experience.cpp:146-149): sum[d], sum_sq[d], max|x|[d],
+/* This store's own sums (experience.cpp:55-58): sum[d], sum_sq[d], max|x|[d],
  * scalars[3] = {n, reward total (index order), max |reward|}. */
 SAIR_API sair_status sair_store_local_stats(sair_store_t h, double* sum, double* sum_sq,
                                             double* xabs, double* scalars);
@@ -199,14 +199,14 @@ SAIR_API sair_status sair_store_set_global(sair_store_t h, uint64_t n_global, co
                                            const double* sum_sq, const double* xabs,
                                            double reward_total, double reward_absmax,
                                            double sigma);
-/* mean[d] and sd[d] of standardize() (experience.cpp:159-165) for this store's
+/* mean[d] and sd[d] of standardize() (experience.cpp:68-74) for this store's
  * statistics (global ones in shard mode). */
 SAIR_API sair_status sair_store_moments(sair_store_t h, double* mean, double* sd);
 /* The global indices refresh_sigma_cache samples from an n-record buffer
- * (experience.cpp:173-182); m <= 512 returned. */
+ * (experience.cpp:82-91); m <= 512 returned. */
 SAIR_API sair_status sair_sigma_sample_indices(uint64_t n, int64_t* idx, size_t* m);
 /* The median pairwise z-distance of m raw rows (m x dim) standardized with
- * mean/sd (experience.cpp:183-203), computed on `device`. */
+ * mean/sd (experience.cpp:92-112), computed on `device`. */
 SAIR_API sair_status sair_sigma_rows(const double* rows, size_t m, int dim, const double* mean,
                                      const double* sd, int device, double* out);
 /* select() on a shard: as sair_store_select plus each pick's reward and round
@@ -223,7 +223,7 @@ SAIR_API sair_status sair_store_select_shard(sair_store_t h, const double* queri
 SAIR_API sair_status sair_merge_topk_packed(const double* d_parts, size_t nshards, size_t nq,
                                             size_t m, int device, void* stream, double* d_out);
 /* The shard's side of select() for lambda_div > 0 on a buffer spread over
- * ranks (experience.cpp:261-285 with the arg-max taken across shards by the
+ * ranks (experience.cpp:170-194 with the arg-max taken across shards by the
  * caller between steps; sharded.py).  greedy_begin scores this shard for nq
  * queries (global statistics, exact fp64) and writes per query the shard's
  * best untaken record as nq x (6 + dim) doubles: gain, round, global index

@@ -15,7 +15,7 @@
  *
  * One deliberate restructuring, bit-identical by construction:
  * ExperienceBuffer::loo_mean re-sums every reward on every call
- * (src/experience.cpp:229-231), making select O(n^2).  The sum is
+ * (src/experience.cpp:138-140), making select O(n^2).  The sum is
  * loop-invariant and always accumulated in index order from 0.0, so it is
  * computed once per select here: same additions, same order, same bits.
  *
@@ -35,7 +35,7 @@
 /* Retrieval                                                                */
 /* ------------------------------------------------------------------------ */
 
-/* Running per-dimension sums in append order: src/experience.cpp:146-149. */
+/* Running per-dimension sums in append order: src/experience.cpp:55-58. */
 ORC_API void orc_stats(const double* ctx, size_t n, int d, double* sum, double* sum_sq) {
     for (int k = 0; k < d; ++k) { sum[k] = 0.0; sum_sq[k] = 0.0; }
     for (size_t i = 0; i < n; ++i) {
@@ -47,14 +47,14 @@ ORC_API void orc_stats(const double* ctx, size_t n, int d, double* sum, double* 
     }
 }
 
-/* Reward total in index order, from 0.0: src/experience.cpp:229-230. */
+/* Reward total in index order, from 0.0: src/experience.cpp:138-139. */
 ORC_API double orc_reward_total(const double* reward, size_t n) {
     double total = 0.0;
     for (size_t i = 0; i < n; ++i) total += reward[i];
     return total;
 }
 
-/* ExperienceBuffer::standardize, src/experience.cpp:155-169.  n == 0 copies x. */
+/* ExperienceBuffer::standardize, src/experience.cpp:64-78.  n == 0 copies x. */
 ORC_API void orc_standardize(size_t n, int d, const double* sum, const double* sum_sq,
                              const double* x, double* z) {
     if (n == 0) {
@@ -72,7 +72,7 @@ ORC_API void orc_standardize(size_t n, int d, const double* sum, const double* s
     }
 }
 
-/* similarity, src/experience.cpp:121-131 (caller guarantees sigma > 0). */
+/* similarity, src/experience.cpp:30-40 (caller guarantees sigma > 0). */
 ORC_API double orc_similarity(const double* a, const double* b, int d, double sigma) {
     double d2 = 0.0;
     for (int k = 0; k < d; ++k) {
@@ -87,7 +87,7 @@ static int cmp_double(const void* a, const void* b) {
     return (x > y) - (x < y);
 }
 
-/* refresh_sigma_cache, src/experience.cpp:171-205: median pairwise z-distance
+/* refresh_sigma_cache, src/experience.cpp:80-114: median pairwise z-distance
  * over the strided 512-subsample; the element nth_element places at size/2,
  * i.e. the (size/2)-th order statistic.  Returns 1.0 for < 2 rows. */
 ORC_API double orc_sigma_median(const double* ctx, size_t n, int d, const double* sum,
@@ -141,7 +141,7 @@ typedef struct {
     size_t n_loo; /* records of the whole buffer (== n unless this is a shard) */
 } orc_store;
 
-/* Per-record surprisal score: src/experience.cpp:254-258 with the global
+/* Per-record surprisal score: src/experience.cpp:163-167 with the global
  * leave-one-out mean of :214-231 (locally_weighted_mean == false). */
 static void score_all(const orc_store* s, const double* zq, double sigma, double* score,
                       double* sim_curr, double* ztmp) {
@@ -157,7 +157,7 @@ static void score_all(const orc_store* s, const double* zq, double sigma, double
     }
 }
 
-/* Kernel-weighted leave-one-out mean, src/experience.cpp:216-228, falling back
+/* Kernel-weighted leave-one-out mean, src/experience.cpp:125-137, falling back
  * to the global mean when the weights vanish. */
 static double loo_local(const orc_store* s, size_t i, double sigma, double* zi, double* zj) {
     size_t n = s->n;
@@ -176,7 +176,7 @@ static double loo_local(const orc_store* s, size_t i, double sigma, double* zi, 
     return (s->total - s->reward[i]) / (double)(n - 1);
 }
 
-/* ExperienceBuffer::select, src/experience.cpp:242-296.
+/* ExperienceBuffer::select, src/experience.cpp:151-205.
  * Writes up to min(m, n) picks in curriculum order (stable sort by reward asc,
  * round asc over pick order, :290-294).  Returns the number written. */
 static size_t select_one(const orc_store* s, const double* x, size_t m, double lambda,
@@ -262,7 +262,7 @@ ORC_API size_t orc_select(const double* ctx, const double* reward, const int32_t
 
 /* select() restricted to one shard [0, n) of a buffer of n_global records whose
  * sums / reward total are given: the reference's per-record arithmetic with
- * the buffer's n (experience.cpp:159-166, :229-231); indices are shard-local. */
+ * the buffer's n (experience.cpp:68-75, :229-231); indices are shard-local. */
 ORC_API size_t orc_select_shard(const double* ctx, const double* reward, const int32_t* round,
                                 size_t n, int d, const double* sum, const double* sum_sq,
                                 size_t n_global, double total, const double* x, size_t m,
@@ -273,7 +273,7 @@ ORC_API size_t orc_select_shard(const double* ctx, const double* reward, const i
 }
 
 /* refresh_sigma_cache's median over given subsample rows (m x d), standardized
- * with an n-record buffer's sums (experience.cpp:183-203). */
+ * with an n-record buffer's sums (experience.cpp:92-112). */
 ORC_API double orc_sigma_rows(const double* rows, size_t m, int d, size_t n, const double* sum,
                               const double* sum_sq) {
     double* z = (double*)malloc((m ? m : 1) * (size_t)d * sizeof(double));
@@ -301,7 +301,7 @@ ORC_API double orc_sigma_rows(const double* rows, size_t m, int d, size_t n, con
     return sigma;
 }
 
-/* ExperienceBuffer::surprisal, src/experience.cpp:234-240. */
+/* ExperienceBuffer::surprisal, src/experience.cpp:143-149. */
 ORC_API double orc_surprisal(const double* ctx, const double* reward, size_t n, int d,
                              const double* sum, const double* sum_sq, size_t index,
                              const double* x, double sigma, int local_mean) {
@@ -495,7 +495,7 @@ ORC_API double orc_pareto_reward(const double* fl, const double* fc, size_t F, d
 }
 
 /* Batch: score each of T normalized points against the fixed frontier
- * (the scoring half of compute_reward, src/reward.cpp:251). */
+ * (the scoring half of compute_reward, src/reward.cpp:42-43). */
 ORC_API void orc_pareto_reward_batch(const double* fl, const double* fc, size_t F,
                                      const double* pts, size_t T, double* out) {
     for (size_t t = 0; t < T; ++t)

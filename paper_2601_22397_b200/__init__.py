@@ -228,7 +228,7 @@ class ExperienceBuffer:
         return ctx, rw, rd
 
     def store(self, e: Experience) -> bool:
-        """experience.cpp:135-153: False (and counted) when reward <= r_min."""
+        """experience.cpp:44-62: False (and counted) when reward <= r_min."""
         x = _f64(e.context)
         acc = np.zeros(1, np.uint8)
         n_acc = C.c_size_t()
@@ -354,7 +354,7 @@ class ExperienceBuffer:
         return out + (nn_i, nn_s) if nearest else out
 
     def select(self, x_curr, cfg: Optional[SelectionConfig] = None) -> List[SelectedExperience]:
-        """experience.cpp:242-296: greedy diversity-regularised pick of up to m
+        """experience.cpp:151-205: greedy diversity-regularised pick of up to m
         experiences in curriculum (reward-ascending) order."""
         idx, sim, sc, cnt = self.select_batch(_f64(x_curr)[None, :], cfg)
         out = []

@@ -177,11 +177,11 @@ std::vector<std::vector<SelectedExperience>> ExperienceBuffer::select_batch(
 
 std::vector<SelectedExperience> ExperienceBuffer::select(const std::vector<double>& x_curr,
                                                          const SelectionConfig& cfg) const {
-    if (items_.empty() || cfg.m == 0) return {};  // experience.cpp:245
+    if (items_.empty() || cfg.m == 0) return {};  // experience.cpp:154
     return std::move(select_batch({x_curr}, cfg)[0]);
 }
 
-// ---- persistence: the reference's JSONL format (experience.cpp:298-362) --
+// ---- persistence: the reference's JSONL format (experience.cpp:207-271) --
 
 void ExperienceBuffer::persist(const std::string& path) const {
     std::ofstream out(path, std::ios::trunc);

@@ -175,7 +175,7 @@ sair_status sair_store_export(sair_store_t h, size_t offset, size_t count, doubl
 sair_status sair_store_standardize(sair_store_t h, const double* x, int dim, double* z) {
     if (!h) return bad("null handle");
     return guard([&] {
-        if (h->n == 0) {  // experience.cpp:156
+        if (h->n == 0) {  // experience.cpp:65
             std::memcpy(z, x, (size_t)dim * sizeof(double));
             return;
         }
@@ -193,7 +193,7 @@ sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double*
 sair_status sair_similarity(const double* a, size_t len_a, const double* b, size_t len_b,
                             double sigma, double* out) {
     if (!out) return bad("null output");
-    // experience.cpp:122-124: the dimension check, then the sigma check
+    // experience.cpp:31-33: the dimension check, then the sigma check
     if (len_a != len_b) return bad("similarity: dimension mismatch");
     if (sigma <= 0.0) return bad("similarity: sigma must be positive");
     return guard([&] { *out = sair::similarity(a, b, (int)len_a, sigma, 0); });
@@ -203,7 +203,7 @@ sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, 
                                  const sair_select_config* cfg, double* out) {
     if (!h || !out) return bad("null handle");
     return guard([&] {
-        // items_.at(index) first (experience.cpp:236), then standardize(x)
+        // items_.at(index) first (experience.cpp:145), then standardize(x)
         if (index >= h->n) throw sair::Error(SAIR_ERANGE, "vector::_M_range_check");
         if (dim != h->d)
             throw sair::Error(SAIR_EINVAL, "experience store: feature dimension mismatch");

@@ -40,7 +40,7 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
-// similarity(), experience.cpp:121-131 on standardized vectors:
+// similarity(), experience.cpp:30-40 on standardized vectors:
 // d2 = sum_k (a_k - b_k)^2 in k order, exp(-d2 / (2 sigma sigma)).
 __device__ __forceinline__ double sim_from_d2(double d2, double two_s2) {
     return exp(ddiv(-d2, two_s2));

@@ -89,7 +89,7 @@ struct sair_store_s {
 
     double r_min = 0.0;
     uint64_t rejected = 0;
-    int d = 0;   // 0 until the first accepted row fixes it (experience.cpp:140-145)
+    int d = 0;   // 0 until the first accepted row fixes it (experience.cpp:49-54)
     int dp = 0;  // padded dimension of the fp32 page layout
     size_t n = 0, cap = 0;
     int64_t gbase = 0;  // global index of local record 0 (shard offset)
@@ -169,7 +169,7 @@ struct sair_frontier_set_s {
 
 namespace sair {
 
-// statistics the reference's formulas see: the whole buffer's (experience.cpp:159-166, :229-231)
+// statistics the reference's formulas see: the whole buffer's (experience.cpp:68-75, :229-231)
 inline const StoreStats& eff_stats(const sair_store_s* s) { return s->sharded ? s->gst : s->stats; }
 inline uint64_t eff_n(const sair_store_s* s) { return s->sharded ? s->n_global : s->n; }
 

@@ -1439,7 +1439,7 @@ struct DecisionTail {
 // Everything after the select, one CTA: compute_reward against the frontier
 // before the update (reward.cpp:21-44), insert_normalized (pareto.cpp:43-54)
 // and its commit, hypervolume() (pareto.cpp:56-65), and the store() row
-// behind the r_min gate on the reward total (experience.cpp:136-139).
+// behind the r_min gate on the reward total (experience.cpp:45-48).
 __global__ void __launch_bounds__(1024) decision_tail_kernel(const DecisionTail a) {
     __shared__ double srw[7];
     __shared__ unsigned long long sres[2];

@@ -1,6 +1,6 @@
 // select.cu -- surprisal-guided retrieval on the device (the fast path).
 //
-// Restates ExperienceBuffer::select (experience.cpp:242-296) and the
+// Restates ExperienceBuffer::select (experience.cpp:151-205) and the
 // MockBackend veto scan (policy.cpp:140-157) as three kernels per group of up
 // to 8 queries:
 //
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs* __restric
     const double Eq = a.gamma * sq * sq + 0x1p-11 * pmx * (1.0 + 1e-6) +
                       a.bq_rel * sqrt(pmx * a.cc[q]) + 1e-30;
 
-    // exact score of every candidate: experience.cpp:254-258 with the
+    // exact score of every candidate: experience.cpp:163-167 with the
     // reference's rounding sequence (standardize :162-166, similarity
     // :125-130, loo_mean :229-231).  Select and veto candidates form one work
     // list; a warp takes 8 at a time: its lanes compute the squared
@@ -941,7 +941,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     s->last.queries = nq;
     if (nq == 0) return;
     const size_t m = cfg.m;
-    if (s->n == 0 || m == 0) {  // experience.cpp:245
+    if (s->n == 0 || m == 0) {  // experience.cpp:154
         for (size_t i = 0; i < nq; ++i) out_count[i] = 0;
         if (out_nn)
             for (size_t i = 0; i < nq; ++i) {
@@ -1395,7 +1395,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
 
 // Per query: the union of the shards' top-m (exact fp64 scores over the
 // buffer's global statistics) holds the buffer's top-m when lambda_div == 0;
-// pick it by (score desc, round asc, global index asc) -- experience.cpp:268-278
+// pick it by (score desc, round asc, global index asc) -- experience.cpp:177-187
 // -- then order it by (reward asc, round asc, pick order) -- :290-294.
 __global__ void merge_topk_kernel(const double* __restrict__ score, const double* __restrict__ sim,
                                   const double* __restrict__ rew, const int32_t* __restrict__ rnd,

@@ -8,7 +8,7 @@
 
 namespace sair {
 
-// Greedy pick key, experience.cpp:268-278: gain desc, then round asc, then the
+// Greedy pick key, experience.cpp:177-187: gain desc, then round asc, then the
 // first index scanned (index asc).  j < 0 marks "none".
 struct Best {
     double g;
@@ -40,7 +40,7 @@ __device__ __forceinline__ Best warp_best(Best b) {
 }
 
 // Host-side per-call constants: the reference's standardize statistics and the
-// standardized queries (experience.cpp:159-166), sigma and 2 sigma^2 (:130).
+// standardized queries (experience.cpp:68-75), sigma and 2 sigma^2 (:130).
 struct QueryPrep {
     std::vector<double> mean, sd, z;  // z: [nq][d]
     double sigma = 1.0, two_s2 = 2.0;

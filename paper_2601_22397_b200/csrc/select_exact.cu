@@ -1,7 +1,7 @@
 // select_exact.cu -- the full fp64 pass over the store (x64 rows).
 //
 // The fallback for a query the fast filter cannot certify, the
-// SAIR_SELECT_EXACT mode, locally_weighted_mean (experience.cpp:216-228) and
+// SAIR_SELECT_EXACT mode, locally_weighted_mean (experience.cpp:125-137) and
 // surprisal() (:234-240).  Every record's score follows the reference's exact
 // rounding sequence (standardize :162-166, similarity :125-130, loo_mean
 // :229-231, gain :270); the greedy loop is one arg-max pass per pick and one
@@ -24,7 +24,7 @@ struct ExactArgs {
     const double* zq;  // [d]
     int d;
     size_t n;     // records in this store
-    size_t n_loo; // records of the whole buffer (loo_mean's n, experience.cpp:231)
+    size_t n_loo; // records of the whole buffer (loo_mean's n, experience.cpp:140)
     double total, two_s2, lambda;
     const double* loo;  // locally weighted LOO means (nullable)
     double* score;      // [n]
@@ -56,7 +56,7 @@ __global__ void exact_score_kernel(const ExactArgs a) {
     }
 }
 
-// locally weighted leave-one-out mean, experience.cpp:216-228 (sequential in j
+// locally weighted leave-one-out mean, experience.cpp:125-137 (sequential in j
 // per record, so the sums round exactly as the reference's loop)
 __global__ void local_loo_kernel(const ExactArgs a, double* __restrict__ loo) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < a.n;
@@ -336,7 +336,7 @@ double store_surprisal(sair_store_s* s, size_t index, const double* x,
 
 namespace sair {
 
-// similarity(), experience.cpp:121-131, on two host vectors
+// similarity(), experience.cpp:30-40, on two host vectors
 __global__ void similarity_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                   int d, double two_s2, double* out) {
     if (threadIdx.x || blockIdx.x) return;

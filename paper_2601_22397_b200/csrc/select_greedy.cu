@@ -2,7 +2,7 @@
 // lock-step (the path for lambda_div > 0 above the small-store size, and the
 // exact fallback of any uncertified batch).
 //
-// experience.cpp:242-296 with the reference's rounding order throughout (fp64,
+// experience.cpp:151-205 with the reference's rounding order throughout (fp64,
 // no contraction): every record's score for every query of a batch of G
 // queries, then `want` greedy steps.  State per (query, record): score, penalty
 // (fp64) and a taken flag, so a step is one pass:

@@ -1,12 +1,12 @@
 // select_small.cu -- the whole exact select() of a small store in one launch.
 //
-// ExperienceBuffer::select (experience.cpp:242-296) for stores of up to 64k
+// ExperienceBuffer::select (experience.cpp:151-205) for stores of up to 64k
 // records, any lambda_div: one thread-block cluster of up to 8 CTAs per
 // query (distributed shared memory), each CTA holding its slice of the
 // records' exact scores, penalties and taken flags in shared memory.
 //
 //   zrows_kernel          standardize() of every stored row once per call
-//                         (experience.cpp:162-166, the reference's rounding:
+//                         (experience.cpp:71-75, the reference's rounding:
 //                         (x - mean) / sd), shared by all the call's queries;
 //   small_select_kernel   per query: exact scores (:254-258), the veto scan's
 //                         nearest record (policy.cpp:140-157), then `want`
@@ -73,7 +73,7 @@ __global__ void zrows_kernel(const double* __restrict__ x64, const double* __res
     }
 }
 
-// locally_weighted_mean LOO, experience.cpp:216-228 (loo_mean with
+// locally_weighted_mean LOO, experience.cpp:125-137 (loo_mean with
 // cfg.locally_weighted_mean): for record i, sum_{j != i} w_ij r_j / sum w_ij
 // with w_ij = similarity(z_j, z_i) (the reference calls similarity(
 // standardize(items_[j].context), zi) -- z_j first), sequential in j; the
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) small_select_kernel(const __gri
 
     for (int k = tid; k < d; k += blockDim.x) zq[k] = a.zq[(size_t)q * d + k];
     __syncthreads();
-    // exact scores, experience.cpp:254-258 (standardize, similarity, loo_mean)
+    // exact scores, experience.cpp:163-167 (standardize, similarity, loo_mean)
     for (size_t j = tid; j < ns; j += blockDim.x) {
         const double* zi = a.z + lo + j;
         double d2 = 0.0;

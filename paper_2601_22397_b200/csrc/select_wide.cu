@@ -730,7 +730,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
 }
 
 // per page: the largest record-constant residual |r c1 - c0| (the reward
-// factor of the key, |r - loo mean| scaled, experience.cpp:139-140,148)
+// factor of the key, |r - loo mean| scaled, experience.cpp:138-140,148)
 __global__ void page_resid_kernel(const float* __restrict__ r32, uint32_t n, uint32_t npages,
                                   float c1, float c0, float* __restrict__ out,
                                   uint32_t* __restrict__ ids) {

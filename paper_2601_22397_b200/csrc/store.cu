@@ -2,7 +2,7 @@
 //
 // Host side keeps exactly the reference's bookkeeping in fp64 (gate, running
 // sums in append order, reward total, sigma cache state machine;
-// experience.cpp:135-153, :171-212).  Device side holds the SoA arrays
+// experience.cpp:44-62, :171-212).  Device side holds the SoA arrays
 // (DESIGN.md "Data layout in HBM"); rows arrive through pinned staging and a
 // scatter kernel that also writes the fp32 page layout.
 #include <cub/device/device_radix_sort.cuh>
@@ -111,7 +111,7 @@ __global__ void synth_rows_kernel(uint64_t seed, int clustered, int64_t gbase, s
     for (int t = threadIdx.x; t < d + 1; t += blockDim.x) atomicMax(&amax[t], shmax[t]);
 }
 
-// sigma refresh (experience.cpp:171-205): z-rows of the subsample, then every
+// sigma refresh (experience.cpp:80-114): z-rows of the subsample, then every
 // pairwise distance sqrt(sum (z_i - z_j)^2) in the reference's rounding order.
 __global__ void sigma_z_kernel(const double* __restrict__ x64, const int64_t* __restrict__ idx,
                                int m, int d, const double* __restrict__ mean,
@@ -254,13 +254,13 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
         int32_t* hround = reinterpret_cast<int32_t*>(hr + take);
         size_t k = 0;
         for (size_t i = done; i < done + take; ++i) {
-            // gate, experience.cpp:136-139
+            // gate, experience.cpp:45-48
             if (!(reward[i] > s->r_min)) {
                 ++s->rejected;
                 if (accepted) accepted[i] = 0;
                 continue;
             }
-            // dimension fixed on first accepted row, experience.cpp:140-145
+            // dimension fixed on first accepted row, experience.cpp:49-54
             if (s->n + k == 0) {
                 fix_dim(s, dim, ctx + i * (size_t)dim);
             } else if (dim != s->d) {
@@ -269,19 +269,19 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
             }
             const double* x = ctx + i * (size_t)dim;
             auto& st = s->stats;
-            for (int j = 0; j < dim; ++j) {  // experience.cpp:146-149
+            for (int j = 0; j < dim; ++j) {  // experience.cpp:55-58
                 st.sum[j] += x[j];
                 st.sum_sq[j] += x[j] * x[j];
                 st.xabs[j] = std::max(st.xabs[j], std::fabs(x[j]));
             }
-            st.total += reward[i];  // loo_mean's total, same order (experience.cpp:229-230)
+            st.total += reward[i];  // loo_mean's total, same order (experience.cpp:138-139)
             st.rabs = std::max(st.rabs, std::fabs(reward[i]));
             std::memcpy(hx + k * (size_t)dim, x, (size_t)dim * sizeof(double));
             hr[k] = reward[i];
             hround[k] = round[i];
             if (accepted) accepted[i] = 1;
             ++k;
-            ++s->stale;  // experience.cpp:151
+            ++s->stale;  // experience.cpp:60
         }
         if (k) {
             store_reserve(s, s->n + k);
@@ -316,7 +316,7 @@ bool store_append_one_commit(sair_store_s* s, const double* x, double reward) {
         return false;
     }
     auto& st = s->stats;
-    for (int j = 0; j < s->d; ++j) {  // experience.cpp:146-149
+    for (int j = 0; j < s->d; ++j) {  // experience.cpp:55-58
         st.sum[j] += x[j];
         st.sum_sq[j] += x[j] * x[j];
         st.xabs[j] = std::max(st.xabs[j], std::fabs(x[j]));
@@ -324,7 +324,7 @@ bool store_append_one_commit(sair_store_s* s, const double* x, double reward) {
     st.total += reward;
     st.rabs = std::max(st.rabs, std::fabs(reward));
     s->n += 1;
-    ++s->stale;  // experience.cpp:151
+    ++s->stale;  // experience.cpp:60
     return true;
 }
 
@@ -371,7 +371,7 @@ void store_append_synthetic(sair_store_s* s, uint64_t seed, size_t count, int di
 }
 
 void store_mean_sd(const sair_store_s* s, double* mean, double* sd) {
-    // standardize's per-dimension statistics, experience.cpp:159-165
+    // standardize's per-dimension statistics, experience.cpp:68-74
     const StoreStats& st = eff_stats(s);
     double nn = static_cast<double>(eff_n(s));
     for (int k = 0; k < s->d; ++k) {
@@ -385,14 +385,14 @@ void store_mean_sd(const sair_store_s* s, double* mean, double* sd) {
 }
 
 void store_standardize(const sair_store_s* s, const double* x, double* z) {
-    // experience.cpp:155-169 (callers check emptiness / dimension)
+    // experience.cpp:64-78 (callers check emptiness / dimension)
     std::vector<double> mean(s->d), sd(s->d);
     store_mean_sd(s, mean.data(), sd.data());
     for (int k = 0; k < s->d; ++k) z[k] = (x[k] - mean[k]) / sd[k];
 }
 
 // median pairwise z-distance of the rows idx of `x64` (device, record-major),
-// experience.cpp:183-203: z rows, every pair's distance, the order statistic
+// experience.cpp:92-112: z rows, every pair's distance, the order statistic
 // at size/2 (what nth_element places there) via a device radix sort.
 static double sigma_of_rows(cudaStream_t st, DBuf& scratch, const double* x64,
                             const std::vector<int64_t>& idx, int d, const double* mean,
@@ -426,7 +426,7 @@ static double sigma_of_rows(cudaStream_t st, DBuf& scratch, const double* x64,
     return mid > 1e-12 ? mid : 1.0;
 }
 
-// the strided subsample of refresh_sigma_cache, experience.cpp:173-182
+// the strided subsample of refresh_sigma_cache, experience.cpp:82-91
 std::vector<int64_t> sigma_sample(uint64_t n) {
     const size_t capn = 512;
     std::vector<int64_t> idx;
@@ -466,7 +466,7 @@ double sigma_rows(const double* rows, size_t m, int d, const double* mean, const
 }
 
 double store_effective_sigma(sair_store_s* s, double sigma_sim) {
-    // experience.cpp:207-212
+    // experience.cpp:116-121
     if (sigma_sim > 0.0) return sigma_sim;
     if (s->sharded) {  // the buffer's sigma, computed over its global subsample
         if (s->n_global < 2) return 1.0;

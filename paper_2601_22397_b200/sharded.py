@@ -2,14 +2,14 @@
 
 One process per GPU (torch.distributed, NCCL over NVLink; gloo for CPU tests).
 Rank r owns the contiguous global slice [lo_r, hi_r) of the buffer.  Exactness
-with the single-buffer reference (experience.cpp:242-296) rests on three
+with the single-buffer reference (experience.cpp:151-205) rests on three
 exchanges, each deterministic (rank order):
 
 1. statistics -- every rank all-gathers the shards' running sums and combines
-   them in rank order (sum_, sum_sq_, the reward total; experience.cpp:146-149,
+   them in rank order (sum_, sum_sq_, the reward total; experience.cpp:55-58,
    :229-230).  For the synthetic generator every partial sum is exact, so the
    combined sums are bit-identical to the sequential reference's;
-2. sigma -- the buffer's 512-row subsample (experience.cpp:173-182) is gathered
+2. sigma -- the buffer's 512-row subsample (experience.cpp:82-91) is gathered
    from the owning ranks and every rank computes the same median on its device;
 3. candidates -- each shard's certified top-m (exact fp64 scores over the
    global statistics, each pick's reward and round) is all-gathered and merged
@@ -68,7 +68,7 @@ def combine_stats(parts: List[np.ndarray], d: int):
 
 
 def moments(n: int, s: np.ndarray, ss: np.ndarray):
-    """standardize()'s mean / sd, experience.cpp:159-165 (numpy fp64, same
+    """standardize()'s mean / sd, experience.cpp:68-74 (numpy fp64, same
     operation order -- used only to feed the device sigma kernel)."""
     mean = s / float(n)
     var = np.maximum(0.0, ss / float(n) - mean * mean)
@@ -211,7 +211,7 @@ class ShardedExperienceBuffer:
 
 def global_winner(parts: np.ndarray) -> np.ndarray:
     """Per query the rank whose best wins: gain desc, round asc, global index
-    asc (experience.cpp:268-278); parts = [ranks][nq][>= 3] (gain, round, gidx)."""
+    asc (experience.cpp:177-187); parts = [ranks][nq][>= 3] (gain, round, gidx)."""
     gain, rnd, gi = parts[:, :, 0], parts[:, :, 1], parts[:, :, 2]
     # lexsort: last key primary; -inf gains (no candidate) sort last
     keys = np.lexsort((gi, rnd, -gain), axis=0)

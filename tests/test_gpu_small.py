@@ -94,7 +94,7 @@ def test_small_ties_and_tiny_stores(orc):
 
 @pytest.mark.parametrize("lam", [0.0, 0.1])
 def test_small_local_mean_matches_reference(ref, lam):
-    """locally_weighted_mean (experience.cpp:216-228): the LOO means once per
+    """locally_weighted_mean (experience.cpp:125-137): the LOO means once per
     call on the device (query-independent), then the one-launch select."""
     rng = np.random.default_rng(23)
     n, d = 4000, 12

@@ -28,7 +28,7 @@ def _buffer(ref, ctx, rew, rounds, r_min=0.0):
 def test_standardize_and_sigma_bit_identical(orc, ref, n, d):
     rng = np.random.default_rng(n * 7 + d)
     ctx = rng.normal(size=(n, d)) * rng.uniform(0.1, 100, size=d) + rng.uniform(-50, 50, d)
-    ctx[:, 0] = 3.0  # a zero-variance dimension (sd := 1, experience.cpp:165)
+    ctx[:, 0] = 3.0  # a zero-variance dimension (sd := 1, experience.cpp:74)
     rew = rng.uniform(0.01, 1.0, n)
     b = _buffer(ref, ctx, rew, np.arange(n))
     s, ss = orc.stats(ctx)
