@@ -84,12 +84,24 @@ class COracle:
         L.orc_frontier_insert_seq.argtypes = [_dp, _dp, _sz, _dp, _sz, _u8p]
         L.orc_frontier_insert_seq.restype = _sz
         L.orc_dominance_counts.argtypes = [_dp, _sz, C.c_int, _u32p, _u8p]
+        L.orc_dominance_counts_mt.argtypes = [_dp, _sz, C.c_int, C.c_int, _u32p, _u8p]
+        L.orc_dominance_counts2_sorted.argtypes = [_dp, _sz, _u32p, _u8p]
+        L.orc_frontier_sorted.argtypes = [_dp, _sz, _dp, _dp]
+        L.orc_frontier_sorted.restype = _sz
+        L.orc_synth_contexts.argtypes = [C.c_int64, _sz, _sz, C.c_int, C.c_int, _dp]
         L.orc_action_magnitude.argtypes = [_i32p, _sz]
         L.orc_action_magnitude.restype = C.c_double
         L.orc_compute_reward.argtypes = [_dp, C.c_double, _dp, _dp, _sz, C.c_double, C.c_double,
                                          _dp, _dp]
 
     # -- retrieval --
+    def synth_contexts(self, seed, start, count, d, nthreads=None):
+        """synth.contexts (non-clustered) on host threads: [count, d] float64."""
+        out = np.empty((count, d), np.float64)
+        self.lib.orc_synth_contexts(seed, start, count, d, nthreads or os.cpu_count() or 1,
+                                    _p(out, _dp))
+        return out
+
     def stats(self, ctx):
         ctx = np.ascontiguousarray(ctx, np.float64)
         n, d = ctx.shape
@@ -225,6 +237,32 @@ class COracle:
         mem = np.zeros(T, np.uint8)
         self.lib.orc_dominance_counts(_p(t, _dp), T, K, _p(cnt, _u32p), _p(mem, _u8p))
         return cnt, mem.astype(bool)
+
+    def dominance_counts_mt(self, tuples, nthreads=None):
+        """dominance_counts on all host threads (same per-tuple loop)."""
+        t = np.ascontiguousarray(tuples, np.float64)
+        T, K = t.shape
+        cnt = np.zeros(T, np.uint32)
+        mem = np.zeros(T, np.uint8)
+        self.lib.orc_dominance_counts_mt(_p(t, _dp), T, K, nthreads or os.cpu_count() or 1,
+                                         _p(cnt, _u32p), _p(mem, _u8p))
+        return cnt, mem.astype(bool)
+
+    def dominance_counts2_sorted(self, tuples):
+        """Two-objective counts in O(T log T) (sweep + Fenwick tree)."""
+        t = np.ascontiguousarray(tuples, np.float64).reshape(-1, 2)
+        cnt = np.zeros(len(t), np.uint32)
+        mem = np.zeros(len(t), np.uint8)
+        self.lib.orc_dominance_counts2_sorted(_p(t, _dp), len(t), _p(cnt, _u32p), _p(mem, _u8p))
+        return cnt, mem.astype(bool)
+
+    def frontier_sorted(self, pts):
+        """The frontier the sequential insert loop leaves, for millions of points."""
+        t = np.ascontiguousarray(pts, np.float64).reshape(-1, 2)
+        fl = np.zeros(max(len(t), 1))
+        fc = np.zeros(max(len(t), 1))
+        F = self.lib.orc_frontier_sorted(_p(t, _dp), len(t), _p(fl, _dp), _p(fc, _dp))
+        return fl[:F].copy(), fc[:F].copy()
 
     def action_magnitude(self, deltas):
         d = np.ascontiguousarray(deltas, np.int32).reshape(-1, 4)

@@ -391,6 +391,59 @@ ORC_API void orc_select_batch(const double* ctx, const double* reward, const int
 }
 
 /* ------------------------------------------------------------------------ */
+/* Synthetic stores at full size (test infrastructure)                       */
+/* ------------------------------------------------------------------------ */
+
+/* paper_2601_22397_b200/synth.py contexts()/rewards() restated in C on host
+ * threads, so a 16M x 64 host copy of a device-generated store takes seconds
+ * (pinned == synth.py in tests/test_oracle.py). */
+static uint64_t sm64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static uint64_t synth_key(int64_t seed, uint64_t stream) {
+    return (uint64_t)seed * 0x100000001B3ull + stream * 0x9E3779B1ull;
+}
+
+typedef struct {
+    int64_t seed;
+    size_t start, r0, r1;
+    int d;
+    double* out;
+} synth_job;
+
+static void* synth_worker(void* p) {
+    synth_job* j = (synth_job*)p;
+    uint64_t key = synth_key(j->seed, 1);
+    for (size_t r = j->r0; r < j->r1; ++r)
+        for (int k = 0; k < j->d; ++k) {
+            uint64_t h = sm64(((uint64_t)(j->start + r) * (uint64_t)j->d + (uint64_t)k) ^ key);
+            int64_t s = (int64_t)(h & 0xFFF) + (int64_t)((h >> 12) & 0xFFF) +
+                        (int64_t)((h >> 24) & 0xFFF) + (int64_t)((h >> 36) & 0xFFF);
+            j->out[r * (size_t)j->d + (size_t)k] = (double)(s - 8190) * (1.0 / 2048.0);
+        }
+    return NULL;
+}
+
+ORC_API void orc_synth_contexts(int64_t seed, size_t start, size_t count, int d, int nthreads,
+                                double* out) {
+    if (nthreads < 1) nthreads = 1;
+    pthread_t* th = (pthread_t*)malloc((size_t)nthreads * sizeof(pthread_t));
+    synth_job* jobs = (synth_job*)malloc((size_t)nthreads * sizeof(synth_job));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = (synth_job){seed, start, count * (size_t)t / (size_t)nthreads,
+                              count * (size_t)(t + 1) / (size_t)nthreads, d, out};
+        pthread_create(&th[t], NULL, synth_worker, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(jobs);
+    free(th);
+}
+
+/* ------------------------------------------------------------------------ */
 /* Pareto frontier (2 objectives) -- src/pareto.cpp                         */
 /* ------------------------------------------------------------------------ */
 
@@ -550,6 +603,145 @@ ORC_API void orc_dominance_counts(const double* tuples, size_t T, int K, uint32_
         if (counts) counts[i] = c;
         if (member) member[i] = (uint8_t)(c == 0 && !dup_before);
     }
+}
+
+/* The same counts on `nthreads` host threads: tuple i's count is the loop of
+ * orc_dominance_counts above, rows of i partitioned across threads (the
+ * per-i arithmetic is unchanged, so the result is identical). */
+typedef struct {
+    const double* t;
+    size_t T, i0, i1;
+    int K;
+    uint32_t* counts;
+    uint8_t* member;
+} domk_job;
+
+static void* domk_worker(void* p) {
+    domk_job* j = (domk_job*)p;
+    for (size_t i = j->i0; i < j->i1; ++i) {
+        const double* pi = j->t + i * (size_t)j->K;
+        uint32_t c = 0;
+        int dup_before = 0;
+        for (size_t q = 0; q < j->T; ++q) {
+            if (q == i) continue;
+            const double* pq = j->t + q * (size_t)j->K;
+            if (domk(pq, pi, j->K)) {
+                ++c;
+            } else if (q < i && !dup_before) {
+                int eq = 1;
+                for (int k = 0; k < j->K; ++k) eq &= pq[k] == pi[k];
+                dup_before = eq;
+            }
+        }
+        if (j->counts) j->counts[i] = c;
+        if (j->member) j->member[i] = (uint8_t)(c == 0 && !dup_before);
+    }
+    return NULL;
+}
+
+ORC_API void orc_dominance_counts_mt(const double* tuples, size_t T, int K, int nthreads,
+                                     uint32_t* counts, uint8_t* member) {
+    if (nthreads < 1) nthreads = 1;
+    pthread_t* th = (pthread_t*)malloc((size_t)nthreads * sizeof(pthread_t));
+    domk_job* jobs = (domk_job*)malloc((size_t)nthreads * sizeof(domk_job));
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = (domk_job){tuples, T, T * (size_t)t / (size_t)nthreads,
+                             T * (size_t)(t + 1) / (size_t)nthreads, K, counts, member};
+        pthread_create(&th[t], NULL, domk_worker, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    free(jobs);
+    free(th);
+}
+
+/* Two objectives at millions of tuples, O(T log T) (an independent algorithm
+ * from the device's merge counting; pinned == orc_dominance_counts and the
+ * sequential insert loop at small T in tests/test_oracle.py):
+ *   count_i = #{j : l_j <= l_i and c_j <= c_i} - #{j : (l_j, c_j) == (l_i, c_i)}
+ * (dominates(), src/pareto.cpp:9-12: <= on both axes minus exact equals),
+ * by a sweep in (l asc, c asc) order with a Fenwick tree over the c-ranks;
+ * a whole run of equal l is inserted before any of its members is counted. */
+static const double* g_sort_t; /* qsort has no context argument */
+static int cmp_lc(const void* a, const void* b) {
+    size_t i = *(const size_t*)a, j = *(const size_t*)b;
+    const double *p = g_sort_t + 2 * i, *q = g_sort_t + 2 * j;
+    if (p[0] != q[0]) return p[0] < q[0] ? -1 : 1;
+    if (p[1] != q[1]) return p[1] < q[1] ? -1 : 1;
+    return (i > j) - (i < j);
+}
+
+static int cmp_dbl(const void* a, const void* b) {
+    double x = *(const double*)a, y = *(const double*)b;
+    return (x > y) - (x < y);
+}
+
+ORC_API void orc_dominance_counts2_sorted(const double* t, size_t T, uint32_t* counts,
+                                          uint8_t* member) {
+    size_t* ord = (size_t*)malloc((T ? T : 1) * sizeof(size_t));
+    double* cs = (double*)malloc((T ? T : 1) * sizeof(double));
+    uint32_t* fen = (uint32_t*)calloc(T + 1, sizeof(uint32_t));
+    for (size_t i = 0; i < T; ++i) { ord[i] = i; cs[i] = t[2 * i + 1]; }
+    g_sort_t = t;
+    qsort(ord, T, sizeof(size_t), cmp_lc);
+    qsort(cs, T, sizeof(double), cmp_dbl);
+    size_t a = 0;
+    while (a < T) {
+        size_t b = a;
+        while (b < T && t[2 * ord[b]] == t[2 * ord[a]]) ++b;  /* run of equal l */
+        for (size_t r = a; r < b; ++r) {                        /* insert the run */
+            double c = t[2 * ord[r] + 1];
+            size_t lo = 0, hi = T;                               /* rank = #{c' < c} + 1 */
+            while (lo < hi) { size_t md = (lo + hi) / 2; if (cs[md] < c) lo = md + 1; else hi = md; }
+            for (size_t k = lo + 1; k <= T; k += k & (~k + 1)) fen[k]++;
+        }
+        size_t r = a;
+        while (r < b) {                                          /* runs of equal (l, c) */
+            size_t e = r;
+            while (e < b && t[2 * ord[e] + 1] == t[2 * ord[r] + 1]) ++e;
+            double c = t[2 * ord[r] + 1];
+            size_t lo = 0, hi = T;                               /* #{c' <= c} */
+            while (lo < hi) { size_t md = (lo + hi) / 2; if (cs[md] <= c) lo = md + 1; else hi = md; }
+            uint32_t le = 0;
+            for (size_t k = lo; k > 0; k -= k & (~k + 1)) le += fen[k];
+            uint32_t cnt = le - (uint32_t)(e - r);
+            for (size_t q = r; q < e; ++q) {
+                size_t i = ord[q];
+                if (counts) counts[i] = cnt;
+                /* the first occurrence (lowest index) of a value: ord is
+                 * index-ascending inside an equal run */
+                if (member) member[i] = (uint8_t)(cnt == 0 && q == r);
+            }
+            r = e;
+        }
+        a = b;
+    }
+    free(fen);
+    free(cs);
+    free(ord);
+}
+
+/* The frontier the sequential insert loop leaves (src/pareto.cpp:43-54 over
+ * every point), for millions of points: insert_normalized keeps exactly the
+ * non-dominated distinct values, sorted by latency (the loop's result does not
+ * depend on the order, tests/test_pareto.cpp:127-147); here the points with a
+ * zero count.  fl/fc have capacity T; returns F. */
+ORC_API size_t orc_frontier_sorted(const double* t, size_t T, double* fl, double* fc) {
+    uint8_t* member = (uint8_t*)malloc(T ? T : 1);
+    orc_dominance_counts2_sorted(t, T, NULL, member);
+    size_t F = 0;
+    for (size_t i = 0; i < T; ++i)
+        if (member[i]) { fl[F] = t[2 * i]; fc[F] = t[2 * i + 1]; ++F; }
+    free(member);
+    /* sort by latency (distinct frontier points have distinct latencies) */
+    size_t* ord = (size_t*)malloc((F ? F : 1) * sizeof(size_t));
+    double* tmp = (double*)malloc((F ? F : 1) * 2 * sizeof(double));
+    for (size_t i = 0; i < F; ++i) { ord[i] = i; tmp[2 * i] = fl[i]; tmp[2 * i + 1] = fc[i]; }
+    g_sort_t = tmp;
+    qsort(ord, F, sizeof(size_t), cmp_lc);
+    for (size_t i = 0; i < F; ++i) { fl[i] = tmp[2 * ord[i]]; fc[i] = tmp[2 * ord[i] + 1]; }
+    free(tmp);
+    free(ord);
+    return F;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -238,6 +238,35 @@ def test_dominance_counts_brute(orc):
             assert fr == list(zip(fl, fc))
 
 
+
+def test_scalable_pareto_checkers_equal_brute_force(orc):
+    """The checkers the full-size (4M-tuple) GPU parity tests use -- the
+    threaded k-D counts, the O(T log T) two-objective counts and the sorted
+    frontier -- equal the brute-force loop and the sequential insert loop
+    (src/pareto.cpp:43-54) on tie-heavy grids and continuous data."""
+    gen = np.random.default_rng(17)
+    for K in (2, 3, 4):
+        for grid in (4, 16, 0):
+            t = gen.uniform(size=(2000, K))
+            if grid:
+                t = np.floor(t * grid) / grid
+            cnt, mem = orc.dominance_counts(t)
+            c2, m2 = orc.dominance_counts_mt(t, nthreads=5)
+            assert np.array_equal(cnt, c2) and np.array_equal(mem, m2)
+            if K == 2:
+                c3, m3 = orc.dominance_counts2_sorted(t)
+                assert np.array_equal(cnt, c3) and np.array_equal(mem, m3)
+                fl, fc, _ = orc.frontier_from_points(t)
+                sl, sc = orc.frontier_sorted(t)
+                assert np.array_equal(fl, sl) and np.array_equal(fc, sc)
+    # anti-correlated: a frontier of most of the points
+    x = gen.uniform(size=3000)
+    t = np.stack([x, 1.0 - x + gen.uniform(-0.01, 0.01, 3000)], 1)
+    fl, fc, _ = orc.frontier_from_points(t)
+    sl, sc = orc.frontier_sorted(t)
+    assert len(fl) > 100 and np.array_equal(fl, sl) and np.array_equal(fc, sc)
+    assert np.array_equal(orc.dominance_counts2_sorted(t)[0], orc.dominance_counts(t)[0])
+
 # ------------------------------------------------------------------- reward ---
 
 CFG_DEFAULT = (500.0, 0.0, 10.0, 0.7, 0.3, 0.3, 5.0)
@@ -302,3 +331,10 @@ def test_action_magnitude(orc, ref):
     import ctypes as C
     assert orc.action_magnitude(d) == ref.lib.ref_action_magnitude(
         d.ctypes.data_as(C.POINTER(C.c_int32)), 2)
+
+
+def test_threaded_synth_equals_synth_py(orc):
+    from paper_2601_22397_b200 import synth
+    for seed, start, count, d in ((2026, 0, 3000, 64), (7, 123457, 999, 23), (11, 0, 5, 1)):
+        assert np.array_equal(orc.synth_contexts(seed, start, count, d, nthreads=3),
+                              synth.contexts(seed, start, count, d))
