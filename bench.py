@@ -56,12 +56,16 @@ def parse():
     ap.add_argument("--lambda-div", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pareto", action="store_true")
-    # N > 1: "queries" -- every rank holds the whole store (4.4 GB of 180 GB)
-    # and serves a contiguous slice of each step's queries, no collective;
-    # "records" -- the store is sharded by records (sharded.py) and every
-    # query's per-shard top-m are merged through NCCL (stores beyond one GPU)
-    ap.add_argument("--shard", default=os.environ.get("SAIR_BENCH_SHARD", "queries"),
+    # N > 1: "records" (configs[3]: "16M experiences sharded over 8 B200 ...
+    # per-shard top-k merged via NCCL allgather") -- the store is sharded by
+    # records (sharded.py) and every query's per-shard top-m are merged after
+    # an NCCL all-gather; "queries" -- every rank holds the whole store and
+    # serves a slice of each step's queries, no collective (reported as an
+    # extra key, "query_shards", when the headline runs record shards)
+    ap.add_argument("--shard", default=os.environ.get("SAIR_BENCH_SHARD", "records"),
                     choices=["queries", "records"])
+    # launcher self-test (CPU, gloo): start the ranks, rendezvous, print the line
+    ap.add_argument("--launcher-check", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -174,46 +178,48 @@ def run_ours(a, rank, world, local_rank):
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(backend)
-    if world > 1 and a.shard == "queries":
-        # the whole store on every rank (device-generated from the same seed:
-        # identical replicas); this rank's slice of every step's queries
-        lo, hi = 0, n_total
-        qlo, qhi = shard_range(a.queries, rank, world)
-        buf = sair.ExperienceBuffer(0.0, device=dev)
-        buf.store_synthetic(SEED, n_total, DIM)
 
-        def select(q):
-            k = len(q)
-            a_, b_ = shard_range(k, rank, world)
-            return buf.select_batch(q[a_:b_], cfg)
+    def make(mode):
+        """(buffer, select, select_whole, lo, hi) for one way of spreading the
+        step over the ranks."""
+        if world > 1 and mode == "queries":
+            # the whole store on every rank (device-generated from the same
+            # seed: identical replicas); this rank's slice of every step's queries
+            b = sair.ExperienceBuffer(0.0, device=dev)
+            b.store_synthetic(SEED, n_total, DIM)
 
-        def select_whole(q):  # the north star's few-query latency target: one GPU's pass
-            return buf.select_batch(q, cfg)
-    elif world > 1:
-        lo, hi = shard_range(n_total, rank, world)
-        sharded = ShardedExperienceBuffer(dist, dev)
-        sharded.store_synthetic(SEED, n_total, DIM)
-        buf = sharded.local
+            def sel(q):
+                a_, b_ = shard_range(len(q), rank, world)
+                return b.select_batch(q[a_:b_], cfg)
 
-        def select(q):
-            return sharded.select_batch(q, cfg)
-    else:
-        lo, hi = 0, n_total
-        buf = sair.ExperienceBuffer(0.0, device=dev)
-        buf.store_synthetic(SEED, n_total, DIM)
+            return b, sel, (lambda q: b.select_batch(q, cfg)), 0, n_total
+        if world > 1:
+            lo_, hi_ = shard_range(n_total, rank, world)
+            sh = ShardedExperienceBuffer(dist, dev)
+            sh.store_synthetic(SEED, n_total, DIM)
 
-        def select(q):
-            return buf.select_batch(q, cfg)
-    if not (world > 1 and a.shard == "queries"):
-        select_whole = select
+            def sel(q):
+                return sh.select_batch(q, cfg)
+
+            return sh.local, sel, sel, lo_, hi_
+        b = sair.ExperienceBuffer(0.0, device=dev)
+        b.store_synthetic(SEED, n_total, DIM)
+
+        def sel(q):
+            return b.select_batch(q, cfg)
+
+        return b, sel, sel, 0, n_total
+
+    buf, select, select_whole, lo, hi = make(a.shard)
     gen_s = time.time() - t0
     qpool = synth.queries(SEED, (a.warmup + a.steps) * a.queries, DIM).reshape(
         a.warmup + a.steps, a.queries, DIM)
-    stream = torch.cuda.ExternalStream(buf.stream_ptr(), device=dev)
     hbm_peak, bf16_peak, peak_kind = measured_peaks()
 
-    def timed(qs, steps, select=select):
+    def timed(qs, steps, select=select, b=None):
         """device time (CUDA events on the store's stream, max over ranks)"""
+        b = b or buf
+        stream = torch.cuda.ExternalStream(b.stream_ptr(), device=dev)
         stats = []
         if dist:
             dist.barrier()
@@ -222,7 +228,7 @@ def run_ours(a, rank, world, local_rank):
         e0.record(stream)
         for i in range(steps):
             select(qs[i])
-            stats.append(buf.last_stats())
+            stats.append(b.last_stats())
         e1.record(stream)
         torch.cuda.synchronize()
         if dist:
@@ -295,6 +301,19 @@ def run_ours(a, rank, world, local_rank):
             "value": round(a.steps * qn / (ms_q / 1e3), 2), "unit": "queries/s",
             "ms_per_step": round(ms_q / a.steps, 4), "frac": rq["frac"]}
 
+    other = None
+    if world > 1:
+        # the other way to spread the step: query shards over replicated stores
+        # (records mode headline) or record shards (queries mode headline)
+        mode = "queries" if a.shard == "records" else "records"
+        b2, sel2, _, _, _ = make(mode)
+        for i in range(a.warmup):
+            sel2(qpool[i])
+        ms2, _ = timed(qpool[a.warmup:], a.steps, sel2, b2)
+        other = {"split": mode, "value": round(a.steps * a.queries / (ms2 / 1e3), 2),
+                 "unit": "queries/s", "ms_per_step": round(ms2 / a.steps, 4)}
+        del b2, sel2
+
     out = {
         "metric": "retrieval queries/s @16M exps k=32",
         "value": round(value, 2),
@@ -324,12 +343,16 @@ def run_ours(a, rank, world, local_rank):
         "store_build_s": round(gen_s, 3),
         "hbm_target": hbm_target,
     }
+    if other:
+        out["query_shards" if other["split"] == "queries" else "record_shards"] = other
     if rank == 0 and world == 1 and not a.no_pareto:
         out["config1"] = bench_config1(dev)
         out["config2"] = bench_config2(dev, a.steps)
         out["config5_step"] = bench_decision_step(buf, dev)
     if rank == 0 and not a.no_pareto:
         out["pareto"] = bench_pareto(dev)
+        if not a.no_cpu_baseline:
+            out["pareto"]["cpu_baseline"] = cpu_baseline_pareto()
     if rank == 0:
         out["clocks"] = clk.summary()
         if not a.no_cpu_baseline:
@@ -472,24 +495,40 @@ def bench_pareto(dev):
     dout = torch.empty(PARETO_T, dtype=torch.float64, device=f"cuda:{dev}")
     ddom = torch.empty(PARETO_T, dtype=torch.uint8, device=f"cuda:{dev}")
     s = torch.cuda.current_stream(dev)
-    for _ in range(3):
-        f2.score_batch_device(dpts.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def score_ms(fr, dp, reps=10):
+        """reward() of every tuple (score_batch_kernel), cold L2: a 512 MB
+        write (4x the L2) before every launch, CUDA events around the launch
+        alone on its stream; mean over reps."""
+        fr.score_batch_device(dp.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
                               s.cuda_stream)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    e0.record(s)
-    for _ in range(reps):
-        f2.score_batch_device(dpts.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
-                              s.cuda_stream)
-    e1.record(s)
-    torch.cuda.synchronize()
-    sc_ms = e0.elapsed_time(e1) / reps
+        tot = 0.0
+        for _ in range(reps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            fr.score_batch_device(dp.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
+                                  s.cuda_stream)
+            e1.record(s)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot / reps
+
+    sc_ms = score_ms(f2, dpts)
+    hbm_peak, _, peak_kind = measured_peaks()
+    # algorithmic bytes per tuple: 16 B in (l, c), 8 B reward + 1 B dominated out
+    sbytes = PARETO_T * (16 + 8 + 1)
     res.update({"value": round(PARETO_T / (sc_ms / 1e3), 1), "unit": "tuples/s",
                 "score_ms": round(sc_ms, 4), "frontier_size": F,
                 "frontier_insert_tuples_per_s": round(PARETO_T / ins_s, 1),
                 "frontier_insert_s_e2e": round(ins_s, 4),
-                "score_hbm_gbs": round(PARETO_T * (16 + 8 + 1) / (sc_ms / 1e3) / 1e9, 1)})
+                "l2": "flushed before every timed launch (512 MB write)",
+                "roofline": {"bound": "hbm", "achieved": round(sbytes / (sc_ms / 1e3) / 1e9, 1),
+                             "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,
+                             "frac": round(sbytes / (sc_ms / 1e3) / 1e9 / hbm_peak, 4),
+                             "algorithmic_bytes_per_launch": sbytes,
+                             "kernel": "sair::score_batch_kernel"}})
     # prefix-sequential replay (SURVEY 8(f) row 4): 4M rounds, 85 % updating
     rng = np.random.default_rng(SEED)
     T = PARETO_T
@@ -524,16 +563,7 @@ def bench_pareto(dev):
         Fd = fd.insert_batch(pd)
         ins = time.perf_counter() - t0
         dp_ = torch.from_numpy(pd).to(f"cuda:{dev}")
-        fd.score_batch_device(dp_.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
-                              s.cuda_stream)
-        torch.cuda.synchronize()
-        e0.record(s)
-        for _ in range(3):
-            fd.score_batch_device(dp_.data_ptr(), PARETO_T, dout.data_ptr(), ddom.data_ptr(),
-                                  s.cuda_stream)
-        e1.record(s)
-        torch.cuda.synchronize()
-        sms = e0.elapsed_time(e1) / 3
+        sms = score_ms(fd, dp_, reps=3)
         t0 = time.perf_counter()
         _, md = sair.dominance_counts(pd)
         dc = time.perf_counter() - t0
@@ -554,32 +584,62 @@ def bench_pareto(dev):
     return res
 
 
+def _host_store(orc, n, threads):
+    """The host copy of the bench's device-generated store (synth.py; the
+    oracle's threaded restatement of the generator) and its statistics."""
+    from paper_2601_22397_b200 import synth
+    ctx = orc.synth_contexts(SEED, 0, n, DIM, nthreads=threads)
+    return ctx, synth.rewards(SEED, 0, n), synth.rounds(0, n), orc.stats(ctx)
+
+
 def cpu_baseline_port():
-    """The oracle's bit-identical restatement (hoisted Sigma r) on all host
-    threads, on a bounded sample: 1M of the same synthetic records, 2 queries
-    per thread; throughput scaled to the 16M store (the restated select is
-    linear in N)."""
+    """The oracle's bit-identical restatement of select (hoisted Sigma r,
+    SURVEY F3) on all host threads, at the bench's own size (16M x 64, k = 32,
+    lambda 0): a bounded sample of 2 queries per thread, no scaling.  The
+    literal reference select is O(N^2) (loo_mean re-sums every reward per
+    record, experience.cpp:138-140 inside :163-167): ~2.3 days per query at
+    16M, so the restatement is the only CPU path that can run this workload."""
     from oracle.oracle import COracle
     from paper_2601_22397_b200 import synth
     orc = COracle()
-    n_s = 1 << 20
-    ctx = synth.contexts(SEED, 0, n_s, DIM)
-    rew = synth.rewards(SEED, 0, n_s)
-    rnd = synth.rounds(0, n_s)
     threads = os.cpu_count() or 1
+    ctx, rew, rnd, st = _host_store(orc, N_RECORDS, threads)
+    sigma = orc.sigma_median(ctx)
     nq = 2 * threads
     xq = synth.queries(SEED + 1, nq, DIM)
-    s, ss = orc.stats(ctx)
-    sigma = orc.sigma_median(ctx)
     t0 = time.perf_counter()
-    orc.select_batch(ctx, rew, rnd, xq, K_SEL, 0.0, sigma, nthreads=threads, stats=(s, ss))
+    orc.select_batch(ctx, rew, rnd, xq, K_SEL, 0.0, sigma, nthreads=threads, stats=st)
     dt = time.perf_counter() - t0
-    qps_at_sample = nq / dt
-    return {"value": round(qps_at_sample * n_s / N_RECORDS, 4), "unit": "queries/s",
-            "cores": threads, "kind": "port",
-            "sample": f"oracle restatement, {nq} queries x {n_s} records x d={DIM}, k={K_SEL}, "
-                      f"{dt:.2f}s on {threads} threads; scaled x{n_s}/{N_RECORDS} (linear in N)",
+    return {"value": round(nq / dt, 4), "unit": "queries/s", "cores": threads, "kind": "port",
+            "sample": f"oracle restatement (oracle/sair_oracle.c), {nq} queries x {N_RECORDS} "
+                      f"records x d={DIM}, k={K_SEL}, lambda 0: {dt:.2f}s on {threads} threads",
             "cpu_model": _cpu_model()}
+
+
+def cpu_baseline_pareto(T=PARETO_T):
+    """The reference's own Pareto path (oracle/_ref: pareto.cpp compiled
+    unmodified, -O3 -DNDEBUG), single thread like one reference run: the
+    literal update loop over the 4M uniform tuples (pareto.cpp:36-54, the
+    harness's per-round frontier.update), then reward() of every tuple against
+    the resulting frontier (pareto.cpp:86-89, the scoring half of
+    compute_reward) -- "Pareto-scored tuples/s"."""
+    from oracle.oracle import REF_SO, Ref, RefFrontier
+    from paper_2601_22397_b200 import synth
+    if not REF_SO.exists():
+        return None
+    pts = synth.tuples(SEED, T, 2, "uniform")
+    f = RefFrontier(Ref(), 1.0, 1.0)
+    t0 = time.perf_counter()
+    f.insert_batch(pts)
+    ins = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    f.reward_batch(pts)
+    sc = time.perf_counter() - t0
+    return {"value": round(T / sc, 1), "unit": "tuples/s", "cores": 1, "kind": "reference",
+            "sample": f"oracle/_ref ParetoFrontier: {T} uniform 2-objective tuples, literal "
+                      f"update loop {ins:.3f}s ({T / ins:.4g} tuples/s), reward() of every "
+                      f"tuple vs the {len(f.points()[0])}-point frontier {sc:.3f}s",
+            "update_tuples_per_s": round(T / ins, 1), "cpu_model": _cpu_model()}
 
 
 def _cpu_model():
@@ -595,63 +655,116 @@ def _cpu_model():
 # ------------------------------------------------------------- reference ---
 
 def run_reference(a):
-    """The reference's own select (oracle/_ref: proj/src/experience.cpp compiled
-    unmodified, -O3 -DNDEBUG) on the host cores.  The literal select is O(N^2)
-    (experience.cpp:138-140 inside :163-167), so each step is a bounded sample:
-    Q queries over an n_s-record buffer on Q threads; the 16M-equivalent rate
-    is extrapolated from a quadratic fit through two sample sizes."""
-    from oracle.oracle import REF_SO, Ref, RefBuffer
+    """The reference arm: the reference's CPU implementation of the path on
+    the host cores, on this arm's config (16M x 64, Q = 4096 per step, k = 32).
+
+    oracle/_ref is the reference compiled unmodified, but its literal select
+    is O(N^2) -- loo_mean re-sums every reward for every record
+    (experience.cpp:138-140 inside :163-167): ~2.3 days per query at 16M --
+    so the timed path is the oracle's restatement (kind "port"), which is
+    bit-identical to _ref (hoisting that loop-invariant sum is the one
+    change; pinned == _ref in tests/test_oracle.py): the reference's
+    arithmetic at its best possible complexity, on all host threads (queries
+    partitioned like the reference's sweep pool, scalelab_cli.cpp:67-76).
+    Each step is a bounded sample of the step's 4096 queries: one query per
+    thread over the full 16M-record store.  The literal _ref select is timed
+    once at n = 8192 for the record (not extrapolated)."""
+    from oracle.oracle import REF_SO, COracle, Ref, RefBuffer
     from paper_2601_22397_b200 import synth
-    if not REF_SO.exists():
-        return {"impl": "reference", "unavailable": "oracle/_ref/libsair_ref.so not built"}
-    ref = Ref()
-    threads = min(os.cpu_count() or 1, a.queries)
-    q_s = min(a.queries, 2 * threads)  # bounded sample of each step's query batch
-    sizes = (4096, 8192)
-    per_q = {}
-    for n_s in sizes:
-        b = RefBuffer(ref, 0.0)
-        b.store_many(synth.contexts(SEED, 0, n_s, DIM), synth.rewards(SEED, 0, n_s),
-                     synth.rounds(0, n_s))
+    orc = COracle()
+    threads = os.cpu_count() or 1
+    q_s = min(a.queries, threads)
+    ctx, rew, rnd, st = _host_store(orc, a.records, threads)
+    sigma = orc.sigma_median(ctx)
+    xq = synth.queries(SEED, q_s * (a.warmup + a.steps), DIM)
+    for i in range(a.warmup):
+        orc.select_batch(ctx, rew, rnd, xq[i * q_s:(i + 1) * q_s], K_SEL, a.lambda_div, sigma,
+                         nthreads=threads, stats=st)
+    t0 = time.perf_counter()
+    for i in range(a.warmup, a.warmup + a.steps):
+        orc.select_batch(ctx, rew, rnd, xq[i * q_s:(i + 1) * q_s], K_SEL, a.lambda_div, sigma,
+                         nthreads=threads, stats=st)
+    dt = time.perf_counter() - t0
+    value = a.steps * q_s / dt
+    literal = None
+    if REF_SO.exists():
+        n_l = 8192
+        b = RefBuffer(Ref(), 0.0)
+        b.store_many(ctx[:n_l], rew[:n_l], rnd[:n_l])
         b.effective_sigma(0.0)
-        xq = synth.queries(SEED, q_s * (a.warmup + a.steps), DIM)
-        for i in range(a.warmup):
-            b.select_batch(xq[i * q_s:(i + 1) * q_s], K_SEL, a.lambda_div, 0.0, nthreads=threads)
-        t0 = time.perf_counter()
-        for i in range(a.warmup, a.warmup + a.steps):
-            b.select_batch(xq[i * q_s:(i + 1) * q_s], K_SEL, a.lambda_div, 0.0, nthreads=threads)
-        per_q[n_s] = (time.perf_counter() - t0) / (a.steps * q_s) * threads
-    # t(n) = c1 n + c2 n^2 per query per thread
-    n1, n2 = sizes
-    t1, t2 = per_q[n1], per_q[n2]
-    c2 = (t2 / n2 - t1 / n1) / (n2 - n1)
-    c1 = t1 / n1 - c2 * n1
-    c2 = max(c2, 0.0)
-    t_full = max(c1, 0.0) * N_RECORDS + c2 * N_RECORDS ** 2
-    value = threads / t_full
-    sample = (f"literal reference select, {a.steps} steps x {q_s} of the {a.queries} queries on {threads} "
-              f"threads at n={n1} ({t1 * 1e3:.1f} ms/query) and n={n2} ({t2 * 1e3:.1f} ms/query), "
-              f"extrapolated to N={N_RECORDS} by t(n) = c1 n + c2 n^2")
+        t1 = time.perf_counter()
+        b.select_batch(xq[:threads], K_SEL, a.lambda_div, 0.0, nthreads=threads)
+        literal = {"records": n_l, "queries": threads, "threads": threads,
+                   "ms_per_query_per_thread": round((time.perf_counter() - t1) * 1e3, 2)}
+    sample = (f"oracle restatement of select (hoisted Sigma r, == oracle/_ref), {a.steps} steps x "
+              f"{q_s} of the {a.queries} queries (one per thread) over {a.records} records x "
+              f"d={DIM}, k={K_SEL}, lambda {a.lambda_div}: {dt:.2f}s on {threads} threads")
     return {
-        "metric": "retrieval queries/s @16M exps k=32", "value": value, "unit": "queries/s",
-        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": t_full / threads * a.queries * 1e3,
+        "metric": "retrieval queries/s @16M exps k=32", "value": round(value, 4),
+        "unit": "queries/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": round(a.queries / value * 1e3, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (synth.py)", "impl": "reference",
-        "config": {"workload": f"configs[3]: {N_RECORDS} records x d={DIM}, Q={a.queries} "
+        "data": "synthetic (synth.py, same store and queries as the ours arm)",
+        "impl": "reference",
+        "config": {"workload": f"configs[3]: {a.records} records x d={DIM}, Q={a.queries} "
                                f"queries/step, k={K_SEL}, lambda_div={a.lambda_div}"},
-        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": threads,
-                         "kind": "reference", "sample": sample, "cpu_model": _cpu_model()},
-        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0,
+        "cpu_baseline": {"value": round(value, 4), "unit": "queries/s", "cores": threads,
+                         "kind": "port", "sample": sample, "cpu_model": _cpu_model()},
+        "e2e": {"value": round(value, 4), "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_literal_select": literal,
     }
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch(a) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: start N
+    ranks (one per GPU) through torch.distributed.run on 127.0.0.1 and return
+    its exit code; rank 0 prints the JSON line.  NCCL_DEBUG=INFO (unless set)
+    puts NCCL's communicator / transport lines on stderr."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def launcher_check(a, rank, world):
+    """The multi-rank plumbing without kernels (CPU tests): rendezvous, one
+    max-over-ranks all-reduce like the timed region's, rank 0's JSON line."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank + 1)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mx = float(t.item())
+        dist.destroy_process_group()
+    else:
+        mx = 1.0
+    if rank == 0:
+        print(json.dumps({"launcher_check": True, "n_gpus": world, "max_over_ranks": mx,
+                          "shard": a.shard}), flush=True)
 
 
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(a))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if a.launcher_check:
+        launcher_check(a, rank, world)
+        return
     if a.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(a)), flush=True)
