@@ -153,6 +153,14 @@ def _stream_roofline(stats, n_local, hbm_peak, peak_kind, bf16_peak, qw):
         out["tensor"] = {"achieved_tflops": round(tf, 1), "tf32_peak_tflops": round(bf16_peak / 2, 1),
                          "frac": round(tf / (bf16_peak / 2), 4),
                          "peak_note": "TF32 dense = measured bf16 / 2 (nominal ratio)"}
+        if out["tensor"]["frac"] > out["frac"]:
+            # 256 queries per page visit: the launch does twice the tensor work
+            # per HBM byte of a 128-query pass -- report it against the tensor
+            # roofline (the HBM figures stay under "hbm")
+            out["hbm"] = {k: out[k] for k in ("achieved", "peak", "unit", "frac", "peak_kind")}
+            out.update({"bound": "tensor", "achieved": round(tf, 1), "peak": round(bf16_peak / 2, 1),
+                        "unit": "TFLOP/s", "frac": out["tensor"]["frac"],
+                        "peak_kind": peak_kind + " (bf16 / 2)"})
     return out
 
 

@@ -2,7 +2,7 @@
 //
 // For Q >= 32 queries per call the Q x N similarity contraction is a real GEMM
 // (SURVEY.md 8(a) A9 "K4", configs 2/4/5), so one pass over the store serves
-// QW = 32/64/128 queries at once instead of one pass per 8 (select_mma.cu):
+// QW = 32/64/128/256 queries at once instead of one pass per 8 (select_mma.cu):
 //
 //   warp 16 (producer) one bulk copy (TMA engine) per page into an NST-deep
 //                      shared-memory ring; pages are stored as ready MN-major
@@ -55,9 +55,20 @@ using namespace umma;
 namespace {
 
 // warp roles: 0-11 epilogue (three groups of four TMEM lane quarters taking
-// every third page), 12-15 record constants (two pairs taking alternate
-// pages; they own the shared page stage), 16 producer, 17 MMA
+// every third unit), 12-15 record constants (two pairs taking alternate
+// pages; they own the shared page stage), 16 producer, 17 MMA.
+//
+// A unit is one (page, query sub-group) accumulator: QW <= 128 is one
+// sub-group per page; QW = 256 serves two sub-groups of 128 queries from the
+// same shared page stage -- per page two sets of MMAs (N = 128, the B tile's
+// halves) into two TMEM stages, each committed on its own -- so the store is
+// streamed once per 256 queries while TMEM keeps four 128-column stages and
+// the epilogue drains one (page, half) while the tensor core fills the next.
+// (A single N = 256 accumulator leaves two TMEM stages: measured 1.45 ms per
+// 16M-record pass against 1.2 here -- the MMA of page i + 2 waits on page i's
+// whole epilogue.)
 constexpr int WE = 12;                 // three groups of four epilogue warps
+
 constexpr int NEG = WE / 4;
 constexpr int W_REC = WE, W_PROD = WE + 4, W_MMA = WE + 5;
 constexpr int WIDE_THREADS = (WE + 6) * 32;
@@ -88,7 +99,7 @@ struct WideArgs {
     uint32_t* oidx;
     int kout;
     unsigned int* pmax;       // max P over records (float bits)
-    uint32_t tcols;           // TMEM columns allocated (power of two >= ntm * QW)
+    uint32_t tcols;           // TMEM columns allocated (power of two >= ntm * min(QW, 128))
     int probe;                // diagnostics (SAIR_PROBE_WIDE=1): skip the epilogue math
 };
 
@@ -125,6 +136,8 @@ __device__ __forceinline__ float transpose_max(const float (&v)[32], int lane) {
 template <int DP, int QW>
 __global__ void __launch_bounds__(WIDE_THREADS, 1)
     stream_wide_kernel(const __grid_constant__ WideArgs a) {
+    constexpr int NH = QW > 128 ? QW / 128 : 1;  // query sub-groups (units) per page
+    constexpr int QS = QW / NH;                  // queries per unit (MMA N)
     constexpr int BOX_BYTES = 32 * DP * 4;     // 32 records x DP dims
     constexpr int PAGE_BYTES = 4 * BOX_BYTES;  // 128 records
     constexpr int KSTEPS = DP / 8;
@@ -135,7 +148,11 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     // smem page stages, TMEM accumulator stages (decoupled: a page's shared
     // stage is released once the MMA has read it and P is done, its TMEM stage
     // once the epilogue is done), record-constant slots (>= ntm + 1 apart)
-    const int nst = a.nst, ntm = a.ntm, PR = a.nst + a.ntm;
+    // prec slots: the record-constant warps write page it's slot only once the
+    // producer has refilled stage it % nst, i.e. once the MMAs of page it - nst
+    // are done, which waited on the epilogue of every unit of page
+    // it - nst - ntm / NH: nst + ntm / NH slots never overwrite a live one
+    const int nst = a.nst, ntm = a.ntm, PR = a.nst + (a.ntm + NH - 1) / NH;
     unsigned char* stage = smem;
     float* btile = reinterpret_cast<float*>(stage + (size_t)nst * PAGE_BYTES);  // [2][KSTEPS]
     float* prec = btile + WB * KSTEPS * BT_BYTES / 4;  // [PR][4][PAGE]: Asel, Ann, P, lg
@@ -146,8 +163,11 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     float* sM = sB + 2 * QW;     // [2] max |B| per list kind
     uint32_t* scnt = reinterpret_cast<uint32_t*>(sM + 4);  // [2QW] CTA list fill
     uint32_t* sdrop = scnt + 2 * QW;                       // [2QW] dropped max ordinal
-    uint32_t* whist = sdrop + 2 * QW;                      // [WE][256] compaction histograms
-    uint64_t* full = reinterpret_cast<uint64_t*>(whist + WE * 256);
+    // [WE][256] compaction histograms: aliased onto the page stages, which are
+    // idle once every unit's epilogue is done (all copies landed, every MMA
+    // and every record-constant read of them finished before)
+    uint32_t* whist = reinterpret_cast<uint32_t*>(stage);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sdrop + 2 * QW);
     uint64_t* empty = full + 8;
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 8;
@@ -205,7 +225,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         }
         for (int s = 0; s < ntm; ++s) {
             bar_init(&tfull[s], 1);
-            bar_init(&tempty[s], 4);  // the four epilogue warps of the page's group
+            bar_init(&tempty[s], 4);  // the four epilogue warps of the unit's group
         }
         for (int p = 0; p < PR; ++p) bar_init(&pready[p], 2);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -251,29 +271,34 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     } else if (warp == W_MMA) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            // D f32, A/B tf32, A MN-major, B K-major, N = QW, M = 128
+            // D f32, A/B tf32, A MN-major, B K-major, N = QS, M = 128
             constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
-                                       ((uint32_t)(QW >> 3) << 17) | ((128u >> 4) << 24);
+                                       ((uint32_t)(QS >> 3) << 17) | ((128u >> 4) << 24);
             const uint32_t bbase = su32(btile);
             for (uint32_t it = 0; it < mine; ++it) {
                 const uint32_t s = it % nst, ph = (it / nst) & 1u;
-                const uint32_t ts = it % ntm, tph = (it / ntm) & 1u;
                 bar_wait(&full[s], ph);
-                if (it >= (uint32_t)ntm) bar_wait(&tempty[ts], tph ^ 1u);
-                tc_fence_after();
                 const uint32_t abase = su32(stage + (size_t)s * PAGE_BYTES);
-                const uint32_t dcol = tmem + (uint32_t)(ts * QW);
 #pragma unroll
-                for (int ks = 0; ks < KSTEPS; ++ks) {
-                    const uint64_t ad = umma_desc(abase + ks * 1024, BOX_BYTES, 512, 1);
+                for (int h = 0; h < NH; ++h) {
+                    const uint32_t u = it * NH + h;  // unit: (page it, sub-group h)
+                    const uint32_t ts = u % ntm, tph = (u / ntm) & 1u;
+                    if (u >= (uint32_t)ntm) bar_wait(&tempty[ts], tph ^ 1u);
+                    tc_fence_after();
+                    const uint32_t dcol = tmem + (uint32_t)(ts * QS);
 #pragma unroll
-                    for (int h = 0; h < WB; ++h) {
-                        const uint64_t bd =
-                            umma_desc(bbase + (h * KSTEPS + ks) * BT_BYTES, 128, 256, 0);
-                        umma_tf32(dcol, ad, bd, IDESC, ks > 0 || h > 0 ? 1u : 0u);
+                    for (int ks = 0; ks < KSTEPS; ++ks) {
+                        const uint64_t ad = umma_desc(abase + ks * 1024, BOX_BYTES, 512, 1);
+#pragma unroll
+                        for (int w = 0; w < WB; ++w) {
+                            // sub-group h: rows [h QS, h QS + QS) of the K-step's B tile
+                            const uint64_t bd = umma_desc(
+                                bbase + (w * KSTEPS + ks) * BT_BYTES + h * QS * 32, 128, 256, 0);
+                            umma_tf32(dcol, ad, bd, IDESC, ks > 0 || w > 0 ? 1u : 0u);
+                        }
                     }
+                    umma_commit(&tfull[ts]);
                 }
-                umma_commit(&tfull[ts]);
                 umma_commit(&empty[s]);  // the stage is free once these MMAs are done
             }
         }
@@ -356,11 +381,17 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             if (lane == 0) atomicMax(a.pmax, __float_as_uint(pmax));
         }
     } else {
-        // ---------------- epilogue: two groups of four lane quarters ----------------
+        // ---------------- epilogue: three groups of four lane quarters ----------------
+        // group `par` takes every NEG-th unit u = (page u / NH, sub-group u % NH)
         const int par = warp >> 2, quarter = warp & 3;
         const int rloc = quarter * 32 + lane;
-        for (uint32_t it = par; it < mine; it += NEG) {
-            const uint32_t s = it % ntm, ph = (it / ntm) & 1u;  // TMEM stage
+        // (all twelve warps on every unit, three per lane quarter splitting its
+        // chunks, measured 1.95 ms per 16M-record pass at QW = 256 against 1.33)
+        for (uint32_t u = par; u < mine * NH; u += NEG) {
+            const uint32_t it = u / NH;
+            const int cbeg = (int)(u % NH) * QS, cend = cbeg + QS;  // this unit's queries
+            const int cu = cbeg;  // the unit's first query (TMEM column 0)
+            const uint32_t s = u % ntm, ph = (u / ntm) & 1u;  // TMEM stage
             const uint32_t rec = page_of(it) * PAGE + rloc;
             bar_wait(&pready[it % PR], (it / PR) & 1u);
             const float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
@@ -368,10 +399,12 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             const float P = pr[2 * PAGE + rloc], lg = pr[3 * PAGE + rloc];
             bar_wait(&tfull[s], ph);
             tc_fence_after();
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(s * QW);
+            // TMEM column c0 - cbeg of the unit's stage holds query c0
+            const uint32_t taddr =
+                tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(s * QS) - (uint32_t)cu;
             if (a.probe != 1) {
 #pragma unroll 1
-                for (int c0 = 0; c0 < QW; c0 += 32) {
+                for (int c0 = cbeg; c0 < cend; c0 += 32) {
                     float acc[32];
                     tmem_ld32(taddr + c0, acc);
                     if (a.mode == 1) {
@@ -690,7 +723,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.pmax = pmax;
     a.probe = std::getenv("SAIR_PROBE_WIDE") ? std::atoi(std::getenv("SAIR_PROBE_WIDE")) : 0;
     a.tcols = 32;
-    while (a.tcols < (uint32_t)(pl.ntm * QW)) a.tcols <<= 1;
+    while (a.tcols < (uint32_t)(pl.ntm * std::min(QW, 128))) a.tcols <<= 1;
     SAIR_CUDA(cudaFuncSetAttribute(stream_wide_kernel<DP, QW>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     if (!io.t0_override) {
@@ -767,14 +800,16 @@ WideFn wide_pick_qw(int qw) {
     switch (qw) {
         case 32: return wide_launch_t<DP, 32>;
         case 64: return wide_launch_t<DP, 64>;
-        default: return wide_launch_t<DP, 128>;
+        case 128: return wide_launch_t<DP, 128>;
+        default: return wide_launch_t<DP, 256>;
     }
 }
 
 size_t wide_smem(int dp, int qw, int nst, int ntm) {
+    const int nh = qw > 128 ? qw / 128 : 1;
     return 1024 + (size_t)nst * 4 * 32 * dp * 4 + WB * (size_t)(dp / 8) * qw * 32 +
-           (size_t)(nst + ntm) * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 + 16 + 4 * qw * 4 +
-           WE * 256 * 4 + 48 * 8 + 16;
+           (size_t)(nst + (ntm + nh - 1) / nh) * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 +
+           16 + 4 * qw * 4 + 48 * 8 + 16;
 }
 
 }  // namespace
@@ -838,7 +873,12 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
                     WidePlan* pl) {
     if (std::getenv("SAIR_NO_WIDE") || nq < 32 || s->dp < 8 || s->dp > 64) return false;
     pl->dp = s->dp;
-    pl->qw = nq >= 128 ? 128 : (nq >= 64 ? 64 : 32);
+    // 256 queries per page visit when the batch has them (two TMEM stages of
+    // 256 columns); SAIR_WIDE_QW caps it (A/B and tests)
+    int qmax = 256;
+    if (const char* e = std::getenv("SAIR_WIDE_QW")) qmax = std::max(32, std::atoi(e));
+    pl->qw = nq >= 256 && qmax >= 256 ? 256 : nq >= 128 && qmax >= 128 ? 128
+             : (nq >= 64 && qmax >= 64 ? 64 : 32);
     pl->kp = 32;
     const size_t want_pool = lambda != 0.0 ? 4 * m : 2 * m;
     while ((size_t)pl->kp < want_pool && pl->kp < 512) pl->kp <<= 1;
@@ -863,9 +903,10 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
     // threshold retry and the exact fallback)
     if (const char* e = std::getenv("SAIR_WIDE_CAP")) pl->cap = (uint32_t)std::max(1, std::atoi(e));
     const size_t limit = 227 * 1024;
-    // TMEM: ntm stages x QW columns <= 512; as many shared page stages as fit
-    pl->ntm = std::min(8, 512 / pl->qw);
-    pl->nst = 8;
+    // TMEM: ntm stages x min(QW, 128) columns <= 512; as many shared page stages as fit
+    pl->ntm = std::min(8, 512 / std::min(pl->qw, 128));  // 128-column units for QW = 256
+    // four page stages (a fifth measured 4 % slower at QW = 128)
+    pl->nst = 4;
     while (pl->nst > 2 && wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm) > limit) --pl->nst;
     if (wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm) > limit) return false;
     pl->smem = wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm);
