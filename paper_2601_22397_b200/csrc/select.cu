@@ -536,6 +536,7 @@ struct RefineArgs {
     size_t n_loo;  // records of the whole buffer (loo_mean's n)
     double total, two_s2, lambda, beta, gamma, key_slack_abs;
     double bq_rel;  // relative rounding of the MMA's query operand (wide pass), else 0
+    double bias_rel;  // wide pass: D = D' - B_q from an accumulator that also held B_q
     int has_excl, has_excl_nn;
     int nq;                // queries of this group (<= QB)
     const float* ckey;
@@ -612,8 +613,16 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs* __restric
     const double sq = sqrt(pmx) + sqrt(a.cc[q]);
     // + the TF32 rounding of the stored records: d2_true >= d2 (1 - 2^-11) - 2^-11 P
     // + the rounded query operand: |<x, b' - b>| <= bq_rel sqrt(P C_q)
-    const double Eq = a.gamma * sq * sq + 0x1p-11 * pmx * (1.0 + 1e-6) +
-                      a.bq_rel * sqrt(pmx * a.cc[q]) + 1e-30;
+    // + (wide pass) the accumulator also summed B_q = t0_q / alpha + cc_q (the
+    //   pre-test constant, select_wide.cu): D = D' - B_q carries the fp32
+    //   rounding of partial sums up to |D| + |B_q| <= Pmax + 2 cc_q + |B_q|
+    double Eq = a.gamma * sq * sq + 0x1p-11 * pmx * (1.0 + 1e-6) +
+                a.bq_rel * sqrt(pmx * a.cc[q]) + 1e-30;
+    if (a.bias_rel != 0.0 && a.t0) {
+        const double tq = (double)a.t0[q];
+        const double Bq = fabs(tq) < 1e30 ? fabs(tq) / (a.beta * (1.0 - 0x1p-11)) + a.cc[q] : 0.0;
+        Eq += a.bias_rel * (pmx + 2.0 * a.cc[q] + Bq);
+    }
 
     // exact score of every candidate: experience.cpp:163-167 with the
     // reference's rounding sequence (standardize :162-166, similarity
@@ -1251,6 +1260,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                                 : (use_mma ? (pl.dp + 24) * u + 0x1p-20 : (pl.dp + 16) * u);
             ra.key_slack_abs = key_slack_abs;
             ra.bq_rel = use_wide ? wide_bq_rel() : 0.0;
+            ra.bias_rel = use_wide ? 0x1p-19 : 0.0;
             ra.has_excl = n > (size_t)kp;
             ra.has_excl_nn = n > (size_t)knn;
             ra.ckey = mk;

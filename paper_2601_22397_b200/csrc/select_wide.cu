@@ -100,7 +100,8 @@ struct WideArgs {
     int kout;
     unsigned int* pmax;       // max P over records (float bits)
     uint32_t tcols;           // TMEM columns allocated (power of two >= ntm * min(QW, 128))
-    int probe;                // diagnostics (SAIR_PROBE_WIDE=1): skip the epilogue math
+    unsigned long long* trace;  // diagnostics (SAIR_WIDE_TRACE): CTA 0 event clocks, or null
+    int probe;                // diagnostics (SAIR_PROBE_WIDE): 1 skip the epilogue math, 2 also the MMAs
 };
 
 // Candidate append: the slot comes from a shared-memory counter (no global
@@ -117,6 +118,19 @@ __device__ __forceinline__ void list_append(const WideArgs& a, uint32_t* scnt, u
     } else {
         atomicMax(&sdrop[L], f2ord(key));
     }
+}
+
+// diagnostics: clock of event ev of page/unit i (CTA 0, i in [TR0, TR0 + 64))
+constexpr uint32_t TR0 = 100;
+__device__ __forceinline__ void trace_ev(const WideArgs& a, uint32_t i, int ev) {
+    if (a.trace && blockIdx.x == 0 && i >= TR0 && i < TR0 + 64) a.trace[(i - TR0) * 16 + ev] = clock64();
+}
+
+// nearest TF32 (ties away), as a float
+__device__ __forceinline__ float tf32_rna(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
 }
 
 // lane l ends with max over the warp of v[l]: one redux.sync.max.f32 per
@@ -154,8 +168,13 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     // it - nst - ntm / NH: nst + ntm / NH slots never overwrite a live one
     const int nst = a.nst, ntm = a.ntm, PR = a.nst + (a.ntm + NH - 1) / NH;
     unsigned char* stage = smem;
-    float* btile = reinterpret_cast<float*>(stage + (size_t)nst * PAGE_BYTES);  // [2][KSTEPS]
-    float* prec = btile + WB * KSTEPS * BT_BYTES / 4;  // [PR][4][PAGE]: Asel, Ann, P, lg
+    // the bias K-step's A operand: four 32-record boxes whose dimension rows 0
+    // and 1 are 1.0 (the rest 0), so the MMA adds B row 0 + B row 1 of every
+    // query column to each record (swizzling permutes within a row: invariant)
+    float* aconst = reinterpret_cast<float*>(stage + (size_t)nst * PAGE_BYTES);  // [4][8][32]
+    float* btile = aconst + 4 * 8 * 32;  // [WB][KSTEPS] data K-steps, then the bias K-step
+    float* bbias = btile + WB * KSTEPS * BT_BYTES / 4;
+    float* prec = bbias + BT_BYTES / 4;  // [PR][4][PAGE]: Asel, Ann, P, lg
     float* ss = prec + (size_t)PR * 4 * PAGE;
     float* scc = ss + DP;
     float* sthr = scc + QW;
@@ -197,14 +216,42 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     // margin far above the fp32 rounding of both forms.  The hot loop runs
     // the loose test (2 instructions per pair); the rare warp whose records
     // pass re-runs the exact formula on the passing columns.
+    // Stream mode folds B_q into the accumulator: a ninth K-step multiplies
+    // the ones of `aconst` with B_q split into two TF32 parts (hi + lo within
+    // 2^-22 |B_q|), so TMEM holds D' = D + B_q and the hot loop is a plain
+    // minimum (no per-column shared-memory operand: those loads were half of
+    // the pass's shared-memory wavefronts, which the MMA's operand reads need).
+    // The veto lists keep a per-column constant: D' + (Bn_q - B_q).
+    for (int i = tid; i < 4 * 8 * 32; i += WIDE_THREADS) aconst[i] = ((i >> 5) & 7) < 2 ? 1.f : 0.f;
     if (warp == 0) {
         float mb[2] = {0.f, 0.f};
-        for (int i = lane; i < 2 * QW; i += 32) {
-            const int q = i < QW ? i : i - QW;
-            const float B = i < QW ? sthr[i] / a.alpha + scc[q] : sthr[i] + scc[q];
-            sB[i] = B;
-            mb[i >= QW] = fmaxf(mb[i >= QW], fabsf(B));
+        // a query without a start threshold (t0 = -FLT_MAX: every record
+        // passes) has no finite B_q; then the whole launch keeps B in shared
+        // memory (the bias tile is zero and the loop adds B per column)
+        bool fin = true;
+        for (int q = lane; q < QW; q += 32) fin &= fabsf(sthr[q] / a.alpha + scc[q]) < 0x1p60f;
+        const bool bias = a.mode == 1 && __all_sync(0xffffffffu, fin);
+        for (int q = lane; q < QW; q += 32) {
+            const float B = sthr[q] / a.alpha + scc[q];
+            float hi = 0.f, lo = 0.f;
+            if (bias) {
+                hi = tf32_rna(B);
+                lo = tf32_rna(B - hi);
+            }
+            // K-major core-matrix image (as the host builds the data K-steps)
+            float* bq = bbias + (q & 7) * 4 + (q >> 3) * 64;
+            *reinterpret_cast<float4*>(bq) = make_float4(hi, lo, 0.f, 0.f);
+            *reinterpret_cast<float4*>(bq + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float beff = hi + lo;
+            sB[q] = B;
+            // |D| <= P + cc_q: the margins below cover the accumulator's
+            // rounding of D + B_q as well
+            mb[0] = fmaxf(mb[0], fabsf(B) + scc[q]);
+            const float Bn = sthr[QW + q] + scc[q];
+            sB[QW + q] = Bn - beff;  // veto pre-test on D': D' + (Bn - B)
+            mb[1] = fmaxf(mb[1], fabsf(Bn) + fabsf(Bn - beff) + fabsf(beff) + scc[q]);
         }
+        if (lane == 0) sM[2] = bias ? 1.f : 0.f;
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             mb[0] = fmaxf(mb[0], __shfl_xor_sync(0xffffffffu, mb[0], o));
@@ -243,6 +290,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     const uint32_t tmem = *tmem_slot;
 
     const uint32_t units = a.mode == 0 ? a.spages + a.nhot : a.npages;
+    const bool bias_on = sM[2] != 0.f;  // B folded into the accumulator (stream mode)
     const uint32_t G = gridDim.x, r0 = blockIdx.x;
     const uint32_t mine = r0 < units ? (units - 1 - r0) / G + 1 : 0;
     auto page_of = [&](uint32_t it) -> uint32_t {
@@ -263,6 +311,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             for (uint32_t it = 0; it < mine; ++it) {
                 const uint32_t s = it % nst, ph = (it / nst) & 1u;
                 if (it >= (uint32_t)nst) bar_wait(&empty[s], ph ^ 1u);
+                trace_ev(a, it, 0);  // producer: stage free, copy issued
                 bar_expect_tx(&full[s], PAGE_BYTES);
                 bulk_g2s(stage + (size_t)s * PAGE_BYTES, a.pages + (size_t)page_of(it) * DP * PAGE,
                          PAGE_BYTES, &full[s]);
@@ -278,12 +327,14 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             for (uint32_t it = 0; it < mine; ++it) {
                 const uint32_t s = it % nst, ph = (it / nst) & 1u;
                 bar_wait(&full[s], ph);
+                trace_ev(a, it, 1);  // MMA: page landed
                 const uint32_t abase = su32(stage + (size_t)s * PAGE_BYTES);
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     const uint32_t u = it * NH + h;  // unit: (page it, sub-group h)
                     const uint32_t ts = u % ntm, tph = (u / ntm) & 1u;
                     if (u >= (uint32_t)ntm) bar_wait(&tempty[ts], tph ^ 1u);
+                    trace_ev(a, it, 2 + h);  // MMA: TMEM stage of unit (it, h) free
                     tc_fence_after();
                     const uint32_t dcol = tmem + (uint32_t)(ts * QS);
 #pragma unroll
@@ -294,12 +345,19 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                             // sub-group h: rows [h QS, h QS + QS) of the K-step's B tile
                             const uint64_t bd = umma_desc(
                                 bbase + (w * KSTEPS + ks) * BT_BYTES + h * QS * 32, 128, 256, 0);
-                            umma_tf32(dcol, ad, bd, IDESC, ks > 0 || w > 0 ? 1u : 0u);
+                            if (a.probe != 2) umma_tf32(dcol, ad, bd, IDESC, ks > 0 || w > 0 ? 1u : 0u);
                         }
+                    }
+                    if (bias_on && a.probe != 2) {
+                        // D += 1 * (hi_q + lo_q): the pre-test constant, in the accumulator
+                        const uint64_t ad = umma_desc(su32(aconst), 1024, 512, 1);
+                        const uint64_t bd = umma_desc(su32(bbias) + h * QS * 32, 128, 256, 0);
+                        umma_tf32(dcol, ad, bd, IDESC, 1u);
                     }
                     umma_commit(&tfull[ts]);
                 }
                 umma_commit(&empty[s]);  // the stage is free once these MMAs are done
+                trace_ev(a, it, 4);  // MMA: page's MMAs issued
             }
         }
     } else if (warp >= W_REC) {
@@ -373,6 +431,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             if (lane == 0) {
                 bar_arrive(&pready[it % PR]);
                 bar_arrive(&empty[s]);  // no wait for the MMA: its commit also arrives
+                trace_ev(a, it, 5 + half);  // record constants written
             }
         }
         if (a.mode == 1) {
@@ -393,33 +452,43 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             const int cu = cbeg;  // the unit's first query (TMEM column 0)
             const uint32_t s = u % ntm, ph = (u / ntm) & 1u;  // TMEM stage
             const uint32_t rec = page_of(it) * PAGE + rloc;
+            if (quarter == 0) trace_ev(a, it, 7 + 3 * (u % NH));  // epilogue: unit start
             bar_wait(&pready[it % PR], (it / PR) & 1u);
             const float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
             const float Asel = pr[rloc], Ann = pr[PAGE + rloc];
             const float P = pr[2 * PAGE + rloc], lg = pr[3 * PAGE + rloc];
             bar_wait(&tfull[s], ph);
+            if (quarter == 0) trace_ev(a, it, 8 + 3 * (u % NH));  // epilogue: accumulator ready
             tc_fence_after();
             // TMEM column c0 - cbeg of the unit's stage holds query c0
             const uint32_t taddr =
                 tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(s * QS) - (uint32_t)cu;
-            if (a.probe != 1) {
+            if (a.probe == 0) {
 #pragma unroll 1
                 for (int c0 = cbeg; c0 < cend; c0 += 32) {
                     float acc[32];
                     tmem_ld32(taddr + c0, acc);
                     if (a.mode == 1) {
-                        // min over the chunk of D + B (FADD2 + 3-input min: one
-                        // instruction per pair), two independent chains per list
+                        // min over the chunk of D' = D + B (one 3-input min per two
+                        // pairs), two independent chains
                         float m0 = INFINITY, m1 = INFINITY;
+                        if (bias_on) {
 #pragma unroll
-                        for (int j = 0; j < 32; j += 4) {
-                            const float4 b4 = *reinterpret_cast<const float4*>(sB + c0 + j);
-                            const float2 u = __fadd2_rn(make_float2(acc[j], acc[j + 1]),
-                                                        make_float2(b4.x, b4.y));
-                            const float2 v = __fadd2_rn(make_float2(acc[j + 2], acc[j + 3]),
-                                                        make_float2(b4.z, b4.w));
-                            m0 = fminf(m0, fminf(u.x, u.y));
-                            m1 = fminf(m1, fminf(v.x, v.y));
+                            for (int j = 0; j < 32; j += 4) {
+                                m0 = fminf(m0, fminf(acc[j], acc[j + 1]));
+                                m1 = fminf(m1, fminf(acc[j + 2], acc[j + 3]));
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                const float4 b4 = *reinterpret_cast<const float4*>(sB + c0 + j);
+                                const float2 u = __fadd2_rn(make_float2(acc[j], acc[j + 1]),
+                                                            make_float2(b4.x, b4.y));
+                                const float2 v = __fadd2_rn(make_float2(acc[j + 2], acc[j + 3]),
+                                                            make_float2(b4.z, b4.w));
+                                m0 = fminf(m0, fminf(u.x, u.y));
+                                m1 = fminf(m1, fminf(v.x, v.y));
+                            }
                         }
                         bool hit = fminf(m0, m1) < Asel;
                         if (a.knn) {
@@ -444,14 +513,21 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                             uint32_t ms = 0, mn = 0;
 #pragma unroll
                             for (int j = 0; j < 32; ++j) {
-                                ms |= acc[j] + sB[c0 + j] < Asel ? 1u << j : 0u;
+                                ms |= acc[j] + (bias_on ? 0.f : sB[c0 + j]) < Asel ? 1u << j : 0u;
                                 if (a.knn) mn |= acc[j] + sB[QW + c0 + j] < Ann ? 1u << j : 0u;
                             }
                             uint32_t U = __reduce_or_sync(0xffffffffu, ms | mn);
                             while (U) {
                                 const int j = __ffs(U) - 1;
                                 U &= U - 1;
-                                const float v = tmem_ld1(taddr + c0 + j);
+                                // D = D' - (hi + lo), in the order the bias was split
+                                const float Bj = sB[c0 + j];
+                                float hi = 0.f, lo = 0.f;
+                                if (bias_on) {
+                                    hi = tf32_rna(Bj);
+                                    lo = tf32_rna(Bj - hi);
+                                }
+                                const float v = (tmem_ld1(taddr + c0 + j) - hi) - lo;
                                 const float d2 = (P + scc[c0 + j]) + v;
                                 const float key = fmaf(-d2, a.alpha, lg);
                                 if (((ms >> j) & 1u) && key > sthr[c0 + j])
@@ -493,6 +569,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) bar_arrive(&tempty[s]);
+            if (quarter == 0) trace_ev(a, it, 9 + 3 * (u % NH));  // epilogue: unit done
         }
         if (a.mode == 1) {
             asm volatile("bar.sync 1, %0;" ::"n"(WE * 32) : "memory");
@@ -722,6 +799,10 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     a.kout = pl.kmax;
     a.pmax = pmax;
     a.probe = std::getenv("SAIR_PROBE_WIDE") ? std::atoi(std::getenv("SAIR_PROBE_WIDE")) : 0;
+    static unsigned long long* dtrace = nullptr;
+    if (std::getenv("SAIR_WIDE_TRACE") && !dtrace) SAIR_CUDA(cudaMalloc(&dtrace, 64 * 16 * 8));
+    a.trace = nullptr;
+
     a.tcols = 32;
     while (a.tcols < (uint32_t)(pl.ntm * std::min(QW, 128))) a.tcols <<= 1;
     SAIR_CUDA(cudaFuncSetAttribute(stream_wide_kernel<DP, QW>,
@@ -739,8 +820,25 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     SAIR_CUDA(cudaEventRecord(io.e_mid, s->st));
     a.mode = 1;
     a.pl_out = io.pl_out;  // the first stream pass of a call caches (P, lg) per record
+    if (dtrace) {
+        SAIR_CUDA(cudaMemsetAsync(dtrace, 0, 64 * 16 * 8, s->st));
+        a.trace = dtrace;
+    }
     stream_wide_kernel<DP, QW><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
     SAIR_LAUNCH("stream_wide_kernel(stream)");
+    if (dtrace) {  // diagnostics: per-page event clocks of CTA 0, relative to the first
+        std::vector<unsigned long long> h(64 * 16);
+        SAIR_CUDA(cudaMemcpyAsync(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost, s->st));
+        SAIR_CUDA(cudaStreamSynchronize(s->st));
+        const unsigned long long t0c = h[0];
+        fprintf(stderr, "[trace] page: prod mfull mtm0 mtm1 missued rec0 rec1 | e0s e0r e0d | e1s e1r e1d\n");
+        for (int i = 0; i < 64; ++i) {
+            fprintf(stderr, "[trace] %3d:", i + (int)TR0);
+            for (int e = 0; e < 13; ++e)
+                fprintf(stderr, " %7lld", h[i * 16 + e] ? (long long)(h[i * 16 + e] - t0c) : -1LL);
+            fprintf(stderr, "\n");
+        }
+    }
     SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
     // the per-query top-K' across the CTAs' compacted lists (io.lists_key:
     // [G][2QW][kmax], K' each) is merged by the caller, all groups at once
@@ -807,7 +905,8 @@ WideFn wide_pick_qw(int qw) {
 
 size_t wide_smem(int dp, int qw, int nst, int ntm) {
     const int nh = qw > 128 ? qw / 128 : 1;
-    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + WB * (size_t)(dp / 8) * qw * 32 +
+    // + the bias K-step: its constant A tile (4 KB) and B tile (qw x 32 B)
+    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + 4096 + (WB * (size_t)(dp / 8) + 1) * qw * 32 +
            (size_t)(nst + (ntm + nh - 1) / nh) * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 +
            16 + 4 * qw * 4 + 48 * 8 + 16;
 }
