@@ -127,7 +127,7 @@ def _launches(stats):
     """Our kernels per select() call, from its stats: per query group the
     threshold pre-pass (2), the stream pass and the list merge (wide: per-list
     top-K') and refine; 3 + 3m per exact fallback query."""
-    per = {2: 5, 1: 5, 0: 3}
+    per = {3: 5, 2: 5, 1: 5, 0: 3}
     return sum(per[s["tensor_core"]] * s["stream_launches"] + s["exact_fallbacks"] * (3 + 3 * K_SEL)
                for s in stats)
 
@@ -136,11 +136,13 @@ def _stream_roofline(stats, n_local, hbm_peak, peak_kind, bf16_peak, qw):
     """Roofline of the dominant kernel (the stream pass): algorithmic bytes =
     records x (4 d_pad + 4) per launch (the fp32 page row + the fp32 reward)
     / its CUDA-event time; the wide pass (qw > 0) reads the call's cached
-    (P, log residual) pair instead of the reward: 4 d_pad + 8."""
+    (P, log residual) pair instead of the reward: 4 d_pad + 8; on the bf16
+    page copy (tensor_core 3) 2 d_pad + 8, and its GEMM runs at the bf16 rate."""
     launches = sum(s["stream_launches"] for s in stats)
     stream_ms = sum(s["stream_ms"] for s in stats)
     dp = 64 if DIM > 32 else 32
-    alg_bytes = n_local * (4 * dp + (8 if qw else 4))
+    b16 = bool(stats) and stats[0]["tensor_core"] == 3
+    alg_bytes = n_local * ((2 if b16 else 4) * dp + (8 if qw else 4))
     per_launch_s = max(stream_ms / 1e3 / max(launches, 1), 1e-12)
     achieved = alg_bytes / per_launch_s / 1e9 if launches else 0.0
     out = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -148,19 +150,21 @@ def _stream_roofline(stats, n_local, hbm_peak, peak_kind, bf16_peak, qw):
            "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": round(per_launch_s * 1e3, 4),
            "prepass_ms_per_launch": round(sum(s["prepass_ms"] for s in stats) / max(launches, 1), 4)}
     if qw:
-        # the same launch as a GEMM: 2 x records x d_pad x QW TF32 flops
+        # the same launch as a GEMM: 2 x records x d_pad x QW flops, TF32 or bf16
         tf = 2.0 * n_local * dp * qw / per_launch_s / 1e12
-        out["tensor"] = {"achieved_tflops": round(tf, 1), "tf32_peak_tflops": round(bf16_peak / 2, 1),
-                         "frac": round(tf / (bf16_peak / 2), 4),
-                         "peak_note": "TF32 dense = measured bf16 / 2 (nominal ratio)"}
+        tpeak = bf16_peak if b16 else bf16_peak / 2
+        out["tensor"] = {"achieved_tflops": round(tf, 1), "dtype": "bf16" if b16 else "tf32",
+                         "peak_tflops": round(tpeak, 1), "frac": round(tf / tpeak, 4),
+                         "peak_note": ("bf16 dense, measured (MEASURED_PEAKS.json)" if b16 else
+                                       "TF32 dense = measured bf16 / 2 (nominal ratio)")}
         if out["tensor"]["frac"] > out["frac"]:
             # 256 queries per page visit: the launch does twice the tensor work
             # per HBM byte of a 128-query pass -- report it against the tensor
             # roofline (the HBM figures stay under "hbm")
             out["hbm"] = {k: out[k] for k in ("achieved", "peak", "unit", "frac", "peak_kind")}
-            out.update({"bound": "tensor", "achieved": round(tf, 1), "peak": round(bf16_peak / 2, 1),
+            out.update({"bound": "tensor", "achieved": round(tf, 1), "peak": round(tpeak, 1),
                         "unit": "TFLOP/s", "frac": out["tensor"]["frac"],
-                        "peak_kind": peak_kind + " (bf16 / 2)"})
+                        "peak_kind": peak_kind + ("" if b16 else " (bf16 / 2)")})
     return out
 
 
@@ -269,11 +273,13 @@ def run_ours(a, rank, world, local_rank):
         e2e_s = float(t.item())
     e2e = a.steps * a.queries / e2e_s
 
-    qw = stats[0]["qb"] if stats[0]["tensor_core"] == 2 else 0
+    qw = stats[0]["qb"] if stats[0]["tensor_core"] in (2, 3) else 0
     roof = _stream_roofline(stats, hi - lo, hbm_peak, peak_kind, bf16_peak, qw)
     tc = stats[0]["tensor_core"]
     dp = 64 if DIM > 32 else 32
-    roof["kernel"] = (f"sair::stream_wide_kernel<{dp},{qw}> (tcgen05, {qw} queries/pass)" if tc == 2
+    roof["kernel"] = (f"sair::stream_wide16_kernel<{qw}> (tcgen05 kind::f16, bf16 page copy, "
+                      f"{qw} queries/pass)" if tc == 3
+                      else f"sair::stream_wide_kernel<{dp},{qw},1> (tcgen05, {qw} queries/pass)" if tc == 2
                       else f"sair::stream_mma_kernel<{dp},8> (tcgen05)" if tc == 1
                       else f"sair::stream_kernel<{dp},8>")
     tp = ROOT / "profiles" / "stream_kernel_traffic.json"
@@ -331,7 +337,8 @@ def run_ours(a, rank, world, local_rank):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32/tf32 filter + f64 refine",
+        "dtype": ("bf16 filter (tcgen05 kind::f16) + f64 refine" if tc == 3
+                  else "f32/tf32 filter + f64 refine"),
         "data": "synthetic (device-generated, synth.py; store 16M x 64, i.i.d. Irwin-Hall contexts)",
         "config": {"workload": f"configs[3]: {n_total} records x d={DIM}, Q={a.queries} "
                                f"queries/step, k={K_SEL}, lambda_div={a.lambda_div}",
@@ -346,8 +353,18 @@ def run_ours(a, rank, world, local_rank):
                 "d2h_bytes_per_step": a.queries * K_SEL * 24 + a.queries * 8},
         "gpu_launches": gpu_launches,
         "roofline": roof,
+        # the whole step against the Q x N x d contraction it must do (2 Q N d
+        # flops at d = 64), at the TF32 and the bf16 measured peaks
+        "step_tensor": {"flops_per_step": 2.0 * a.queries * n_total * DIM,
+                        "tflops": round(2.0 * a.queries * n_total * DIM / (ms / a.steps / 1e3) / 1e12 / world, 1),
+                        "frac_tf32_peak": round(2.0 * a.queries * n_total * DIM / (ms / a.steps / 1e3)
+                                                / 1e12 / world / (bf16_peak / 2), 4),
+                        "frac_bf16_peak": round(2.0 * a.queries * n_total * DIM / (ms / a.steps / 1e3)
+                                                / 1e12 / world / bf16_peak, 4),
+                        "note": "per GPU"},
         "certified_queries": sum(s["certified"] for s in stats),
         "exact_fallbacks": sum(s["exact_fallbacks"] for s in stats),
+        "retried_queries": sum(s["retried"] for s in stats),
         "store_build_s": round(gen_s, 3),
         "hbm_target": hbm_target,
     }

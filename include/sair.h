@@ -79,7 +79,8 @@ typedef struct {
     float stream_ms;        /* device time of the streaming kernels (CUDA events) */
     float total_ms;         /* device time of the whole call */
     float prepass_ms;       /* device time of the threshold sample pre-pass (tensor-core path) */
-    int tensor_core;        /* 1: tcgen05 8-query stream pass; 2: tcgen05 wide (32-128 query) pass */
+    int tensor_core;        /* 1: tcgen05 8-query stream pass; 2: tcgen05 wide (32-256 query)
+                               TF32 pass; 3: the 256-query wide pass on the bf16 page copy */
     int small;              /* 1: the whole call ran as the one-launch exact small-store select */
     size_t retried;         /* queries given a second wide pass with raised thresholds */
 } sair_select_stats;

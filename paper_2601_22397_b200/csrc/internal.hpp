@@ -126,6 +126,12 @@ struct sair_store_s {
     sair::DBuf b_grp;     // per query group of one select call: merged lists, thresholds, ...
     sair::DBuf b_wlists;  // the wide pass's compacted CTA lists of every group of a call
     sair::DBuf b_pl;      // per record (P, log residual) of the current call (wide pass)
+    // bf16 filter copy of the pages for the 256-query wide pass (DESIGN.md
+    // "K4 bf16"): [page][128 rows][64 dims] K-major, 128-byte swizzled; derived
+    // from `pages` on demand, valid for records [0, pages16_n)
+    sair::DBuf b_pages16;
+    size_t pages16_n = 0;
+    sair::DBuf b_pl16;    // (P, log residual) of the bf16 records (the bf16 pass's cache)
     bool defer_sync = false;         // decision step: the small select leaves its copy-out
     std::function<void()> pending;   // pending, and its host unpack here
     sair::DBuf b_hot;     // the wide sample's highest-residual pages ...
@@ -136,6 +142,7 @@ struct sair_store_s {
     std::shared_ptr<sair::GreedySession> greedy;  // sharded lambda > 0 select in progress
     std::vector<cudaEvent_t> gev;  // per query group: start, end of pre-pass, end of stream
     const float* mma_t0 = nullptr;
+    const float* mma_t0safe = nullptr;  // wide pass: the sample's guaranteed start thresholds
     const unsigned int* mma_dropped = nullptr;
     sair_select_stats last{};
 };

@@ -537,12 +537,14 @@ struct RefineArgs {
     double total, two_s2, lambda, beta, gamma, key_slack_abs;
     double bq_rel;  // relative rounding of the MMA's query operand (wide pass), else 0
     double bias_rel;  // wide pass: D = D' - B_q from an accumulator that also held B_q
+    double rec_rel;   // relative rounding of the stored records (TF32 2^-11; bf16 pass)
     int has_excl, has_excl_nn;
     int nq;                // queries of this group (<= QB)
     const float* ckey;
     const uint32_t* cidx;  // merged, sorted [2QB][kmax]
     const float* cthr;     // [2QB]
     const float* t0;                // [2QB] stream-pass start thresholds (MMA path) or null
+    const float* t0safe;            // [2QB] wide pass: the sample's guaranteed ones (retry), or null
     const unsigned int* dropped;    // [2QB] max ordinal key dropped on a full list, or null
     double* zs;            // scratch [QB][kp][d]
     int64_t gbase;
@@ -616,11 +618,11 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs* __restric
     // + (wide pass) the accumulator also summed B_q = t0_q / alpha + cc_q (the
     //   pre-test constant, select_wide.cu): D = D' - B_q carries the fp32
     //   rounding of partial sums up to |D| + |B_q| <= Pmax + 2 cc_q + |B_q|
-    double Eq = a.gamma * sq * sq + 0x1p-11 * pmx * (1.0 + 1e-6) +
+    double Eq = a.gamma * sq * sq + a.rec_rel * pmx * (1.0 + 1e-6) +
                 a.bq_rel * sqrt(pmx * a.cc[q]) + 1e-30;
     if (a.bias_rel != 0.0 && a.t0) {
         const double tq = (double)a.t0[q];
-        const double Bq = fabs(tq) < 1e30 ? fabs(tq) / (a.beta * (1.0 - 0x1p-11)) + a.cc[q] : 0.0;
+        const double Bq = fabs(tq) < 1e30 ? fabs(tq) / (a.beta * (1.0 - a.rec_rel)) + a.cc[q] : 0.0;
         Eq += a.bias_rel * (pmx + 2.0 * a.cc[q] + Bq);
     }
 
@@ -796,8 +798,10 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs* __restric
         if (a.out_thr) {
             a.out_thr[q] = s_thr[0];
             a.out_thr[a.QB + q] = a.knn ? s_thr[1] : -INFINITY;
-            a.out_thr[2 * a.QB + q] = a.t0 ? a.t0[q] : -INFINITY;
-            a.out_thr[3 * a.QB + q] = a.t0 && a.knn ? a.t0[a.QB + q] : -INFINITY;
+            // the retry's start: the guaranteed threshold where the pass used an estimate
+            const float* ts = a.t0safe ? a.t0safe : a.t0;
+            a.out_thr[2 * a.QB + q] = ts ? ts[q] : -INFINITY;
+            a.out_thr[3 * a.QB + q] = ts && a.knn ? ts[a.QB + q] : -INFINITY;
         }
     }
     if (a.knn == 0) return;
@@ -821,7 +825,7 @@ __global__ void __launch_bounds__(256) refine_kernel(const RefineArgs* __restric
         if (a.has_excl_nn) {
             // excluded records have d2_32 >= D = -U_nn, so true d2 >= D - E_q
             const double D = -excl_bound(a, a.QB + q, s_thr[1]);
-            const double lo = fmax(D * (1.0 - 0x1p-11) - Eq, 0.0);
+            const double lo = fmax(D * (1.0 - a.rec_rel) - Eq, 0.0);
             cert = c.g > exp(-lo / a.two_s2) * (1.0 + 1e-12);
         }
         a.out_nn[q] = a.gbase + c.i;
@@ -1045,7 +1049,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         const double rdel = 4.0 * u * (est.rabs * c1d + std::fabs(c0d)) * 1.01 + 1e-30;
         const float rdelta = (float)rdel;
         const double beta = 1.4426950408889634 / p.two_s2;  // log2(e) / (2 sigma^2)
-        const float alpha = (float)(beta * (1.0 - 0x1p-11));  // TF32 storage, see Eq
+        // TF32 (or, the bf16 wide pass, bf16) storage of the records, see Eq
+        const double rec_rel = use_wide ? wide_rec_rel(wp) : 0x1p-11;
+        const float alpha = (float)(beta * (1.0 - rec_rel));
         const double lg_hi = std::log2(est.rabs * c1d + std::fabs(c0d) + rdel);
         const double key_slack_abs = 1.0 + 2.0 * (std::fabs(std::log2(rdel)) + std::fabs(lg_hi));
 
@@ -1147,6 +1153,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         // (one standardization, one set of reward constants) -- computed by the
         // first stream pass, read by every later launch
         float* pl_cache = use_wide ? s->b_pl.as<float>(((n + PAGE - 1) / PAGE) * PAGE * 2) : nullptr;
+        float* pl16_cache =
+            use_wide && wp.bf16 ? s->b_pl16.as<float>(((n + PAGE - 1) / PAGE) * PAGE * 2) : nullptr;
         uint32_t* li_g = use_wide ? reinterpret_cast<uint32_t*>(lk_g + ngroups * lstride) : nullptr;
         RefineArgs* ra_host = reinterpret_cast<RefineArgs*>(
             s->h_ra.get(ngroups * sizeof(RefineArgs) + 64));
@@ -1158,7 +1166,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                                        (int)refine_smem));
         s->last.candidates = kp;
         s->last.qb = qb;
-        s->last.tensor_core = use_wide ? 2 : (use_mma ? 1 : 0);
+        s->last.tensor_core = use_wide ? (wp.bf16 ? 3 : 2) : (use_mma ? 1 : 0);
         // wide pass: a group's constants on the host (phase 1 of wfill) and the
         // refine's cc; they go up in two copies per call -- group 0's, then,
         // computed while the device runs group 0, every later group's -- not
@@ -1190,7 +1198,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                 const double* z = zgrp + (size_t)(qq < nqg ? qq : 0) * d;
                 for (int k = 0; k < d; ++k) hc[2 * (size_t)d + (size_t)qq * d + k] = z[k];
             }
-            const GroupIo io{hstage_all ? hstage_all + g * hstride : nullptr, s->gev[3 * g + 1],
+            GroupIo io{hstage_all ? hstage_all + g * hstride : nullptr, s->gev[3 * g + 1],
                              s->gev[3 * g + 2], t0o ? t0o->data() + g * 2 * qb : nullptr,
                              use_wide ? lk_g + g * lstride : nullptr,
                              use_wide ? li_g + g * lstride : nullptr,
@@ -1198,6 +1206,8 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                              use_wide && !pl_ready ? pl_cache : nullptr, hot, nhot,
                              use_wide ? 2 : 0, use_wide ? wc_g + g * hstride : nullptr,
                              use_wide ? wcnt_g + g * 4 * (size_t)qb : nullptr};
+            io.pl16_in = pl16_cache && pl_ready ? pl16_cache : nullptr;
+            io.pl16_out = pl16_cache && !pl_ready ? pl16_cache : nullptr;
             if (use_wide) pl_ready = true;
             const O D = carve(dout + g * ob);
             float* mk = mk_g + g * mstride;
@@ -1259,14 +1269,16 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             ra.gamma = use_wide ? (2 * pl.dp + 32) * u + 0x1p-20
                                 : (use_mma ? (pl.dp + 24) * u + 0x1p-20 : (pl.dp + 16) * u);
             ra.key_slack_abs = key_slack_abs;
-            ra.bq_rel = use_wide ? wide_bq_rel() : 0.0;
+            ra.bq_rel = use_wide ? wide_bq_rel(wp) : 0.0;
             ra.bias_rel = use_wide ? 0x1p-19 : 0.0;
+            ra.rec_rel = rec_rel;
             ra.has_excl = n > (size_t)kp;
             ra.has_excl_nn = n > (size_t)knn;
             ra.ckey = mk;
             ra.cidx = mi;
             ra.cthr = mthr;
             ra.t0 = use_wide ? s->mma_t0 : (use_mma ? t0_g + g * 2 * qb : nullptr);
+            ra.t0safe = use_wide ? s->mma_t0safe : nullptr;
             ra.dropped = use_wide ? s->mma_dropped : (use_mma ? drop_g + g * 2 * qb : nullptr);
             ra.zs = zs_g + g * zstride;
             ra.gbase = s->gbase;

@@ -79,6 +79,8 @@ struct GroupIo {
     int phase;
     float* dconsts;
     uint32_t* dcnt;
+    const float* pl16_in;  // bf16 wide pass: its own (P, lg) cache (bf16 records)
+    float* pl16_out;
 };
 
 // select_mma.cu: the tcgen05 streaming kernel (plan + launcher)
@@ -98,6 +100,10 @@ bool make_mma_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bo
 struct WidePlan {
     int dp, qw, kp, knn, kmax, nst, ntm, grid;
     size_t smem;
+    int cg, nst2;  // stream passes: CTAs per MMA group (2 = CTA pairs) and their page stages
+    size_t smem2;
+    int bf16, nst16;  // 256-query stream passes on the bf16 page copy (select_wide.cu)
+    size_t smem16;
     uint32_t cap, spages;
 };
 using WideFn = void (*)(sair_store_s*, const WidePlan&, const QueryPrep&, const double*, int, float,
@@ -108,7 +114,9 @@ WideFn pick_wide(int dp, int qw);
 // ones >= npages), or null
 const uint32_t* wide_hot_pages(sair_store_s* s, const WidePlan& pl, float c1, float c0,
                                uint32_t* nhot);
-double wide_bq_rel();  // relative error bound of the wide pass's query operand
+double wide_bq_rel(const WidePlan& pl);   // relative error bound of the wide pass's query operand
+double wide_rec_rel(const WidePlan& pl);  // relative error bound of its stored records
+void ensure_pages16(sair_store_s* s);     // the bf16 page copy covers every record
 bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                     WidePlan* pl);
 

@@ -42,6 +42,7 @@
 #include <vector>
 
 #include <cub/cub.cuh>
+#include <cuda_bf16.h>
 
 #include "select_common.cuh"
 #include "topk_select.cuh"
@@ -100,6 +101,8 @@ struct WideArgs {
     int kout;
     unsigned int* pmax;       // max P over records (float bits)
     uint32_t tcols;           // TMEM columns allocated (power of two >= ntm * min(QW, 128))
+    const uint16_t* pages16;  // bf16 pass: the bf16 page copy
+    const void* consts16;     // bf16 pass: the query tile (QW rows x 128 B, swizzled)
     unsigned long long* trace;  // diagnostics (SAIR_WIDE_TRACE): CTA 0 event clocks, or null
     int probe;                // diagnostics (SAIR_PROBE_WIDE): 1 skip the epilogue math, 2 also the MMAs
 };
@@ -147,15 +150,24 @@ __device__ __forceinline__ float transpose_max(const float (&v)[32], int lane) {
     return out;
 }
 
-template <int DP, int QW>
+// CG = 1: one CTA per SM, M = 128 MMAs.  CG = 2 (stream mode): CTA pairs
+// (cluster of two SMs, cta_group::2): rank 0 issues M = 256 MMAs whose A rows
+// are both CTAs' pages and whose B columns are split between them (each CTA
+// holds half of every unit's queries), so each SM's tensor core reads half
+// the B operand from its shared memory -- the MMA's operand reads were the
+// largest shared-memory consumer -- and the halved B tile leaves room for a
+// fifth page stage (more bytes in flight per SM: the stage ring is bounded
+// by HBM latency, not bandwidth).
+template <int DP, int QW, int CG>
 __global__ void __launch_bounds__(WIDE_THREADS, 1)
     stream_wide_kernel(const __grid_constant__ WideArgs a) {
     constexpr int NH = QW > 128 ? QW / 128 : 1;  // query sub-groups (units) per page
     constexpr int QS = QW / NH;                  // queries per unit (MMA N)
+    constexpr int QH = QS / CG;                  // B rows of a unit in this CTA
     constexpr int BOX_BYTES = 32 * DP * 4;     // 32 records x DP dims
     constexpr int PAGE_BYTES = 4 * BOX_BYTES;  // 128 records
     constexpr int KSTEPS = DP / 8;
-    constexpr int BT_BYTES = QW * 32;          // one K-step B tile: QW rows x 8 tf32
+    constexpr int BT_BYTES = QW * 32 / CG;     // one K-step B tile: this CTA's rows x 8 tf32
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -191,15 +203,24 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     uint64_t* tfull = empty + 8;
     uint64_t* tempty = tfull + 8;
     uint64_t* pready = tempty + 8;  // [16]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pready + 16);
+    uint64_t* pfull = pready + 16;  // [8] CG = 2, rank 0: the peer's page of the stage landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + 8);
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0u;
 
     // B operand, K-major without swizzle, arranged on the host in shared-memory
     // order (per K-step QW/8 groups of two 8x16B core matrices): a straight
     // coalesced copy
+    // (CG = 2: this CTA's rows -- queries h QS + crank QH + j of unit h --
+    // are whole 8-row core-matrix groups of the host image, 256 B each)
     {
         const float4* src = reinterpret_cast<const float4*>(a.consts);
         float4* dst = reinterpret_cast<float4*>(btile);
-        for (int i = tid; i < WB * KSTEPS * BT_BYTES / 16; i += WIDE_THREADS) dst[i] = src[i];
+        constexpr int GRP = BT_BYTES / 256;  // 8-row groups per K-step in this CTA
+        for (int i = tid; i < WB * KSTEPS * BT_BYTES / 16; i += WIDE_THREADS) {
+            const int kk = i / (BT_BYTES / 16), g = (i / 16) % GRP, e = i % 16;
+            const int gsrc = CG == 1 ? g : (g / (QH / 8)) * (QS / 8) + (int)crank * (QH / 8) + g % (QH / 8);
+            dst[i] = src[(size_t)kk * (QW * 2) + gsrc * 16 + e];
+        }
     }
     const float* cs = a.consts + WB * DP * QW;
     for (int i = tid; i < DP; i += WIDE_THREADS) ss[i] = cs[i];
@@ -238,10 +259,15 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                 hi = tf32_rna(B);
                 lo = tf32_rna(B - hi);
             }
-            // K-major core-matrix image (as the host builds the data K-steps)
-            float* bq = bbias + (q & 7) * 4 + (q >> 3) * 64;
-            *reinterpret_cast<float4*>(bq) = make_float4(hi, lo, 0.f, 0.f);
-            *reinterpret_cast<float4*>(bq + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+            // K-major core-matrix image (as the host builds the data K-steps),
+            // this CTA's rows only
+            const int jj = q % QS;
+            if (CG == 1 || jj / QH == (int)crank) {
+                const int lr = (q / QS) * QH + jj % QH;
+                float* bq = bbias + (lr & 7) * 4 + (lr >> 3) * 64;
+                *reinterpret_cast<float4*>(bq) = make_float4(hi, lo, 0.f, 0.f);
+                *reinterpret_cast<float4*>(bq + 32) = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
             const float beff = hi + lo;
             sB[q] = B;
             // |D| <= P + cc_q: the margins below cover the accumulator's
@@ -272,27 +298,43 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         }
         for (int s = 0; s < ntm; ++s) {
             bar_init(&tfull[s], 1);
-            bar_init(&tempty[s], 4);  // the four epilogue warps of the unit's group
+            // the four epilogue warps of the unit's group (CG = 2: in both CTAs;
+            // only rank 0's barrier is used)
+            bar_init(&tempty[s], 4 * CG);
         }
         for (int p = 0; p < PR; ++p) bar_init(&pready[p], 2);
+        for (int s = 0; s < nst; ++s) bar_init(&pfull[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (warp == W_MMA) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         su32(tmem_slot)),
-                     "r"(a.tcols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             su32(tmem_slot)),
+                         "r"(a.tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             su32(tmem_slot)),
+                         "r"(a.tcols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
+    // the peer's barriers are initialised before any remote arrival
+    if (CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
     const uint32_t units = a.mode == 0 ? a.spages + a.nhot : a.npages;
     const bool bias_on = sM[2] != 0.f;  // B folded into the accumulator (stream mode)
     const uint32_t G = gridDim.x, r0 = blockIdx.x;
-    const uint32_t mine = r0 < units ? (units - 1 - r0) / G + 1 : 0;
+    const uint32_t mine_self = r0 < units ? (units - 1 - r0) / G + 1 : 0;
+    // CG = 2: both CTAs of a pair run rank 0's page count (rank 1's extra
+    // iterations are empty pages: no copy, every record invalid)
+    const uint32_t rb = r0 & ~1u;
+    const uint32_t mine = CG == 1 ? mine_self : (rb < units ? (units - 1 - rb) / G + 1 : 0);
     auto page_of = [&](uint32_t it) -> uint32_t {
         const uint32_t u = r0 + it * G;
         if (a.mode != 0) return u;
@@ -301,6 +343,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         return h < a.npages ? h : 0u;  // an empty slot reads page 0, all its records invalid
     };
     auto empty_unit = [&](uint32_t it) -> bool {
+        if (it >= mine_self) return true;
         const uint32_t u = r0 + it * G;
         return a.mode == 0 && u >= a.spages && a.hot[u - a.spages] >= a.npages;
     };
@@ -312,6 +355,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                 const uint32_t s = it % nst, ph = (it / nst) & 1u;
                 if (it >= (uint32_t)nst) bar_wait(&empty[s], ph ^ 1u);
                 trace_ev(a, it, 0);  // producer: stage free, copy issued
+                if (it >= mine_self) {
+                    bar_arrive(&full[s]);  // CG = 2: an empty page of rank 1
+                    continue;
+                }
                 bar_expect_tx(&full[s], PAGE_BYTES);
                 bulk_g2s(stage + (size_t)s * PAGE_BYTES, a.pages + (size_t)page_of(it) * DP * PAGE,
                          PAGE_BYTES, &full[s]);
@@ -319,21 +366,25 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
         }
     } else if (warp == W_MMA) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            // D f32, A/B tf32, A MN-major, B K-major, N = QS, M = 128
+        if (lane == 0 && crank == 0) {
+            // D f32, A/B tf32, A MN-major, B K-major, N = QS, M = 128 CG
             constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
-                                       ((uint32_t)(QS >> 3) << 17) | ((128u >> 4) << 24);
+                                       ((uint32_t)(QS >> 3) << 17) | ((uint32_t)(128 * CG >> 4) << 24);
             const uint32_t bbase = su32(btile);
             for (uint32_t it = 0; it < mine; ++it) {
                 const uint32_t s = it % nst, ph = (it / nst) & 1u;
                 bar_wait(&full[s], ph);
+                if (CG == 2) bar_wait_cluster(&pfull[s], ph);  // and the peer's page
                 trace_ev(a, it, 1);  // MMA: page landed
                 const uint32_t abase = su32(stage + (size_t)s * PAGE_BYTES);
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     const uint32_t u = it * NH + h;  // unit: (page it, sub-group h)
                     const uint32_t ts = u % ntm, tph = (u / ntm) & 1u;
-                    if (u >= (uint32_t)ntm) bar_wait(&tempty[ts], tph ^ 1u);
+                    if (u >= (uint32_t)ntm) {
+                        if (CG == 1) bar_wait(&tempty[ts], tph ^ 1u);
+                        else bar_wait_cluster(&tempty[ts], tph ^ 1u);
+                    }
                     trace_ev(a, it, 2 + h);  // MMA: TMEM stage of unit (it, h) free
                     tc_fence_after();
                     const uint32_t dcol = tmem + (uint32_t)(ts * QS);
@@ -342,21 +393,28 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
                         const uint64_t ad = umma_desc(abase + ks * 1024, BOX_BYTES, 512, 1);
 #pragma unroll
                         for (int w = 0; w < WB; ++w) {
-                            // sub-group h: rows [h QS, h QS + QS) of the K-step's B tile
+                            // sub-group h: this CTA's rows [h QH, h QH + QH) of the K-step's B tile
                             const uint64_t bd = umma_desc(
-                                bbase + (w * KSTEPS + ks) * BT_BYTES + h * QS * 32, 128, 256, 0);
-                            if (a.probe != 2) umma_tf32(dcol, ad, bd, IDESC, ks > 0 || w > 0 ? 1u : 0u);
+                                bbase + (w * KSTEPS + ks) * BT_BYTES + h * QH * 32, 128, 256, 0);
+                            if (a.probe != 2) {
+                                if (CG == 1) umma_tf32(dcol, ad, bd, IDESC, ks > 0 || w > 0 ? 1u : 0u);
+                                else umma_tf32_pair(dcol, ad, bd, IDESC, ks > 0 || w > 0 ? 1u : 0u);
+                            }
                         }
                     }
                     if (bias_on && a.probe != 2) {
                         // D += 1 * (hi_q + lo_q): the pre-test constant, in the accumulator
                         const uint64_t ad = umma_desc(su32(aconst), 1024, 512, 1);
-                        const uint64_t bd = umma_desc(su32(bbias) + h * QS * 32, 128, 256, 0);
-                        umma_tf32(dcol, ad, bd, IDESC, 1u);
+                        const uint64_t bd = umma_desc(su32(bbias) + h * QH * 32, 128, 256, 0);
+                        if (CG == 1) umma_tf32(dcol, ad, bd, IDESC, 1u);
+                        else umma_tf32_pair(dcol, ad, bd, IDESC, 1u);
                     }
-                    umma_commit(&tfull[ts]);
+                    if (CG == 1) umma_commit(&tfull[ts]);
+                    else umma_commit_pair(&tfull[ts]);
                 }
-                umma_commit(&empty[s]);  // the stage is free once these MMAs are done
+                // the stage is free once these MMAs are done (CG = 2: in both CTAs)
+                if (CG == 1) umma_commit(&empty[s]);
+                else umma_commit_pair(&empty[s]);
                 trace_ev(a, it, 4);  // MMA: page's MMAs issued
             }
         }
@@ -377,17 +435,27 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             const bool live = !empty_unit(it);
             const bool v0 = live && rec < a.n, v1 = live && rec + 1 < a.n;
             float2 P2, L2;  // P = ||y||^2 and the log residual of the two records
+            // CG = 2, rank 1: tell rank 0's MMA issuer that this page landed
+            auto relay = [&] {
+                if (CG == 2 && crank == 1 && half == 0 && lane == 0)
+                    bar_arrive_remote(peer_addr(&pfull[s], 0));
+            };
             if (a.pl_in) {
                 // computed by an earlier launch of this call (same statistics)
-                const float4 v = __ldg(reinterpret_cast<const float4*>(a.pl_in) + rec / 2);
-                P2 = make_float2(v.x, v.z);
-                L2 = make_float2(v.y, v.w);
+                P2 = L2 = make_float2(0.f, 0.f);
+                if (live) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(a.pl_in) + rec / 2);
+                    P2 = make_float2(v.x, v.z);
+                    L2 = make_float2(v.y, v.w);
+                }
                 bar_wait(&full[s], ph);
+                relay();
             } else {
                 float2 r2 = make_float2(0.f, 0.f);
                 if (v1) r2 = __ldg(reinterpret_cast<const float2*>(a.r32 + rec));
                 else if (v0) r2.x = __ldg(a.r32 + rec);
                 bar_wait(&full[s], ph);
+                relay();
                 const unsigned char* box = stage + (size_t)s * PAGE_BYTES + box_i * BOX_BYTES;
                 float2 Pa = make_float2(0.f, 0.f), Pb = Pa;
 #pragma unroll
@@ -568,7 +636,10 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) bar_arrive(&tempty[s]);
+            if (lane == 0) {
+                if (CG == 1) bar_arrive(&tempty[s]);
+                else bar_arrive_remote(peer_addr(&tempty[s], 0));  // rank 0's issuer waits
+            }
             if (quarter == 0) trace_ev(a, it, 9 + 3 * (u % NH));  // epilogue: unit done
         }
         if (a.mode == 1) {
@@ -597,30 +668,467 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    // CG = 2: rank 0's MMAs write both CTAs' TMEM; neither frees it before
+    // both are done
+    if (CG == 2) cluster_sync_all();
+    if (warp == W_MMA) {
+        tc_fence_after();
+        if (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tcols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tcols));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4 bf16: the 256-query stream pass on a bf16 copy of the pages.
+//
+// At 256 queries per page visit the TF32 pass is bound by its operand
+// traffic, not by arithmetic: per 128-record page 32 KB of HBM and, for the
+// MMAs, 128 KB of shared-memory operand reads, with the TMA's 32 KB writes
+// into the same shared memory -- the ring's stages sit landed-but-unread for
+// ~2000 cycles and only four fit (the 72 KB B tile), too few bytes in flight
+// for the HBM latency (traced, profiles/r02).  A bf16 copy (kind::f16,
+// K = 16 per MMA) halves every one of those: 16 KB pages, twice the MACs per
+// operand byte, and eight stages in the same shared memory.
+//
+// The filter stays exact by construction: the bf16 rounding of the records
+// (relative 2^-9 + 2^-11 of the stored TF32 value) and of the query operand
+// (2^-9) enter the certification bound exactly like the TF32 storage did
+// (DESIGN.md "Exactness"), with a 128-entry candidate pool (the measured gap
+// between the 32nd and the 128th key of a 16M-record store is ~0.03 log2
+// units against a bound of ~0.007).
+//
+// Layout: pages16 [page][128 rows][128 B], row = record, K-major with the
+// 128-byte swizzle (16-byte chunk c of row r at (c ^ (r % 8)) * 16), so a
+// K = 16 step is the same descriptor advanced by 32 bytes; the query tile is
+// the same layout with rows = queries.  The bias K-step (ones x hi/mid/lo of
+// B_q, three bf16 parts: 2^-27 |B_q|) uses unswizzled K-major tiles.
+// Roles, barriers and the epilogue are those of stream_wide_kernel.
+// ---------------------------------------------------------------------------
+constexpr float REL16 = 0x1.42p-9f;  // |bf16(t) - v| <= (2^-9 + 2^-11)(1 + 2^-7) |v|, t = tf32(v)
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ uint16_t bf16_rn(float v) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+
+// fp32 pages -> the bf16 copy, pages [p0, p1): one thread per (record, 8 dims)
+__global__ void pages16_kernel(const float* __restrict__ pages, uint32_t p0, uint32_t p1,
+                               uint4* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t total = (size_t)(p1 - p0) * PAGE * 8;
+    if (i >= total) return;
+    const uint32_t c = (uint32_t)(i & 7u);               // 8-dim chunk
+    const size_t rec = (size_t)p0 * PAGE + (i >> 3);     // record
+    const uint32_t r = (uint32_t)(rec % PAGE);
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int k = 8 * (int)c + 2 * j;
+        const uint16_t lo = bf16_rn(__ldg(pages + page_index(rec, k, 64)));
+        const uint16_t hi = bf16_rn(__ldg(pages + page_index(rec, k + 1, 64)));
+        w[j] = (uint32_t)lo | ((uint32_t)hi << 16);
+    }
+    out[(rec / PAGE) * (PAGE * 8) + r * 8 + (c ^ (r & 7u))] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int QW>
+__global__ void __launch_bounds__(WIDE_THREADS, 1)
+    stream_wide16_kernel(const __grid_constant__ WideArgs a) {
+    constexpr int DP = 64;
+    constexpr int NH = QW / 128, QS = 128;
+    constexpr int PAGE_BYTES = PAGE * DP * 2;  // 16 KB
+    constexpr int KSTEPS = DP / 16;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nst = a.nst, ntm = a.ntm, PR = a.nst + (a.ntm + NH - 1) / NH;
+    unsigned char* stage = smem;
+    unsigned char* btile = stage + (size_t)nst * PAGE_BYTES;  // [QW rows][128 B], swizzled
+    unsigned char* aconst = btile + QW * 128;                 // [128 rows][32 B] bias A
+    unsigned char* bbias = aconst + 128 * 32;                 // [QW rows][32 B] bias B
+    float* prec = reinterpret_cast<float*>(bbias + QW * 32);  // [PR][4][PAGE]
+    float* ss = prec + (size_t)PR * 4 * PAGE;
+    float* scc = ss + DP;
+    float* sthr = scc + QW;
+    float* sB = sthr + 2 * QW;
+    float* sM = sB + 2 * QW;
+    uint32_t* scnt = reinterpret_cast<uint32_t*>(sM + 4);
+    uint32_t* sdrop = scnt + 2 * QW;
+    uint32_t* whist = reinterpret_cast<uint32_t*>(stage);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sdrop + 2 * QW);
+    uint64_t* empty = full + 8;
+    uint64_t* tfull = empty + 8;
+    uint64_t* tempty = tfull + 8;
+    uint64_t* pready = tempty + 8;  // [16]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pready + 16);
+
+    // query tile (bf16, swizzled, built on the host) and constants
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.consts16);
+        uint4* dst = reinterpret_cast<uint4*>(btile);
+        for (int i = tid; i < QW * 128 / 16; i += WIDE_THREADS) dst[i] = src[i];
+    }
+    const float* cs = a.consts + DP * QW;  // after the TF32 image: s, cc, t0
+    for (int i = tid; i < DP; i += WIDE_THREADS) ss[i] = cs[i];
+    for (int i = tid; i < QW; i += WIDE_THREADS) scc[i] = cs[DP + i];
+    for (int i = tid; i < 2 * QW; i += WIDE_THREADS)
+        sthr[i] = (i < QW || a.knn) ? cs[DP + QW + i] : FLT_MAX;
+    for (int i = tid; i < 4 * QW; i += WIDE_THREADS) scnt[i] = 0;
+    // bias A: ones in dims 0-2 of every row (K-major, 8-row core groups of
+    // 2 x 128 B: row r at (r / 8) * 256 + (r % 8) * 16, dims 8-15 at +128)
+    for (int i = tid; i < 128 * 16; i += WIDE_THREADS) {
+        const int r = i >> 4, k = i & 15;
+        reinterpret_cast<uint16_t*>(aconst)[((r >> 3) * 256 + (r & 7) * 16 + (k >> 3) * 128 + (k & 7) * 2) / 2] =
+            k < 3 ? (uint16_t)0x3F80u : (uint16_t)0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        float mb[2] = {0.f, 0.f};
+        bool fin = true;
+        for (int q = lane; q < QW; q += 32) fin &= fabsf(sthr[q] / a.alpha + scc[q]) < 0x1p60f;
+        const bool bias = __all_sync(0xffffffffu, fin);
+        for (int q = lane; q < QW; q += 32) {
+            const float B = sthr[q] / a.alpha + scc[q];
+            float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+            if (bias) {
+                p0 = __bfloat162float(__float2bfloat16_rn(B));
+                p1 = __bfloat162float(__float2bfloat16_rn(B - p0));
+                p2 = __bfloat162float(__float2bfloat16_rn((B - p0) - p1));
+            }
+            uint16_t* row = reinterpret_cast<uint16_t*>(bbias + (q >> 3) * 256 + (q & 7) * 16);
+            row[0] = bf16_rn(p0);
+            row[1] = bf16_rn(p1);
+            row[2] = bf16_rn(p2);
+#pragma unroll
+            for (int k = 3; k < 8; ++k) row[k] = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) row[64 + k] = 0;  // dims 8-15 (+128 B)
+            const float beff = (p0 + p1) + p2;
+            sB[q] = B;
+            mb[0] = fmaxf(mb[0], fabsf(B) + scc[q]);
+            const float Bn = sthr[QW + q] + scc[q];
+            sB[QW + q] = Bn - beff;
+            mb[1] = fmaxf(mb[1], fabsf(Bn) + fabsf(Bn - beff) + fabsf(beff) + scc[q]);
+        }
+        if (lane == 0) sM[2] = bias ? 1.f : 0.f;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            mb[0] = fmaxf(mb[0], __shfl_xor_sync(0xffffffffu, mb[0], o));
+            mb[1] = fmaxf(mb[1], __shfl_xor_sync(0xffffffffu, mb[1], o));
+        }
+        if (lane == 0) {
+            sM[0] = mb[0];
+            sM[1] = mb[1];
+        }
+    }
+    if (tid == 0) {
+        for (int s = 0; s < nst; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 3);
+        }
+        for (int s = 0; s < ntm; ++s) {
+            bar_init(&tfull[s], 1);
+            bar_init(&tempty[s], 4);
+        }
+        for (int p = 0; p < PR; ++p) bar_init(&pready[p], 2);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == W_MMA) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         su32(tmem_slot)),
+                     "r"(a.tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const bool bias_on = sM[2] != 0.f;
+
+    const uint32_t G = gridDim.x, r0 = blockIdx.x;
+    const uint32_t mine = r0 < a.npages ? (a.npages - 1 - r0) / G + 1 : 0;
+    auto page_of = [&](uint32_t it) -> uint32_t { return r0 + it * G; };
+
+    if (warp == W_PROD) {
+        if (lane == 0) {
+            for (uint32_t it = 0; it < mine; ++it) {
+                const uint32_t s = it % nst, ph = (it / nst) & 1u;
+                if (it >= (uint32_t)nst) bar_wait(&empty[s], ph ^ 1u);
+                trace_ev(a, it, 0);
+                bar_expect_tx(&full[s], PAGE_BYTES);
+                bulk_g2s(stage + (size_t)s * PAGE_BYTES,
+                         a.pages16 + (size_t)page_of(it) * (PAGE_BYTES / 2), PAGE_BYTES, &full[s]);
+            }
+        }
+    } else if (warp == W_MMA) {
+        if (lane == 0) {
+            // D f32, A/B bf16, both K-major, N = 128, M = 128
+            constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) |
+                                       ((uint32_t)(QS >> 3) << 17) | ((128u >> 4) << 24);
+            const uint32_t bbase = su32(btile);
+            for (uint32_t it = 0; it < mine; ++it) {
+                const uint32_t s = it % nst, ph = (it / nst) & 1u;
+                bar_wait(&full[s], ph);
+                trace_ev(a, it, 1);
+                const uint32_t abase = su32(stage + (size_t)s * PAGE_BYTES);
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    const uint32_t u = it * NH + h;
+                    const uint32_t ts = u % ntm, tph = (u / ntm) & 1u;
+                    if (u >= (uint32_t)ntm) bar_wait(&tempty[ts], tph ^ 1u);
+                    trace_ev(a, it, 2 + h);
+                    tc_fence_after();
+                    const uint32_t dcol = tmem + (uint32_t)(ts * QS);
+#pragma unroll
+                    for (int ks = 0; ks < KSTEPS; ++ks) {
+                        // K-major, 128-byte swizzle: a K = 16 step is +32 B
+                        const uint64_t ad = umma_desc(abase + ks * 32, 16, 1024, 2);
+                        const uint64_t bd = umma_desc(bbase + h * QS * 128 + ks * 32, 16, 1024, 2);
+                        if (a.probe != 2) umma_bf16(dcol, ad, bd, IDESC, ks > 0 ? 1u : 0u);
+                    }
+                    if (bias_on && a.probe != 2) {
+                        const uint64_t ad = umma_desc(su32(aconst), 128, 256, 0);
+                        const uint64_t bd = umma_desc(su32(bbias) + h * QS * 32, 128, 256, 0);
+                        umma_bf16(dcol, ad, bd, IDESC, 1u);
+                    }
+                    umma_commit(&tfull[ts]);
+                }
+                umma_commit(&empty[s]);
+                trace_ev(a, it, 4);
+            }
+        }
+    } else if (warp >= W_REC) {
+        // record constants: a pair of warps per page (pairs alternate pages);
+        // thread t of the pair owns rows t and t + 64 (32 consecutive rows per
+        // warp: the swizzle spreads their 16-byte chunks over all banks)
+        const int w = warp - W_REC, half = w & 1;
+        const int ra = 32 * half + lane;
+        float pmax = 0.f;
+        for (uint32_t it = (uint32_t)(w >> 1); it < mine; it += 2) {
+            const uint32_t s = it % nst, ph = (it / nst) & 1u;
+            const uint32_t pbase = page_of(it) * PAGE;
+            float P[2], L[2];
+            bool v[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) v[e] = pbase + ra + 64 * e < a.n;
+            if (a.pl_in) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const float2 pl = __ldg(reinterpret_cast<const float2*>(a.pl_in) + pbase + ra + 64 * e);
+                    P[e] = pl.x;
+                    L[e] = pl.y;
+                }
+                bar_wait(&full[s], ph);
+            } else {
+                float r[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) r[e] = v[e] ? __ldg(a.r32 + pbase + ra + 64 * e) : 0.f;
+                bar_wait(&full[s], ph);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = ra + 64 * e;
+                    const unsigned char* rp = stage + (size_t)s * PAGE_BYTES + row * 128;
+                    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 q = *reinterpret_cast<const uint4*>(rp + ((c ^ (row & 7)) << 4));
+                        const float4 s0 = *reinterpret_cast<const float4*>(ss + 8 * c);
+                        const float4 s1 = *reinterpret_cast<const float4*>(ss + 8 * c + 4);
+                        const uint32_t wq[4] = {q.x, q.y, q.z, q.w};
+                        const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float2 x = make_float2(__uint_as_float(wq[j] << 16),
+                                                         __uint_as_float(wq[j] & 0xFFFF0000u));
+                            const float2 y = __fmul2_rn(x, make_float2(sv[2 * j], sv[2 * j + 1]));
+                            acc = __ffma2_rn(y, y, acc);
+                        }
+                    }
+                    P[e] = acc.x + acc.y;
+                    L[e] = log2f(fabsf(fmaf(r[e], a.c1, -a.c0)) + a.rdelta);
+                    if (a.pl_out && v[e])
+                        reinterpret_cast<float2*>(a.pl_out)[pbase + row] = make_float2(P[e], L[e]);
+                }
+            }
+            float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = ra + 64 * e;
+                if (v[e]) pmax = fmaxf(pmax, P[e]);
+                const float A = L[e] / a.alpha - P[e];
+                pr[row] = v[e] ? A + 0x1p-19f * (fabsf(A) + P[e] + sM[0]) : -INFINITY;
+                pr[PAGE + row] = v[e] ? -P[e] + 0x1p-19f * (2.f * P[e] + sM[1]) : -INFINITY;
+                pr[2 * PAGE + row] = P[e];
+                pr[3 * PAGE + row] = v[e] ? L[e] : -INFINITY;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                bar_arrive(&pready[it % PR]);
+                bar_arrive(&empty[s]);
+                trace_ev(a, it, 5 + half);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+        if (lane == 0) atomicMax(a.pmax, __float_as_uint(pmax));
+    } else {
+        // epilogue: as stream_wide_kernel's stream mode
+        const int par = warp >> 2, quarter = warp & 3;
+        const int rloc = quarter * 32 + lane;
+        for (uint32_t u = par; u < mine * NH; u += NEG) {
+            const uint32_t it = u / NH;
+            const int cbeg = (int)(u % NH) * QS, cend = cbeg + QS;
+            const uint32_t s = u % ntm, ph = (u / ntm) & 1u;
+            const uint32_t rec = page_of(it) * PAGE + rloc;
+            if (quarter == 0) trace_ev(a, it, 7 + 3 * (u % NH));
+            bar_wait(&pready[it % PR], (it / PR) & 1u);
+            const float* pr = prec + (size_t)(it % PR) * 4 * PAGE;
+            const float Asel = pr[rloc], Ann = pr[PAGE + rloc];
+            const float P = pr[2 * PAGE + rloc], lg = pr[3 * PAGE + rloc];
+            bar_wait(&tfull[s], ph);
+            if (quarter == 0) trace_ev(a, it, 8 + 3 * (u % NH));
+            tc_fence_after();
+            const uint32_t taddr =
+                tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(s * QS) - (uint32_t)cbeg;
+            if (a.probe == 0) {
+#pragma unroll 1
+                for (int c0 = cbeg; c0 < cend; c0 += 32) {
+                    float acc[32];
+                    tmem_ld32(taddr + c0, acc);
+                    float m0 = INFINITY, m1 = INFINITY;
+                    if (bias_on) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            m0 = fminf(m0, fminf(acc[j], acc[j + 1]));
+                            m1 = fminf(m1, fminf(acc[j + 2], acc[j + 3]));
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 b4 = *reinterpret_cast<const float4*>(sB + c0 + j);
+                            const float2 x = __fadd2_rn(make_float2(acc[j], acc[j + 1]),
+                                                        make_float2(b4.x, b4.y));
+                            const float2 y = __fadd2_rn(make_float2(acc[j + 2], acc[j + 3]),
+                                                        make_float2(b4.z, b4.w));
+                            m0 = fminf(m0, fminf(x.x, x.y));
+                            m1 = fminf(m1, fminf(y.x, y.y));
+                        }
+                    }
+                    bool hit = fminf(m0, m1) < Asel;
+                    if (a.knn) {
+                        m0 = m1 = INFINITY;
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 b4 = *reinterpret_cast<const float4*>(sB + QW + c0 + j);
+                            const float2 x = __fadd2_rn(make_float2(acc[j], acc[j + 1]),
+                                                        make_float2(b4.x, b4.y));
+                            const float2 y = __fadd2_rn(make_float2(acc[j + 2], acc[j + 3]),
+                                                        make_float2(b4.z, b4.w));
+                            m0 = fminf(m0, fminf(x.x, x.y));
+                            m1 = fminf(m1, fminf(y.x, y.y));
+                        }
+                        hit |= fminf(m0, m1) < Ann;
+                    }
+                    if (__any_sync(0xffffffffu, hit)) {
+                        uint32_t ms = 0, mn = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            ms |= acc[j] + (bias_on ? 0.f : sB[c0 + j]) < Asel ? 1u << j : 0u;
+                            if (a.knn) mn |= acc[j] + sB[QW + c0 + j] < Ann ? 1u << j : 0u;
+                        }
+                        uint32_t U = __reduce_or_sync(0xffffffffu, ms | mn);
+                        while (U) {
+                            const int j = __ffs(U) - 1;
+                            U &= U - 1;
+                            // D = D' - (p0 + p1 + p2), in the order the bias was split
+                            const float Bj = sB[c0 + j];
+                            float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+                            if (bias_on) {
+                                p0 = __bfloat162float(__float2bfloat16_rn(Bj));
+                                p1 = __bfloat162float(__float2bfloat16_rn(Bj - p0));
+                                p2 = __bfloat162float(__float2bfloat16_rn((Bj - p0) - p1));
+                            }
+                            const float vv = ((tmem_ld1(taddr + c0 + j) - p0) - p1) - p2;
+                            const float d2 = (P + scc[c0 + j]) + vv;
+                            const float key = fmaf(-d2, a.alpha, lg);
+                            if (((ms >> j) & 1u) && key > sthr[c0 + j])
+                                list_append(a, scnt, sdrop, 2 * QW, c0 + j, key, rec);
+                            if (((mn >> j) & 1u) && -d2 > sthr[QW + c0 + j])
+                                list_append(a, scnt, sdrop, 2 * QW, QW + c0 + j, -d2, rec);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&tempty[s]);
+            if (quarter == 0) trace_ev(a, it, 9 + 3 * (u % NH));
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(WE * 32) : "memory");
+        for (int L = warp; L < 2 * QW; L += WE) {
+            const int K = L < QW ? a.kp : a.kv;
+            if (K == 0) continue;
+            const size_t o = ((size_t)blockIdx.x * 2 * QW + L) * a.cap;
+            int c = (int)min(scnt[L], a.cap);
+            if (c > K) {
+                warp_keep_topk(a.lkey + o, a.lidx + o, c, K, whist + warp * 256, lane);
+                c = K;
+            }
+            const size_t oo = ((size_t)blockIdx.x * 2 * QW + L) * a.kout;
+            for (int j = lane; j < K; j += 32) {
+                const bool have = j < c;
+                a.okey[oo + j] = have ? a.lkey[o + j] : -INFINITY;
+                a.oidx[oo + j] = have ? a.lidx[o + j] : 0xFFFFFFFFu - (uint32_t)j;
+            }
+            if (lane == 0 && sdrop[L]) atomicMax(&a.dropped[L], sdrop[L]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
     if (warp == W_MMA) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tcols));
     }
 }
 
-// t0[L] <= the K-th largest of list L's S block maxima (S up to 4 * 8192):
-// one histogram over the ordinal range present; the lower edge of the bin
-// where the count from the top reaches K, lowered by a relative 1e-6.
-// Fewer than K non-empty maxima: no threshold (-FLT_MAX).
+// Start thresholds from the sample's S block maxima of list L (S up to 4 * 8192):
+// tsafe[L] <= the K-th largest (distinct records: <= the store's K-th key, so
+// at least K records pass), t0[L] = the J-th largest for selection lists
+// (J < K: an estimate -- ~J / f records of the store beat it, f the sampled
+// fraction -- that admits a few times m records instead of ~K / f).  Any
+// threshold is sound (the certification bound takes max(t0, K'-th kept
+// key)); a query whose pool then falls short of certifying gets one more
+// pass from tsafe.  One histogram over the ordinal range present; a bin's
+// lower edge, lowered by a relative 1e-6.  Fewer than K non-empty maxima: no
+// threshold (-FLT_MAX).
 __global__ void __launch_bounds__(1024)
-    wide_kth_kernel(const float* __restrict__ smax, uint32_t S, int QW, int kp, int knn,
-                    float* __restrict__ t0) {
+    wide_kth_kernel(const float* __restrict__ smax, uint32_t S, int QW, int kp, int knn, int jsel,
+                    float tmargin, float* __restrict__ t0, float* __restrict__ tsafe) {
     constexpr int NB = 2048;
     __shared__ uint32_t hist[NB];
-    __shared__ uint32_t sh_lo, sh_hi, sh_bin, sh_valid;
+    __shared__ uint32_t sh_lo, sh_hi, sh_bin[2], sh_valid;
     const int L = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
     const uint32_t K = (uint32_t)(L < QW ? kp : knn);
+    const uint32_t J = L < QW ? min((uint32_t)max(jsel, 1), K) : K;
     const float* v = smax + (size_t)L * S;
     for (int b = tid; b < NB; b += blockDim.x) hist[b] = 0;
     if (tid == 0) {
         sh_lo = 0xFFFFFFFFu;
         sh_hi = 0;
-        sh_bin = 0xFFFFFFFFu;
+        sh_bin[0] = sh_bin[1] = 0xFFFFFFFFu;
         sh_valid = 0;
     }
     __syncthreads();
@@ -646,7 +1154,7 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     if (K == 0 || sh_valid < K) {
-        if (tid == 0) t0[L] = -FLT_MAX;
+        if (tid == 0) t0[L] = tsafe[L] = -FLT_MAX;
         return;
     }
     const uint32_t blo = sh_lo, span = sh_hi - sh_lo;
@@ -656,7 +1164,8 @@ __global__ void __launch_bounds__(1024)
         if (o > (uint32_t)PAD_TOP) atomicAdd(&hist[(o - blo) >> sh], 1u);
     }
     __syncthreads();
-    if (tid < 32) {
+    if (tid < 64) {  // warp 0: the bin where the count from the top reaches K; warp 1: J
+        const uint32_t T = tid < 32 ? K : J;
         uint32_t sum = 0;
         for (int j = 0; j < NB / 32; ++j) sum += hist[NB - 1 - (lane * (NB / 32) + j)];
         uint32_t incl = sum;
@@ -665,14 +1174,14 @@ __global__ void __launch_bounds__(1024)
             if (lane >= d) incl += t;
         }
         const uint32_t excl = incl - sum;
-        const unsigned own = __ballot_sync(0xffffffffu, excl < K && K <= incl);
+        const unsigned own = __ballot_sync(0xffffffffu, excl < T && T <= incl);
         if (lane == __ffs(own) - 1) {
             uint32_t c = excl;
             for (int j = 0; j < NB / 32; ++j) {
                 const int b = NB - 1 - (lane * (NB / 32) + j);
                 c += hist[b];
-                if (c >= K) {
-                    sh_bin = (uint32_t)b;
+                if (c >= T) {
+                    sh_bin[tid >> 5] = (uint32_t)b;
                     break;
                 }
             }
@@ -680,8 +1189,12 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     if (tid == 0) {
-        const float e = ord2f(blo + (sh_bin << sh));
-        t0[L] = e - 1e-6f * (fabsf(e) + 1.f);
+        const float es = ord2f(blo + (sh_bin[0] << sh)), ea = ord2f(blo + (sh_bin[1] << sh));
+        // (tmargin: the stream pass's keys may round below the sample's,
+        // bf16 against TF32 records; only the pool's fill depends on it)
+        const float m = L < QW ? tmargin : 0.f;
+        tsafe[L] = es - 1e-6f * (fabsf(es) + 1.f) - m;
+        t0[L] = ea - 1e-6f * (fabsf(ea) + 1.f) - m;
     }
 }
 
@@ -704,12 +1217,24 @@ inline float tf32_rn(double v) {
     return f;
 }
 
+// host RN-even float -> bf16 (finite inputs)
+inline uint16_t bf16_host(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
 template <int DP, int QW>
 void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, const double* zgrp,
                    int nqg, float c1, float c0, float rdelta, float alpha, float* mk,
                    uint32_t* mi, float* mthr, unsigned int* pmax, std::vector<double>& cc_out,
                    const GroupIo& io) {
     const int d = s->d;
+    // the 256-query stream pass on the bf16 page copy
+    constexpr bool can16 = DP == 64 && QW == 256;
+    const bool use16 = can16 && pl.bf16;
+    const size_t n16 = use16 ? (size_t)DP * QW / 2 : 0;  // floats of the bf16 query tile
     const size_t nc = WB * (size_t)DP * QW + DP + QW + 2 * QW;
     float* hb = io.hstage;  // nc floats
     float* sv = hb + WB * (size_t)DP * QW;
@@ -731,6 +1256,11 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
                 // (k % 4) * 4 + (k / 4) * 128 bytes within K-step k / 8
                 const size_t off = (size_t)(k / 8) * QW * 8 + (q % 8) * 4 + (q / 8) * 64 +
                                    (k % 4) + ((k % 8) / 4) * 32;
+                // the bf16 pass's query tile: row q = the B-constants of query q
+                // (RN bf16), K-major with the 128-byte swizzle
+                if (use16)
+                    reinterpret_cast<uint16_t*>(hb + nc)[(size_t)q * 64 + (((k / 8) ^ (q % 8)) * 8) +
+                                                         (k % 8)] = bf16_host((float)bk);
                 if (WB == 1) {
                     hb[off] = tf32_rn(bk);
                 } else {
@@ -742,15 +1272,20 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
             ccv[q] = (float)cc;
             cc_out[q] = cc;
         }
-        if (io.t0_override) std::copy(io.t0_override, io.t0_override + L, hb + (nc - L));
+        if (io.t0_override) {
+            std::copy(io.t0_override, io.t0_override + L, hb + (nc - L));
+            std::copy(io.t0_override, io.t0_override + L, hb + nc + n16);
+        }
     }
     if (io.phase == 1) return;
     // device: consts | lists | counters
     const size_t S4 = 4 * ((size_t)pl.spages + (io.hot ? io.nhot : 0));
-    char* base = static_cast<char*>(s->b_mmab.get(nc * 4 + 256 + L * 8 + S4 * L * 4 + 256));
+    // consts | the bf16 query tile | safe start thresholds [2QW] | counters ...
+    const size_t nct = nc + n16 + L;
+    char* base = static_cast<char*>(s->b_mmab.get(nct * 4 + 256 + L * 8 + S4 * L * 4 + 256));
     float* dc = reinterpret_cast<float*>(base);
     float* dt0 = dc + WB * (size_t)DP * QW + DP + QW;  // the t0 slot of consts
-    uint32_t* dcnt = reinterpret_cast<uint32_t*>(base + ((nc * 4 + 255) & ~(size_t)255));
+    uint32_t* dcnt = reinterpret_cast<uint32_t*>(base + ((nct * 4 + 255) & ~(size_t)255));
     unsigned int* ddrop = dcnt + L;
     float* const dsmax = reinterpret_cast<float*>(ddrop + L);
     const size_t lent = (size_t)pl.grid * L * pl.cap;
@@ -766,6 +1301,12 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
         // a retry (start thresholds given, no sample pass) uploads them too
         SAIR_CUDA(cudaMemcpyAsync(dc, hb, (io.t0_override ? nc : nc - L) * sizeof(float),
                                   cudaMemcpyHostToDevice, s->st));
+        if (n16)
+            SAIR_CUDA(cudaMemcpyAsync(dc + nc, hb + nc, n16 * sizeof(float), cudaMemcpyHostToDevice,
+                                      s->st));
+        if (io.t0_override)  // (a retry's thresholds are its safe ones too)
+            SAIR_CUDA(cudaMemcpyAsync(dc + nc + n16, hb + nc + n16, L * sizeof(float),
+                                      cudaMemcpyHostToDevice, s->st));
         SAIR_CUDA(cudaMemsetAsync(dcnt, 0, 2 * L * sizeof(uint32_t), s->st));
     }
 
@@ -805,16 +1346,34 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
 
     a.tcols = 32;
     while (a.tcols < (uint32_t)(pl.ntm * std::min(QW, 128))) a.tcols <<= 1;
-    SAIR_CUDA(cudaFuncSetAttribute(stream_wide_kernel<DP, QW>,
+    SAIR_CUDA(cudaFuncSetAttribute(stream_wide_kernel<DP, QW, 1>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    // bf16 stream passes keep their own (P, lg) cache; the TF32 sample then
+    // fills the TF32 one for its pages (the same pages every group)
+    if (use16) a.pl_out = io.pl_out;
+    // the sample's keys (TF32 records) may exceed the bf16 pass's keys of the
+    // same records by their rounding difference: lower its start threshold by
+    // a typical (not worst-case) amount -- only the pool's fill depends on it
+    float tmargin = 0.f;
+    if (use16) {
+        double ccmax = 0.0;
+        for (int q = 0; q < QW; ++q) ccmax = std::max(ccmax, (double)hb[WB * (size_t)DP * QW + DP + q]);
+        tmargin = (float)(alpha * 0x1p-7 * std::sqrt(4.0 * d * ccmax));
+    }
     if (!io.t0_override) {
         // sample pass -> t0 (written into the consts the stream pass reads)
         a.mode = 0;
-        stream_wide_kernel<DP, QW><<<(int)std::min<uint32_t>(pl.spages + a.nhot, (uint32_t)pl.grid),
-                                     WIDE_THREADS, pl.smem, s->st>>>(a);
+        stream_wide_kernel<DP, QW, 1><<<(int)std::min<uint32_t>(pl.spages + a.nhot, (uint32_t)pl.grid),
+                                        WIDE_THREADS, pl.smem, s->st>>>(a);
         SAIR_LAUNCH("stream_wide_kernel(sample)");
-        wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(dsmax, (uint32_t)S4, QW, pl.kp,
-                                                                 pl.knn, dt0);
+        // the selection lists' start: ~aggr K' records of the store above it
+        // (an estimate from the sampled fraction; SAIR_WIDE_AGGR=0: the safe K'-th)
+        const double aggr = std::getenv("SAIR_WIDE_AGGR") ? std::atof(std::getenv("SAIR_WIDE_AGGR")) : 2.5;
+        const double frac = std::min(1.0, (double)(pl.spages + a.nhot) / (double)a.npages);
+        int jsel = pl.kp;
+        if (aggr > 0.0) jsel = std::max(4, std::min(pl.kp, (int)std::ceil(aggr * pl.kp * frac)));
+        wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(
+            dsmax, (uint32_t)S4, QW, pl.kp, pl.knn, jsel, tmargin, dt0, dc + nc + n16);
         SAIR_LAUNCH("wide_kth_kernel");
     }
     SAIR_CUDA(cudaEventRecord(io.e_mid, s->st));
@@ -824,7 +1383,41 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
         SAIR_CUDA(cudaMemsetAsync(dtrace, 0, 64 * 16 * 8, s->st));
         a.trace = dtrace;
     }
-    stream_wide_kernel<DP, QW><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
+    if (use16) {
+        // 256 queries per visit of the bf16 page copy (stream_wide16_kernel)
+        ensure_pages16(s);
+        constexpr auto kern16 = stream_wide16_kernel<can16 ? QW : 256>;
+        SAIR_CUDA(cudaFuncSetAttribute(kern16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pl.smem16));
+        WideArgs b = a;
+        b.nst = pl.nst16;
+        b.pages16 = static_cast<const uint16_t*>(s->b_pages16.p);
+        b.consts16 = dc + nc;
+        b.pl_in = io.pl16_in;
+        b.pl_out = io.pl16_out;
+        kern16<<<pl.grid, WIDE_THREADS, pl.smem16, s->st>>>(b);
+    } else if (QW == 256 && pl.cg == 2) {
+        // CTA pairs: clusters of two, rank 0 of each issuing the M = 256 MMAs
+        constexpr auto kern = stream_wide_kernel<DP, QW == 256 ? 256 : 128, 2>;
+        SAIR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)pl.smem2));
+        a.nst = pl.nst2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)pl.grid);
+        cfg.blockDim = dim3(WIDE_THREADS);
+        cfg.dynamicSmemBytes = pl.smem2;
+        cfg.stream = s->st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SAIR_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    } else {
+        stream_wide_kernel<DP, QW, 1><<<pl.grid, WIDE_THREADS, pl.smem, s->st>>>(a);
+    }
     SAIR_LAUNCH("stream_wide_kernel(stream)");
     if (dtrace) {  // diagnostics: per-page event clocks of CTA 0, relative to the first
         std::vector<unsigned long long> h(64 * 16);
@@ -857,6 +1450,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
                 (double)ht[0]);
     }
     s->mma_t0 = dt0;
+    s->mma_t0safe = dc + nc + n16;
     s->mma_dropped = ddrop;
 }
 
@@ -903,12 +1497,21 @@ WideFn wide_pick_qw(int qw) {
     }
 }
 
-size_t wide_smem(int dp, int qw, int nst, int ntm) {
-    const int nh = qw > 128 ? qw / 128 : 1;
-    // + the bias K-step: its constant A tile (4 KB) and B tile (qw x 32 B)
-    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + 4096 + (WB * (size_t)(dp / 8) + 1) * qw * 32 +
-           (size_t)(nst + (ntm + nh - 1) / nh) * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 +
+// the bf16 pass (dp = 64): stages of 16 KB, the swizzled query tile, the bias tiles
+size_t wide16_smem(int qw, int nst, int ntm) {
+    const int nh = qw / 128;
+    return 1024 + (size_t)nst * PAGE * 128 + (size_t)qw * 128 + 128 * 32 + (size_t)qw * 32 +
+           (size_t)(nst + (ntm + nh - 1) / nh) * 4 * PAGE * 4 + 64 * 4 + qw * 4 + 4 * qw * 4 +
            16 + 4 * qw * 4 + 48 * 8 + 16;
+}
+
+size_t wide_smem(int dp, int qw, int nst, int ntm, int cg) {
+    const int nh = qw > 128 ? qw / 128 : 1;
+    // + the bias K-step: its constant A tile (4 KB) and B tile (qw x 32 B);
+    // a CTA pair (cg = 2) holds half of every B tile in each CTA
+    return 1024 + (size_t)nst * 4 * 32 * dp * 4 + 4096 + (WB * (size_t)(dp / 8) + 1) * qw * 32 / cg +
+           (size_t)(nst + (ntm + nh - 1) / nh) * 4 * PAGE * 4 + dp * 4 + qw * 4 + 4 * qw * 4 +
+           16 + 4 * qw * 4 + 56 * 8 + 16;
 }
 
 }  // namespace
@@ -966,7 +1569,26 @@ WideFn pick_wide(int dp, int qw) {
     }
 }
 
-double wide_bq_rel() { return WB == 1 ? 0x1p-10 * 1.01 : 0.0; }
+double wide_bq_rel(const WidePlan& pl) {
+    // |<x, b' - b>| <= rel |b| |x| with |b| = 2 sqrt(C): 2 x the operand's rounding
+    return pl.bf16 ? 0x1p-8 * 1.01 : (WB == 1 ? 0x1p-10 * 1.01 : 0.0);
+}
+double wide_rec_rel(const WidePlan& pl) { return pl.bf16 ? (double)REL16 : 0x1p-11; }
+
+void ensure_pages16(sair_store_s* s) {
+    const size_t npages = (s->n + PAGE - 1) / PAGE;
+    if (s->pages16_n > s->n) s->pages16_n = 0;
+    if (s->pages16_n == s->n || npages == 0) return;
+    void* before = s->b_pages16.p;
+    uint4* out = static_cast<uint4*>(s->b_pages16.get(npages * PAGE * 128));
+    if (out != before) s->pages16_n = 0;  // reallocated: convert everything
+    // from the page holding the first unconverted record (it may have grown)
+    const uint32_t p0 = (uint32_t)(s->pages16_n / PAGE), p1 = (uint32_t)npages;
+    const size_t threads = (size_t)(p1 - p0) * PAGE * 8;
+    pages16_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s->st>>>(s->pages, p0, p1, out);
+    SAIR_LAUNCH("pages16_kernel");
+    s->pages16_n = s->n;
+}
 
 bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, bool nn,
                     WidePlan* pl) {
@@ -979,7 +1601,16 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
     pl->qw = nq >= 256 && qmax >= 256 ? 256 : nq >= 128 && qmax >= 128 ? 128
              : (nq >= 64 && qmax >= 64 ? 64 : 32);
     pl->kp = 32;
-    const size_t want_pool = lambda != 0.0 ? 4 * m : 2 * m;
+    // 256-query passes over d <= 64 run on the bf16 page copy (SAIR_WIDE_BF16=0:
+    // the TF32 pass, for A/B); its looser filter gets a pool twice as deep
+    const char* b16e = std::getenv("SAIR_WIDE_BF16");
+    // (from 8M records: below, the deeper pool and sample cost more than the
+    // pass saves -- measured at 1M / 4M / 16M records, 256-query batches)
+    pl->bf16 = pl->qw == 256 && s->dp == 64 && !(b16e && std::atoi(b16e) == 0) &&
+                       (s->n >= ((size_t)8 << 20) || (b16e && std::atoi(b16e) == 1))
+                   ? 1
+                   : 0;
+    const size_t want_pool = (lambda != 0.0 ? 4 * m : 2 * m) * (pl->bf16 ? 2 : 1);
     while ((size_t)pl->kp < want_pool && pl->kp < 512) pl->kp <<= 1;
     pl->knn = nn ? 16 : 0;
     pl->kmax = std::max(pl->kp, pl->knn);
@@ -1006,12 +1637,36 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
     pl->ntm = std::min(8, 512 / std::min(pl->qw, 128));  // 128-column units for QW = 256
     // four page stages (a fifth measured 4 % slower at QW = 128)
     pl->nst = 4;
-    while (pl->nst > 2 && wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm) > limit) --pl->nst;
-    if (wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm) > limit) return false;
-    pl->smem = wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm);
+    while (pl->nst > 2 && wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm, 1) > limit) --pl->nst;
+    if (wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm, 1) > limit) return false;
+    pl->smem = wide_smem(pl->dp, pl->qw, pl->nst, pl->ntm, 1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
     pl->grid = (int)std::max<size_t>(1, std::min<size_t>(npages, (size_t)nsm));
+    if (pl->bf16) {
+        int n16 = std::getenv("SAIR_WIDE_NST16") ? std::atoi(std::getenv("SAIR_WIDE_NST16")) : 8;
+        n16 = std::max(2, std::min(8, n16));
+        while (n16 > 2 && wide16_smem(pl->qw, n16, pl->ntm) > limit) --n16;
+        pl->nst16 = n16;
+        pl->smem16 = wide16_smem(pl->qw, n16, pl->ntm);
+    }
+    // 256-query stream passes run on CTA pairs (an even grid): up to six page
+    // stages in the shared memory the halved B tile leaves (SAIR_WIDE_CG=1:
+    // single CTAs, for A/B)
+    pl->cg = 1;
+    pl->nst2 = pl->nst;
+    pl->smem2 = pl->smem;
+    const char* cge = std::getenv("SAIR_WIDE_CG");
+    if (pl->qw == 256 && pl->grid % 2 == 0 && !(cge && std::atoi(cge) == 1)) {
+        int n2 = std::getenv("SAIR_WIDE_NST2") ? std::atoi(std::getenv("SAIR_WIDE_NST2")) : 6;
+        n2 = std::max(2, std::min(8, n2));
+        while (n2 > 2 && wide_smem(pl->dp, pl->qw, n2, pl->ntm, 2) > limit) --n2;
+        if (wide_smem(pl->dp, pl->qw, n2, pl->ntm, 2) <= limit) {
+            pl->cg = 2;
+            pl->nst2 = n2;
+            pl->smem2 = wide_smem(pl->dp, pl->qw, n2, pl->ntm, 2);
+        }
+    }
     return true;
 }
 

@@ -177,8 +177,9 @@ void store_free(sair_store_s* s) {
     for (auto* b : {&s->b_stage, &s->b_cand, &s->b_merged, &s->b_thr, &s->b_z, &s->b_consts,
                     &s->b_out, &s->b_exact, &s->b_sigma, &s->b_red, &s->b_mmab, &s->b_sample,
                     &s->b_loo, &s->b_greedy, &s->b_grp,
-                    &s->b_wlists, &s->b_pl, &s->b_hot})
+                    &s->b_wlists, &s->b_pl, &s->b_hot, &s->b_pages16, &s->b_pl16})
         b->release();
+    s->pages16_n = 0;
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : s->gev) cudaEventDestroy(e);
