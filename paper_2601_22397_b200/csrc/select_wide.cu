@@ -1650,14 +1650,15 @@ bool make_wide_plan(const sair_store_s* s, size_t nq, size_t m, double lambda, b
         pl->nst16 = n16;
         pl->smem16 = wide16_smem(pl->qw, n16, pl->ntm);
     }
-    // 256-query stream passes run on CTA pairs (an even grid): up to six page
-    // stages in the shared memory the halved B tile leaves (SAIR_WIDE_CG=1:
-    // single CTAs, for A/B)
+    // SAIR_WIDE_CG=2: 256-query TF32 stream passes on CTA pairs (an even
+    // grid; up to six page stages in the shared memory the halved B tile
+    // leaves) -- measured 7 % slower than single CTAs at 16M records (the pair
+    // waits on the slower of its two pages), so not the default
     pl->cg = 1;
     pl->nst2 = pl->nst;
     pl->smem2 = pl->smem;
     const char* cge = std::getenv("SAIR_WIDE_CG");
-    if (pl->qw == 256 && pl->grid % 2 == 0 && !(cge && std::atoi(cge) == 1)) {
+    if (pl->qw == 256 && pl->grid % 2 == 0 && cge && std::atoi(cge) == 2) {
         int n2 = std::getenv("SAIR_WIDE_NST2") ? std::atoi(std::getenv("SAIR_WIDE_NST2")) : 6;
         n2 = std::max(2, std::min(8, n2));
         while (n2 > 2 && wide_smem(pl->dp, pl->qw, n2, pl->ntm, 2) > limit) --n2;
