@@ -606,6 +606,16 @@ def bench_pareto(dev):
         res[f"dominance_counts_K{K}"] = {"tuples": T, "s_e2e": round(dt, 4),
                                          "tuples_per_s": round(T / dt, 1),
                                          "frontier": int(mem.sum())}
+    # configs[2] at its stated size for 3 and 4 objectives: the pairwise K7
+    # kernel (dominance4_kernel), T^2/2 rank-vector comparisons
+    for K in (3, 4):
+        t = synth.tuples(SEED + 10 + K, PARETO_T, K, "uniform")
+        t0 = time.perf_counter()
+        cnt, mem = sair.dominance_counts(t)
+        dt = time.perf_counter() - t0
+        res[f"dominance_counts_K{K}_4M"] = {
+            "tuples": PARETO_T, "s_e2e": round(dt, 4), "tuples_per_s": round(PARETO_T / dt, 1),
+            "pairs_per_s": round(PARETO_T * (PARETO_T - 1) / 2 / dt, 1), "frontier": int(mem.sum())}
     return res
 
 

@@ -154,7 +154,9 @@ SAIR_API sair_status sair_store_standardize(sair_store_t h, const double* x, int
 SAIR_API sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double* out);
 
 /* similarity(a, b, sigma), experience.cpp:30-40: SAIR_EINVAL when the
- * lengths differ or sigma <= 0. */
+ * lengths differ or sigma <= 0.  Host arithmetic (two host vectors, O(d),
+ * bit-identical to the reference), like sair_store_standardize; the
+ * data-parallel veto scan is sair_store_nearest. */
 SAIR_API sair_status sair_similarity(const double* a, size_t len_a, const double* b, size_t len_b,
                                      double sigma, double* out);
 

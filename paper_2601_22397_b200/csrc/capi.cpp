@@ -1,5 +1,6 @@
 // capi.cpp -- the extern "C" boundary (include/sair.h).  Every entry point
 // translates C++ exceptions into sair_status codes + a thread-local message.
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <string>
@@ -196,7 +197,20 @@ sair_status sair_similarity(const double* a, size_t len_a, const double* b, size
     // experience.cpp:31-33: the dimension check, then the sigma check
     if (len_a != len_b) return bad("similarity: dimension mismatch");
     if (sigma <= 0.0) return bad("similarity: sigma must be positive");
-    return guard([&] { *out = sair::similarity(a, b, (int)len_a, sigma, 0); });
+    // Host arithmetic, like sair_store_standardize: an O(d) function of two
+    // host vectors (the reference's own scalar helper, called per stored
+    // record by the unmodified policy's veto loop, policy.cpp:146-153).  A
+    // device round trip per call would cost ~10 us against ~30 ns; the
+    // data-parallel veto scan is sair_store_nearest / the fused select.
+    // Same additions in the same order and glibc's exp: bit-identical.
+    return guard([&] {
+        double d2 = 0.0;
+        for (size_t i = 0; i < len_a; ++i) {
+            const double d = a[i] - b[i];
+            d2 += d * d;
+        }
+        *out = std::exp(-d2 / (2.0 * sigma * sigma));
+    });
 }
 
 sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, int dim,

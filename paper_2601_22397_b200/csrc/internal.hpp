@@ -247,7 +247,6 @@ void frontier_set_step(sair_frontier_set_s* s, const sair_reward_inputs* in, con
                        sair_reward_breakdown* out);
 size_t frontier_set_points(sair_frontier_set_s* s, size_t p, double* l, double* c, size_t cap,
                            double* hv);
-double similarity(const double* a, const double* b, int d, double sigma, int device);
 
 // select_greedy.cu: a shard's side of the distributed exact greedy
 void greedy_begin(sair_store_s* s, const double* q, size_t nq, int dim,

@@ -41,69 +41,167 @@ struct FrontierView {
     const double* c;
     size_t F;
     double hv;  // hypervolume of the view (reference sequence)
+    // K8 on frontiers too large for shared memory: li[j] = l[j S] (j < nli),
+    // a coarse index in shared memory that narrows each search to S entries
+    const double* li = nullptr;
+    uint32_t S = 1, nli = 0;
+    // K8 on bucketed tuples: frontier points [wbase, wbase + wlen) staged in
+    // shared memory (wl, wc); every other index reads l / c
+    const double* wl = nullptr;
+    const double* wc = nullptr;
+    uint32_t wbase = 0, wlen = 0;
 };
+// point i of the view (W: through the staged window where it covers i)
+template <bool W>
+__device__ __forceinline__ double at_l(const FrontierView& f, uint32_t i) {
+    return W && i - f.wbase < f.wlen ? f.wl[i - f.wbase] : f.l[i];
+}
+template <bool W>
+__device__ __forceinline__ double at_c(const FrontierView& f, uint32_t i) {
+    return W && i - f.wbase < f.wlen ? f.wc[i - f.wbase] : f.c[i];
+}
 
-// first index with l[i] > x
-__device__ __forceinline__ size_t upper_bound_l(const FrontierView& f, double x) {
-    size_t lo = 0, hi = f.F;
+// first index with l[i] > x (gt) / l[i] >= x (!gt), within [lo, hi)
+// (32-bit indices: a frontier holds < 2^32 points)
+template <bool GT>
+__device__ __forceinline__ uint32_t bound_l(const double* l, double x, uint32_t lo, uint32_t hi) {
     while (lo < hi) {
-        size_t mid = (lo + hi) >> 1;
-        if (f.l[mid] > x) hi = mid; else lo = mid + 1;
+        const uint32_t mid = (lo + hi) >> 1;
+        if (GT ? l[mid] > x : !(l[mid] < x)) hi = mid; else lo = mid + 1;
     }
     return lo;
 }
+template <bool GT>
+__device__ __forceinline__ uint32_t bound_lv(const FrontierView& f, double x) {
+    const uint32_t F = (uint32_t)f.F;
+    if (!f.li) return bound_l<GT>(f.l, x, 0, F);
+    // coarse: first index entry past x; the answer lies in ((j - 1) S, j S]
+    const uint32_t j = bound_l<GT>(f.li, x, 0, f.nli);
+    if (j == 0) return 0;
+    return bound_l<GT>(f.l, x, (j - 1) * f.S + 1, min(j * f.S, F));
+}
+// first index with l[i] > x
+__device__ __forceinline__ uint32_t upper_bound_l(const FrontierView& f, double x) {
+    return bound_lv<true>(f, x);
+}
 // first index with l[i] >= x
-__device__ __forceinline__ size_t lower_bound_l(const FrontierView& f, double x) {
-    size_t lo = 0, hi = f.F;
-    while (lo < hi) {
-        size_t mid = (lo + hi) >> 1;
-        if (f.l[mid] < x) lo = mid + 1; else hi = mid;
-    }
-    return lo;
+__device__ __forceinline__ uint32_t lower_bound_l(const FrontierView& f, double x) {
+    return bound_lv<false>(f, x);
 }
 
 // strictly_dominated, pareto.cpp:31-34: the candidate dominator is the point
 // with the largest latency <= pl (the cheapest among those, costs descend).
-__device__ bool f_dominated(const FrontierView& f, double pl, double pc) {
-    size_t u = upper_bound_l(f, pl);
+template <bool W = false>
+__device__ __forceinline__ bool f_dominated_u(const FrontierView& f, uint32_t u, double pl,
+                                              double pc) {
     if (u == 0) return false;
-    return dom2(f.l[u - 1], f.c[u - 1], pl, pc);
+    return dom2(at_l<W>(f, u - 1), at_c<W>(f, u - 1), pl, pc);
+}
+__device__ __forceinline__ bool f_dominated(const FrontierView& f, double pl, double pc) {
+    return f_dominated_u(f, upper_bound_l(f, pl), pl, pc);
 }
 
 // distance, pareto.cpp:75-84: min over points of dl^2 + dc^2, then sqrt.
-// Latencies are sorted, so scanning outwards from pl can stop once dl^2
-// alone reaches the best value; the minimum is the same value as the
-// reference's full scan.
-__device__ double f_distance(const FrontierView& f, double pl, double pc) {
+// Latencies ascend and costs descend along the frontier, so scanning outwards
+// from pl can stop once no further point can come closer: backwards when
+// dl^2 alone reaches the best value, or once c >= pc (from there both |dl|
+// and |dc| only grow); forwards (l > pl, and c < pc for a dominated p) as
+// soon as a point is no closer (both grow from there on).  The minimum is
+// the same value as the reference's full scan.
+template <bool W = false>
+__device__ __forceinline__ double f_distance_u(const FrontierView& f, uint32_t u, double pl,
+                                               double pc) {
     double best = INFINITY;
-    size_t u = upper_bound_l(f, pl);
-    for (size_t i = u; i-- > 0;) {
-        double dl = dsub(pl, f.l[i]);
-        double dl2 = dmul(dl, dl);
-        if (dl2 >= best) break;
-        double dc = dsub(pc, f.c[i]);
-        double v = dadd(dl2, dmul(dc, dc));
-        best = fmin(best, v);
+    const uint32_t F = (uint32_t)f.F;
+    if (F >= 256) {
+        // Blocks of 32 points: a block's box is [l_first, l_last] x [c_last,
+        // c_first] (l ascends, c descends), and the distance to it bounds every
+        // point inside from below -- in rounded arithmetic too, rounding being
+        // monotone -- so a block whose bound reaches `best` is skipped whole.
+        // Same exits as the point scan below; the same minimum.
+        auto box_lb = [&](uint32_t a, uint32_t b) {  // points a..b (a <= b)
+            const double l0 = at_l<W>(f, a), l1 = at_l<W>(f, b);
+            const double c0 = at_c<W>(f, a), c1 = at_c<W>(f, b);  // c0 >= c1
+            const double dx = pl < l0 ? dsub(l0, pl) : (pl > l1 ? dsub(pl, l1) : 0.0);
+            const double dy = pc < c1 ? dsub(c1, pc) : (pc > c0 ? dsub(pc, c0) : 0.0);
+            return dadd(dmul(dx, dx), dmul(dy, dy));
+        };
+        // backwards: blocks [s, e] with e from u - 1 down
+        for (uint32_t e = u; e > 0;) {
+            const uint32_t hi = e - 1, lo = hi >= 31 ? hi - 31 : 0;
+            e = lo;
+            {
+                const double dl = dsub(pl, at_l<W>(f, hi));
+                if (dmul(dl, dl) >= best) break;  // the block's nearest latency already too far
+            }
+            if (box_lb(lo, hi) >= best) continue;
+            bool stop = false;
+            for (uint32_t i = hi + 1; i-- > lo;) {
+                double dl = dsub(pl, at_l<W>(f, i));
+                double dl2 = dmul(dl, dl);
+                if (dl2 >= best) { stop = true; break; }
+                double dc = dsub(pc, at_c<W>(f, i));
+                double v = dadd(dl2, dmul(dc, dc));
+                best = fmin(best, v);
+                if (dc <= 0.0 && v >= best) { stop = true; break; }
+            }
+            if (stop) break;
+        }
+        for (uint32_t s0 = u; s0 < F;) {
+            const uint32_t lo = s0, hi = min(F - 1, s0 + 31);
+            s0 = hi + 1;
+            {
+                const double dl = dsub(pl, at_l<W>(f, lo));
+                if (dmul(dl, dl) >= best) break;
+            }
+            if (box_lb(lo, hi) >= best) continue;
+            bool stop = false;
+            for (uint32_t i = lo; i <= hi; ++i) {
+                double dl = dsub(pl, at_l<W>(f, i));
+                double dl2 = dmul(dl, dl);
+                if (dl2 >= best) { stop = true; break; }
+                double dc = dsub(pc, at_c<W>(f, i));
+                double v = dadd(dl2, dmul(dc, dc));
+                best = fmin(best, v);
+                if (dc >= 0.0 && v >= best) { stop = true; break; }
+            }
+            if (stop) break;
+        }
+        return sqrt(best);
     }
-    for (size_t i = u; i < f.F; ++i) {
-        double dl = dsub(pl, f.l[i]);
+    for (uint32_t i = u; i-- > 0;) {
+        double dl = dsub(pl, at_l<W>(f, i));
         double dl2 = dmul(dl, dl);
         if (dl2 >= best) break;
-        double dc = dsub(pc, f.c[i]);
+        double dc = dsub(pc, at_c<W>(f, i));
         double v = dadd(dl2, dmul(dc, dc));
         best = fmin(best, v);
+        if (dc <= 0.0 && v >= best) break;
+    }
+    for (uint32_t i = u; i < F; ++i) {
+        double dl = dsub(pl, at_l<W>(f, i));
+        double dl2 = dmul(dl, dl);
+        if (dl2 >= best) break;
+        double dc = dsub(pc, at_c<W>(f, i));
+        double v = dadd(dl2, dmul(dc, dc));
+        best = fmin(best, v);
+        if (dc >= 0.0 && v >= best) break;
     }
     return sqrt(best);
+}
+__device__ __forceinline__ double f_distance(const FrontierView& f, double pl, double pc) {
+    return f_distance_u(f, upper_bound_l(f, pl), pl, pc);
 }
 
 // contribution, pareto.cpp:67-73, for a non-dominated p.  For small frontiers
 // the reference's exact sequence is replayed (copy, insert, hypervolume of the
 // result minus hypervolume()), so the value is bit-identical; for large ones
 // the exclusive area is summed locally over p's dominated run.
-__device__ double f_contribution(const FrontierView& f, double pl, double pc) {
-    size_t a = lower_bound_l(f, pl);
-    if (a < f.F && f.l[a] == pl && f.c[a] == pc) return 0.0;  // duplicate: no-op insert
-    if (f.F <= 64) {
+template <bool W = false>
+__device__ double f_contribution_a(const FrontierView& f, uint32_t a, double pl, double pc) {
+    const uint32_t F = (uint32_t)f.F;
+    if (a < F && at_l<W>(f, a) == pl && at_c<W>(f, a) == pc) return 0.0;  // duplicate: no-op insert
+    if (F <= 64) {
         // hypervolume (pareto.cpp:56-65) of: survivors l < pl, p, survivors l > pl
         double hv = 0.0;
         bool placed = false;
@@ -115,8 +213,8 @@ __device__ double f_contribution(const FrontierView& f, double pl, double pc) {
             cur_c = c;
             have = true;
         };
-        for (size_t i = 0; i < f.F; ++i) {
-            double l = f.l[i], c = f.c[i];
+        for (uint32_t i = 0; i < F; ++i) {
+            double l = at_l<W>(f, i), c = at_c<W>(f, i);
             if (dom2(pl, pc, l, c)) continue;  // erased by insert_normalized
             if (!placed && !(l < pl)) {
                 emit(pl, pc);
@@ -129,22 +227,36 @@ __device__ double f_contribution(const FrontierView& f, double pl, double pc) {
         return dsub(hv, f.hv);
     }
     // exclusive area of [pl,1]x[pc,1] not covered by the frontier's boxes
-    double c_prev = a > 0 ? f.c[a - 1] : 1.0;
-    double l_next = a < f.F ? f.l[a] : 1.0;
+    double c_prev = a > 0 ? at_c<W>(f, a - 1) : 1.0;
+    double l_next = a < F ? at_l<W>(f, a) : 1.0;
     double area = dmul(dsub(l_next, pl), dsub(fmin(c_prev, 1.0), pc));
-    for (size_t j = a; j < f.F && f.c[j] >= pc; ++j) {
-        double ln = j + 1 < f.F ? f.l[j + 1] : 1.0;
-        area = dadd(area, dmul(dsub(ln, f.l[j]), dsub(f.c[j], pc)));
+    for (uint32_t j = a; j < F && at_c<W>(f, j) >= pc; ++j) {
+        double ln = j + 1 < F ? at_l<W>(f, j + 1) : 1.0;
+        area = dadd(area, dmul(dsub(ln, at_l<W>(f, j)), dsub(at_c<W>(f, j), pc)));
     }
     return area;
 }
+__device__ double f_contribution(const FrontierView& f, double pl, double pc) {
+    return f_contribution_a(f, lower_bound_l(f, pl), pl, pc);
+}
 
 // reward, pareto.cpp:86-89
-__device__ double f_reward(const FrontierView& f, double pl, double pc, bool* dominated) {
-    bool dm = f_dominated(f, pl, pc);
+// (u = upper_bound of pl: the one binary search every branch shares;
+// lower_bound differs only on points with l == pl, just before u)
+template <bool W = false>
+__device__ double f_reward_u(const FrontierView& f, uint32_t u, double pl, double pc,
+                             bool* dominated) {
+    bool dm = f_dominated_u<W>(f, u, pl, pc);
     if (dominated) *dominated = dm;
-    if (!dm) return dadd(1.0, f_contribution(f, pl, pc));
-    return ddiv(0.8, dadd(1.0, f_distance(f, pl, pc)));
+    if (!dm) {
+        uint32_t a = u;
+        while (a > 0 && !(at_l<W>(f, a - 1) < pl)) --a;
+        return dadd(1.0, f_contribution_a<W>(f, a, pl, pc));
+    }
+    return ddiv(0.8, dadd(1.0, f_distance_u<W>(f, u, pl, pc)));
+}
+__device__ double f_reward(const FrontierView& f, double pl, double pc, bool* dominated) {
+    return f_reward_u(f, upper_bound_l(f, pl), pl, pc, dominated);
 }
 
 // normalize, pareto.cpp:20-29
@@ -163,30 +275,166 @@ __device__ __forceinline__ void f_normalize(double l_max, double c_max, double l
 
 // ----------------------------------------------------------------- kernels --
 
-// K8: one tuple per thread; a frontier of up to SCORE_SMEM_F points is staged
-// in shared memory (every tuple's binary search and scans hit it), tuples are
-// read as one 16-byte load
-constexpr size_t SCORE_SMEM_F = 4096;
-__global__ void score_batch_kernel(FrontierView f, const double* __restrict__ pts, size_t T,
-                                   double* __restrict__ out, uint8_t* __restrict__ dom_out) {
-    extern __shared__ double fs[];  // [F] l | [F] c  (when staged)
-    FrontierView v = f;
-    if (f.F <= SCORE_SMEM_F) {
-        for (size_t i = threadIdx.x; i < f.F; i += blockDim.x) {
+// K8: one tuple per thread, tuples read as one 16-byte load.  The frontier
+// goes to shared memory as far as SCORE_SMEM_B allows (every tuple's binary
+// search and scans hit it): both coordinates (F <= 6144), the latencies only
+// (F <= 12288; costs from L2), or a coarse index of every S-th latency (each
+// search finishes within S entries in L2) -- an anti-correlated 4M-tuple set
+// has F ~ 17.6k, which used to fall back to global-memory searches entirely.
+constexpr size_t SCORE_SMEM_B = 96 * 1024;
+constexpr uint32_t SCORE_SMEM_F = SCORE_SMEM_B / 16;
+// larger frontiers: a coarse index of at most SCORE_IDX latencies (16 KB, so
+// four 512-thread blocks fit an SM: the searches' L2 latency needs the warps)
+constexpr uint32_t SCORE_IDX = 2048;
+__global__ void __launch_bounds__(512) score_batch_kernel(FrontierView f, const double* __restrict__ pts,
+                                                          size_t T, double* __restrict__ out,
+                                                          uint8_t* __restrict__ dom_out) {
+    extern __shared__ double fs[];
+    const double2* p2 = reinterpret_cast<const double2*>(pts);
+    // (each branch inlines its own loop, so the staged arrays are addressed as
+    // shared memory, not through generic loads)
+    auto run = [&](const FrontierView& v) {
+        for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < T;
+             t += (size_t)gridDim.x * blockDim.x) {
+            const double2 q = p2[t];
+            bool dm;
+            out[t] = f_reward(v, q.x, q.y, &dm);
+            if (dom_out) dom_out[t] = dm;
+        }
+    };
+    const uint32_t F = (uint32_t)f.F;
+    if (F <= SCORE_SMEM_F) {  // [F] l | [F] c
+        for (uint32_t i = threadIdx.x; i < F; i += blockDim.x) {
             fs[i] = f.l[i];
-            fs[f.F + i] = f.c[i];
+            fs[F + i] = f.c[i];
         }
         __syncthreads();
+        FrontierView v = f;
         v.l = fs;
-        v.c = fs + f.F;
+        v.c = fs + F;
+        run(v);
+    } else {  // [nli] every S-th l (S = 1: all of them), costs and the fine search from L2
+        FrontierView v = f;
+        v.S = (F + SCORE_IDX - 1) / SCORE_IDX;
+        v.nli = (F + v.S - 1) / v.S;
+        for (uint32_t j = threadIdx.x; j < v.nli; j += blockDim.x) fs[j] = f.l[(size_t)j * v.S];
+        __syncthreads();
+        v.li = fs;
+        run(v);
     }
+}
+
+// K8 on frontiers beyond shared memory (anti-correlated sets: F ~ 17.6k at
+// 4M tuples): the tuples are bucketed by their position on the frontier
+// (upper_bound of the latency, SCORE_NB buckets over the frontier's indices),
+// so a block's tuples need only a window of the frontier -- their positions
+// plus the scans' reach -- which it stages in shared memory; a scan that
+// leaves the window reads L2.  Results go back to the tuples' own slots.
+constexpr int SCORE_WIN = 6144;  // staged points per block (96 KB)
+constexpr int SCORE_CH = 1024;   // sorted tuples per block
+
+__global__ void __launch_bounds__(512) score_bucket_kernel(FrontierView f, const double* __restrict__ pts,
+                                                           size_t T, uint32_t NB, uint32_t* __restrict__ upos,
+                                                           uint32_t* __restrict__ hist) {
+    extern __shared__ double fs[];
+    uint32_t* sh = reinterpret_cast<uint32_t*>(fs + SCORE_IDX);
+    const uint32_t F = (uint32_t)f.F;
+    FrontierView v = f;
+    v.S = (F + SCORE_IDX - 1) / SCORE_IDX;
+    v.nli = (F + v.S - 1) / v.S;
+    for (uint32_t j = threadIdx.x; j < v.nli; j += blockDim.x) fs[j] = f.l[(size_t)j * v.S];
+    for (uint32_t b = threadIdx.x; b < NB; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    v.li = fs;
     const double2* p2 = reinterpret_cast<const double2*>(pts);
     for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < T;
          t += (size_t)gridDim.x * blockDim.x) {
-        const double2 q = p2[t];
-        bool dm;
-        out[t] = f_reward(v, q.x, q.y, &dm);
-        if (dom_out) dom_out[t] = dm;
+        const uint32_t u = upper_bound_l(v, p2[t].x);
+        upos[t] = u;
+        atomicAdd(&sh[(uint32_t)((uint64_t)u * NB / (F + 1))], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < NB; b += blockDim.x)
+        if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+// one block per SCATTER_CH tuples: counts per bucket in shared memory, one
+// global reservation per (block, bucket), then the scatter
+constexpr int SCATTER_CH = 8192;
+__global__ void __launch_bounds__(512) score_scatter_kernel(const double* __restrict__ pts,
+                                                            const uint32_t* __restrict__ upos, size_t T,
+                                                            uint32_t F, uint32_t NB,
+                                                            uint32_t* __restrict__ cursor,
+                                                            double2* __restrict__ spts,
+                                                            uint32_t* __restrict__ su,
+                                                            uint32_t* __restrict__ sidx) {
+    extern __shared__ uint32_t scnt[];  // [NB] counts, then bases
+    const double2* p2 = reinterpret_cast<const double2*>(pts);
+    const size_t t0 = (size_t)blockIdx.x * SCATTER_CH, t1 = min(t0 + SCATTER_CH, T);
+    for (uint32_t b = threadIdx.x; b < NB; b += blockDim.x) scnt[b] = 0;
+    __syncthreads();
+    for (size_t t = t0 + threadIdx.x; t < t1; t += blockDim.x)
+        atomicAdd(&scnt[(uint32_t)((uint64_t)upos[t] * NB / (F + 1))], 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < NB; b += blockDim.x)
+        if (scnt[b]) scnt[b] = atomicAdd(&cursor[b], scnt[b]);
+    __syncthreads();
+    for (size_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        const uint32_t u = upos[t];
+        const uint32_t pos = atomicAdd(&scnt[(uint32_t)((uint64_t)u * NB / (F + 1))], 1u);
+        spts[pos] = p2[t];
+        su[pos] = u;
+        sidx[pos] = (uint32_t)t;
+    }
+}
+
+__global__ void __launch_bounds__(512) score_window_kernel(FrontierView f, const double2* __restrict__ spts,
+                                                           const uint32_t* __restrict__ su,
+                                                           const uint32_t* __restrict__ sidx, size_t T,
+                                                           double* __restrict__ out,
+                                                           uint8_t* __restrict__ dom_out) {
+    extern __shared__ double fs[];  // [SCORE_WIN] l | [SCORE_WIN] c
+    __shared__ uint32_t s_lo, s_hi;
+    const uint32_t F = (uint32_t)f.F;
+    for (size_t c0 = (size_t)blockIdx.x * SCORE_CH; c0 < T; c0 += (size_t)gridDim.x * SCORE_CH) {
+        const size_t c1 = min(c0 + SCORE_CH, T);
+        if (threadIdx.x == 0) {
+            s_lo = 0xFFFFFFFFu;
+            s_hi = 0;
+        }
+        __syncthreads();
+        uint32_t lo = 0xFFFFFFFFu, hi = 0;
+        for (size_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+            lo = min(lo, su[p]);
+            hi = max(hi, su[p]);
+        }
+        atomicMin(&s_lo, lo);
+        atomicMax(&s_hi, hi);
+        __syncthreads();
+        // the window: the chunk's positions with a margin each side for the scans
+        const uint32_t span = s_hi - s_lo + 1;
+        const uint32_t margin = span >= SCORE_WIN ? 0 : (SCORE_WIN - span) / 2;
+        const uint32_t wb = s_lo > margin ? s_lo - margin : 0;
+        const uint32_t we = min(F, wb + SCORE_WIN);
+        FrontierView v = f;
+        v.wl = fs;
+        v.wc = fs + SCORE_WIN;
+        v.wbase = wb;
+        v.wlen = we - wb;
+        for (uint32_t i = threadIdx.x; i < v.wlen; i += blockDim.x) {
+            fs[i] = f.l[wb + i];
+            fs[SCORE_WIN + i] = f.c[wb + i];
+        }
+        __syncthreads();
+        for (size_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+            const double2 q = spts[p];
+            bool dm;
+            const double r = f_reward_u<true>(v, su[p], q.x, q.y, &dm);
+            const uint32_t t = sidx[p];
+            out[t] = r;
+            if (dom_out) dom_out[t] = dm;
+        }
+        __syncthreads();
     }
 }
 
@@ -452,6 +700,96 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+
+// K <= 4: the same counts with a leaner inner loop.  A j-tile is staged as
+// one 16-byte word per tuple (its ranks, padded with 0), so each (i, j) pair
+// is one broadcast LDS.128 and K unsigned compares folded into one predicate.
+// Tuples are sorted by rank sum: every j before the first position whose sum
+// reaches the tile's smallest sum has a strictly smaller sum than every i of
+// the tile, so there dominance is just `all(r_j <= r_i)` (equal vectors have
+// equal sums); only the j with sums in the tile's own range -- a handful --
+// take the exact test with the duplicate rule (pareto.cpp:43-54 keeps the
+// first of equal points).  A warp vote ends the scan early when only
+// frontier membership is wanted.
+template <int K>
+__global__ void __launch_bounds__(256)
+    dominance4_kernel(const uint32_t* __restrict__ sr, const uint32_t* __restrict__ ssum,
+                      const uint32_t* __restrict__ perm, size_t T, size_t i_begin, int members_only,
+                      uint32_t* __restrict__ counts, uint8_t* __restrict__ member) {
+    static_assert(K >= 1 && K <= 4, "packed ranks: K <= 4");
+    constexpr int TILE = 256;
+    __shared__ uint4 tj[TILE];
+    __shared__ uint32_t tsum[TILE], tp[TILE];
+    const size_t i0 = i_begin + (size_t)blockIdx.x * TILE;
+    const size_t i = i0 + threadIdx.x;
+    const bool valid = i < T;
+    uint32_t rr[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < K; ++k) rr[k] = valid ? sr[i * K + k] : 0xFFFFFFFFu;
+    const uint4 ri = make_uint4(rr[0], rr[1], rr[2], rr[3]);
+    const uint32_t pi = valid ? perm[i] : 0xFFFFFFFFu;
+    const uint32_t sumi = valid ? ssum[i] : 0xFFFFFFFFu;
+    const size_t ilast = min(i0 + TILE, T) - 1;
+    const uint32_t smax = ssum[ilast], smin = ssum[i0];
+    auto first_above = [&](uint32_t v, size_t lo) {  // first index with ssum > v
+        size_t hi = T;
+        while (lo < hi) {
+            const size_t mid = (lo + hi) >> 1;
+            if (ssum[mid] > v) hi = mid; else lo = mid + 1;
+        }
+        return lo;
+    };
+    const size_t jend = first_above(smax, ilast);
+    // first index with ssum >= smin (= first_above(smin - 1)): before it, sums are < every sum_i
+    const size_t jsame = smin == 0 ? 0 : min(first_above(smin - 1, 0), jend);
+    uint32_t cnt = 0;
+    bool dup = false;
+    for (size_t j0 = 0; j0 < jend; j0 += TILE) {
+        __syncthreads();
+        {
+            const size_t j = j0 + threadIdx.x;
+            uint32_t v[4] = {0u, 0u, 0u, 0u};
+            if (j < jend) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) v[k] = sr[j * K + k];
+            } else {
+                v[0] = 0xFFFFFFFFu;  // never <= a valid rank vector ... (ranks < T)
+            }
+            tj[threadIdx.x] = make_uint4(v[0], v[1], v[2], v[3]);
+            tsum[threadIdx.x] = j < jend ? ssum[j] : 0xFFFFFFFFu;
+            tp[threadIdx.x] = j < jend ? perm[j] : 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        const int lim = (int)min((size_t)TILE, jend - j0);
+        // [0, lim_strict): sums strictly below the whole i-tile
+        const int lim_strict = j0 >= jsame ? 0 : (int)min((size_t)lim, jsame - j0);
+        int t = 0;
+#pragma unroll 8
+        for (; t < lim_strict; ++t) {
+            const uint4 v = tj[t];
+            bool le = v.x <= ri.x;
+            if (K > 1) le &= v.y <= ri.y;
+            if (K > 2) le &= v.z <= ri.z;
+            if (K > 3) le &= v.w <= ri.w;
+            cnt += le ? 1u : 0u;
+        }
+        for (; t < lim; ++t) {
+            const uint4 v = tj[t];
+            bool le = v.x <= ri.x;
+            if (K > 1) le &= v.y <= ri.y;
+            if (K > 2) le &= v.z <= ri.z;
+            if (K > 3) le &= v.w <= ri.w;
+            const uint32_t sj = tsum[t];
+            cnt += (le && sj < sumi) ? 1u : 0u;
+            dup |= le && sj == sumi && tp[t] < pi;  // an equal vector seen earlier
+        }
+        if (members_only && __syncthreads_and(!valid || cnt > 0 || dup)) break;
+    }
+    if (valid) {
+        if (counts) counts[pi] = cnt;
+        if (member) member[pi] = (cnt == 0 && !dup) ? 1 : 0;
+    }
+}
 
 // ---- K7 for two objectives: O(T log T) counting ----------------------------
 //
@@ -809,11 +1147,16 @@ static int grid_for(size_t n, int threads = 256) {
 static FrontierView view(const sair_frontier_s* f) { return FrontierView{f->fl, f->fc, f->F, f->hv}; }
 
 static size_t score_smem(size_t F) {
-    if (F > SCORE_SMEM_F) return 0;
-    const size_t b = F * 16;
+    const size_t b = F <= SCORE_SMEM_F ? F * 16 : (size_t)SCORE_IDX * 8;
     if (b > 48 * 1024) cudaFuncSetAttribute(score_batch_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b);
     return b;
+}
+// K8 grid: persistent, several 512-thread blocks per SM (two at the largest
+// shared-memory footprint)
+static int score_grid(size_t T, size_t F) {
+    const int per_sm = score_smem(F) > 64 * 1024 ? 2 : 4;
+    return (int)std::max<size_t>(1, std::min<size_t>((T + 511) / 512, (size_t)148 * per_sm));
 }
 
 void frontier_init(sair_frontier_s* f, double l_max, double c_max, int device) {
@@ -1004,6 +1347,56 @@ double frontier_point_query(sair_frontier_s* f, double pl, double pc, int op, do
     return h[0];
 }
 
+// K8 launch: the frontier in shared memory when it fits, else bucketed tuples
+// against staged frontier windows (score_window_kernel)
+static void score_launch(sair_frontier_s* f, const double* dp, size_t T, double* dout,
+                         uint8_t* ddom, cudaStream_t st) {
+    if (f->F <= SCORE_SMEM_F || T < 65536) {
+        score_batch_kernel<<<score_grid(T, f->F), 512, score_smem(f->F), st>>>(view(f), dp, T, dout,
+                                                                             ddom);
+        SAIR_LAUNCH("score_batch_kernel");
+        return;
+    }
+    const uint32_t F = (uint32_t)f->F;
+    const uint32_t NB = std::min<uint32_t>(16384u, std::max<uint32_t>(64u, F / 32));
+    size_t off = 0;
+    auto take = [&](size_t b) { const size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
+    const size_t o_u = take(T * 4), o_su = take(T * 4), o_si = take(T * 4), o_sp = take(T * 16),
+                 o_h = take((size_t)NB * 4), o_c = take((size_t)NB * 4);
+    size_t scan_b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)NB);
+    const size_t o_t = take(scan_b);
+    char* b = static_cast<char*>(f->b_sort.get(off + 256));
+    uint32_t* upos = reinterpret_cast<uint32_t*>(b + o_u);
+    uint32_t* su = reinterpret_cast<uint32_t*>(b + o_su);
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(b + o_si);
+    double2* spts = reinterpret_cast<double2*>(b + o_sp);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(b + o_h);
+    uint32_t* cursor = reinterpret_cast<uint32_t*>(b + o_c);
+    SAIR_CUDA(cudaMemsetAsync(hist, 0, (size_t)NB * 4, st));
+    const size_t bsm = SCORE_IDX * 8 + (size_t)NB * 4;
+    if (bsm > 48 * 1024)
+        SAIR_CUDA(cudaFuncSetAttribute(score_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)bsm));
+    const int gb = (int)std::min<size_t>((T + 511) / 512, 148 * 2);
+    score_bucket_kernel<<<gb, 512, bsm, st>>>(view(f), dp, T, NB, upos, hist);
+    SAIR_LAUNCH("score_bucket_kernel");
+    size_t tb = scan_b;
+    SAIR_CUDA(cub::DeviceScan::ExclusiveSum(b + o_t, tb, hist, cursor, (int)NB, st));
+    if (NB * 4 > 48 * 1024)
+        SAIR_CUDA(cudaFuncSetAttribute(score_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(NB * 4)));
+    score_scatter_kernel<<<(int)((T + SCATTER_CH - 1) / SCATTER_CH), 512, NB * 4, st>>>(
+        dp, upos, T, F, NB, cursor, spts, su, sidx);
+    SAIR_LAUNCH("score_scatter_kernel");
+    const size_t wsm = (size_t)SCORE_WIN * 16;
+    SAIR_CUDA(cudaFuncSetAttribute(score_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)wsm));
+    const int gw = (int)std::min<size_t>((T + SCORE_CH - 1) / SCORE_CH, 148 * 2);
+    score_window_kernel<<<gw, 512, wsm, st>>>(view(f), spts, su, sidx, T, dout, ddom);
+    SAIR_LAUNCH("score_window_kernel");
+}
+
 void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, double* out,
                           uint8_t* dom) {
     if (T == 0) return;
@@ -1013,8 +1406,7 @@ void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
     double* dout = dp + 2 * T;
     uint8_t* ddom = reinterpret_cast<uint8_t*>(dout + T);
     SAIR_CUDA(cudaMemcpyAsync(dp, pts, T * 16, cudaMemcpyHostToDevice, f->st));
-    score_batch_kernel<<<grid_for(T), 256, score_smem(f->F), f->st>>>(view(f), dp, T, dout, ddom);
-    SAIR_LAUNCH("score_batch_kernel");
+    score_launch(f, dp, T, dout, ddom, f->st);
     SAIR_CUDA(cudaMemcpyAsync(out, dout, T * 8, cudaMemcpyDeviceToHost, f->st));
     if (dom) SAIR_CUDA(cudaMemcpyAsync(dom, ddom, T, cudaMemcpyDeviceToHost, f->st));
     SAIR_CUDA(cudaStreamSynchronize(f->st));
@@ -1023,8 +1415,7 @@ void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
 // device-pointer variant (bench: tuples resident in HBM)
 void frontier_score_batch_device(sair_frontier_s* f, const double* dpts, size_t T, double* dout,
                                  uint8_t* ddom, cudaStream_t st) {
-    score_batch_kernel<<<grid_for(T), 256, score_smem(f->F), st>>>(view(f), dpts, T, dout, ddom);
-    SAIR_LAUNCH("score_batch_kernel");
+    score_launch(f, dpts, T, dout, ddom, st);
 }
 
 void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_t* counts,
@@ -1142,7 +1533,9 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
     const size_t i_begin = t_lo * 256;
     if (blocks > 0) switch (K) {
 #define DK(KK) case KK: dominance_kernel<KK><<<blocks, 256, 0, st>>>(sranks, ssum, perm, T, i_begin, members_only, dcnt, dmem); break;
-        DK(1) DK(2) DK(3) DK(4) DK(5) DK(6) DK(7) DK(8)
+#define DK4(KK) case KK: dominance4_kernel<KK><<<blocks, 256, 0, st>>>(sranks, ssum, perm, T, i_begin, members_only, dcnt, dmem); break;
+        DK4(1) DK4(2) DK4(3) DK4(4) DK(5) DK(6) DK(7) DK(8)
+#undef DK4
 #undef DK
     }
     SAIR_LAUNCH("dominance_kernel");

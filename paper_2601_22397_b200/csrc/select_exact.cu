@@ -334,36 +334,4 @@ double store_surprisal(sair_store_s* s, size_t index, const double* x,
 
 }  // namespace sair
 
-namespace sair {
 
-// similarity(), experience.cpp:30-40, on two host vectors
-__global__ void similarity_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                                  int d, double two_s2, double* out) {
-    if (threadIdx.x || blockIdx.x) return;
-    double d2 = 0.0;
-    for (int k = 0; k < d; ++k) {
-        const double t = dsub(a[k], b[k]);
-        d2 = dadd(d2, dmul(t, t));
-    }
-    *out = sim_from_d2(d2, two_s2);
-}
-
-double similarity(const double* a, const double* b, int d, double sigma, int device) {
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-        throw Error(SAIR_ECUDA, "no CUDA device (libsair has no CPU fallback)");
-    DeviceGuard g(device);
-    DBuf buf;
-    double* dv = static_cast<double*>(buf.get((2 * (size_t)d + 1) * 8 + 64));
-    if (d) {
-        SAIR_CUDA(cudaMemcpy(dv, a, d * 8, cudaMemcpyHostToDevice));
-        SAIR_CUDA(cudaMemcpy(dv + d, b, d * 8, cudaMemcpyHostToDevice));
-    }
-    similarity_kernel<<<1, 32>>>(dv, dv + d, d, 2.0 * sigma * sigma, dv + 2 * d);
-    SAIR_LAUNCH("similarity_kernel");
-    double v = 0.0;
-    SAIR_CUDA(cudaMemcpy(&v, dv + 2 * d, 8, cudaMemcpyDeviceToHost));
-    return v;
-}
-
-}  // namespace sair

@@ -58,3 +58,28 @@ def test_status_codes_for_bad_arguments():
     assert L.sair_store_create(0.0, 0, 0, None) == _lib.SAIR_EINVAL
     assert L.sair_store_size(None, None) == _lib.SAIR_EINVAL
     assert L.sair_store_destroy(None) == _lib.SAIR_OK
+
+
+def test_similarity_is_the_references(ref):
+    """sair_similarity (host arithmetic, like standardize) is bit-identical to
+    the reference's similarity() (experience.cpp:30-40), including its errors."""
+    import numpy as np
+    L = _lib.lib()
+    rng = np.random.default_rng(5)
+    dp = C.POINTER(C.c_double)
+    for d in (1, 7, 37, 64, 300):
+        for _ in range(20):
+            a, b = rng.normal(size=d) * 50, rng.normal(size=d) * 50
+            sig = float(rng.uniform(0.5, 200))
+            got, want = C.c_double(), C.c_double()
+            assert L.sair_similarity(a.ctypes.data_as(dp), d, b.ctypes.data_as(dp), d, sig,
+                                     C.byref(got)) == _lib.SAIR_OK
+            assert ref.lib.ref_similarity(a.ctypes.data_as(dp), b.ctypes.data_as(dp), d, d, sig,
+                                          C.byref(want)) == 0
+            assert got.value == want.value
+    a = np.zeros(3)
+    out = C.c_double()
+    assert L.sair_similarity(a.ctypes.data_as(dp), 3, a.ctypes.data_as(dp), 2, 1.0,
+                             C.byref(out)) == _lib.SAIR_EINVAL
+    assert L.sair_similarity(a.ctypes.data_as(dp), 3, a.ctypes.data_as(dp), 3, 0.0,
+                             C.byref(out)) == _lib.SAIR_EINVAL

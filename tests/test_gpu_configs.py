@@ -196,3 +196,24 @@ def test_config2_k_objective_counts_vs_oracle(orc, K, dist):
     cnt, mem = sair.dominance_counts(t)
     ocnt, omem = orc.dominance_counts_mt(t, nthreads=THREADS)
     assert np.array_equal(cnt, ocnt) and np.array_equal(mem, omem)
+
+
+def test_config2_windowed_scoring_of_every_tuple(orc):
+    """K8 on a frontier beyond shared memory (anti-correlated 4M tuples, F ~
+    17.6k): the bucketed windowed path (T >= 64k) scores every tuple exactly
+    as the direct kernel does (chunks below 64k) and as the oracle (sample)."""
+    T = 4 * 1024 * 1024
+    pts = synth.tuples(2031, T, 2, "anti")
+    f = sair.ParetoFrontier(1.0, 1.0)
+    F = f.insert_batch(pts)
+    assert F > 6144
+    got, dom = f.score_batch(pts)
+    ref_r = np.empty(T)
+    ref_d = np.empty(T, bool)
+    for s in range(0, T, 60000):
+        r, d = f.score_batch(pts[s:s + 60000])
+        ref_r[s:s + 60000], ref_d[s:s + 60000] = r, d
+    assert np.array_equal(got, ref_r) and np.array_equal(dom, ref_d)
+    fl, fc = orc.frontier_sorted(pts)
+    probe = np.arange(0, T, 997)
+    assert near(got[probe], orc.pareto_reward_batch(fl, fc, pts[probe]))

@@ -1,0 +1,99 @@
+"""The wide pass's variants against the oracle (select_wide.cu, DESIGN.md
+"K4"): the bf16 page copy (stream_wide16_kernel; the default from 8M records,
+forced here on smaller stores), CTA pairs (SAIR_WIDE_CG=2), the guaranteed
+start thresholds (SAIR_WIDE_AGGR=0) and estimated ones tight enough that some
+pools fall short and take the retry.  Indices bit-exact, scores within 1e-12
+relative -- the same bar as test_gpu_wide.py."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2601_22397_b200 import ExperienceBuffer, SelectionConfig, synth  # noqa: E402
+
+
+class env:
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            os.environ[k] = str(v)
+
+    def __exit__(self, *a):
+        for k in self.kv:
+            os.environ.pop(k, None)
+
+
+def near(got, want, rel):
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    return np.all(np.abs(got - want) <= rel * np.maximum(1.0, np.abs(want)))
+
+
+@pytest.fixture(scope="module")
+def store():
+    n, d = 300000, 64
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(91, n, d)
+    return db, synth.contexts(91, 0, n, d), synth.rewards(91, 0, n), synth.rounds(0, n)
+
+
+@pytest.mark.parametrize("knobs,tc", [({"SAIR_WIDE_BF16": 1}, 3),
+                                      ({"SAIR_WIDE_BF16": 1, "SAIR_WIDE_AGGR": 0}, 3),
+                                      ({"SAIR_WIDE_BF16": 0, "SAIR_WIDE_CG": 2}, 2),
+                                      ({"SAIR_WIDE_BF16": 0, "SAIR_WIDE_AGGR": 0}, 2),
+                                      ({"SAIR_WIDE_BF16": 1, "SAIR_WIDE_AGGR": 0.3}, 3)])
+@pytest.mark.parametrize("lam", [0.0, 0.1])
+def test_wide_variant_matches_oracle(orc, store, knobs, tc, lam):
+    db, ctx, rew, rnd = store
+    sigma = db.effective_sigma()
+    xq = synth.queries(92, 256, 64)
+    m = 32 if lam == 0.0 else 8
+    with env(**knobs):
+        idx, sim, sc, cnt, nn_i, nn_s = db.select_batch(xq, SelectionConfig(m=m, lambda_div=lam),
+                                                        nearest=True)
+        st = db.last_stats()
+    assert st["tensor_core"] == tc, st
+    if lam == 0.0:
+        assert st["certified"] == 256 and st["exact_fallbacks"] == 0, st
+    pick = np.arange(0, 256, 16) if lam == 0.0 else np.arange(0, 256, 64)
+    oi, osim, osc, ocnt = orc.select_batch(ctx, rew, rnd, xq[pick], m, lam, sigma)
+    assert np.array_equal(cnt[pick], ocnt)
+    assert np.array_equal(idx[pick], oi)
+    assert near(sc[pick], osc, 1e-12) and near(sim[pick], osim, 1e-12)
+    for j, q in enumerate(pick[:4]):
+        oj, os_ = orc.nearest(ctx, xq[q], sigma)
+        assert nn_i[q] == oj and abs(nn_s[q] - os_) <= 1e-12
+
+
+def test_bf16_copy_follows_appends(orc):
+    """The bf16 page copy is derived lazily: appends after a call (partial last
+    page, then new pages) are converted before the next pass reads them."""
+    n0, d = 200000, 64
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(93, n0, d)
+    xq = synth.queries(94, 256, d)
+    with env(SAIR_WIDE_BF16=1):
+        db.select_batch(xq, SelectionConfig(m=16, lambda_div=0.0))
+        # rows far from the mean with extreme rewards: they must reach the pool
+        extra = synth.contexts(95, 0, 300, d) * 0.05 + xq[:1]
+        rew = np.full(300, 5.0)
+        db.store_many(extra[:100], rew[:100], np.arange(n0, n0 + 100))  # partial last page
+        db.select_batch(xq, SelectionConfig(m=16, lambda_div=0.0))
+        db.store_many(extra[100:], rew[100:], np.arange(n0 + 100, n0 + 300))
+        idx, sim, sc, cnt = db.select_batch(xq, SelectionConfig(m=16, lambda_div=0.0))
+        assert db.last_stats()["tensor_core"] == 3
+    ctx = np.concatenate([synth.contexts(93, 0, n0, d), extra])
+    rw = np.concatenate([synth.rewards(93, 0, n0), rew])
+    rd = np.concatenate([synth.rounds(0, n0), np.arange(n0, n0 + 300, dtype=np.int32)])
+    sigma = db.effective_sigma()
+    pick = np.array([0, 1, 100, 255])
+    oi, osim, osc, ocnt = orc.select_batch(ctx, rw, rd, xq[pick], 16, 0.0, sigma)
+    assert np.array_equal(idx[pick], oi)
+    assert near(sc[pick], osc, 1e-12)
