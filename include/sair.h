@@ -83,6 +83,8 @@ typedef struct {
                                TF32 pass; 3: the 256-query wide pass on the bf16 page copy */
     int small;              /* 1: the whole call ran as the one-launch exact small-store select */
     size_t retried;         /* queries given a second wide pass with raised thresholds */
+    size_t greedy32;        /* queries whose greedy ran fp32-filtered, fp64-decided (lambda != 0) */
+    size_t greedy32_candidates; /* (query, step) candidates verified in fp64 by that path */
 } sair_select_stats;
 
 SAIR_API const char* sair_last_error(void);

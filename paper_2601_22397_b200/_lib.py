@@ -36,7 +36,8 @@ class SelectStatsC(C.Structure):
                 ("exact_fallbacks", C.c_size_t), ("candidates", C.c_size_t), ("qb", C.c_int),
                 ("stream_launches", C.c_int), ("stream_ms", C.c_float), ("total_ms", C.c_float),
                 ("prepass_ms", C.c_float), ("tensor_core", C.c_int), ("small", C.c_int),
-                ("retried", C.c_size_t)]
+                ("retried", C.c_size_t), ("greedy32", C.c_size_t),
+                ("greedy32_candidates", C.c_size_t)]
 
 
 class RewardConfigC(C.Structure):

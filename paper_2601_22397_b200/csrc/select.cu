@@ -1388,10 +1388,23 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         for (size_t i = 0; i < nq; ++i)
             if (!done[i]) rest.push_back(i);
         if (!rest.empty()) {
-            greedy_select(s, p, rest, m, cfg.lambda_div, loo_pre, out_nn != nullptr, out_idx,
-                          out_sim, out_score, out_count, out_nn, out_nn_sim, out_reward,
-                          out_round);
-            s->last.exact_fallbacks += rest.size();
+            // fp32-filtered, fp64-decided steps (select_greedy32.cu); the fp64
+            // greedy for what that path declines (SAIR_GREEDY64=1: always)
+            std::vector<size_t> fb;
+            const bool g32 = std::getenv("SAIR_GREEDY64") == nullptr &&
+                             greedy32_select(s, p, rest, m, cfg.lambda_div, loo_pre, out_nn != nullptr,
+                                             out_idx, out_sim, out_score, out_count, out_nn,
+                                             out_nn_sim, out_reward, out_round, &fb);
+            if (g32) {
+                s->last.greedy32 = rest.size() - fb.size();
+                for (size_t i : rest) done[i] = 1;
+                rest.swap(fb);
+            }
+            if (!rest.empty())
+                greedy_select(s, p, rest, m, cfg.lambda_div, loo_pre, out_nn != nullptr, out_idx,
+                              out_sim, out_score, out_count, out_nn, out_nn_sim, out_reward,
+                              out_round);
+            s->last.exact_fallbacks += (g32 ? s->last.greedy32 : 0) + rest.size();
             for (size_t i : rest) done[i] = 1;
         }
     }

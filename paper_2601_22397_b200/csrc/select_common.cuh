@@ -114,6 +114,14 @@ WideFn pick_wide(int dp, int qw);
 // ones >= npages), or null
 const uint32_t* wide_hot_pages(sair_store_s* s, const WidePlan& pl, float c1, float c0,
                                uint32_t* nhot);
+// select_greedy32.cu: lambda != 0 over a large store, fp32-filtered steps
+// decided in fp64 (false: not applicable -- d > 64 or m > 256); queries whose
+// candidate set overflowed are appended to `fallback` (the fp64 greedy's)
+bool greedy32_select(sair_store_s* s, const QueryPrep& p, const std::vector<size_t>& qidx,
+                     size_t m, double lambda, const double* loo, bool want_nn, int64_t* out_idx,
+                     double* out_sim, double* out_score, size_t* out_count, int64_t* out_nn,
+                     double* out_nn_sim, double* out_reward, int32_t* out_round,
+                     std::vector<size_t>* fallback);
 double wide_bq_rel(const WidePlan& pl);   // relative error bound of the wide pass's query operand
 double wide_rec_rel(const WidePlan& pl);  // relative error bound of its stored records
 void ensure_pages16(sair_store_s* s);     // the bf16 page copy covers every record
