@@ -412,6 +412,48 @@ SAIR_API sair_status sair_frontier_set_points(sair_frontier_set_t s, size_t p, d
                                               double* c, size_t cap, size_t* F,
                                               double* hypervolume);
 
+/* ---------------------------------------------- multi-GPU (one process) --
+ * One logical ExperienceBuffer / ParetoFrontier over several GPUs of this
+ * process (the one-process-per-GPU mirror is sharded.py).
+ * A communicator spans a device list: NCCL (ncclCommInitAll, loaded at run
+ * time) when the devices are distinct, else device-to-device copies.  A
+ * sharded store keeps the global insertion order: shard r holds a contiguous
+ * slice, appends fill the shards in order (capacity / shards records each),
+ * and select() equals the single-buffer select() (experience.cpp:151-205):
+ * the buffer's statistics and sigma on every shard, each shard's top-m, an
+ * all-gather of the per-shard candidates and the exact merge (lambda 0), or
+ * the distributed greedy (lambda != 0). */
+typedef struct sair_comm_s* sair_comm_t;
+typedef struct sair_sharded_s* sair_sharded_t;
+SAIR_API sair_status sair_comm_create(const int* devices, int ndev, sair_comm_t* out);
+SAIR_API sair_status sair_comm_destroy(sair_comm_t c);
+/* devices in the communicator; *nccl = 1 when NCCL carries its collectives */
+SAIR_API sair_status sair_comm_info(sair_comm_t c, int* ndev, int* nccl);
+/* capacity: the records the buffer is sized for (shard quota = capacity / ndev) */
+SAIR_API sair_status sair_sharded_create(sair_comm_t c, double r_min, size_t capacity,
+                                         sair_sharded_t* out);
+SAIR_API sair_status sair_sharded_destroy(sair_sharded_t h);
+/* store() of count rows in order (experience.cpp:44-62) */
+SAIR_API sair_status sair_sharded_append(sair_sharded_t h, const double* ctx, size_t count,
+                                         int dim, const double* reward, const int32_t* round,
+                                         uint8_t* accepted, size_t* n_accepted);
+SAIR_API sair_status sair_sharded_append_synthetic(sair_sharded_t h, uint64_t seed, size_t count,
+                                                   int dim, int clustered);
+/* records stored / rejected; per-shard sizes into shard_n (ndev entries, or null) */
+SAIR_API sair_status sair_sharded_size(sair_sharded_t h, size_t* n, uint64_t* rejected,
+                                       size_t* shard_n);
+SAIR_API sair_status sair_sharded_effective_sigma(sair_sharded_t h, double sigma_sim, double* out);
+/* ExperienceBuffer::select for nq queries over the sharded buffer (global indices) */
+SAIR_API sair_status sair_store_select_sharded(sair_sharded_t h, const double* queries, size_t nq,
+                                               int dim, const sair_select_config* cfg,
+                                               int64_t* out_idx, double* out_sim,
+                                               double* out_score, size_t* out_count);
+/* T sequential insert_normalized() calls into f (pareto.cpp:36-54), the batch
+ * reduced on every device of c first (K6 per slice; frontier of the union) */
+SAIR_API sair_status sair_frontier_insert_batch_sharded(sair_comm_t c, sair_frontier_t f,
+                                                        const double* pts, size_t T,
+                                                        size_t* new_size);
+
 #ifdef __cplusplus
 }
 #endif

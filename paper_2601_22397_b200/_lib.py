@@ -106,6 +106,18 @@ SIGNATURES = {
                                           _i64p, _dp, _dp, _dp, _i32p, _szp]),
     "sair_merge_topk": (C.c_int, [_dp, _dp, _dp, _i32p, _i64p, _szp, C.c_size_t, C.c_size_t,
                                   C.c_size_t, C.c_int, _i64p, _dp, _dp, _szp]),
+    "sair_comm_create": (C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(_vp)]),
+    "sair_comm_destroy": (C.c_int, [_vp]),
+    "sair_comm_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "sair_sharded_create": (C.c_int, [_vp, C.c_double, C.c_size_t, C.POINTER(_vp)]),
+    "sair_sharded_destroy": (C.c_int, [_vp]),
+    "sair_sharded_append": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int, _dp, _i32p, _u8p, _szp]),
+    "sair_sharded_append_synthetic": (C.c_int, [_vp, C.c_uint64, C.c_size_t, C.c_int, C.c_int]),
+    "sair_sharded_size": (C.c_int, [_vp, _szp, C.POINTER(C.c_uint64), _szp]),
+    "sair_sharded_effective_sigma": (C.c_int, [_vp, C.c_double, _dp]),
+    "sair_store_select_sharded": (C.c_int, [_vp, _dp, C.c_size_t, C.c_int,
+                                            C.POINTER(SelectConfigC), _i64p, _dp, _dp, _szp]),
+    "sair_frontier_insert_batch_sharded": (C.c_int, [_vp, _vp, _dp, C.c_size_t, _szp]),
     "sair_frontier_create": (C.c_int, [C.c_double, C.c_double, C.c_int, C.POINTER(_vp)]),
     "sair_frontier_destroy": (C.c_int, [_vp]),
     "sair_frontier_clone": (C.c_int, [_vp, C.POINTER(_vp)]),

@@ -79,9 +79,20 @@ public:
         std::vector<std::int64_t>* nearest = nullptr,
         std::vector<double>* nearest_sim = nullptr) const;
     sair_store_t handle() const { return h_; }
+    // GPUs select() runs on (SAIR_DEVICES=0,1,...: >= 2 entries shard the
+    // buffer over them; 1 otherwise)
+    int select_devices() const;
 
 private:
+    void open_shards();        // SAIR_DEVICES -> comm_ / sh_
+    void close_shards();
+    void mirror_append(const double* ctx, std::size_t count, int dim, const double* reward,
+                       const std::int32_t* round);
     sair_store_t h_ = nullptr;
+    // multi-GPU select: the records also live in a sharded store over the
+    // listed GPUs (sair_store_select_sharded); the other members use h_
+    sair_comm_t comm_ = nullptr;
+    sair_sharded_t sh_ = nullptr;
     double r_min_ = 0.0;
     std::vector<Experience> items_;
 };

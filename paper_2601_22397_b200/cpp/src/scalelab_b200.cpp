@@ -2,6 +2,7 @@
 // the libsair C ABI (include/sair.h).  Every number comes from the device; the
 // host holds only what the reference's callers hold (Experience records for
 // all(), the frontier's points for points()) and does the JSONL I/O.
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
@@ -77,14 +78,59 @@ double similarity(const std::vector<double>& a, const std::vector<double>& b, do
 
 ExperienceBuffer::ExperienceBuffer(double r_min) : r_min_(r_min) {
     check(sair_store_create(r_min, 0, 0, &h_));
+    open_shards();
 }
 
 ExperienceBuffer::ExperienceBuffer(const ExperienceBuffer& o) : r_min_(o.r_min_), items_(o.items_) {
     check(sair_store_clone(o.h_, &h_));
+    open_shards();
+    if (sh_) {  // the copy's shards: the same records in the same order
+        for (const auto& e : items_) {
+            const int32_t rd = e.round;
+            mirror_append(e.context.data(), 1, static_cast<int>(e.context.size()), &e.reward, &rd);
+        }
+    }
 }
 
 ExperienceBuffer::ExperienceBuffer(ExperienceBuffer&& o) noexcept
-    : h_(std::exchange(o.h_, nullptr)), r_min_(o.r_min_), items_(std::move(o.items_)) {}
+    : h_(std::exchange(o.h_, nullptr)), comm_(std::exchange(o.comm_, nullptr)),
+      sh_(std::exchange(o.sh_, nullptr)), r_min_(o.r_min_), items_(std::move(o.items_)) {}
+
+void ExperienceBuffer::open_shards() {
+    const char* e = std::getenv("SAIR_DEVICES");
+    if (!e || !*e) return;
+    std::vector<int> dev;
+    for (const char* p = e; *p;) {
+        char* end = nullptr;
+        const long v = std::strtol(p, &end, 10);
+        if (end == p) throw std::invalid_argument("SAIR_DEVICES: a comma-separated device list");
+        dev.push_back(static_cast<int>(v));
+        p = *end == ',' ? end + 1 : end;
+    }
+    if (dev.size() < 2) return;
+    const char* cap = std::getenv("SAIR_SHARD_CAPACITY");
+    check(sair_comm_create(dev.data(), static_cast<int>(dev.size()), &comm_));
+    check(sair_sharded_create(comm_, r_min_, cap ? std::strtoull(cap, nullptr, 10) : (1u << 24),
+                              &sh_));
+}
+
+void ExperienceBuffer::close_shards() {
+    sair_sharded_destroy(sh_);
+    sair_comm_destroy(comm_);
+    sh_ = nullptr;
+    comm_ = nullptr;
+}
+
+void ExperienceBuffer::mirror_append(const double* ctx, std::size_t count, int dim,
+                                     const double* reward, const std::int32_t* round) {
+    if (sh_) check(sair_sharded_append(sh_, ctx, count, dim, reward, round, nullptr, nullptr));
+}
+
+int ExperienceBuffer::select_devices() const {
+    int n = 1;
+    if (comm_) sair_comm_info(comm_, &n, nullptr);
+    return n;
+}
 
 ExperienceBuffer& ExperienceBuffer::operator=(const ExperienceBuffer& o) {
     if (this != &o) {
@@ -97,21 +143,30 @@ ExperienceBuffer& ExperienceBuffer::operator=(const ExperienceBuffer& o) {
 ExperienceBuffer& ExperienceBuffer::operator=(ExperienceBuffer&& o) noexcept {
     if (this != &o) {
         sair_store_destroy(h_);
+        close_shards();
         h_ = std::exchange(o.h_, nullptr);
+        comm_ = std::exchange(o.comm_, nullptr);
+        sh_ = std::exchange(o.sh_, nullptr);
         r_min_ = o.r_min_;
         items_ = std::move(o.items_);
     }
     return *this;
 }
 
-ExperienceBuffer::~ExperienceBuffer() { sair_store_destroy(h_); }
+ExperienceBuffer::~ExperienceBuffer() {
+    sair_store_destroy(h_);
+    close_shards();
+}
 
 bool ExperienceBuffer::store(Experience e) {
     uint8_t acc = 0;
     const int32_t round = e.round;
     check(sair_store_append(h_, e.context.data(), 1, static_cast<int>(e.context.size()),
                             &e.reward, &round, &acc, nullptr));
-    if (acc) items_.push_back(std::move(e));
+    if (acc) {
+        mirror_append(e.context.data(), 1, static_cast<int>(e.context.size()), &e.reward, &round);
+        items_.push_back(std::move(e));
+    }
     return acc != 0;
 }
 
@@ -165,9 +220,18 @@ std::vector<std::vector<SelectedExperience>> ExperienceBuffer::select_batch(
     if (nearest) nearest->assign(nq, -1);
     if (nearest_sim) nearest_sim->assign(nq, -1.0);
     const sair_select_config c = to_c(cfg);
-    check(sair_store_select(h_, q.data(), nq, d, &c, idx.data(), sim.data(), score.data(),
-                            cnt.data(), nearest ? nearest->data() : nullptr,
-                            nearest_sim ? nearest_sim->data() : nullptr));
+    if (sh_) {
+        // over the GPUs of SAIR_DEVICES; the veto scan on the primary store
+        check(sair_store_select_sharded(sh_, q.data(), nq, d, &c, idx.data(), sim.data(),
+                                        score.data(), cnt.data()));
+        if (nearest)
+            check(sair_store_nearest(h_, q.data(), nq, d, cfg.sigma_sim, nearest->data(),
+                                     nearest_sim->data()));
+    } else {
+        check(sair_store_select(h_, q.data(), nq, d, &c, idx.data(), sim.data(), score.data(),
+                                cnt.data(), nearest ? nearest->data() : nullptr,
+                                nearest_sim ? nearest_sim->data() : nullptr));
+    }
     for (std::size_t i = 0; i < nq; ++i)
         for (std::size_t j = 0; j < cnt[i]; ++j)
             out[i].push_back({items_.at(static_cast<std::size_t>(idx[i * m + j])),
@@ -252,6 +316,7 @@ ExperienceBuffer ExperienceBuffer::load(const std::string& path, double r_min,
         }
         check(sair_store_append(buf.h_, ctx.data(), rows.size(), d, rew.data(), rnd.data(),
                                 acc.data(), nullptr));
+        buf.mirror_append(ctx.data(), rows.size(), d, rew.data(), rnd.data());
         for (std::size_t i = 0; i < rows.size(); ++i)
             if (acc[i]) buf.items_.push_back(std::move(rows[i]));
     } else {

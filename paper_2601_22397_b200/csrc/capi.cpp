@@ -646,3 +646,114 @@ sair_status sair_frontier_set_points(sair_frontier_set_t s, size_t p, double* l,
 }
 
 }  // extern "C"
+
+// --------------------------------------------------------- multi-GPU ----
+
+sair_status sair_comm_create(const int* devices, int ndev, sair_comm_t* out) {
+    if (!out || !devices) return bad("null input");
+    return guard([&] {
+        auto* c = new sair_comm_s();
+        try {
+            sair::comm_create(devices, ndev, c);
+        } catch (...) {
+            sair::comm_free(c);
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+sair_status sair_comm_destroy(sair_comm_t c) {
+    if (!c) return SAIR_OK;
+    return guard([&] {
+        sair::comm_free(c);
+        delete c;
+    });
+}
+
+sair_status sair_comm_info(sair_comm_t c, int* ndev, int* nccl) {
+    if (!c) return bad("null handle");
+    if (ndev) *ndev = (int)c->dev.size();
+    if (nccl) *nccl = c->nc.empty() ? 0 : 1;
+    return SAIR_OK;
+}
+
+sair_status sair_sharded_create(sair_comm_t c, double r_min, size_t capacity, sair_sharded_t* out) {
+    if (!c || !out) return bad("null input");
+    return guard([&] {
+        auto* h = new sair_sharded_s();
+        try {
+            sair::sharded_init(h, c, r_min, capacity);
+        } catch (...) {
+            sair::sharded_free(h);
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+sair_status sair_sharded_destroy(sair_sharded_t h) {
+    if (!h) return SAIR_OK;
+    return guard([&] {
+        sair::sharded_free(h);
+        delete h;
+    });
+}
+
+sair_status sair_sharded_append(sair_sharded_t h, const double* ctx, size_t count, int dim,
+                                const double* reward, const int32_t* round, uint8_t* accepted,
+                                size_t* n_accepted) {
+    if (!h) return bad("null handle");
+    if (count && (!ctx || !reward)) return bad("null input");
+    if (dim <= 0) return bad("experience store: dimension must be positive");
+    return guard([&] {
+        const size_t a = sair::sharded_append(h, ctx, count, dim, reward, round, accepted);
+        if (n_accepted) *n_accepted = a;
+    });
+}
+
+sair_status sair_sharded_append_synthetic(sair_sharded_t h, uint64_t seed, size_t count, int dim,
+                                          int clustered) {
+    if (!h) return bad("null handle");
+    if (dim <= 0) return bad("experience store: dimension must be positive");
+    return guard([&] { sair::sharded_append_synthetic(h, seed, count, dim, clustered); });
+}
+
+sair_status sair_sharded_size(sair_sharded_t h, size_t* n, uint64_t* rejected, size_t* shard_n) {
+    if (!h) return bad("null handle");
+    if (n) *n = h->n;
+    if (rejected) *rejected = h->rejected;
+    if (shard_n)
+        for (size_t r = 0; r < h->sh.size(); ++r) shard_n[r] = h->sh[r]->n;
+    return SAIR_OK;
+}
+
+sair_status sair_sharded_effective_sigma(sair_sharded_t h, double sigma_sim, double* out) {
+    if (!h || !out) return bad("null input");
+    return guard([&] { *out = sair::sharded_effective_sigma(h, sigma_sim); });
+}
+
+sair_status sair_store_select_sharded(sair_sharded_t h, const double* queries, size_t nq, int dim,
+                                      const sair_select_config* cfg, int64_t* out_idx,
+                                      double* out_sim, double* out_score, size_t* out_count) {
+    if (!h) return bad("null handle");
+    if (nq && (!queries || !out_idx || !out_sim || !out_score || !out_count))
+        return bad("null input");
+    return guard([&] {
+        sair::sharded_select(h, queries, nq, dim, defaults(cfg), out_idx, out_sim, out_score,
+                             out_count);
+    });
+}
+
+sair_status sair_frontier_insert_batch_sharded(sair_comm_t c, sair_frontier_t f, const double* pts,
+                                               size_t T, size_t* new_size) {
+    if (!c || !f) return bad("null handle");
+    if (T && !pts) return bad("null input");
+    return guard([&] {
+        const size_t F = sair::frontier_insert_batch_sharded(c, f, pts, T);
+        if (new_size) *new_size = F;
+    });
+}
+

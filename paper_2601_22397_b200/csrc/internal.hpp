@@ -174,6 +174,33 @@ struct sair_frontier_set_s {
     sair::DBuf b_in;
 };
 
+// ------------------------------------------------- multi-GPU (sharded.cpp) --
+struct sair_comm_s {
+    std::vector<int> dev;
+    std::vector<cudaStream_t> st;
+    std::vector<void*> nc;  // ncclComm_t per device (NCCL transport), or empty (copies)
+};
+
+struct sair_sharded_s {
+    sair_comm_s* comm = nullptr;
+    std::vector<sair_store_s*> sh;
+    std::vector<size_t> lo;   // global index of each shard's first record
+    size_t quota = 0, n = 0;
+    uint64_t rejected = 0;
+    double r_min = 0.0;
+    int d = 0;
+    // the buffer-level sigma cache (experience.hpp:87-88) and what the
+    // shards' global statistics were last set to
+    double cached_sigma = 0.0;
+    // the buffer's running sums, accumulated in insertion order on the host
+    // (experience.cpp:55-58, :138-139): bit-identical to one buffer's, not a
+    // shard-order recombination
+    sair::StoreStats gst;
+    size_t stale = 0, synced_n = (size_t)-1;
+    double synced_sigma = -1.0;
+    std::vector<sair::DBuf> b_pack;  // per device: own pack | gathered packs | merged
+};
+
 namespace sair {
 
 // statistics the reference's formulas see: the whole buffer's (experience.cpp:68-75, :229-231)
@@ -247,6 +274,22 @@ void frontier_set_step(sair_frontier_set_s* s, const sair_reward_inputs* in, con
                        sair_reward_breakdown* out);
 size_t frontier_set_points(sair_frontier_set_s* s, size_t p, double* l, double* c, size_t cap,
                            double* hv);
+
+// sharded.cpp: one buffer / frontier over the GPUs of this process
+void comm_create(const int* devices, int n, sair_comm_s* c);
+void comm_free(sair_comm_s* c);
+void sharded_init(sair_sharded_s* h, sair_comm_s* c, double r_min, size_t capacity);
+void sharded_free(sair_sharded_s* h);
+size_t sharded_append(sair_sharded_s* h, const double* ctx, size_t count, int dim,
+                      const double* reward, const int32_t* round, uint8_t* accepted);
+void sharded_append_synthetic(sair_sharded_s* h, uint64_t seed, size_t count, int dim,
+                              int clustered);
+double sharded_effective_sigma(sair_sharded_s* h, double sigma_sim);
+void sharded_select(sair_sharded_s* h, const double* q, size_t nq, int dim,
+                    const sair_select_config& cfg, int64_t* out_idx, double* out_sim,
+                    double* out_score, size_t* out_count);
+size_t frontier_insert_batch_sharded(sair_comm_s* c, sair_frontier_s* f, const double* pts,
+                                     size_t T);
 
 // select_greedy.cu: a shard's side of the distributed exact greedy
 void greedy_begin(sair_store_s* s, const double* q, size_t nq, int dim,

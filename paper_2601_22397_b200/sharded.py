@@ -341,3 +341,91 @@ def sharded_dominance_counts(dist, local_tuples, device: int):
     cnt, mem = combine_parts(dist, cnt, mem, f"cuda:{device}")
     lo = sum(len(p) for p in parts[:dist.get_rank()])
     return cnt[lo:lo + len(t)], mem[lo:lo + len(t)], int(mem.sum())
+
+
+# ------------------------------------------------- one process, many GPUs --
+
+class DeviceComm:
+    """sair_comm_t: the GPUs of this process (NCCL when the devices are distinct)."""
+
+    def __init__(self, devices):
+        devs = (C.c_int * len(devices))(*devices)
+        self._h = C.c_void_p()
+        _check(lib().sair_comm_create(devs, len(devices), C.byref(self._h)))
+        self.devices = list(devices)
+
+    def info(self):
+        n, nc = C.c_int(), C.c_int()
+        _check(lib().sair_comm_info(self._h, C.byref(n), C.byref(nc)))
+        return n.value, bool(nc.value)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sair_comm_destroy(self._h)
+            self._h = None
+
+
+class MultiGPUExperienceBuffer:
+    """One ExperienceBuffer over the GPUs of a DeviceComm, entirely in the C
+    ABI (sharded.cpp): the path the C++ drop-in takes without Python."""
+
+    def __init__(self, comm: DeviceComm, r_min: float = 0.0, capacity: int = 1 << 20):
+        self.comm = comm
+        self._h = C.c_void_p()
+        _check(lib().sair_sharded_create(comm._h, r_min, capacity, C.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sair_sharded_destroy(self._h)
+            self._h = None
+
+    def store_many(self, contexts, rewards, rounds) -> int:
+        x = _f64(contexts)
+        r = _f64(rewards)
+        rd = np.ascontiguousarray(rounds, dtype=np.int32)
+        n, d = x.shape
+        acc = np.zeros(n, np.uint8)
+        na = C.c_size_t()
+        _check(lib().sair_sharded_append(self._h, _dp(x), n, d, _dp(r),
+                                         rd.ctypes.data_as(C.POINTER(C.c_int32)),
+                                         acc.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(na)))
+        return na.value
+
+    def store_synthetic(self, seed: int, n: int, dim: int, clustered: bool = False):
+        _check(lib().sair_sharded_append_synthetic(self._h, seed, n, dim, int(clustered)))
+
+    def size(self):
+        n, rej = C.c_size_t(), C.c_uint64()
+        sh = np.zeros(len(self.comm.devices), np.uintp)
+        _check(lib().sair_sharded_size(self._h, C.byref(n), C.byref(rej),
+                                       sh.ctypes.data_as(C.POINTER(C.c_size_t))))
+        return n.value, rej.value, sh.astype(np.int64)
+
+    def effective_sigma(self, sigma_sim: float = 0.0) -> float:
+        out = C.c_double()
+        _check(lib().sair_sharded_effective_sigma(self._h, sigma_sim, C.byref(out)))
+        return out.value
+
+    def select_batch(self, queries, cfg: SelectionConfig):
+        q = _f64(queries)
+        if q.ndim == 1:
+            q = q[None, :]
+        nq, d = q.shape
+        m = max(cfg.m, 1)
+        idx = np.full((nq, m), -1, np.int64)
+        sim, sc = np.zeros((nq, m)), np.zeros((nq, m))
+        cnt = np.zeros(nq, np.uintp)
+        c = cfg._c()
+        _check(lib().sair_store_select_sharded(
+            self._h, _dp(q), nq, d, C.byref(c), idx.ctypes.data_as(C.POINTER(C.c_int64)),
+            _dp(sim), _dp(sc), cnt.ctypes.data_as(C.POINTER(C.c_size_t))))
+        return idx, sim, sc, cnt.astype(np.int64)
+
+
+def frontier_insert_batch_multi(comm: DeviceComm, frontier: ParetoFrontier, pts) -> int:
+    """insert_batch on one frontier with the batch reduced on every GPU of comm."""
+    a = _f64(pts).reshape(-1, 2)
+    F = C.c_size_t()
+    _check(lib().sair_frontier_insert_batch_sharded(comm._h, frontier._h, _dp(a), len(a),
+                                                    C.byref(F)))
+    return F.value

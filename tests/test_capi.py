@@ -83,3 +83,15 @@ def test_similarity_is_the_references(ref):
                              C.byref(out)) == _lib.SAIR_EINVAL
     assert L.sair_similarity(a.ctypes.data_as(dp), 3, a.ctypes.data_as(dp), 3, 0.0,
                              C.byref(out)) == _lib.SAIR_EINVAL
+
+
+def test_multigpu_entry_points_fail_loudly_without_a_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    L = _lib.lib()
+    devs = (C.c_int * 2)(0, 1)
+    h = C.c_void_p()
+    assert L.sair_comm_create(devs, 2, C.byref(h)) == _lib.SAIR_ECUDA
+    assert L.sair_comm_destroy(None) == _lib.SAIR_OK
+    assert L.sair_sharded_create(None, 0.0, 10, C.byref(h)) == _lib.SAIR_EINVAL

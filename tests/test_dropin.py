@@ -45,15 +45,23 @@ def test_cpp_dropin_meets_reference_expectations():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["", "0,0"], ids=["one-gpu", "sharded"])
 @pytest.mark.parametrize("scenario", SCEN, ids=[s.stem for s in SCEN])
-def test_reference_decision_loop_identical_with_dropin(tmp_path, scenario):
+def test_reference_decision_loop_identical_with_dropin(tmp_path, scenario, devices):
+    """devices "0,0": the drop-in's select() runs over a buffer sharded over
+    two GPU slots (SAIR_DEVICES; one B200 per test box, so both on device 0 --
+    on a multi-GPU node the same run takes distinct GPUs over NCCL)."""
+    import os
     _need(REF_BIN)
     _need(B200_BIN)
     a, b = tmp_path / "ref.csv", tmp_path / "b200.csv"
     ra = subprocess.run([str(REF_BIN), str(scenario), str(a)], capture_output=True, text=True,
                         timeout=600)
+    env = dict(os.environ)
+    if devices:
+        env["SAIR_DEVICES"] = devices
     rb = subprocess.run([str(B200_BIN), str(scenario), str(b)], capture_output=True, text=True,
-                        timeout=600)
+                        timeout=600, env=env)
     assert ra.returncode == 0, ra.stderr
     assert rb.returncode == 0, rb.stderr
     assert ra.stdout == rb.stdout  # run summary: p99 and frontier hypervolume
