@@ -5,13 +5,23 @@
 #include <new>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.hpp"
 
 namespace {
 thread_local std::string g_err;
 
+// one NVTX range per entry point (the C ABI's name): what a profiler's
+// timeline shows around the kernels of a call; free without a tool attached
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <class F>
-sair_status guard(F&& f) {
+sair_status guard(const char* name, F&& f) {
+    NvtxRange r(name);
     try {
         f();
         return SAIR_OK;
@@ -51,7 +61,7 @@ sair_status sair_internal_fail(sair_status code, const char* msg) {  // hidden: 
 int sair_version(void) { return 1; }
 
 sair_status sair_device_count(int* out) {
-    return guard([&] {
+    return guard(__func__, [&] {
         int n = 0;
         if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
         *out = n;
@@ -63,7 +73,7 @@ sair_status sair_device_count(int* out) {
 
 sair_status sair_store_create(double r_min, int device, size_t capacity_hint, sair_store_t* out) {
     if (!out) return bad("null out");
-    return guard([&] {
+    return guard(__func__, [&] {
         auto* s = new sair_store_s();
         try {
             sair::store_init(s, r_min, device, capacity_hint);
@@ -77,7 +87,7 @@ sair_status sair_store_create(double r_min, int device, size_t capacity_hint, sa
 
 sair_status sair_store_destroy(sair_store_t h) {
     if (!h) return SAIR_OK;
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::store_free(h);
         delete h;
     });
@@ -85,7 +95,7 @@ sair_status sair_store_destroy(sair_store_t h) {
 
 sair_status sair_store_clone(sair_store_t h, sair_store_t* out) {
     if (!h || !out) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         auto* o = new sair_store_s();
         try {
             sair::store_clone(h, o);
@@ -102,7 +112,7 @@ sair_status sair_store_append(sair_store_t h, const double* ctx, size_t count, i
                               size_t* n_accepted) {
     if (!h) return bad("null handle");
     if (count && (!ctx || !reward || !round)) return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         size_t k = sair::store_append(h, ctx, count, dim, reward, round, accepted);
         if (n_accepted) *n_accepted = k;
     });
@@ -111,7 +121,7 @@ sair_status sair_store_append(sair_store_t h, const double* ctx, size_t count, i
 sair_status sair_store_append_synthetic(sair_store_t h, uint64_t seed, size_t count, int dim,
                                         int clustered) {
     if (!h) return bad("null handle");
-    return guard([&] { sair::store_append_synthetic(h, seed, count, dim, clustered); });
+    return guard(__func__, [&] { sair::store_append_synthetic(h, seed, count, dim, clustered); });
 }
 
 sair_status sair_store_size(sair_store_t h, size_t* n) {
@@ -138,7 +148,7 @@ sair_status sair_store_r_min(sair_store_t h, double* out) {
 sair_status sair_store_get(sair_store_t h, size_t index, double* ctx, double* reward,
                            int32_t* round) {
     if (!h) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         if (index >= h->n) throw sair::Error(SAIR_ERANGE, "vector::_M_range_check");
         sair::DeviceGuard g(h->device);
         if (ctx)
@@ -155,7 +165,7 @@ sair_status sair_store_get(sair_store_t h, size_t index, double* ctx, double* re
 sair_status sair_store_export(sair_store_t h, size_t offset, size_t count, double* ctx,
                               double* reward, int32_t* round) {
     if (!h) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         if (offset > h->n || count > h->n - offset)
             throw sair::Error(SAIR_ERANGE, "export range outside the store");
         if (count == 0) return;
@@ -175,7 +185,7 @@ sair_status sair_store_export(sair_store_t h, size_t offset, size_t count, doubl
 
 sair_status sair_store_standardize(sair_store_t h, const double* x, int dim, double* z) {
     if (!h) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         if (h->n == 0) {  // experience.cpp:65
             std::memcpy(z, x, (size_t)dim * sizeof(double));
             return;
@@ -188,7 +198,7 @@ sair_status sair_store_standardize(sair_store_t h, const double* x, int dim, dou
 
 sair_status sair_store_effective_sigma(sair_store_t h, double sigma_sim, double* out) {
     if (!h || !out) return bad("null handle");
-    return guard([&] { *out = sair::store_effective_sigma(h, sigma_sim); });
+    return guard(__func__, [&] { *out = sair::store_effective_sigma(h, sigma_sim); });
 }
 
 sair_status sair_similarity(const double* a, size_t len_a, const double* b, size_t len_b,
@@ -203,7 +213,7 @@ sair_status sair_similarity(const double* a, size_t len_a, const double* b, size
     // device round trip per call would cost ~10 us against ~30 ns; the
     // data-parallel veto scan is sair_store_nearest / the fused select.
     // Same additions in the same order and glibc's exp: bit-identical.
-    return guard([&] {
+    return guard(__func__, [&] {
         double d2 = 0.0;
         for (size_t i = 0; i < len_a; ++i) {
             const double d = a[i] - b[i];
@@ -216,7 +226,7 @@ sair_status sair_similarity(const double* a, size_t len_a, const double* b, size
 sair_status sair_store_surprisal(sair_store_t h, size_t index, const double* x, int dim,
                                  const sair_select_config* cfg, double* out) {
     if (!h || !out) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         // items_.at(index) first (experience.cpp:145), then standardize(x)
         if (index >= h->n) throw sair::Error(SAIR_ERANGE, "vector::_M_range_check");
         if (dim != h->d)
@@ -232,7 +242,7 @@ sair_status sair_store_select(sair_store_t h, const double* queries, size_t nq, 
     if (!h) return bad("null handle");
     if (nq && (!queries || !out_count)) return bad("null input");
     if ((out_nn_idx == nullptr) != (out_nn_sim == nullptr)) return bad("nn outputs come in pairs");
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::store_select(h, queries, nq, dim, defaults(cfg), out_idx, out_sim, out_score,
                            out_count, out_nn_idx, out_nn_sim);
     });
@@ -241,7 +251,7 @@ sair_status sair_store_select(sair_store_t h, const double* queries, size_t nq, 
 sair_status sair_store_nearest(sair_store_t h, const double* queries, size_t nq, int dim,
                                double sigma_sim, int64_t* out_idx, double* out_sim) {
     if (!h) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         // a select with m = 1 computes the same pass; only the nearest is kept
         sair_select_config c{};
         c.m = 1;
@@ -320,7 +330,7 @@ sair_status sair_sigma_sample_indices(uint64_t n, int64_t* idx, size_t* m) {
 sair_status sair_sigma_rows(const double* rows, size_t m, int dim, const double* mean,
                             const double* sd, int device, double* out) {
     if (!out || (m && (!rows || !mean || !sd))) return bad("null input");
-    return guard([&] { *out = sair::sigma_rows(rows, m, dim, mean, sd, device); });
+    return guard(__func__, [&] { *out = sair::sigma_rows(rows, m, dim, mean, sd, device); });
 }
 
 sair_status sair_store_select_shard(sair_store_t h, const double* queries, size_t nq, int dim,
@@ -329,7 +339,7 @@ sair_status sair_store_select_shard(sair_store_t h, const double* queries, size_
                                     int32_t* out_round, size_t* out_count) {
     if (!h) return bad("null handle");
     if (nq && (!queries || !out_count)) return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::store_select(h, queries, nq, dim, defaults(cfg), out_idx, out_sim, out_score,
                            out_count, nullptr, nullptr, out_reward, out_round);
     });
@@ -338,13 +348,13 @@ sair_status sair_store_select_shard(sair_store_t h, const double* queries, size_
 sair_status sair_store_greedy_begin(sair_store_t h, const double* queries, size_t nq, int dim,
                                     const sair_select_config* cfg, double* out_best) {
     if (!h || !queries || !out_best) return bad("null input");
-    return guard([&] { sair::greedy_begin(h, queries, nq, dim, defaults(cfg), out_best); });
+    return guard(__func__, [&] { sair::greedy_begin(h, queries, nq, dim, defaults(cfg), out_best); });
 }
 
 sair_status sair_store_greedy_next(sair_store_t h, const int64_t* picks, const double* rows,
                                    double* out_best) {
     if (!h || !picks || !rows || !out_best) return bad("null input");
-    return guard([&] { sair::greedy_next(h, picks, rows, out_best); });
+    return guard(__func__, [&] { sair::greedy_next(h, picks, rows, out_best); });
 }
 
 sair_status sair_merge_topk(const double* score, const double* sim, const double* reward,
@@ -353,7 +363,7 @@ sair_status sair_merge_topk(const double* score, const double* sim, const double
                             double* out_sim, double* out_score, size_t* out_count) {
     if (nq && (!out_count || !count)) return bad("null input");
     if (m > 4096) return bad("merge: m too large");
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::merge_topk(score, sim, reward, round, gidx, count, nshards, nq, m, device, out_idx,
                          out_sim, out_score, out_count);
     });
@@ -363,7 +373,7 @@ sair_status sair_merge_topk_packed(const double* d_parts, size_t nshards, size_t
                                    int device, void* stream, double* d_out) {
     if (nq && (!d_parts || !d_out)) return bad("null input");
     if (m > 4096) return bad("merge: m too large");
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::merge_packed(d_parts, nshards, nq, m, device, static_cast<cudaStream_t>(stream), d_out);
     });
 }
@@ -378,7 +388,7 @@ sair_status sair_store_stream(sair_store_t h, void** stream) {
 
 sair_status sair_frontier_create(double l_max_ms, double c_max, int device, sair_frontier_t* out) {
     if (!out) return bad("null out");
-    return guard([&] {
+    return guard(__func__, [&] {
         auto* f = new sair_frontier_s();
         try {
             sair::frontier_init(f, l_max_ms, c_max, device);
@@ -392,7 +402,7 @@ sair_status sair_frontier_create(double l_max_ms, double c_max, int device, sair
 
 sair_status sair_frontier_destroy(sair_frontier_t f) {
     if (!f) return SAIR_OK;
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::frontier_free(f);
         delete f;
     });
@@ -400,7 +410,7 @@ sair_status sair_frontier_destroy(sair_frontier_t f) {
 
 sair_status sair_frontier_clone(sair_frontier_t f, sair_frontier_t* out) {
     if (!f || !out) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         auto* o = new sair_frontier_s();
         try {
             sair::frontier_clone(f, o);
@@ -437,7 +447,7 @@ sair_status sair_frontier_normalize(sair_frontier_t f, double l_ms, double cost,
 sair_status sair_frontier_update(sair_frontier_t f, double l_ms, double cost, int* inserted,
                                  int* clamped) {
     if (!f) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         double pl, pc;
         int cl = 0;
         normalize_host(f, l_ms, cost, &pl, &pc, &cl);
@@ -449,7 +459,7 @@ sair_status sair_frontier_update(sair_frontier_t f, double l_ms, double cost, in
 
 sair_status sair_frontier_insert_normalized(sair_frontier_t f, double l, double c, int* inserted) {
     if (!f) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         bool ins = sair::frontier_insert_one(f, l, c);
         if (inserted) *inserted = ins;
     });
@@ -459,7 +469,7 @@ sair_status sair_frontier_insert_batch(sair_frontier_t f, const double* pts, siz
                                        size_t* new_size) {
     if (!f) return bad("null handle");
     if (T && !pts) return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         size_t F = sair::frontier_insert_batch(f, pts, T);
         if (new_size) *new_size = F;
     });
@@ -491,17 +501,17 @@ sair_status sair_frontier_bounds(sair_frontier_t f, double* l_max, double* c_max
 
 sair_status sair_frontier_hypervolume(sair_frontier_t f, double* out) {
     if (!f || !out) return bad("null handle");
-    return guard([&] { *out = sair::frontier_point_query(f, 0.0, 0.0, sair::Q_HV, nullptr); });
+    return guard(__func__, [&] { *out = sair::frontier_point_query(f, 0.0, 0.0, sair::Q_HV, nullptr); });
 }
 
 sair_status sair_frontier_strictly_dominated(sair_frontier_t f, double l, double c, int* out) {
     if (!f || !out) return bad("null handle");
-    return guard([&] { *out = sair::frontier_point_query(f, l, c, sair::Q_DOMINATED, nullptr) != 0.0; });
+    return guard(__func__, [&] { *out = sair::frontier_point_query(f, l, c, sair::Q_DOMINATED, nullptr) != 0.0; });
 }
 
 sair_status sair_frontier_contribution(sair_frontier_t f, double l, double c, double* out) {
     if (!f || !out) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         double dom = 0.0;
         double v = sair::frontier_point_query(f, l, c, sair::Q_CONTRIB, &dom);
         if (dom != 0.0)  // pareto.cpp:68-69
@@ -513,7 +523,7 @@ sair_status sair_frontier_contribution(sair_frontier_t f, double l, double c, do
 
 sair_status sair_frontier_distance(sair_frontier_t f, double l, double c, double* out, int* has) {
     if (!f || !out) return bad("null handle");
-    return guard([&] {
+    return guard(__func__, [&] {
         double v = sair::frontier_point_query(f, l, c, sair::Q_DISTANCE, nullptr);
         if (has) *has = f->F > 0;
         *out = f->F > 0 ? v : 0.0;
@@ -522,14 +532,14 @@ sair_status sair_frontier_distance(sair_frontier_t f, double l, double c, double
 
 sair_status sair_frontier_reward(sair_frontier_t f, double l, double c, double* out) {
     if (!f || !out) return bad("null handle");
-    return guard([&] { *out = sair::frontier_point_query(f, l, c, sair::Q_REWARD, nullptr); });
+    return guard(__func__, [&] { *out = sair::frontier_point_query(f, l, c, sair::Q_REWARD, nullptr); });
 }
 
 sair_status sair_frontier_score_batch(sair_frontier_t f, const double* pts, size_t T,
                                       double* out_reward, uint8_t* out_dominated) {
     if (!f) return bad("null handle");
     if (T && (!pts || !out_reward)) return bad("null input");
-    return guard([&] { sair::frontier_score_batch(f, pts, T, out_reward, out_dominated); });
+    return guard(__func__, [&] { sair::frontier_score_batch(f, pts, T, out_reward, out_dominated); });
 }
 
 sair_status sair_frontier_score_batch_device(sair_frontier_t f, const double* pts, size_t T,
@@ -537,7 +547,7 @@ sair_status sair_frontier_score_batch_device(sair_frontier_t f, const double* pt
                                              void* stream) {
     if (!f) return bad("null handle");
     if (T && (!pts || !out_reward)) return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::DeviceGuard g(f->device);
         sair::frontier_score_batch_device(f, pts, T, out_reward, out_dominated,
                                           static_cast<cudaStream_t>(stream));
@@ -547,27 +557,27 @@ sair_status sair_frontier_score_batch_device(sair_frontier_t f, const double* pt
 sair_status sair_dominance_counts(const double* tuples, size_t T, int K, int device,
                                   uint32_t* counts, uint8_t* member) {
     if (T && !tuples) return bad("null input");
-    return guard([&] { sair::dominance_counts(tuples, T, K, device, counts, member); });
+    return guard(__func__, [&] { sair::dominance_counts(tuples, T, K, device, counts, member); });
 }
 
 sair_status sair_dominance_counts_part(const double* tuples, size_t T, int K, int device, int part,
                                        int nparts, uint32_t* counts, uint8_t* member) {
     if (T && !tuples) return bad("null input");
-    return guard([&] { sair::dominance_counts(tuples, T, K, device, counts, member, part, nparts); });
+    return guard(__func__, [&] { sair::dominance_counts(tuples, T, K, device, counts, member, part, nparts); });
 }
 
 // ---------------------------------------------------------------- reward --
 
 sair_status sair_action_magnitude(const int32_t* deltas, size_t stages, double* out) {
     if (!out || (stages && !deltas)) return bad("null input");
-    return guard([&] { *out = sair::action_magnitude(deltas, stages, 0); });
+    return guard(__func__, [&] { *out = sair::action_magnitude(deltas, stages, 0); });
 }
 
 sair_status sair_compute_reward(const sair_reward_inputs* in, const int32_t* deltas, size_t stages,
                                 sair_frontier_t f, const sair_reward_config* cfg,
                                 sair_reward_breakdown* out) {
     if (!in || !f || !cfg || !out || (stages && !deltas)) return bad("null input");
-    return guard([&] { sair::compute_reward_batch(in, deltas, stages, 1, f, cfg, out); });
+    return guard(__func__, [&] { sair::compute_reward_batch(in, deltas, stages, 1, f, cfg, out); });
 }
 
 sair_status sair_decision_step(sair_store_t h, sair_frontier_t f, const double* x, int dim,
@@ -583,7 +593,7 @@ sair_status sair_decision_step(sair_store_t h, sair_frontier_t f, const double* 
         (stages && !deltas))
         return bad("null input");
     if ((out_nn_idx == nullptr) != (out_nn_sim == nullptr)) return bad("nn outputs come in pairs");
-    return guard([&] {
+    return guard(__func__, [&] {
         double pl = 0.0, pc = 0.0;
         normalize_host(f, in->l_after_ms, in->c_after, &pl, &pc, nullptr);
         sair::decision_step(h, f, x, dim, defaults(cfg), in, deltas, stages, rcfg, update != 0,
@@ -596,7 +606,7 @@ sair_status sair_compute_reward_batch(const sair_reward_inputs* in, const int32_
                                       size_t stages, size_t T, sair_frontier_t f,
                                       const sair_reward_config* cfg, sair_reward_breakdown* out) {
     if (!f || !cfg || (T && (!in || !out)) || (T && stages && !deltas)) return bad("null input");
-    return guard([&] { sair::compute_reward_batch(in, deltas, stages, T, f, cfg, out); });
+    return guard(__func__, [&] { sair::compute_reward_batch(in, deltas, stages, T, f, cfg, out); });
 }
 
 sair_status sair_compute_reward_replay(const sair_reward_inputs* in, const int32_t* deltas,
@@ -605,7 +615,7 @@ sair_status sair_compute_reward_replay(const sair_reward_inputs* in, const int32
                                        sair_reward_breakdown* out) {
     if (!f || !cfg || (T && (!in || !out || !update)) || (T && stages && !deltas))
         return bad("null input");
-    return guard([&] { sair::compute_reward_replay(in, deltas, stages, T, update, f, cfg, out); });
+    return guard(__func__, [&] { sair::compute_reward_replay(in, deltas, stages, T, update, f, cfg, out); });
 }
 
 // ---------------------------------------------------------- frontier set --
@@ -615,7 +625,7 @@ sair_status sair_frontier_set_create(size_t P, double l_max_ms, double c_max, in
     if (!out) return bad("null out");
     auto* s = new (std::nothrow) sair_frontier_set_s();
     if (!s) return SAIR_ENOMEM;
-    sair_status st = guard([&] { sair::frontier_set_init(s, P, l_max_ms, c_max, device); });
+    sair_status st = guard(__func__, [&] { sair::frontier_set_init(s, P, l_max_ms, c_max, device); });
     if (st != SAIR_OK) {
         delete s;
         return st;
@@ -626,7 +636,7 @@ sair_status sair_frontier_set_create(size_t P, double l_max_ms, double c_max, in
 
 sair_status sair_frontier_set_destroy(sair_frontier_set_t s) {
     if (!s) return SAIR_OK;
-    sair_status st = guard([&] { sair::frontier_set_free(s); });
+    sair_status st = guard(__func__, [&] { sair::frontier_set_free(s); });
     delete s;
     return st;
 }
@@ -636,13 +646,13 @@ sair_status sair_frontier_set_step(sair_frontier_set_t s, const sair_reward_inpu
                                    const sair_reward_config* cfg, sair_reward_breakdown* out) {
     if (!s || !cfg || (s->P && (!in || !out || !update)) || (s->P && stages && !deltas))
         return bad("null input");
-    return guard([&] { sair::frontier_set_step(s, in, deltas, stages, update, cfg, out); });
+    return guard(__func__, [&] { sair::frontier_set_step(s, in, deltas, stages, update, cfg, out); });
 }
 
 sair_status sair_frontier_set_points(sair_frontier_set_t s, size_t p, double* l, double* c,
                                      size_t cap, size_t* F, double* hypervolume) {
     if (!s || !F) return bad("null input");
-    return guard([&] { *F = sair::frontier_set_points(s, p, l, c, cap, hypervolume); });
+    return guard(__func__, [&] { *F = sair::frontier_set_points(s, p, l, c, cap, hypervolume); });
 }
 
 }  // extern "C"
@@ -651,7 +661,7 @@ sair_status sair_frontier_set_points(sair_frontier_set_t s, size_t p, double* l,
 
 sair_status sair_comm_create(const int* devices, int ndev, sair_comm_t* out) {
     if (!out || !devices) return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         auto* c = new sair_comm_s();
         try {
             sair::comm_create(devices, ndev, c);
@@ -666,7 +676,7 @@ sair_status sair_comm_create(const int* devices, int ndev, sair_comm_t* out) {
 
 sair_status sair_comm_destroy(sair_comm_t c) {
     if (!c) return SAIR_OK;
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::comm_free(c);
         delete c;
     });
@@ -681,7 +691,7 @@ sair_status sair_comm_info(sair_comm_t c, int* ndev, int* nccl) {
 
 sair_status sair_sharded_create(sair_comm_t c, double r_min, size_t capacity, sair_sharded_t* out) {
     if (!c || !out) return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         auto* h = new sair_sharded_s();
         try {
             sair::sharded_init(h, c, r_min, capacity);
@@ -696,7 +706,7 @@ sair_status sair_sharded_create(sair_comm_t c, double r_min, size_t capacity, sa
 
 sair_status sair_sharded_destroy(sair_sharded_t h) {
     if (!h) return SAIR_OK;
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::sharded_free(h);
         delete h;
     });
@@ -708,7 +718,7 @@ sair_status sair_sharded_append(sair_sharded_t h, const double* ctx, size_t coun
     if (!h) return bad("null handle");
     if (count && (!ctx || !reward)) return bad("null input");
     if (dim <= 0) return bad("experience store: dimension must be positive");
-    return guard([&] {
+    return guard(__func__, [&] {
         const size_t a = sair::sharded_append(h, ctx, count, dim, reward, round, accepted);
         if (n_accepted) *n_accepted = a;
     });
@@ -718,7 +728,7 @@ sair_status sair_sharded_append_synthetic(sair_sharded_t h, uint64_t seed, size_
                                           int clustered) {
     if (!h) return bad("null handle");
     if (dim <= 0) return bad("experience store: dimension must be positive");
-    return guard([&] { sair::sharded_append_synthetic(h, seed, count, dim, clustered); });
+    return guard(__func__, [&] { sair::sharded_append_synthetic(h, seed, count, dim, clustered); });
 }
 
 sair_status sair_sharded_size(sair_sharded_t h, size_t* n, uint64_t* rejected, size_t* shard_n) {
@@ -732,7 +742,7 @@ sair_status sair_sharded_size(sair_sharded_t h, size_t* n, uint64_t* rejected, s
 
 sair_status sair_sharded_effective_sigma(sair_sharded_t h, double sigma_sim, double* out) {
     if (!h || !out) return bad("null input");
-    return guard([&] { *out = sair::sharded_effective_sigma(h, sigma_sim); });
+    return guard(__func__, [&] { *out = sair::sharded_effective_sigma(h, sigma_sim); });
 }
 
 sair_status sair_store_select_sharded(sair_sharded_t h, const double* queries, size_t nq, int dim,
@@ -741,7 +751,7 @@ sair_status sair_store_select_sharded(sair_sharded_t h, const double* queries, s
     if (!h) return bad("null handle");
     if (nq && (!queries || !out_idx || !out_sim || !out_score || !out_count))
         return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         sair::sharded_select(h, queries, nq, dim, defaults(cfg), out_idx, out_sim, out_score,
                              out_count);
     });
@@ -751,7 +761,7 @@ sair_status sair_frontier_insert_batch_sharded(sair_comm_t c, sair_frontier_t f,
                                                size_t T, size_t* new_size) {
     if (!c || !f) return bad("null handle");
     if (T && !pts) return bad("null input");
-    return guard([&] {
+    return guard(__func__, [&] {
         const size_t F = sair::frontier_insert_batch_sharded(c, f, pts, T);
         if (new_size) *new_size = F;
     });

@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
     float* ss = cs + DP * QB;                           // [DP]
     uint64_t* full = reinterpret_cast<uint64_t*>(ss + DP);
     uint64_t* empty = full + 8;
-    float* thr = reinterpret_cast<float*>(empty + 4);
+    // (8 slots each: nst goes up to 8 -- racecheck caught empty[4..7] overlapping thr)
+    float* thr = reinterpret_cast<float*>(empty + 8);
     int* cnt = reinterpret_cast<int*>(thr + 2 * QB);
     uint32_t* hist = reinterpret_cast<uint32_t*>(cnt + 2 * QB);
     float* lkey = reinterpret_cast<float*>(hist + CONS_WARPS * 256);
@@ -235,6 +236,10 @@ __global__ void __launch_bounds__(STREAM_THREADS, 1)
         consumer_sync();
         bool need = false;
         for (int L = 0; L < nl; ++L) need |= cnt[L] > lcap(L) - 2 * CONS_THREADS;
+        // every consumer has read the counts before any compaction rewrites
+        // one (racecheck: a warp could otherwise see a rewritten count and
+        // skip the barriers below while the others take them)
+        consumer_sync();
         if (need) {
             for (int L = warp; L < nl; L += CONS_WARPS) {
                 if (cnt[L] > lcap(L) - 2 * CONS_THREADS) {

@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(MMA_THREADS, 1)
         // one compaction per list at the end
         for (int L = warp; L < nl; L += MW) {
             const int c = min(cnt[L], lcap(L));
+            __syncwarp();  // every lane has read the count before lane 0 rewrites it
             if (c > lk(L)) {
                 warp_keep_topk(lkey + lbase(L), lidx + lbase(L), c, lk(L), hist + warp * 256, lane);
                 if (lane == 0) cnt[L] = lk(L);

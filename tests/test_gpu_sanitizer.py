@@ -1,0 +1,50 @@
+"""compute-sanitizer over every kernel family (scripts/sanitize_workload.py):
+memcheck and synccheck on all of them; racecheck on the Pareto kernels, the
+decision step and the select paths of the CUDA cores (SAIR_NO_MMA /
+SAIR_NO_WIDE).  The tcgen05 passes order their shared record-constant ring
+through tcgen05.commit -> mbarrier -> TMA completion chains, which racecheck
+does not model: on those kernels it reports write-after-read hazards on that
+ring even though every write waits (through the chain) on the reads' release
+-- recorded in DESIGN.md "Hygiene", not asserted here."""
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = Path(__file__).resolve().parents[1]
+WORK = ROOT / "scripts" / "sanitize_workload.py"
+CS = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+def run(tool, part, extra_env=None):
+    env = dict(os.environ)
+    env.update(extra_env or {})
+    r = subprocess.run([CS, "--tool", tool, "--error-exitcode", "9", "--print-limit", "10",
+                        "python", str(WORK), part], capture_output=True, text=True, timeout=900,
+                       env=env)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "workload done" in out
+    return out
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+@pytest.mark.parametrize("part", ["select", "pareto", "decision"])
+def test_memcheck_synccheck_clean(tool, part):
+    out = run(tool, part)
+    assert "ERROR SUMMARY: 0 errors" in out
+
+
+@pytest.mark.parametrize("part,env", [("pareto", {}), ("decision", {}),
+                                      ("select", {"SAIR_NO_MMA": "1", "SAIR_NO_WIDE": "1"})])
+def test_racecheck_clean(part, env):
+    out = run("racecheck", part, env)
+    assert "0 hazards displayed (0 errors, 0 warnings)" in out
