@@ -372,7 +372,9 @@ def run_ours(a, rank, world, local_rank):
         out["query_shards" if other["split"] == "queries" else "record_shards"] = other
     if rank == 0 and world == 1 and not a.no_pareto:
         out["config1"] = bench_config1(dev)
+        out["config1_traces"] = bench_config1_traces()
         out["config2"] = bench_config2(dev, a.steps)
+        out["config2_lambda"] = bench_config2(dev, 3, lam=0.1)
         out["config5_step"] = bench_decision_step(buf, dev)
     if rank == 0 and not a.no_pareto:
         out["pareto"] = bench_pareto(dev)
@@ -385,6 +387,21 @@ def run_ours(a, rank, world, local_rank):
     if dist:
         dist.destroy_process_group()
     return out
+
+
+def bench_config1_traces():
+    """configs[0] on the bundled traces (scripts/harness_time.py): the
+    reference's unmodified decision loop over a 10k-record store harvested
+    from proj/scenarios, with the reference's own classes vs the drop-in;
+    byte-identical episode logs and stores required."""
+    if not (ROOT / "oracle" / "_ref" / "harness_ref").exists():
+        return {"unavailable": "oracle/_ref harness binaries not built"}
+    r = subprocess.run([sys.executable, str(ROOT / "scripts" / "harness_time.py")],
+                       capture_output=True, text=True, timeout=1800,
+                       env=dict(os.environ, ROUNDS="20"))
+    if r.returncode != 0:
+        return {"unavailable": r.stderr.strip().splitlines()[-1][:200] if r.stderr else "failed"}
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
 def bench_config1(dev, steps=50):
@@ -469,17 +486,20 @@ def bench_decision_step(buf, dev, P=30000, steps=3):
             "reward_and_store_ms": round(times["reward_store"] / steps * 1e3, 3)}
 
 
-def bench_config2(dev, steps):
-    """configs[1]: 1M x 64 store, 256-query batches, k = 32, one GPU."""
+def bench_config2(dev, steps, lam=0.0):
+    """configs[1]: 1M x 64 store, 256-query batches, k = 32, one GPU; lam =
+    0.1 (the reference's default lambda_div, experience.hpp:29): the greedy's
+    steps over the whole store, fp32-filtered and fp64-decided
+    (select_greedy32.cu)."""
     import torch
     import paper_2601_22397_b200 as sair
     from paper_2601_22397_b200 import synth
     n, nq = 1 << 20, 256
     buf = sair.ExperienceBuffer(0.0, device=dev)
     buf.store_synthetic(SEED + 1, n, DIM)
-    cfg = sair.SelectionConfig(m=K_SEL, lambda_div=0.0)
+    cfg = sair.SelectionConfig(m=K_SEL, lambda_div=lam)
     qs = synth.queries(SEED + 2, (3 + steps) * nq, DIM).reshape(3 + steps, nq, DIM)
-    for i in range(3):
+    for i in range(1 if lam else 3):
         buf.select_batch(qs[i], cfg)
     stream = torch.cuda.ExternalStream(buf.stream_ptr(), device=dev)
     torch.cuda.synchronize()
@@ -493,13 +513,21 @@ def bench_config2(dev, steps):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     hbm_peak, bf16_peak, peak_kind = measured_peaks()
-    qw = stats[0]["qb"] if stats[0]["tensor_core"] == 2 else 0
+    qw = stats[0]["qb"] if stats[0]["tensor_core"] in (2, 3) else 0
     roof = _stream_roofline(stats, n, hbm_peak, peak_kind, bf16_peak, qw)
     del buf
-    return {"workload": f"configs[1]: {n} records x d={DIM}, {nq}-query batch, k={K_SEL}",
-            "value": round(steps * nq / (ms / 1e3), 1), "unit": "queries/s",
-            "ms_per_step": round(ms / steps, 4), "roofline": roof,
-            "certified_queries": sum(s["certified"] for s in stats)}
+    out = {"workload": f"configs[1]: {n} records x d={DIM}, {nq}-query batch, k={K_SEL}, "
+                       f"lambda_div={lam}",
+           "value": round(steps * nq / (ms / 1e3), 1), "unit": "queries/s",
+           "ms_per_step": round(ms / steps, 4),
+           "certified_queries": sum(s["certified"] for s in stats)}
+    if lam:
+        out["greedy32_queries"] = sum(s["greedy32"] for s in stats)
+        out["candidates_per_query_step"] = round(
+            sum(s["greedy32_candidates"] for s in stats) / max(1, steps * nq * K_SEL), 3)
+    else:
+        out["roofline"] = roof
+    return out
 
 
 def bench_pareto(dev):

@@ -116,6 +116,14 @@ struct sair_store_s {
     int32_t* rnd = nullptr;  // [cap] rounds (tie-break)
     double* x64 = nullptr;   // [cap][d] exact contexts (record-major, refine/gather)
 
+    // appends: a copy stream and two pinned / device staging buffers, so a
+    // chunk's host->device copy overlaps the previous chunk's scatter and
+    // whatever the compute stream runs
+    cudaStream_t cst = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_scattered[2] = {nullptr, nullptr};
+    sair::HBuf h_app[2];
+    sair::DBuf b_app[2];
+    int app_slot = 0;
     // scratch
     sair::DBuf b_stage, b_cand, b_merged, b_thr, b_z, b_consts, b_out, b_exact, b_sigma, b_red;
     sair::HBuf h_stage, h_out, h_mmab, h_consts;

@@ -8,6 +8,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <new>
 #include <cstring>
 
 #include "internal.hpp"
@@ -148,7 +149,12 @@ void store_init(sair_store_s* s, double r_min, int device, size_t capacity_hint)
     s->r_min = r_min;
     DeviceGuard g(device);
     SAIR_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+    SAIR_CUDA(cudaStreamCreateWithFlags(&s->cst, cudaStreamNonBlocking));
     for (auto& e : s->ev) SAIR_CUDA(cudaEventCreate(&e));
+    for (int i = 0; i < 2; ++i) {
+        SAIR_CUDA(cudaEventCreateWithFlags(&s->ev_copied[i], cudaEventDisableTiming));
+        SAIR_CUDA(cudaEventCreateWithFlags(&s->ev_scattered[i], cudaEventDisableTiming));
+    }
     s->cap = 0;
     (void)capacity_hint;  // capacity is fixed once the dimension is known
     s->last = sair_select_stats{};
@@ -180,6 +186,17 @@ void store_free(sair_store_s* s) {
                     &s->b_wlists, &s->b_pl, &s->b_hot, &s->b_pages16, &s->b_pl16})
         b->release();
     s->pages16_n = 0;
+    if (s->cst) cudaStreamSynchronize(s->cst);
+    for (int i = 0; i < 2; ++i) {
+        s->h_app[i].~HBuf();
+        new (&s->h_app[i]) HBuf();
+        s->b_app[i].release();
+        if (s->ev_copied[i]) cudaEventDestroy(s->ev_copied[i]);
+        if (s->ev_scattered[i]) cudaEventDestroy(s->ev_scattered[i]);
+        s->ev_copied[i] = s->ev_scattered[i] = nullptr;
+    }
+    if (s->cst) cudaStreamDestroy(s->cst);
+    s->cst = nullptr;
     for (auto& e : s->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : s->gev) cudaEventDestroy(e);
@@ -250,7 +267,11 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
     std::string err;
     while (done < count && err.empty()) {
         size_t take = std::min(chunk, count - done);
-        double* hx = s->h_stage.as<double>(take * (size_t)dim + 2 * take);
+        // this chunk's pinned staging: free once its previous copy (two chunks
+        // or calls ago) has landed
+        const int slot = s->app_slot;
+        SAIR_CUDA(cudaEventSynchronize(s->ev_copied[slot]));
+        double* hx = s->h_app[slot].as<double>(take * (size_t)dim + 2 * take);
         double* hr = hx + take * (size_t)dim;
         int32_t* hround = reinterpret_cast<int32_t*>(hr + take);
         size_t k = 0;
@@ -287,20 +308,31 @@ size_t store_append(sair_store_s* s, const double* ctx, size_t count, int dim,
         if (k) {
             store_reserve(s, s->n + k);
             size_t xb = k * (size_t)dim * sizeof(double);
-            char* dst = static_cast<char*>(s->b_stage.get(xb + k * 12 + 64));
+            // The copy runs on the store's copy stream (overlapping the compute
+            // stream's work: a select in flight, the previous chunk's scatter);
+            // the scatter waits for it on the compute stream, so every later
+            // pass sees the rows; the device staging of this slot is rewritten
+            // only after its previous scatter
+            SAIR_CUDA(cudaStreamWaitEvent(s->cst, s->ev_scattered[slot], 0));
+            void* before = s->b_app[slot].p;
+            char* dst = static_cast<char*>(s->b_app[slot].get(xb + k * 12 + 64));
+            if (dst != before) SAIR_CUDA(cudaStreamSynchronize(s->st));  // (reallocated)
             double* dx = reinterpret_cast<double*>(dst);
             double* dr = reinterpret_cast<double*>(dst + xb);
             int32_t* dround = reinterpret_cast<int32_t*>(dst + xb + k * 8);
-            SAIR_CUDA(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, s->st));
-            SAIR_CUDA(cudaMemcpyAsync(dr, hr, k * 8, cudaMemcpyHostToDevice, s->st));
-            SAIR_CUDA(cudaMemcpyAsync(dround, hround, k * 4, cudaMemcpyHostToDevice, s->st));
+            SAIR_CUDA(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, s->cst));
+            SAIR_CUDA(cudaMemcpyAsync(dr, hr, k * 8, cudaMemcpyHostToDevice, s->cst));
+            SAIR_CUDA(cudaMemcpyAsync(dround, hround, k * 4, cudaMemcpyHostToDevice, s->cst));
+            SAIR_CUDA(cudaEventRecord(s->ev_copied[slot], s->cst));
+            SAIR_CUDA(cudaStreamWaitEvent(s->st, s->ev_copied[slot], 0));
             size_t work = k * (size_t)std::max(s->dp, s->d);
             int blocks = (int)std::min<size_t>((work + 255) / 256, 148 * 16);
             scatter_rows_kernel<<<blocks, 256, 0, s->st>>>(dx, dr, dround, s->n, k, s->d, s->dp,
                                                            s->pages, s->r32, s->r64, s->rnd,
                                                            s->x64, s->d_shift);
             SAIR_LAUNCH("scatter_rows_kernel");
-            SAIR_CUDA(cudaStreamSynchronize(s->st));  // staging is reused next chunk
+            SAIR_CUDA(cudaEventRecord(s->ev_scattered[slot], s->st));
+            s->app_slot ^= 1;
             s->n += k;
             n_acc += k;
         }
@@ -484,6 +516,10 @@ double store_effective_sigma(sair_store_s* s, double sigma_sim) {
 }
 
 void store_clone(const sair_store_s* s, sair_store_s* o) {
+    {  // the source's enqueued appends complete before its arrays are copied
+        DeviceGuard g(s->device);
+        SAIR_CUDA(cudaStreamSynchronize(s->st));
+    }
     store_init(o, s->r_min, s->device, 0);
     o->rejected = s->rejected;
     o->gbase = s->gbase;
