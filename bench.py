@@ -398,7 +398,7 @@ def bench_config1_traces():
         return {"unavailable": "oracle/_ref harness binaries not built"}
     r = subprocess.run([sys.executable, str(ROOT / "scripts" / "harness_time.py")],
                        capture_output=True, text=True, timeout=1800,
-                       env=dict(os.environ, ROUNDS="20"))
+                       env=dict(os.environ, ROUNDS1="40", ROUNDS2="160"))
     if r.returncode != 0:
         return {"unavailable": r.stderr.strip().splitlines()[-1][:200] if r.stderr else "failed"}
     return json.loads(r.stdout.strip().splitlines()[-1])

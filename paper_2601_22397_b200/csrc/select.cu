@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(1024)
     const int total = G * K;
     __shared__ uint32_t hist[256];
     __shared__ uint32_t sh_bin, sh_r, sh_pop, sh_cnt, sh_valid;
-    __shared__ unsigned long long skey[512];
+    constexpr int FAST = 2048;  // >= kp, knn (<= 512)
+    __shared__ unsigned long long skey[FAST];
     const int tid = threadIdx.x, lane = tid & 31;
     auto comp = [&](int e) {
         const int g = e / K, j = e - g * K;
@@ -378,6 +379,29 @@ __global__ void __launch_bounds__(1024)
         sh_cnt = 0;
         sh_valid = 0;
     }
+    __syncthreads();
+    // Fast path: the CTAs' lists are mostly padding (a pass's start threshold
+    // admits a few K' records per query over the whole store): gather the
+    // valid entries into shared memory and sort them there when they fit.
+    for (int e = tid; e < total; e += blockDim.x) {
+        const unsigned long long u = comp(e);
+        if ((u >> 32) > PAD_TOP) {
+            const uint32_t p = atomicAdd(&sh_valid, 1u);
+            if (p < (uint32_t)FAST) skey[p] = u;
+        }
+    }
+    __syncthreads();
+    const uint32_t nvf = sh_valid;
+    int P = 1;
+    while (P < K) P <<= 1;
+    if (nvf <= (uint32_t)FAST) {
+        while (P < (int)nvf) P <<= 1;
+        for (int j = (int)nvf + tid; j < P; j += blockDim.x)
+            skey[j] = j < K ? ((PAD_TOP << 32) | (unsigned long long)(uint32_t)j) : 0ull;
+        __syncthreads();
+    } else {
+    if (tid == 0) sh_valid = 0;
+    __syncthreads();
     unsigned long long prefix = 0, pmask = 0;
     uint32_t r = (uint32_t)K;
     bool all_valid = false;
@@ -443,8 +467,6 @@ __global__ void __launch_bounds__(1024)
         }
     }
     // composites are unique: exactly K entries (or every valid one) qualify
-    int P = 1;
-    while (P < K) P <<= 1;
     for (int j = tid; j < P; j += blockDim.x) skey[j] = 0ull;
     __syncthreads();
     for (int e = tid; e < total; e += blockDim.x) {
@@ -457,6 +479,7 @@ __global__ void __launch_bounds__(1024)
     for (int j = (int)sh_cnt + tid; j < K; j += blockDim.x)
         skey[j] = (PAD_TOP << 32) | (unsigned long long)(uint32_t)j;
     __syncthreads();
+    }  // radix path
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int t = tid; t < P / 2; t += blockDim.x) {

@@ -68,7 +68,7 @@ def test_config3_16m_4096_queries_vs_oracle(orc):
     xq = synth.queries(seed + 1, nq, d)
     got = db.select_batch(xq, sair.SelectionConfig(m=m, lambda_div=0.0), nearest=True)
     st = db.last_stats()
-    assert st["tensor_core"] == 2 and st["stream_launches"] == nq // st["qb"], st
+    assert st["tensor_core"] == 3 and st["stream_launches"] == nq // st["qb"], st
     assert st["certified"] == nq and st["exact_fallbacks"] == 0, st
     ctx, rew, rnd = host_store(orc, seed, n, d)
     stats = orc.stats(ctx)
