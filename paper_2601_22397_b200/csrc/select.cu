@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(1024)
             skey[j] = j < K ? ((PAD_TOP << 32) | (unsigned long long)(uint32_t)j) : 0ull;
         __syncthreads();
     } else {
+    __syncthreads();  // (every thread has read nvf before the counter is reused)
     if (tid == 0) sh_valid = 0;
     __syncthreads();
     unsigned long long prefix = 0, pmask = 0;

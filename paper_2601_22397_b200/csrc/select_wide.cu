@@ -1106,25 +1106,30 @@ __global__ void __launch_bounds__(WIDE_THREADS, 1)
 
 // Start thresholds from the sample's S block maxima of list L (S up to 4 * 8192):
 // tsafe[L] <= the K-th largest (distinct records: <= the store's K-th key, so
-// at least K records pass), t0[L] = the J-th largest for selection lists
-// (J < K: an estimate -- ~J / f records of the store beat it, f the sampled
-// fraction -- that admits a few times m records instead of ~K / f).  Any
-// threshold is sound (the certification bound takes max(t0, K'-th kept
+// at least K records pass) and, for selection lists, t0[L] = the highest
+// threshold at which an estimate of the store's passers reaches `target`
+// (a few K' -- instead of ~K' / f).  The first Su maxima come from the
+// uniform sample (fraction fu of the pages: each stands for 1 / fu records),
+// the rest from the highest-residual pages, which are read whole (each
+// stands for itself): est(t) = U(t) / fu + H(t).  Treating the hot pages as
+// uniform would put t0 among a concentrated batch's keys and admit too few.
+// Any threshold is sound (the certification bound takes max(t0, K'-th kept
 // key)); a query whose pool then falls short of certifying gets one more
-// pass from tsafe.  One histogram over the ordinal range present; a bin's
+// pass from tsafe.  Histograms over the ordinal range present; a bin's
 // lower edge, lowered by a relative 1e-6.  Fewer than K non-empty maxima: no
 // threshold (-FLT_MAX).
 __global__ void __launch_bounds__(1024)
-    wide_kth_kernel(const float* __restrict__ smax, uint32_t S, int QW, int kp, int knn, int jsel,
-                    float tmargin, float* __restrict__ t0, float* __restrict__ tsafe) {
+    wide_kth_kernel(const float* __restrict__ smax, uint32_t S, uint32_t Su, int QW, int kp, int knn,
+                    float inv_fu, float target, float tmargin, float* __restrict__ t0,
+                    float* __restrict__ tsafe) {
     constexpr int NB = 2048;
-    __shared__ uint32_t hist[NB];
+    __shared__ uint32_t hist[NB], histu[NB];
     __shared__ uint32_t sh_lo, sh_hi, sh_bin[2], sh_valid;
     const int L = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
     const uint32_t K = (uint32_t)(L < QW ? kp : knn);
-    const uint32_t J = L < QW ? min((uint32_t)max(jsel, 1), K) : K;
+    const bool est = L < QW && target > 0.f;
     const float* v = smax + (size_t)L * S;
-    for (int b = tid; b < NB; b += blockDim.x) hist[b] = 0;
+    for (int b = tid; b < NB; b += blockDim.x) hist[b] = histu[b] = 0;
     if (tid == 0) {
         sh_lo = 0xFFFFFFFFu;
         sh_hi = 0;
@@ -1161,35 +1166,50 @@ __global__ void __launch_bounds__(1024)
     const int sh = span < NB ? 0 : (32 - __clz(span)) - 11;
     for (uint32_t i = tid; i < S; i += blockDim.x) {
         const uint32_t o = f2ord(v[i]);
-        if (o > (uint32_t)PAD_TOP) atomicAdd(&hist[(o - blo) >> sh], 1u);
+        if (o > (uint32_t)PAD_TOP) {
+            atomicAdd(&hist[(o - blo) >> sh], 1u);
+            if (est && i < Su) atomicAdd(&histu[(o - blo) >> sh], 1u);
+        }
     }
     __syncthreads();
-    if (tid < 64) {  // warp 0: the bin where the count from the top reaches K; warp 1: J
-        const uint32_t T = tid < 32 ? K : J;
-        uint32_t sum = 0;
-        for (int j = 0; j < NB / 32; ++j) sum += hist[NB - 1 - (lane * (NB / 32) + j)];
-        uint32_t incl = sum;
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += t;
-        }
-        const uint32_t excl = incl - sum;
-        const unsigned own = __ballot_sync(0xffffffffu, excl < T && T <= incl);
-        if (lane == __ffs(own) - 1) {
-            uint32_t c = excl;
+    if (tid < 64) {
+        // warp 0: the bin where the count from the top reaches K; warp 1 (the
+        // estimate): where U / fu + H -- with H = all - U -- reaches target
+        const bool w1 = tid >= 32;
+        if (!w1 || est) {
+            float sum = 0.f;
             for (int j = 0; j < NB / 32; ++j) {
                 const int b = NB - 1 - (lane * (NB / 32) + j);
-                c += hist[b];
-                if (c >= T) {
-                    sh_bin[tid >> 5] = (uint32_t)b;
-                    break;
+                sum += w1 ? (float)histu[b] * inv_fu + (float)(hist[b] - histu[b]) : (float)hist[b];
+            }
+            float incl = sum;
+            for (int o = 1; o < 32; o <<= 1) {
+                const float t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const float T = w1 ? target : (float)K;
+            const float excl = incl - sum;
+            const unsigned own = __ballot_sync(0xffffffffu, excl < T && T <= incl);
+            if (lane == __ffs(own) - 1) {
+                float c = excl;
+                for (int j = 0; j < NB / 32; ++j) {
+                    const int b = NB - 1 - (lane * (NB / 32) + j);
+                    c += w1 ? (float)histu[b] * inv_fu + (float)(hist[b] - histu[b]) : (float)hist[b];
+                    if (c >= T) {
+                        sh_bin[w1 ? 1 : 0] = (uint32_t)b;
+                        break;
+                    }
                 }
             }
         }
     }
     __syncthreads();
     if (tid == 0) {
-        const float es = ord2f(blo + (sh_bin[0] << sh)), ea = ord2f(blo + (sh_bin[1] << sh));
+        const float es = ord2f(blo + (sh_bin[0] << sh));
+        // (the estimate never goes below the guaranteed threshold; no bin
+        // reaching the target: the guaranteed one)
+        const uint32_t ba = sh_bin[1] == 0xFFFFFFFFu ? sh_bin[0] : max(sh_bin[1], sh_bin[0]);
+        const float ea = est ? ord2f(blo + (ba << sh)) : es;
         // (tmargin: the stream pass's keys may round below the sample's,
         // bf16 against TF32 records; only the pool's fill depends on it)
         const float m = L < QW ? tmargin : 0.f;
@@ -1367,13 +1387,12 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
                                         WIDE_THREADS, pl.smem, s->st>>>(a);
         SAIR_LAUNCH("stream_wide_kernel(sample)");
         // the selection lists' start: ~aggr K' records of the store above it
-        // (an estimate from the sampled fraction; SAIR_WIDE_AGGR=0: the safe K'-th)
+        // (an estimate from the sample; SAIR_WIDE_AGGR=0: the guaranteed K'-th)
         const double aggr = std::getenv("SAIR_WIDE_AGGR") ? std::atof(std::getenv("SAIR_WIDE_AGGR")) : 2.5;
-        const double frac = std::min(1.0, (double)(pl.spages + a.nhot) / (double)a.npages);
-        int jsel = pl.kp;
-        if (aggr > 0.0) jsel = std::max(4, std::min(pl.kp, (int)std::ceil(aggr * pl.kp * frac)));
+        const double fu = std::min(1.0, (double)pl.spages / (double)a.npages);
         wide_kth_kernel<<<pl.knn ? 2 * QW : QW, 1024, 0, s->st>>>(
-            dsmax, (uint32_t)S4, QW, pl.kp, pl.knn, jsel, tmargin, dt0, dc + nc + n16);
+            dsmax, (uint32_t)S4, (uint32_t)(4 * pl.spages), QW, pl.kp, pl.knn, (float)(1.0 / fu),
+            (float)(aggr * pl.kp), tmargin, dt0, dc + nc + n16);
         SAIR_LAUNCH("wide_kth_kernel");
     }
     SAIR_CUDA(cudaEventRecord(io.e_mid, s->st));

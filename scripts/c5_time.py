@@ -6,3 +6,5 @@ import paper_2601_22397_b200 as sair
 buf = sair.ExperienceBuffer(0.0)
 buf.store_synthetic(bench.SEED, bench.N_RECORDS, bench.DIM)
 print(os.environ.get("TAG", ""), json.dumps(bench.bench_decision_step(buf, 0)), flush=True)
+st = buf.last_stats()
+print({k: st[k] for k in ("retried", "certified", "tensor_core", "qb", "candidates")}, flush=True)

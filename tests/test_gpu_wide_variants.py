@@ -97,3 +97,23 @@ def test_bf16_copy_follows_appends(orc):
     oi, osim, osc, ocnt = orc.select_batch(ctx, rw, rd, xq[pick], 16, 0.0, sigma)
     assert np.array_equal(idx[pick], oi)
     assert near(sc[pick], osc, 1e-12)
+
+
+def test_merge_beyond_shared_capacity():
+    """Guaranteed start thresholds on a 8M-record store list more than 2048
+    entries per query across the CTAs, so the merge takes its radix path
+    (select.cu merge_kernel); the picks must equal the estimated-threshold
+    pass's exactly (both are certified-exact)."""
+    n, d = 1 << 23, 64
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(2026, n, d)
+    xq = synth.queries(7, 4096, d)
+    cfg = SelectionConfig(m=32, lambda_div=0.0)
+    a = db.select_batch(xq, cfg)
+    assert db.last_stats()["certified"] == 4096
+    with env(SAIR_WIDE_AGGR=0):
+        b = db.select_batch(xq, cfg)
+        st = db.last_stats()
+    assert st["certified"] == 4096, st
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
