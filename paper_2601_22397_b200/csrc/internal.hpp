@@ -167,6 +167,7 @@ struct sair_frontier_s {
     std::vector<double> hl, hc;  // host mirror for points()
     sair::DBuf b_tmp, b_in, b_out, b_sort;
     sair::HBuf h_io;
+    cudaEvent_t ev_tail = nullptr;  // decision step: reward / frontier work done (pareto.cu)
 };
 
 // ----------------------------------------------------------- frontier set --

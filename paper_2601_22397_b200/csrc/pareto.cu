@@ -1184,6 +1184,8 @@ void frontier_free(sair_frontier_s* f) {
     f->b_in.release();
     f->b_out.release();
     f->b_sort.release();
+    if (f->ev_tail) cudaEventDestroy(f->ev_tail);
+    f->ev_tail = nullptr;
     if (f->st) cudaStreamDestroy(f->st);
     f->st = nullptr;
 }
@@ -1829,11 +1831,11 @@ struct DecisionTail {
     double* out;           // [7] breakdown | [2] insert result | hv | pad | fl [F0+1] | fc [F0+1]
 };
 
-// Everything after the select, one CTA: compute_reward against the frontier
-// before the update (reward.cpp:21-44), insert_normalized (pareto.cpp:43-54)
-// and its commit, hypervolume() (pareto.cpp:56-65), and the store() row
-// behind the r_min gate on the reward total (experience.cpp:45-48).
-__global__ void __launch_bounds__(1024) decision_tail_kernel(const DecisionTail a) {
+// The decision's reward side, one CTA on the frontier's stream (it does not
+// depend on the select, so it runs beside it): compute_reward against the
+// frontier before the update (reward.cpp:21-44), insert_normalized
+// (pareto.cpp:43-54) and its commit, hypervolume() (pareto.cpp:56-65).
+__global__ void __launch_bounds__(1024) decision_reward_kernel(const DecisionTail a) {
     __shared__ double srw[7];
     __shared__ unsigned long long sres[2];
     const int tid = threadIdx.x;
@@ -1873,7 +1875,13 @@ __global__ void __launch_bounds__(1024) decision_tail_kernel(const DecisionTail 
             reinterpret_cast<unsigned long long*>(a.out)[8] = sres[1];
         }
     }
-    const double r = srw[5];
+}
+
+// The store() row behind the r_min gate on the reward total (experience.cpp:
+// 45-48), on the store's stream after the select (which must not see it).
+__global__ void __launch_bounds__(128) decision_append_kernel(const DecisionTail a) {
+    const int tid = threadIdx.x;
+    const double r = a.out[5];
     if (!(r > a.r_min)) return;
     const int w = a.d > a.dp ? a.d : a.dp;  // x64 takes all d columns, the page dp
     for (int k = tid; k < w; k += blockDim.x) {
@@ -1924,19 +1932,8 @@ void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim
     store_reserve(s, s->n + 1);
     if (update) reserve(f, f->F + 1);
     const size_t F0 = f->F;
-    s->defer_sync = true;
-    try {
-        store_select(s, x, 1, dim, cfg, o_idx, o_sim, o_score, o_count, o_nn, o_nn_sim, nullptr,
-                     nullptr);
-    } catch (...) {
-        s->defer_sync = false;
-        s->pending = nullptr;
-        throw;
-    }
-    s->defer_sync = false;
-    const auto t1 = clk::now();
-    cudaStream_t st = s->st;
-    // one input copy, one kernel, one output copy after the select
+    // the reward side first, on the frontier's stream: one input copy, one
+    // kernel -- it overlaps the select
     const int d = s->d;
     const size_t dbytes = S * 4 * 4;
     const size_t xo = (32 + dbytes + 7) & ~(size_t)7;
@@ -1949,7 +1946,7 @@ void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim
     std::memcpy(hb + xo, x, (size_t)d * 8);
     double* dout = reinterpret_cast<double*>(dbase + ((inb + 255) & ~(size_t)255));
     double* hout = reinterpret_cast<double*>(hb + ((inb + 255) & ~(size_t)255));
-    SAIR_CUDA(cudaMemcpyAsync(dbase, hb, inb, cudaMemcpyHostToDevice, st));
+    SAIR_CUDA(cudaMemcpyAsync(dbase, hb, inb, cudaMemcpyHostToDevice, f->st));
     DecisionTail t{};
     t.in = reinterpret_cast<const double*>(dbase);
     t.deltas = reinterpret_cast<const int32_t*>(dbase + 32);
@@ -1980,8 +1977,27 @@ void decision_step(sair_store_s* s, sair_frontier_s* f, const double* x, int dim
     t.x64 = s->x64;
     t.shift = s->d_shift;
     t.out = dout;
-    decision_tail_kernel<<<1, 1024, 0, st>>>(t);
-    SAIR_LAUNCH("decision_tail_kernel");
+    decision_reward_kernel<<<1, 1024, 0, f->st>>>(t);
+    SAIR_LAUNCH("decision_reward_kernel");
+    if (!f->ev_tail) SAIR_CUDA(cudaEventCreateWithFlags(&f->ev_tail, cudaEventDisableTiming));
+    SAIR_CUDA(cudaEventRecord(f->ev_tail, f->st));
+    s->defer_sync = true;
+    try {
+        store_select(s, x, 1, dim, cfg, o_idx, o_sim, o_score, o_count, o_nn, o_nn_sim, nullptr,
+                     nullptr);
+    } catch (...) {
+        s->defer_sync = false;
+        s->pending = nullptr;
+        SAIR_CUDA(cudaStreamSynchronize(f->st));
+        throw;
+    }
+    s->defer_sync = false;
+    const auto t1 = clk::now();
+    cudaStream_t st = s->st;
+    // then, after the select on the store's stream: the new row
+    SAIR_CUDA(cudaStreamWaitEvent(st, f->ev_tail, 0));
+    decision_append_kernel<<<1, 128, 0, st>>>(t);
+    SAIR_LAUNCH("decision_append_kernel");
     SAIR_CUDA(cudaMemcpyAsync(hout, dout, (update ? outn : 7) * 8, cudaMemcpyDeviceToHost, st));
     const auto t2 = clk::now();
     SAIR_CUDA(cudaStreamSynchronize(st));

@@ -457,43 +457,50 @@ static size_t small_smem_bytes(size_t n, int d, size_t m, int cs, bool zs) {
 
 constexpr size_t SMALL_SMEM_MAX = 227 * 1024;
 
-// the kernel's shared-memory limit, raised once per size (the attribute call
-// costs ~1 us per launch otherwise), and whether a cluster of cs CTAs with
-// that much shared memory is schedulable (cs > 8 is a non-portable size: it
-// needs a GPC with 16 free SMs); remembered per process -- the pool's GPUs are
-// identical
+// the kernel's shared-memory limit (set once per variant, to the maximum:
+// the attribute only permits), and whether a cluster of cs CTAs with that
+// much shared memory is schedulable (cs > 8 is a non-portable size: it needs a
+// GPC with 16 free SMs) -- remembered per (variant, cs) as the largest size
+// known to fit and the smallest known not to (a decision step grows the store
+// by one record per call: no query per call)
 static bool small_cluster_ok(bool zs, int cs, size_t smem) {
     static std::mutex mu;
-    static std::vector<std::pair<size_t, bool>> seen;  // (zs | cs | smem, ok)
-    static size_t raised[2] = {0, 0};  // (only ever raised: earlier plans stay launchable)
+    struct Known {
+        size_t ok = 0, bad = SIZE_MAX;
+    };
+    static Known known[2][SMALL_CS_MAX16 + 1];
+    static bool raised[2] = {false, false};
     std::lock_guard<std::mutex> lk(mu);
-    const size_t key = ((size_t)zs << 40) | ((size_t)cs << 32) | smem;
-    for (const auto& k : seen)
-        if (k.first == key) return k.second;
     const void* fn = zs ? (const void*)small_select_kernel<true> : (const void*)small_select_kernel<false>;
-    if (smem > raised[zs]) {
-        SAIR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        raised[zs] = smem;
-    }
-    bool ok = true;
-    if (cs > 8) {
+    if (!raised[zs]) {
+        SAIR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SMALL_SMEM_MAX));
         SAIR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        cudaLaunchConfig_t oc{};
-        oc.gridDim = dim3((unsigned)cs);
-        oc.blockDim = dim3(SMALL_THREADS);
-        oc.dynamicSmemBytes = smem;
-        cudaLaunchAttribute ca[1];
-        ca[0].id = cudaLaunchAttributeClusterDimension;
-        ca[0].val.clusterDim.x = (unsigned)cs;
-        ca[0].val.clusterDim.y = 1;
-        ca[0].val.clusterDim.z = 1;
-        oc.attrs = ca;
-        oc.numAttrs = 1;
-        int nclusters = 0;
-        ok = cudaOccupancyMaxActiveClusters(&nclusters, fn, &oc) == cudaSuccess && nclusters >= 1;
-        if (!ok) cudaGetLastError();
+        raised[zs] = true;
     }
-    seen.push_back({key, ok});
+    if (cs <= 8) return true;
+    Known& k = known[zs][cs];
+    if (smem <= k.ok) return true;
+    if (smem >= k.bad) return false;
+    cudaLaunchConfig_t oc{};
+    oc.gridDim = dim3((unsigned)cs);
+    oc.blockDim = dim3(SMALL_THREADS);
+    oc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute ca[1];
+    ca[0].id = cudaLaunchAttributeClusterDimension;
+    ca[0].val.clusterDim.x = (unsigned)cs;
+    ca[0].val.clusterDim.y = 1;
+    ca[0].val.clusterDim.z = 1;
+    oc.attrs = ca;
+    oc.numAttrs = 1;
+    int nclusters = 0;
+    const bool ok = cudaOccupancyMaxActiveClusters(&nclusters, fn, &oc) == cudaSuccess && nclusters >= 1;
+    if (!ok) {
+        cudaGetLastError();
+        k.bad = smem;
+    } else {
+        k.ok = smem;
+    }
     return ok;
 }
 
