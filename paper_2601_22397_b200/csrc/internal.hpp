@@ -89,6 +89,11 @@ struct sair_store_s {
 
     double r_min = 0.0;
     uint64_t rejected = 0;
+    // lambda > 0: the last filtered attempt certified < 5 % of its queries
+    // (the penalty moves the picks far down the score order): later calls go
+    // straight to the filtered greedy, re-trying the pool every 16th call
+    int lam_pool_fail = 0;
+    uint32_t lam_probe = 0;
     int d = 0;   // 0 until the first accepted row fixes it (experience.cpp:49-54)
     int dp = 0;  // padded dimension of the fp32 page layout
     size_t n = 0, cap = 0;

@@ -1033,8 +1033,10 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     // the filter's certification bounds an outside record's gain by its score,
     // which needs lambda_div >= 0 (a negative lambda rewards similarity; the
     // reference accepts it, scenario.cpp:197): those queries take the exact paths
+    const bool lam_pos = cfg.lambda_div > 0.0;
+    const bool skip_pool = lam_pos && s->lam_pool_fail && (++s->lam_probe % 16u) != 0u;
     const bool fast = cfg.mode != SAIR_SELECT_EXACT && !cfg.locally_weighted_mean && d <= 128 &&
-                      n < (size_t)1 << 31 && m <= 256 && cfg.lambda_div >= 0.0;
+                      n < (size_t)1 << 31 && m <= 256 && cfg.lambda_div >= 0.0 && !skip_pool;
     float stream_ms = 0.f, prepass_ms = 0.f;
     if (fast) {
         // tensor-core streaming kernel when the shape fits,
@@ -1398,6 +1400,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
                 s->last.retried = rest.size();
             }
         }
+        if (lam_pos) s->lam_pool_fail = s->last.certified * 20 < nq ? 1 : 0;
     }
     if (small_ok) {  // the uncertified queries of a small store: one clustered launch
         std::vector<size_t> rest;
