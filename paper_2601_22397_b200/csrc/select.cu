@@ -1034,7 +1034,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
     // which needs lambda_div >= 0 (a negative lambda rewards similarity; the
     // reference accepts it, scenario.cpp:197): those queries take the exact paths
     const bool lam_pos = cfg.lambda_div > 0.0;
-    const bool skip_pool = lam_pos && s->lam_pool_fail && (++s->lam_probe % 16u) != 0u;
+    const bool force_pool = lam_pos && std::getenv("SAIR_LAM_POOL") != nullptr;  // (tests: always try)
+    const bool skip_pool =
+        lam_pos && !force_pool && s->lam_pool_fail && (++s->lam_probe % 16u) != 0u;
     const bool fast = cfg.mode != SAIR_SELECT_EXACT && !cfg.locally_weighted_mean && d <= 128 &&
                       n < (size_t)1 << 31 && m <= 256 && cfg.lambda_div >= 0.0 && !skip_pool;
     float stream_ms = 0.f, prepass_ms = 0.f;

@@ -55,7 +55,9 @@ def test_wide_variant_matches_oracle(orc, store, knobs, tc, lam):
     sigma = db.effective_sigma()
     xq = synth.queries(92, 256, 64)
     m = 32 if lam == 0.0 else 8
-    with env(**knobs):
+    # (SAIR_LAM_POOL: the filtered pool is tried at lambda > 0 even where an
+    # earlier call on this store found it certifying nothing)
+    with env(SAIR_LAM_POOL=1, **knobs):
         idx, sim, sc, cnt, nn_i, nn_s = db.select_batch(xq, SelectionConfig(m=m, lambda_div=lam),
                                                         nearest=True)
         st = db.last_stats()
