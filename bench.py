@@ -525,6 +525,23 @@ def bench_config2(dev, steps, lam=0.0):
         out["greedy32_queries"] = sum(s["greedy32"] for s in stats)
         out["candidates_per_query_step"] = round(
             sum(s["greedy32_candidates"] for s in stats) / max(1, steps * nq * K_SEL), 3)
+        nsteps = sum(s["greedy32_steps"] for s in stats)
+        if nsteps:
+            # the tensor-core greedy step (select_greedy32.cu): per step the
+            # fp32 gain of every (query, record) read and written (8 B) and
+            # the records' 3xTF32 operand image (hi + lo, 8 B per dimension)
+            step_ms = sum(s["greedy32_step_ms"] for s in stats) / nsteps
+            alg = nq * n * 8 + n * DIM * 8
+            achieved = alg / (step_ms / 1e3) / 1e9
+            out["roofline"] = {
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": alg, "avg_launch_ms": round(step_ms, 4),
+                "kernel": "sair::g32_mma_step_kernel (tcgen05 kind::tf32 3xTF32, 128 records x "
+                          "256 rows per tile, gain update + top-2 epilogue)",
+                "traffic": int(1.618604e9 + 1.119989e9),
+                "traffic_source": "ncu --set full, profiles/r02/h_g32mma_step_full_summary.txt "
+                                  "(dram__bytes_read.sum 1.6186 GB + dram__bytes_write.sum 1.1200 GB)"}
     else:
         out["roofline"] = roof
     return out

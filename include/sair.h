@@ -85,6 +85,8 @@ typedef struct {
     size_t retried;         /* queries given a second wide pass with raised thresholds */
     size_t greedy32;        /* queries whose greedy ran fp32-filtered, fp64-decided (lambda != 0) */
     size_t greedy32_candidates; /* (query, step) candidates verified in fp64 by that path */
+    float greedy32_step_ms;     /* device time of that path's step kernels (summed) */
+    int greedy32_steps;         /* and their launches (tensor-core step: 1 per greedy step) */
 } sair_select_stats;
 
 SAIR_API const char* sair_last_error(void);

@@ -37,7 +37,8 @@ class SelectStatsC(C.Structure):
                 ("stream_launches", C.c_int), ("stream_ms", C.c_float), ("total_ms", C.c_float),
                 ("prepass_ms", C.c_float), ("tensor_core", C.c_int), ("small", C.c_int),
                 ("retried", C.c_size_t), ("greedy32", C.c_size_t),
-                ("greedy32_candidates", C.c_size_t)]
+                ("greedy32_candidates", C.c_size_t), ("greedy32_step_ms", C.c_float),
+                ("greedy32_steps", C.c_int)]
 
 
 class RewardConfigC(C.Structure):

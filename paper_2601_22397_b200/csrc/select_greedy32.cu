@@ -854,8 +854,9 @@ void g32_steps(const G32Args& a, int nctas, cudaStream_t st) {
     SAIR_LAUNCH("g32 steps");
 }
 
+// ev: 2 want events (each step kernel's start, end), or empty
 void g32_steps_mma(const G32Args& a, const float* aimg, float* bimg, const float* q32,
-                   cudaStream_t st) {
+                   cudaStream_t st, const std::vector<cudaEvent_t>& ev) {
     static bool attr = false;
     if (!attr) {
         SAIR_CUDA(cudaFuncSetAttribute(g32_mma_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -871,7 +872,9 @@ void g32_steps_mma(const G32Args& a, const float* aimg, float* bimg, const float
             b.prow = a.ppick;
         }
         g32_mma_bimg_kernel<<<64, 256, 0, st>>>(b.row32, a.G, 64, bimg);
+        if (!ev.empty()) SAIR_CUDA(cudaEventRecord(ev[2 * step], st));
         g32_mma_step_kernel<<<grid, MT_THREADS, MT_SMEM, st>>>(b, aimg, bimg, step);
+        if (!ev.empty()) SAIR_CUDA(cudaEventRecord(ev[2 * step + 1], st));
         const size_t smem = (size_t)CMAX * (step + 1) * 8;
         if (smem > 48 * 1024)
             SAIR_CUDA(cudaFuncSetAttribute(g32_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1013,6 +1016,8 @@ bool greedy32_select(sair_store_s* s, const QueryPrep& p, const std::vector<size
     double* o_rew = o_score + G * m;
     int32_t* o_round = reinterpret_cast<int32_t*>(o_rew + G * m);
     s->last.greedy32_candidates = 0;
+    s->last.greedy32_step_ms = 0.f;
+    s->last.greedy32_steps = 0;
     for (size_t b0 = 0; b0 < nq; b0 += G) {
         const int g_n = (int)std::min(G, nq - b0);
         a.G = g_n;
@@ -1039,7 +1044,14 @@ bool greedy32_select(sair_store_s* s, const QueryPrep& p, const std::vector<size
         SAIR_CUDA(cudaMemsetAsync(a.overflow, 0, G * 4 + 64, s->st));
         a.row32 = q32;
         a.prow = q32 + G * DP;
-        if (mma) g32_steps_mma(a, aimg, bimg, q32, s->st);
+        if (mma) {
+            while (s->g32ev.size() < 2 * (size_t)want) {
+                cudaEvent_t e;
+                SAIR_CUDA(cudaEventCreate(&e));
+                s->g32ev.push_back(e);
+            }
+            g32_steps_mma(a, aimg, bimg, q32, s->st, s->g32ev);
+        }
         else switch (DP) {
             case 16: g32_steps<16>(a, nctas, s->st); break;
             case 32: g32_steps<32>(a, nctas, s->st); break;
@@ -1057,6 +1069,13 @@ bool greedy32_select(sair_store_s* s, const QueryPrep& p, const std::vector<size
             SAIR_CUDA(cudaMemcpyAsync(hnns.data(), a.nn_sim, G * 8, cudaMemcpyDeviceToHost, s->st));
         }
         SAIR_CUDA(cudaStreamSynchronize(s->st));
+        if (mma)
+            for (int st_i = 0; st_i < want; ++st_i) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, s->g32ev[2 * st_i], s->g32ev[2 * st_i + 1]);
+                s->last.greedy32_step_ms += ms;
+                s->last.greedy32_steps++;
+            }
         const int64_t* hidx = reinterpret_cast<const int64_t*>(hout);
         const double* hsim = reinterpret_cast<const double*>(hidx + G * m);
         const double* hsc = hsim + G * m;
