@@ -136,3 +136,23 @@ def test_local_mean_large_path_matches_reference(ref):
         r_round, _, r_score = rb.select(xq[q], 8, 0.1, 0.0, True)
         assert list(rounds[idx[q, :int(cnt[q])]]) == list(r_round)
         assert np.all(np.abs(sc[q, :int(cnt[q])] - r_score) <= 1e-12 * np.maximum(1, np.abs(r_score)))
+
+
+def test_local_mean_configs0_size_matches_oracle(orc):
+    """configs[0]'s shape (10k x 32, m = 8, lambda 0.1) with locally_weighted_mean:
+    the tiled exact LOO pass (local_loo_tiled_kernel) against the oracle, every
+    index and score."""
+    n, d = 10000, 32
+    db = ExperienceBuffer(0.0)
+    db.store_synthetic(77, n, d)
+    ctx, rew, rnd = synth.contexts(77, 0, n, d), synth.rewards(77, 0, n), synth.rounds(0, n)
+    xq = synth.queries(78, 2, d)
+    cfg = SelectionConfig(m=8, lambda_div=0.1, locally_weighted_mean=True)
+    idx, sim, sc, cnt = db.select_batch(xq, cfg)
+    sigma = db.effective_sigma()
+    for q in range(len(xq)):
+        oi, osim, osc = orc.select(ctx, rew, rnd, xq[q], 8, 0.1, sigma, local_mean=True)
+        k = int(cnt[q])
+        assert k == len(oi) and np.array_equal(idx[q, :k], oi)
+        assert np.all(np.abs(sc[q, :k] - osc) <= 1e-12 * np.maximum(1, np.abs(osc)))
+        assert np.all(np.abs(sim[q, :k] - osim) <= 1e-12)
