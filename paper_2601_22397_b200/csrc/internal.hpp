@@ -155,6 +155,7 @@ struct sair_store_s {
     std::shared_ptr<sair::GreedySession> greedy;  // sharded lambda > 0 select in progress
     std::vector<cudaEvent_t> gev;  // per query group: start, end of pre-pass, end of stream
     std::vector<cudaEvent_t> g32ev;  // the greedy's step kernels: start, end per step
+    std::vector<cudaEvent_t> cev;    // wide pass: a group's constants landed (copy stream)
     const float* mma_t0 = nullptr;
     const float* mma_t0safe = nullptr;  // wide pass: the sample's guaranteed start thresholds
     const unsigned int* mma_dropped = nullptr;

@@ -1203,9 +1203,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         s->last.qb = qb;
         s->last.tensor_core = use_wide ? (wp.bf16 ? 3 : 2) : (use_mma ? 1 : 0);
         // wide pass: a group's constants on the host (phase 1 of wfill) and the
-        // refine's cc; they go up in two copies per call -- group 0's, then,
-        // computed while the device runs group 0, every later group's -- not
-        // one copy per group between the passes
+        // refine's cc; group 0's go up before its passes, each later group's
+        // are prepared while the device runs the group before it and copied
+        // on the copy stream (the group's passes wait on that copy's event)
         auto wide_prep = [&](size_t g) {
             const size_t g0 = g * qb;
             GroupIo io{};
@@ -1250,6 +1250,7 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             float* mthr = mthr_g + g * 2 * qb;
             unsigned int* dpmax = pmax_g + g;
             double* dc = dc_g + g * nhc;
+            if (use_wide && g > 0) SAIR_CUDA(cudaStreamWaitEvent(s->st, s->cev[g], 0));
             SAIR_CUDA(cudaEventRecord(s->gev[3 * g], s->st));
             if (use_wide)  // sample + stream + per-list top-K' (records e_mid, e_end)
                 wfill(s, wp, p, zgrp, nqg, c1, c0, rdelta, alpha, mk, mi, mthr, dpmax, cc, io);
@@ -1258,11 +1259,20 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             else
                 fill(s, pl, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
             if (!use_wide) SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
-            if (use_wide && g == 0 && ngroups > 1) {
-                for (size_t g2 = 1; g2 < ngroups; ++g2) wide_prep(g2);
-                SAIR_CUDA(cudaMemcpyAsync(wc_g + hstride, hstage_all + hstride,
-                                          (ngroups - 1) * hstride * 4, cudaMemcpyHostToDevice,
-                                          s->st));
+            if (use_wide && g + 1 < ngroups) {
+                // the next group's constants, prepared while the device runs
+                // this group's passes and copied on the copy stream beside
+                // them (one copy for all later groups made the device wait for
+                // the host's whole preparation: 2M records x 4096 queries, ~1 ms)
+                wide_prep(g + 1);
+                while (s->cev.size() < ngroups) {
+                    cudaEvent_t e;
+                    SAIR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    s->cev.push_back(e);
+                }
+                SAIR_CUDA(cudaMemcpyAsync(wc_g + (g + 1) * hstride, hstage_all + (g + 1) * hstride,
+                                          hstride * 4, cudaMemcpyHostToDevice, s->cst));
+                SAIR_CUDA(cudaEventRecord(s->cev[g + 1], s->cst));
             }
             s->last.stream_launches++;
             if (!use_wide)  // (the wide pass's were written by its first loop)

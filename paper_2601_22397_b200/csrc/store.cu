@@ -202,6 +202,8 @@ void store_free(sair_store_s* s) {
     for (auto& e : s->gev) cudaEventDestroy(e);
     for (auto& e : s->g32ev) cudaEventDestroy(e);
     s->g32ev.clear();
+    for (auto& e : s->cev) cudaEventDestroy(e);
+    s->cev.clear();
     s->gev.clear();
     if (s->st) cudaStreamDestroy(s->st);
     s->st = nullptr;
