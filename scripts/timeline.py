@@ -1,22 +1,25 @@
-"""Device timeline of one 16M x 4096 select_batch (torch.profiler / CUPTI sees
+"""Device timeline of one N x NQ select_batch (env N, NQ, LAM; default 16M x 4096) (torch.profiler / CUPTI sees
 the library's kernels and copies): per-op totals and the idle gaps between ops."""
-import json, sys
+import json, os, sys
 sys.path.insert(0, ".")
 import torch
 import paper_2601_22397_b200 as sair
 from paper_2601_22397_b200 import synth
 from torch.profiler import profile, ProfilerActivity
 
-n, nq = 1 << 24, 4096
+n, nq = int(os.environ.get("N", 1 << 24)), int(os.environ.get("NQ", 4096))
 db = sair.ExperienceBuffer(0.0)
 db.store_synthetic(2026, n, 64)
 xq = synth.queries(7, nq * 3, 64).reshape(3, nq, 64)
-cfg = sair.SelectionConfig(m=32, lambda_div=0.0)
+cfg = sair.SelectionConfig(m=32, lambda_div=float(os.environ.get("LAM", 0.0)))
 db.select_batch(xq[0], cfg)
 db.select_batch(xq[1], cfg)
+import time
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+    t_0 = time.perf_counter()
     db.select_batch(xq[2], cfg)
     torch.cuda.synchronize()
+    print(f"host wall {(time.perf_counter() - t_0) * 1e3:.3f} ms (under the profiler)")
 prof.export_chrome_trace("gpurun_out/timeline.json")
 ev = [e for e in json.load(open("gpurun_out/timeline.json"))["traceEvents"]
       if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
