@@ -560,7 +560,17 @@ def bench_pareto(dev):
     f2 = sair.ParetoFrontier(1.0, 1.0, device=dev)
     t0 = time.perf_counter()
     F = f2.insert_batch(pts)
-    ins_s = time.perf_counter() - t0
+    ins_first_s = time.perf_counter() - t0
+    # steady state: a frontier whose scratch already holds a batch of this size
+    # (another 4M batch of the distribution), then the timed batch
+    ins_ws = []
+    for r in range(3):
+        fw = sair.ParetoFrontier(1.0, 1.0, device=dev)
+        fw.insert_batch(synth.tuples(SEED + 100 + r, PARETO_T, 2, "uniform"))
+        t0 = time.perf_counter()
+        fw.insert_batch(pts)
+        ins_ws.append(time.perf_counter() - t0)
+    ins_s = sorted(ins_ws)[1]
     dpts = torch.from_numpy(pts).to(f"cuda:{dev}")
     dout = torch.empty(PARETO_T, dtype=torch.float64, device=f"cuda:{dev}")
     ddom = torch.empty(PARETO_T, dtype=torch.uint8, device=f"cuda:{dev}")
@@ -593,6 +603,10 @@ def bench_pareto(dev):
                 "score_ms": round(sc_ms, 4), "frontier_size": F,
                 "frontier_insert_tuples_per_s": round(PARETO_T / ins_s, 1),
                 "frontier_insert_s_e2e": round(ins_s, 4),
+                "frontier_insert_s_e2e_first_call": round(ins_first_s, 4),
+                "frontier_insert_note": "e2e from the host array (67 MB pageable H2D inside); "
+                                        "median of 3 on warmed scratch; K6 pre-filter + exact "
+                                        "sort path on the survivors",
                 "l2": "flushed before every timed launch (512 MB write)",
                 "roofline": {"bound": "hbm", "achieved": round(sbytes / (sc_ms / 1e3) / 1e9, 1),
                              "peak": hbm_peak, "unit": "GB/s", "peak_kind": peak_kind,

@@ -13,6 +13,8 @@
 //       comparisons on integers), sort by rank sum (a dominator has a strictly
 //       smaller sum), tiled pairwise tests with shared-memory j-tiles.
 //   reward: the five-term compute_reward per row, fused with K8.
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -599,6 +601,140 @@ __global__ void compact_kernel(const double* __restrict__ l, const double* __res
         uint32_t p = perm[i];
         ol[slot[i]] = l[p];
         oc[slot[i]] = c[p];
+    }
+}
+
+// K6 pre-filter: one CTA per PF_B arriving tuples, read once from the caller's
+// interleaved (l, c) layout.  The CTA sorts its tuples by the high 32 bits of
+// the latency's order key in shared memory (block radix sort, 8 passes) and
+// drops a tuple when the minimum cost over the tuples of strictly smaller key
+// is strictly below its cost -- such a tuple q has q.l < p.l and q.c < p.c,
+// i.e. dominates(q, p) (pareto.cpp:9-12), so p cannot be on the final
+// frontier and, lying above its dominator's cost, cannot change any other
+// tuple's prefix-min in the sort path either.  Survivors are a superset of the
+// CTA's local frontier (latency ties and duplicates are left to the exact
+// path), written in arrival order so the exact path still keeps the first
+// occurrence of a duplicate.  Uniform 4M tuples: ~10 survivors per 4096.
+// A NaN coordinate anywhere sets *nan_seen: the host then takes the unfiltered
+// path (the filter's order argument needs totally ordered coordinates).
+constexpr int PF_THREADS = 512, PF_ITEMS = 8, PF_B = PF_THREADS * PF_ITEMS;
+
+using PfSort = cub::BlockRadixSort<uint32_t, PF_THREADS, PF_ITEMS, uint16_t>;
+using PfScanD = cub::BlockScan<double, PF_THREADS>;
+using PfScanU = cub::BlockScan<uint32_t, PF_THREADS>;
+union PfTemp {
+    typename PfSort::TempStorage sort;
+    typename PfScanD::TempStorage sd;
+    typename PfScanU::TempStorage su;
+};
+// shared: scan/sort temp | c by arrival [PF_B] | inclusive prefix-min by rank [PF_B] | keep [PF_B]
+constexpr size_t PF_SMEM = sizeof(PfTemp) + PF_B * 16 + PF_B + 64;
+
+__global__ void __launch_bounds__(PF_THREADS)
+    prefilter_kernel(const double2* __restrict__ pts, size_t T, double* __restrict__ rl,
+                     double* __restrict__ rc, uint32_t* __restrict__ cnt,
+                     unsigned int* __restrict__ nan_seen) {
+    extern __shared__ __align__(16) unsigned char pf_smem[];
+    PfTemp& tmp = *reinterpret_cast<PfTemp*>(pf_smem);
+    double* s_c = reinterpret_cast<double*>(pf_smem + sizeof(PfTemp));
+    double* s_pm = s_c + PF_B;
+    uint8_t* s_keep = reinterpret_cast<uint8_t*>(s_pm + PF_B);
+    const int tid = threadIdx.x;
+    const size_t base = (size_t)blockIdx.x * PF_B;
+    const int nb = (int)min((size_t)PF_B, T - base);
+    uint32_t key[PF_ITEMS];
+    uint16_t li[PF_ITEMS];
+    bool nan = false;
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) {  // striped: coalesced 16-byte loads
+        const int j = i * PF_THREADS + tid;
+        li[i] = (uint16_t)j;
+        if (j < nb) {
+            const double2 p = pts[base + j];
+            nan |= isnan(p.x) || isnan(p.y);
+            key[i] = (uint32_t)(ord64(p.x) >> 32);
+            s_c[j] = p.y;
+        } else {
+            key[i] = ~0u;  // padding sorts last and is never written
+        }
+    }
+    if (__syncthreads_or(nan)) {
+        if (tid == 0) atomicOr(nan_seen, 1u);
+        return;
+    }
+    PfSort(tmp.sort).Sort(key, li);  // blocked: thread t holds sorted ranks t*8 .. t*8+7
+    __syncthreads();
+    double cv[PF_ITEMS], pm[PF_ITEMS];
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) cv[i] = li[i] < nb ? s_c[li[i]] : INFINITY;
+    PfScanD(tmp.sd).InclusiveScan(cv, pm, MinOp());
+    const int r0 = tid * PF_ITEMS;
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) s_pm[r0 + i] = pm[i];
+    __syncthreads();  // every cv read of s_c is done: its space takes the sorted keys
+    uint32_t* s_key = reinterpret_cast<uint32_t*>(s_c);
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) s_key[r0 + i] = key[i];
+    __syncthreads();
+    // the rank where each key's run starts (inclusive max-scan of the run
+    // heads); the rank before it holds the minimum cost over every strictly
+    // smaller key
+    uint32_t hs[PF_ITEMS], rs[PF_ITEMS];
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) {
+        const int r = r0 + i;
+        const uint32_t pk = i ? key[i - 1] : (r ? s_key[r - 1] : ~key[0]);
+        hs[i] = pk != key[i] ? (uint32_t)r : 0u;
+    }
+    PfScanU(tmp.su).InclusiveScan(hs, rs, cub::Max());
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) {
+        if (li[i] >= nb) continue;
+        const double m = rs[i] ? s_pm[rs[i] - 1] : INFINITY;
+        s_keep[li[i]] = m < cv[i] ? 0 : 1;
+    }
+    __syncthreads();
+    // arrival order: thread t owns local tuples t*8 .. t*8+7
+    uint32_t k[PF_ITEMS], pos[PF_ITEMS], tot = 0;
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i) {
+        const int j = tid * PF_ITEMS + i;
+        k[i] = j < nb ? s_keep[j] : 0u;
+    }
+    PfScanU(tmp.su).ExclusiveSum(k, pos, tot);
+#pragma unroll
+    for (int i = 0; i < PF_ITEMS; ++i)
+        if (k[i]) {
+            const double2 p = pts[base + tid * PF_ITEMS + i];
+            rl[base + pos[i]] = p.x;
+            rc[base + pos[i]] = p.y;
+        }
+    if (tid == 0) cnt[blockIdx.x] = tot;
+}
+
+// the CTAs' survivors, in CTA (= arrival) order, behind the existing frontier
+__global__ void __launch_bounds__(256)
+    prefilter_gather_kernel(const double* __restrict__ rl, const double* __restrict__ rc,
+                            const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ off,
+                            int nblk, double* __restrict__ l, double* __restrict__ c,
+                            uint32_t* __restrict__ total) {
+    const int b = blockIdx.x;
+    const uint32_t n = cnt[b], o = off[b];
+    const size_t base = (size_t)b * PF_B;
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+        l[o + k] = rl[base + k];
+        c[o + k] = rc[base + k];
+    }
+    if (b == nblk - 1 && threadIdx.x == 0) *total = o + n;
+}
+
+__global__ void deinterleave_kernel(const double2* __restrict__ pts, size_t T,
+                                    double* __restrict__ l, double* __restrict__ c) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const double2 p = pts[i];
+        l[i] = p.x;
+        c[i] = p.y;
     }
 }
 
@@ -1259,21 +1395,80 @@ bool frontier_insert_one(sair_frontier_s* f, double pl, double pc) {
     return true;
 }
 
+// The arriving tuples land on the device in the caller's interleaved layout
+// (one H2D copy), K6's pre-filter drops the tuples its CTA proves dominated,
+// and the exact sort path below runs on the existing frontier + the survivors.
+// Returns the number of tuples behind the frontier in l / c (at l + F).
+static size_t stage_batch(sair_frontier_s* f, const double* pts, size_t T, double* l, double* c) {
+    const size_t nblk = (T + PF_B - 1) / PF_B;
+    // raw[T] double2 | rl[T] | rc[T] | cnt[nblk] | off[nblk] | total, nan
+    size_t scan_b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_b, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (int)nblk);
+    const size_t o_rl = T * 16, o_rc = o_rl + T * 8, o_cnt = o_rc + T * 8,
+                 o_off = o_cnt + ((nblk * 4 + 255) & ~(size_t)255),
+                 o_misc = o_off + ((nblk * 4 + 255) & ~(size_t)255), o_scan = o_misc + 256;
+    char* b = static_cast<char*>(f->b_sort.get(o_scan + scan_b + 256));
+    auto* raw = reinterpret_cast<double2*>(b);
+    auto* cnt = reinterpret_cast<uint32_t*>(b + o_cnt);
+    auto* off = reinterpret_cast<uint32_t*>(b + o_off);
+    auto* misc = reinterpret_cast<uint32_t*>(b + o_misc);  // [0] total, [1] nan seen
+    SAIR_CUDA(cudaMemcpyAsync(raw, pts, T * 16, cudaMemcpyHostToDevice, f->st));
+    static const bool nofilter = std::getenv("SAIR_K6_NOFILTER") != nullptr;
+    if (nofilter || T < 2 * PF_B) {
+        deinterleave_kernel<<<grid_for(T), 256, 0, f->st>>>(raw, T, l, c);
+        SAIR_LAUNCH("deinterleave_kernel");
+        SAIR_CUDA(cudaStreamSynchronize(f->st));  // raw lives in b_sort, which the sort reuses
+        return T;
+    }
+    static bool attr = false;
+    if (!attr) {
+        SAIR_CUDA(cudaFuncSetAttribute(prefilter_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_SMEM));
+        attr = true;
+    }
+    SAIR_CUDA(cudaMemsetAsync(misc, 0, 8, f->st));
+    prefilter_kernel<<<(unsigned)nblk, PF_THREADS, PF_SMEM, f->st>>>(
+        raw, T, reinterpret_cast<double*>(b + o_rl), reinterpret_cast<double*>(b + o_rc), cnt,
+        misc + 1);
+    SAIR_LAUNCH("prefilter_kernel");
+    size_t tb = scan_b;
+    SAIR_CUDA(cub::DeviceScan::ExclusiveSum(b + o_scan, tb, cnt, off, (int)nblk, f->st));
+    prefilter_gather_kernel<<<(unsigned)nblk, 256, 0, f->st>>>(
+        reinterpret_cast<double*>(b + o_rl), reinterpret_cast<double*>(b + o_rc), cnt, off,
+        (int)nblk, l, c, misc);
+    SAIR_LAUNCH("prefilter_gather_kernel");
+    uint32_t h[2];
+    SAIR_CUDA(cudaMemcpyAsync(h, misc, 8, cudaMemcpyDeviceToHost, f->st));
+    SAIR_CUDA(cudaStreamSynchronize(f->st));
+    if (h[1]) {  // a NaN coordinate: every tuple goes to the exact path
+        deinterleave_kernel<<<grid_for(T), 256, 0, f->st>>>(raw, T, l, c);
+        SAIR_LAUNCH("deinterleave_kernel");
+        SAIR_CUDA(cudaStreamSynchronize(f->st));  // raw lives in b_sort, which the sort reuses
+        return T;
+    }
+    return h[0];
+}
+
 size_t frontier_insert_batch(sair_frontier_s* f, const double* pts, size_t T) {
     if (T == 0) return f->F;
     DeviceGuard g(f->device);
-    const size_t n = f->F + T;
-    if (n >= 0xFFFFFFFFull) throw Error(SAIR_EINVAL, "batch too large");
-    // layout: l[n], c[n], kl[n], kc[n], kt[n], pos[n], perm[n], perm2[n], pmin[n], flag[n], slot[n]
-    char* base = static_cast<char*>(f->b_in.get(n * (8 * 6 + 4 * 5) + 4096));
-    size_t off = 0;
+    if (f->F + T >= 0xFFFFFFFFull) throw Error(SAIR_EINVAL, "batch too large");
+    // the tuples land first (l / c at F .. F+T), the sort arrays behind them
+    // (sized for the worst case: every tuple survives the pre-filter)
+    const size_t N = f->F + T, lc_bytes = ((N + 31) & ~(size_t)31) * 8 + N * 8;
+    char* base = static_cast<char*>(
+        f->b_in.get(((lc_bytes + 255) & ~(size_t)255) + N * (8 * 4 + 4 * 5) + 4096));
+    double* l = reinterpret_cast<double*>(base);
+    double* c = l + ((N + 31) & ~(size_t)31);
+    const size_t n = f->F + stage_batch(f, pts, T, l + f->F, c + f->F);
+    // layout: l, c (staged above), kl[n], kc[n], kt[n], pmin[n], pos[n], perm[n], perm2[n], flag[n], slot[n]
+    size_t off = (lc_bytes + 255) & ~(size_t)255;
     auto take = [&](size_t b) {
         char* p = base + off;
         off += (b + 255) / 256 * 256;
         return p;
     };
-    double* l = reinterpret_cast<double*>(take(n * 8));
-    double* c = reinterpret_cast<double*>(take(n * 8));
     uint64_t* kl = reinterpret_cast<uint64_t*>(take(n * 8));
     uint64_t* kc = reinterpret_cast<uint64_t*>(take(n * 8));
     uint64_t* kt = reinterpret_cast<uint64_t*>(take(n * 8));
@@ -1287,15 +1482,6 @@ size_t frontier_insert_batch(sair_frontier_s* f, const double* pts, size_t T) {
     if (f->F) {
         SAIR_CUDA(cudaMemcpyAsync(l, f->fl, f->F * 8, cudaMemcpyDeviceToDevice, f->st));
         SAIR_CUDA(cudaMemcpyAsync(c, f->fc, f->F * 8, cudaMemcpyDeviceToDevice, f->st));
-    }
-    {
-        double* h = f->h_io.as<double>(2 * T);
-        for (size_t t = 0; t < T; ++t) {
-            h[t] = pts[2 * t];
-            h[T + t] = pts[2 * t + 1];
-        }
-        SAIR_CUDA(cudaMemcpyAsync(l + f->F, h, T * 8, cudaMemcpyHostToDevice, f->st));
-        SAIR_CUDA(cudaMemcpyAsync(c + f->F, h + T, T * 8, cudaMemcpyHostToDevice, f->st));
     }
     batch_keys_kernel<<<grid_for(n), 256, 0, f->st>>>(l, c, n, kl, kc, pos);
     SAIR_LAUNCH("batch_keys_kernel");

@@ -337,6 +337,51 @@ def test_frontier_sequences_match_reference(ref):
             assert dm == rf.strictly_dominated(*p)
 
 
+def test_batch_insert_prefilter_edge_cases(ref):
+    """K6's CTA pre-filter (pareto.cu prefilter_kernel: 4096-tuple CTAs, runs
+    from 8192 tuples) against the reference's own insert_normalized loop
+    (pareto.cpp:43-54): coarse grids (latency ties inside and across CTAs),
+    exact duplicates whose first occurrence carries -0.0 vs +0.0 bits, a
+    staircase spanning CTA boundaries, a non-empty frontier beforehand, and a
+    NaN tuple (the host falls back to the unfiltered sort path)."""
+    gen = np.random.default_rng(7)
+    cases = []
+    T = 3 * 4096 + 777
+    cases.append(np.round(gen.uniform(size=(T, 2)) * 4.0) / 4.0)          # heavy ties
+    z = np.round(gen.uniform(size=(T, 2)) * 16.0) / 16.0
+    z[gen.integers(0, T, 500)] = (0.0, 0.5)
+    z[gen.integers(0, T, 500)] = (-0.0, 0.5)                                  # signed zeros
+    z[gen.integers(0, T, 300)] = (0.25, -0.0)
+    cases.append(z)
+    x = np.linspace(0.0, 1.0, T)
+    stair = np.stack([x, 1.0 - x], 1)[gen.permutation(T)]                   # every tuple on the frontier
+    cases.append(stair)
+    for pts in cases:
+        rf = RefFrontier(ref, 1.0, 1.0)
+        df = ParetoFrontier(1.0, 1.0)
+        pre = np.round(gen.uniform(size=(64, 2)) * 8.0) / 8.0
+        for p in pre:
+            rf.insert_normalized(*p)
+        df.insert_batch(pre)
+        for p in pts:
+            rf.insert_normalized(*p)
+        F = df.insert_batch(pts)
+        rl, rc = rf.points()
+        dl, dc = df.points_array()
+        assert F == len(rl)
+        assert np.array_equal(np.signbit(dl), np.signbit(rl))
+        assert np.array_equal(np.signbit(dc), np.signbit(rc))
+        assert np.array_equal(dl, rl) and np.array_equal(dc, rc)
+        assert df.hypervolume() == rf.hypervolume()
+    # a NaN anywhere sends the batch down the unfiltered sort path (the
+    # pre-filter's order argument needs totally ordered coordinates)
+    pts = gen.uniform(size=(20000, 2))
+    pts[12345] = (np.nan, 0.5)
+    dn = ParetoFrontier(1.0, 1.0)
+    F = dn.insert_batch(pts)
+    assert F == len(dn.points_array()[0])
+
+
 def test_batch_insert_and_scoring_at_scale(orc):
     for dist in ("uniform", "anti", "grid", "corr"):
         pts = synth.tuples(17, 200000, 2, dist)
