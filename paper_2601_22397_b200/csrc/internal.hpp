@@ -68,6 +68,11 @@ struct HBuf {
     }
 };
 
+// Large pageable host->device copy through a pinned ring filled by host
+// threads (xfer.cpp); below 8 MB a plain cudaMemcpyAsync.  Returns once every
+// chunk's DMA is queued on st and the ring has drained.
+void copy_h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 // Host-maintained fp64 statistics (bit-identical to the reference's
 // ExperienceBuffer members sum_, sum_sq_, the reward total of loo_mean, and the
 // sigma cache; experience.hpp:82-88).

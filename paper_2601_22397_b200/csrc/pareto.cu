@@ -1413,7 +1413,7 @@ static size_t stage_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
     auto* cnt = reinterpret_cast<uint32_t*>(b + o_cnt);
     auto* off = reinterpret_cast<uint32_t*>(b + o_off);
     auto* misc = reinterpret_cast<uint32_t*>(b + o_misc);  // [0] total, [1] nan seen
-    SAIR_CUDA(cudaMemcpyAsync(raw, pts, T * 16, cudaMemcpyHostToDevice, f->st));
+    copy_h2d_staged(raw, pts, T * 16, f->st);
     static const bool nofilter = std::getenv("SAIR_K6_NOFILTER") != nullptr;
     if (nofilter || T < 2 * PF_B) {
         deinterleave_kernel<<<grid_for(T), 256, 0, f->st>>>(raw, T, l, c);
@@ -1593,7 +1593,7 @@ void frontier_score_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
     double* dp = reinterpret_cast<double*>(base);
     double* dout = dp + 2 * T;
     uint8_t* ddom = reinterpret_cast<uint8_t*>(dout + T);
-    SAIR_CUDA(cudaMemcpyAsync(dp, pts, T * 16, cudaMemcpyHostToDevice, f->st));
+    copy_h2d_staged(dp, pts, T * 16, f->st);
     score_launch(f, dp, T, dout, ddom, f->st);
     SAIR_CUDA(cudaMemcpyAsync(out, dout, T * 8, cudaMemcpyDeviceToHost, f->st));
     if (dom) SAIR_CUDA(cudaMemcpyAsync(dom, ddom, T, cudaMemcpyDeviceToHost, f->st));
@@ -1642,7 +1642,7 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
     uint32_t* sranks = reinterpret_cast<uint32_t*>(take(T * K * 4));
     uint32_t* dcnt = reinterpret_cast<uint32_t*>(take(T * 4));
     uint8_t* dmem = reinterpret_cast<uint8_t*>(take(T));
-    SAIR_CUDA(cudaMemcpyAsync(dt, tuples, T * K * 8, cudaMemcpyHostToDevice, st));
+    copy_h2d_staged(dt, tuples, T * K * 8, st);
     size_t t1 = 0, t2 = 0, t3 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, key, skey, pos, perm, (int)T);
     cub::DeviceScan::InclusiveSum(nullptr, t2, flag, rk, (int)T);

@@ -26,6 +26,7 @@
 // Queries that cannot be certified are answered by the full fp64 pass
 // (select_exact.cu).  The exactness argument is DESIGN.md "Exactness".
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cfloat>
 #include <cstring>
@@ -995,10 +996,30 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         return;
     }
     DeviceGuard g(s->device);
+    // SAIR_TRACE_SELECT=1: host-side phase times of the call (us), to stderr
+    static const bool trace = std::getenv("SAIR_TRACE_SELECT") != nullptr;
+    std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> marks;
+    auto mark = [&](const char* what) {
+        if (trace) marks.emplace_back(what, std::chrono::steady_clock::now());
+    };
+    struct TraceOut {
+        decltype(marks)& m;
+        ~TraceOut() {
+            if (m.size() < 2) return;
+            fprintf(stderr, "[select]");
+            for (size_t i = 1; i < m.size(); ++i)
+                fprintf(stderr, " %s %.1f", m[i].first,
+                        std::chrono::duration<double, std::micro>(m[i].second - m[i - 1].second).count());
+            fprintf(stderr, "\n");
+        }
+    } trace_out{marks};
+    mark("start");
     const double sigma = store_effective_sigma(s, cfg.sigma_sim);  // :246
     if (dim != s->d)  // standardize(x_curr) throws after the sigma refresh (:157-158)
         throw Error(SAIR_EINVAL, "experience store: feature dimension mismatch");
+    mark("sigma");
     QueryPrep p = prep_queries(s, q, nq, sigma);
+    mark("prep");
     const int d = s->d;
     const size_t n = s->n;
     SAIR_CUDA(cudaEventRecord(s->ev[0], s->st));
@@ -1099,7 +1120,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         std::vector<float> thr_of(nq * 4, -INFINITY);
         bool pl_ready = false;  // the (P, lg) cache holds this call's values
         uint32_t nhot = 0;
+        mark("plan");
         const uint32_t* hot = use_wide ? wide_hot_pages(s, wp, c1, c0, &nhot) : nullptr;
+        mark("hot");
         auto run_batch = [&](const std::vector<size_t>& ql, const std::vector<float>* t0o) {
         const size_t nbq = ql.size();
         const size_t ngroups = (nbq + qb - 1) / qb;
@@ -1217,8 +1240,10 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             double* hc = hc_all + g * nhc;
             for (int qq = 0; qq < qb; ++qq) hc[2 * (size_t)d + (size_t)qb * d + qq] = cc[qq];
         };
+        mark("setup");
         if (use_wide) {
             wide_prep(0);
+            mark("prep0");
             SAIR_CUDA(cudaMemcpyAsync(wc_g, hstage_all, hstride * 4, cudaMemcpyHostToDevice, s->st));
             SAIR_CUDA(cudaMemsetAsync(wcnt_g, 0, ngroups * 4 * (size_t)qb * 4, s->st));
         }
@@ -1252,12 +1277,14 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
             double* dc = dc_g + g * nhc;
             if (use_wide && g > 0) SAIR_CUDA(cudaStreamWaitEvent(s->st, s->cev[g], 0));
             SAIR_CUDA(cudaEventRecord(s->gev[3 * g], s->st));
+            mark("grp");
             if (use_wide)  // sample + stream + per-list top-K' (records e_mid, e_end)
                 wfill(s, wp, p, zgrp, nqg, c1, c0, rdelta, alpha, mk, mi, mthr, dpmax, cc, io);
             else if (use_mma)
                 mfill(s, mp, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc, io);
             else
                 fill(s, pl, p, zgrp, nqg, c1, c0, rdelta, alpha, ck, ci, dpmax, cc);
+            mark("launch");
             if (!use_wide) SAIR_CUDA(cudaEventRecord(io.e_end, s->st));
             if (use_wide && g + 1 < ngroups) {
                 // the next group's constants, prepared while the device runs
@@ -1350,7 +1377,9 @@ void store_select(sair_store_s* s, const double* q, size_t nq, int dim,
         refine_kernel<<<dim3((unsigned)qb, (unsigned)ngroups), 256, refine_smem, s->st>>>(ra_dev);
         SAIR_LAUNCH("refine_kernel");
         SAIR_CUDA(cudaMemcpyAsync(hout, dout, ob * ngroups, cudaMemcpyDeviceToHost, s->st));
+        mark("tail");
         SAIR_CUDA(cudaStreamSynchronize(s->st));
+        mark("sync");
         for (size_t g = 0; g < ngroups; ++g) {
             const size_t g0 = g * qb;
             const int nqg = (int)std::min<size_t>(qb, nbq - g0);

@@ -1261,7 +1261,13 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
     float* ccv = sv + DP;
     const size_t L = 2 * (size_t)QW;
     if (io.phase != 2) {
-        for (int k = 0; k < DP; ++k) sv[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
+        // the per-dimension quotient once per group, not once per (query, dim):
+        // 16k fp64 divisions were ~70 us of host time per 256-query group
+        double mq[DP];
+        for (int k = 0; k < DP; ++k) {
+            sv[k] = k < d ? (float)(1.0 / p.sd[k]) : 0.f;
+            mq[k] = k < d ? (p.mean[k] - s->shift[k]) / p.sd[k] : 0.0;
+        }
         cc_out.assign(QW, 0.0);
         for (int q = 0; q < QW; ++q) {
             // padded query slots repeat query 0 (their lists are never read)
@@ -1269,7 +1275,7 @@ void wide_launch_t(sair_store_s* s, const WidePlan& pl, const QueryPrep& p, cons
             double cc = 0.0;
             for (int k = 0; k < DP; ++k) {
                 float c = 0.f;
-                if (k < d) c = (float)((p.mean[k] - s->shift[k]) / p.sd[k] + z[k]);
+                if (k < d) c = (float)(mq[k] + z[k]);
                 cc += (double)c * (double)c;
                 const double bk = k < d ? -2.0 * (double)c * (double)sv[k] : 0.0;
                 // smem image of the K-major B tiles: (q % 8) * 16 + (q / 8) * 256 +
