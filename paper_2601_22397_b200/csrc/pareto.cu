@@ -927,6 +927,195 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---- K7b: K = 3, 4 over Morton-ordered tiles with bounding boxes ----------
+//
+// The rank-sum order above makes every i-tile scan about half the store.  Here
+// the tuples are sorted by the Morton (bit-interleaved) key of their dense
+// ranks, so 256 consecutive tuples -- a tile -- sit in a compact box of rank
+// space, and 32 consecutive tiles form a super-tile with its own box.  For the
+// j-tile J of a CTA, a box A (all its tuples i) is
+//   NONE    if min_A[k] > max_J[k] for some k: no i is <= any j in k;
+//   FULL    if max_A <= min_J in every k and < in some k: every i dominates
+//           every j (a strict coordinate: no equal vectors);
+//   PARTIAL otherwise: the pairs are tested one by one.
+// FULL boxes add their tuple count to every j of the tile at once; only
+// PARTIAL tiles (the ones whose box touches J's "lower orthant" boundary) are
+// staged in shared memory for the pairwise test `all(r_i <= r_j) && r_i != r_j`
+// plus the duplicate rule (an equal vector with a smaller original index makes
+// j a non-member: pareto.cpp:43-54 keeps the first of equal points).
+constexpr int BX_TILE = 256, BX_SUP = 32, BX_LCAP = 256 * BX_SUP;
+
+template <int K>
+__global__ void morton_key_kernel(const uint32_t* __restrict__ ranks, size_t T, int shift,
+                                  uint64_t* __restrict__ key, uint32_t* __restrict__ pos) {
+    constexpr int B = 64 / K;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t r[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) r[k] = ranks[i * K + k] >> shift;
+        uint64_t m = 0;
+#pragma unroll
+        for (int b = B - 1; b >= 0; --b)
+#pragma unroll
+            for (int k = 0; k < K; ++k) m = (m << 1) | ((r[k] >> b) & 1u);
+        key[i] = m;
+        pos[i] = (uint32_t)i;
+    }
+}
+
+template <int K>
+__global__ void pack4_kernel(const uint32_t* __restrict__ ranks, const uint32_t* __restrict__ perm,
+                             size_t T, uint4* __restrict__ rv) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < T;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const size_t p = perm[i];
+        uint32_t v[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[k] = ranks[p * K + k];
+        rv[i] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+__device__ __forceinline__ uint4 umin4(uint4 a, uint4 b) {
+    return make_uint4(min(a.x, b.x), min(a.y, b.y), min(a.z, b.z), min(a.w, b.w));
+}
+__device__ __forceinline__ uint4 umax4(uint4 a, uint4 b) {
+    return make_uint4(max(a.x, b.x), max(a.y, b.y), max(a.z, b.z), max(a.w, b.w));
+}
+
+// one thread per tile (level 0: tuples -> tile boxes) or per super-tile
+// (level 1: tile boxes -> super boxes)
+__global__ void box_kernel(const uint4* __restrict__ lo_in, const uint4* __restrict__ hi_in,
+                           size_t n_in, int group, size_t n_out, uint4* __restrict__ lo,
+                           uint4* __restrict__ hi) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= n_out) return;
+    const size_t a = t * group, e = min(a + group, n_in);
+    uint4 mn = lo_in[a], mx = hi_in ? hi_in[a] : lo_in[a];
+    for (size_t i = a + 1; i < e; ++i) {
+        mn = umin4(mn, lo_in[i]);
+        mx = umax4(mx, hi_in ? hi_in[i] : lo_in[i]);
+    }
+    lo[t] = mn;
+    hi[t] = mx;
+}
+
+template <int K>
+__device__ __forceinline__ int box_class(uint4 amin, uint4 amax, uint4 jmin, uint4 jmax) {
+    bool none = amin.x > jmax.x, le = amax.x <= jmin.x, lt = amax.x < jmin.x;
+    if (K > 1) { none |= amin.y > jmax.y; le &= amax.y <= jmin.y; lt |= amax.y < jmin.y; }
+    if (K > 2) { none |= amin.z > jmax.z; le &= amax.z <= jmin.z; lt |= amax.z < jmin.z; }
+    if (K > 3) { none |= amin.w > jmax.w; le &= amax.w <= jmin.w; lt |= amax.w < jmin.w; }
+    return none ? 0 : (le && lt ? 1 : 2);
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+    dominance_box_kernel(const uint4* __restrict__ rv, const uint32_t* __restrict__ perm, size_t T,
+                         const uint4* __restrict__ tmin, const uint4* __restrict__ tmax,
+                         const uint4* __restrict__ smin, const uint4* __restrict__ smax,
+                         uint32_t ntiles, uint32_t nsup, uint32_t tile_begin, int members_only,
+                         uint32_t* __restrict__ counts, uint8_t* __restrict__ member,
+                         unsigned long long* __restrict__ stats) {
+    __shared__ uint4 ti[BX_TILE];
+    __shared__ uint32_t tp[BX_TILE];
+    __shared__ uint32_t list[BX_LCAP];
+    __shared__ uint32_t nlist, full_add;
+    const uint32_t J = tile_begin + blockIdx.x;
+    const size_t j = (size_t)J * BX_TILE + threadIdx.x;
+    const bool valid = j < T;
+    const uint4 rj = valid ? rv[j] : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t pj = valid ? perm[j] : 0xFFFFFFFFu;
+    const uint4 jmin = tmin[J], jmax = tmax[J];
+    if (threadIdx.x == 0) {
+        nlist = 0;
+        full_add = 0;
+    }
+    uint32_t cnt = 0;
+    bool dup = false;
+    __syncthreads();
+    for (uint32_t s0 = 0; s0 < nsup; s0 += blockDim.x) {
+        // 1. the CTA's tile box against super-tile boxes, then tile boxes
+        const uint32_t sidx = s0 + threadIdx.x;
+        if (sidx < nsup) {
+            const int c = box_class<K>(smin[sidx], smax[sidx], jmin, jmax);
+            const uint32_t t0 = sidx * BX_SUP, t1 = min(t0 + BX_SUP, ntiles);
+            if (c == 1) {
+                atomicAdd(&full_add,
+                          (uint32_t)(min((size_t)t1 * BX_TILE, T) - (size_t)t0 * BX_TILE));
+            } else if (c == 2) {
+                uint32_t add = 0;
+                for (uint32_t t = t0; t < t1; ++t) {
+                    const uint4 amin = tmin[t], amax = tmax[t];
+                    const int ct = box_class<K>(amin, amax, jmin, jmax);
+                    if (ct == 1) {
+                        add += (uint32_t)(min((size_t)(t + 1) * BX_TILE, T) - (size_t)t * BX_TILE);
+                    } else if (ct == 2) {
+                        // equal vectors need overlapping boxes in every coordinate
+                        bool below = amax.x < jmin.x;
+                        if (K > 1) below |= amax.y < jmin.y;
+                        if (K > 2) below |= amax.z < jmin.z;
+                        if (K > 3) below |= amax.w < jmin.w;
+                        list[atomicAdd(&nlist, 1u)] = t | (below ? 0u : 0x80000000u);
+                    }
+                }
+                if (add) atomicAdd(&full_add, add);
+            }
+        }
+        __syncthreads();
+        if (members_only && full_add > 0) break;  // every j of the tile is dominated
+        // 2. PARTIAL tiles, pairwise.  A tile whose box lies strictly below
+        // J's in some coordinate holds no vector equal to any j: there the
+        // test is `all(r_i <= r_j)` alone (one LDS.128 and K compares a pair)
+        const uint32_t nl = nlist;
+        if (stats && threadIdx.x == 0) atomicAdd(&stats[0], (unsigned long long)nl);
+        for (uint32_t e = 0; e < nl; ++e) {
+            const uint32_t I = list[e] & 0x7FFFFFFFu;
+            const bool exact = (list[e] >> 31) != 0;
+            const size_t i = (size_t)I * BX_TILE + threadIdx.x;
+            ti[threadIdx.x] = i < T ? rv[i] : make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+            if (exact) tp[threadIdx.x] = i < T ? perm[i] : 0xFFFFFFFFu;
+            __syncthreads();
+            const int lim = (int)min((size_t)BX_TILE, T - (size_t)I * BX_TILE);
+            if (!exact) {
+                uint32_t c2 = 0;
+#pragma unroll 8
+                for (int t = 0; t < lim; ++t) {
+                    const uint4 v = ti[t];
+                    bool le = v.x <= rj.x;
+                    if (K > 1) le &= v.y <= rj.y;
+                    if (K > 2) le &= v.z <= rj.z;
+                    if (K > 3) le &= v.w <= rj.w;
+                    c2 += le ? 1u : 0u;
+                }
+                cnt += c2;
+            } else {
+                if (stats && threadIdx.x == 0) atomicAdd(&stats[1], 1ull);
+#pragma unroll 4
+                for (int t = 0; t < lim; ++t) {
+                    const uint4 v = ti[t];
+                    bool le = v.x <= rj.x, eq = v.x == rj.x;
+                    if (K > 1) { le &= v.y <= rj.y; eq &= v.y == rj.y; }
+                    if (K > 2) { le &= v.z <= rj.z; eq &= v.z == rj.z; }
+                    if (K > 3) { le &= v.w <= rj.w; eq &= v.w == rj.w; }
+                    cnt += (le && !eq) ? 1u : 0u;
+                    dup |= eq && tp[t] < pj;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) nlist = 0;
+        __syncthreads();
+        if (members_only && __syncthreads_and(!valid || cnt > 0 || dup)) break;
+    }
+    if (valid) {
+        const uint32_t tot = cnt + full_add;
+        if (counts) counts[pj] = tot;
+        if (member) member[pj] = (tot == 0 && !dup) ? 1 : 0;
+    }
+}
+
 // ---- K7 for two objectives: O(T log T) counting ----------------------------
 //
 // Sort by (rank_l, rank_c, arrival): j dominates i iff j sits before i with
@@ -1690,6 +1879,72 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
             SAIR_CUDA(cudaMemsetAsync(dmem, 0, T, st));
             if (counts) std::memset(counts, 0, T * 4);
         }
+        if (member) SAIR_CUDA(cudaMemcpyAsync(member, dmem, T, cudaMemcpyDeviceToHost, st));
+        SAIR_CUDA(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
+        return;
+    }
+    static const bool pairwise = std::getenv("SAIR_DOM_PAIRWISE") != nullptr;
+    if ((K == 3 || K == 4) && !pairwise) {
+        // K7b: Morton-ordered tiles, box-pruned (FULL / NONE / PARTIAL)
+        int bits = 1;
+        while (((size_t)1 << bits) < T) ++bits;
+        const int B = 64 / K, shift = bits > B ? bits - B : 0;
+        if (K == 3) morton_key_kernel<3><<<gr, 256, 0, st>>>(ranks, T, shift, key, pos);
+        else morton_key_kernel<4><<<gr, 256, 0, st>>>(ranks, T, shift, key, pos);
+        size_t tb = b_tmp.bytes;
+        SAIR_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, key, skey, pos, perm, (int)T, 0, 64, st));
+        // rank vectors in Morton order (16 B each) reuse key | skey (16 B per tuple)
+        uint4* rv = reinterpret_cast<uint4*>(key);
+        if (K == 3) pack4_kernel<3><<<gr, 256, 0, st>>>(ranks, perm, T, rv);
+        else pack4_kernel<4><<<gr, 256, 0, st>>>(ranks, perm, T, rv);
+        const size_t ntiles = (T + BX_TILE - 1) / BX_TILE, nsup = (ntiles + BX_SUP - 1) / BX_SUP;
+        const size_t n32 = (T + 31) / 32;
+        DBuf b_box;
+        uint4* bx = static_cast<uint4*>(b_box.get((n32 + ntiles + nsup) * 32 + 256));
+        uint4 *b32n = bx, *b32x = bx + n32;
+        uint4 *tmn = bx + 2 * n32, *tmx = tmn + ntiles, *smn = tmx + ntiles, *smx = smn + nsup;
+        box_kernel<<<(int)((n32 + 255) / 256), 256, 0, st>>>(rv, nullptr, T, 32, n32, b32n, b32x);
+        box_kernel<<<(int)((ntiles + 255) / 256), 256, 0, st>>>(b32n, b32x, n32, BX_TILE / 32,
+                                                               ntiles, tmn, tmx);
+        box_kernel<<<(int)((nsup + 255) / 256), 256, 0, st>>>(tmn, tmx, ntiles, BX_SUP, nsup, smn,
+                                                             smx);
+        SAIR_LAUNCH("morton tiles");
+        // part p of n: an equal share of the j-tiles (the work per tile is
+        // about uniform); tuples outside the part get count 0 / member 0
+        const size_t t_lo = ntiles * (size_t)part / nparts, t_hi = ntiles * (size_t)(part + 1) / nparts;
+        if (nparts > 1) {
+            SAIR_CUDA(cudaMemsetAsync(dcnt, 0, T * 4, st));
+            SAIR_CUDA(cudaMemsetAsync(dmem, 0, T, st));
+        }
+        const int members_only = counts == nullptr;
+        static const bool dstats = std::getenv("SAIR_DOM_STATS") != nullptr;
+        unsigned long long* dst = nullptr;
+        if (dstats) {
+            SAIR_CUDA(cudaMalloc(&dst, 64));
+            SAIR_CUDA(cudaMemsetAsync(dst, 0, 64, st));
+        }
+        if (t_hi > t_lo) {
+            if (K == 3)
+                dominance_box_kernel<3><<<(int)(t_hi - t_lo), 256, 0, st>>>(
+                    rv, perm, T, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
+                    (uint32_t)t_lo, members_only, dcnt, dmem, dst);
+            else
+                dominance_box_kernel<4><<<(int)(t_hi - t_lo), 256, 0, st>>>(
+                    rv, perm, T, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
+                    (uint32_t)t_lo, members_only, dcnt, dmem, dst);
+        }
+        SAIR_LAUNCH("dominance_box_kernel");
+        if (dst) {  // diagnostics: partial tiles per CTA, of which exact-test tiles
+            unsigned long long h[3];
+            SAIR_CUDA(cudaMemcpyAsync(h, dst, 24, cudaMemcpyDeviceToHost, st));
+            SAIR_CUDA(cudaStreamSynchronize(st));
+            fprintf(stderr, "[dom] T=%zu K=%d tiles=%zu partial tiles/CTA %.1f (exact-test tiles/CTA %.1f)\n",
+                    T, K, ntiles, (double)h[0] / (double)(t_hi - t_lo),
+                    (double)h[1] / (double)(t_hi - t_lo));
+            cudaFree(dst);
+        }
+        if (counts) SAIR_CUDA(cudaMemcpyAsync(counts, dcnt, T * 4, cudaMemcpyDeviceToHost, st));
         if (member) SAIR_CUDA(cudaMemcpyAsync(member, dmem, T, cudaMemcpyDeviceToHost, st));
         SAIR_CUDA(cudaStreamSynchronize(st));
         cudaStreamDestroy(st);

@@ -36,6 +36,7 @@ import paper_2601_22397_b200 as sair  # noqa: E402
 from paper_2601_22397_b200 import decision, synth  # noqa: E402
 
 THREADS = os.cpu_count() or 1
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def near(got, want, rel=1e-12):
@@ -196,6 +197,32 @@ def test_config2_k_objective_counts_vs_oracle(orc, K, dist):
     cnt, mem = sair.dominance_counts(t)
     ocnt, omem = orc.dominance_counts_mt(t, nthreads=THREADS)
     assert np.array_equal(cnt, ocnt) and np.array_equal(mem, omem)
+
+
+def test_config2_k7b_box_pruned_equals_pairwise(tmp_path):
+    """K7b (Morton tiles, FULL / NONE / PARTIAL boxes; pareto.cu
+    dominance_box_kernel) against the rank-sum pairwise kernel
+    (SAIR_DOM_PAIRWISE=1, a child process: the switch is read once) at 1M
+    tuples: uniform and anti-correlated K = 3, correlated and grid K = 4
+    (grid: long runs of equal vectors -- the duplicate rule)."""
+    import subprocess
+    import sys
+    T = 1 << 20
+    cases = [(3, "uniform"), (3, "anti"), (4, "corr"), (4, "grid")]
+    code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+            "import paper_2601_22397_b200 as sair\nfrom paper_2601_22397_b200 import synth\n"
+            "for K, dist in %r:\n"
+            "    c, m = sair.dominance_counts(synth.tuples(3100 + K, %d, K, dist))\n"
+            "    np.save(%r + f'/c{K}{dist}.npy', c); np.save(%r + f'/m{K}{dist}.npy', m)\n"
+            % (str(ROOT), cases, T, str(tmp_path), str(tmp_path)))
+    env = dict(os.environ, SAIR_DOM_PAIRWISE="1")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+    for K, dist in cases:
+        c, m = sair.dominance_counts(synth.tuples(3100 + K, T, K, dist))
+        assert np.array_equal(c, np.load(tmp_path / f"c{K}{dist}.npy")), (K, dist)
+        assert np.array_equal(m, np.load(tmp_path / f"m{K}{dist}.npy")), (K, dist)
+        _, mo = sair.dominance_counts(synth.tuples(3100 + K, T, K, dist), counts=False)
+        assert np.array_equal(mo, m), (K, dist)
 
 
 def test_config2_windowed_scoring_of_every_tuple(orc):
