@@ -31,6 +31,10 @@ def run(tool, part, extra_env=None):
                         "python", str(WORK), part], capture_output=True, text=True, timeout=900,
                        env=env)
     out = r.stdout + r.stderr
+    if r.returncode != 0 and "COMPUTE-SANITIZER" not in out:
+        # the GPU pool may shadow compute-sanitizer with a stub that refuses to
+        # run (it prints its own advice instead of the tool's banner)
+        pytest.skip("compute-sanitizer unavailable on this box: " + out.strip()[:200])
     assert r.returncode == 0, out[-4000:]
     assert "workload done" in out
     return out
