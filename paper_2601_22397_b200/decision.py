@@ -19,7 +19,7 @@ import numpy as np
 import ctypes as C
 
 from . import (Experience, ExperienceBuffer, FrontierSet, ParetoFrontier, RewardBreakdown,
-               RewardConfig, RewardInputs, ScalingAction, SelectionConfig, _lib)
+               RewardConfig, RewardInputs, ScalingAction, SelectionConfig, _check, _f64, _lib, lib)
 
 
 @dataclass
@@ -68,6 +68,35 @@ class ReplayOutputs:
     stored: bool           # store()'s result (the r_min gate)
 
 
+class _ReplayScratch:
+    """replay_step's output arrays, their ctypes pointers and the last
+    converted configs, kept per buffer: building them per call (numpy arrays,
+    seven pointer casts, two config structs, a package import) was ~30 us of
+    a ~130 us decision step."""
+
+    def __init__(self, m: int, d: int):
+        self.m, self.d = m, d
+        self.x = np.zeros(d)
+        self.idx = np.full(m, -1, np.int64)
+        self.sim = np.zeros(m)
+        self.sc = np.zeros(m)
+        self.nn_i = np.full(1, -1, np.int64)
+        self.nn_s = np.zeros(1)
+        self.cnt = C.c_size_t()
+        self.rw = _lib.RewardBreakdownC()
+        self.ins, self.sto = C.c_int(), C.c_int()
+        self.ri = _lib.RewardInputsC()
+        i64, f64 = C.POINTER(C.c_int64), C.POINTER(C.c_double)
+        self.p = (self.x.ctypes.data_as(f64), self.idx.ctypes.data_as(i64),
+                  self.sim.ctypes.data_as(f64), self.sc.ctypes.data_as(f64), C.byref(self.cnt),
+                  self.nn_i.ctypes.data_as(i64), self.nn_s.ctypes.data_as(f64),
+                  C.byref(self.rw), C.byref(self.ins), C.byref(self.sto), C.byref(self.ri))
+        self.skey = self.rkey = self.akey = None
+        self.sc_c = self.rc_c = None
+        self.deltas = None
+        self.p_deltas = None
+
+
 def replay_step(buf: ExperienceBuffer, frontier: ParetoFrontier, x, scfg: SelectionConfig,
                 inp: RewardInputs, action: ScalingAction, rcfg: RewardConfig,
                 update: bool = True, round: int = 0) -> ReplayOutputs:
@@ -76,31 +105,41 @@ def replay_step(buf: ExperienceBuffer, frontier: ParetoFrontier, x, scfg: Select
     the frontier, frontier.update(inp.l_after_ms, inp.c_after), store() of
     (x, reward total, round) -- one device call, one host synchronisation
     (sair_decision_step); the same results as the four calls in that order."""
-    from . import _check, _dp, _f64, lib
-    x = _f64(x).ravel()
+    x = np.asarray(x, dtype=np.float64).reshape(-1)
     m = max(scfg.m, 1)
-    idx = np.full(m, -1, np.int64)
-    sim = np.zeros(m)
-    sc = np.zeros(m)
-    cnt = C.c_size_t()
-    nn_i = np.full(1, -1, np.int64)
-    nn_s = np.zeros(1)
-    ri = _lib.RewardInputsC(inp.l_before_ms, inp.l_after_ms, inp.c_before, inp.c_after)
-    d = action.deltas()
-    rw = _lib.RewardBreakdownC()
-    ins, sto = C.c_int(), C.c_int()
-    c = scfg._c()
-    rc = rcfg._c()
+    sc = getattr(buf, "_replay_scratch", None)
+    if sc is None or sc.m != m or sc.d != len(x):
+        sc = _ReplayScratch(m, len(x))
+        buf._replay_scratch = sc
+    sc.x[:] = x
+    sc.nn_i[0] = -1
+    sc.nn_s[0] = 0.0
+    skey = (scfg.m, scfg.lambda_div, scfg.sigma_sim, scfg.locally_weighted_mean, scfg.mode)
+    if skey != sc.skey:
+        sc.skey, sc.sc_c = skey, scfg._c()
+    rkey = (rcfg.t_sla_ms, rcfg.l_baseline_ms, rcfg.c_budget, rcfg.w_latency, rcfg.w_cost,
+            rcfg.w_proactive, rcfg.r_max)
+    if rkey != sc.rkey:
+        sc.rkey, sc.rc_c = rkey, rcfg._c()
+    akey = tuple((s.replicas, s.cpu_millicores, s.memory_mb, s.rate_ratio_tenths)
+                 for s in action.stages)
+    if akey != sc.akey:
+        sc.akey, sc.deltas = akey, action.deltas()
+        sc.p_deltas = sc.deltas.ctypes.data_as(C.POINTER(C.c_int32))
+    ri = sc.ri
+    ri.l_before_ms, ri.l_after_ms = inp.l_before_ms, inp.l_after_ms
+    ri.c_before, ri.c_after = inp.c_before, inp.c_after
+    px, pidx, psim, psc, pcnt, pnn_i, pnn_s, prw, pins, psto, pri = sc.p
     _check(lib().sair_decision_step(
-        buf._h, frontier._h, _dp(x), len(x), C.byref(c), C.byref(ri),
-        d.ctypes.data_as(C.POINTER(C.c_int32)), len(d), C.byref(rc), int(update), int(round),
-        idx.ctypes.data_as(C.POINTER(C.c_int64)), _dp(sim), _dp(sc), C.byref(cnt),
-        nn_i.ctypes.data_as(C.POINTER(C.c_int64)), _dp(nn_s), C.byref(rw), C.byref(ins),
-        C.byref(sto)))
-    k = int(cnt.value)
+        buf._h, frontier._h, px, sc.d, C.byref(sc.sc_c), pri, sc.p_deltas, len(sc.deltas),
+        C.byref(sc.rc_c), int(update), int(round), pidx, psim, psc, pcnt, pnn_i, pnn_s, prw, pins,
+        psto))
+    k = int(sc.cnt.value)
+    rw = sc.rw
     r = RewardBreakdown(rw.latency, rw.cost, rw.sla, rw.proactive, rw.pareto, rw.total,
                         bool(rw.clipped))
-    if sto.value and buf._mirror:
+    stored = bool(sc.sto.value)
+    if stored and buf._mirror:
         buf._items.append(Experience(list(x), action, r.total, int(round)))
-    return ReplayOutputs(idx[:k], sim[:k], sc[:k], int(nn_i[0]), float(nn_s[0]), r,
-                         bool(ins.value), bool(sto.value))
+    return ReplayOutputs(sc.idx[:k].copy(), sc.sim[:k].copy(), sc.sc[:k].copy(),
+                         int(sc.nn_i[0]), float(sc.nn_s[0]), r, bool(sc.ins.value), stored)
