@@ -19,6 +19,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -1610,11 +1611,14 @@ static size_t stage_batch(sair_frontier_s* f, const double* pts, size_t T, doubl
         SAIR_CUDA(cudaStreamSynchronize(f->st));  // raw lives in b_sort, which the sort reuses
         return T;
     }
-    static bool attr = false;
-    if (!attr) {
+    // the dynamic shared-memory limit is a per-device function attribute (a
+    // sharded insert runs this on several GPUs of the process)
+    static std::atomic<uint64_t> attr_set{0};
+    const uint64_t bit = 1ull << (f->device & 63);
+    if (!(attr_set.load() & bit)) {
         SAIR_CUDA(cudaFuncSetAttribute(prefilter_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PF_SMEM));
-        attr = true;
+        attr_set.fetch_or(bit);
     }
     SAIR_CUDA(cudaMemsetAsync(misc, 0, 8, f->st));
     prefilter_kernel<<<(unsigned)nblk, PF_THREADS, PF_SMEM, f->st>>>(

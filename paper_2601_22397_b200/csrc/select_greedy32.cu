@@ -21,6 +21,7 @@
 // the reference's arg-max (gain desc, round asc, index asc).  The true pick is
 // always a candidate, so the result is the fp64 greedy's, bit for bit.  A
 // query whose candidate set overflows (never seen) goes to the fp64 greedy.
+#include <atomic>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -857,11 +858,15 @@ void g32_steps(const G32Args& a, int nctas, cudaStream_t st) {
 // ev: 2 want events (each step kernel's start, end), or empty
 void g32_steps_mma(const G32Args& a, const float* aimg, float* bimg, const float* q32,
                    cudaStream_t st, const std::vector<cudaEvent_t>& ev) {
-    static bool attr = false;
-    if (!attr) {
+    // a per-device function attribute (sharded stores put shards on several GPUs)
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    SAIR_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_set.load() & bit)) {
         SAIR_CUDA(cudaFuncSetAttribute(g32_mma_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)MT_SMEM));
-        attr = true;
+        attr_set.fetch_or(bit);
     }
     const size_t ntiles = (a.n + MT_REC - 1) / MT_REC;
     const int grid = (int)std::min<size_t>(ntiles, 148);

@@ -563,14 +563,17 @@ static bool small_cluster_ok(bool zs, int cs, size_t smem) {
         size_t ok = 0, bad = SIZE_MAX;
     };
     static Known known[2][SMALL_CS_MAX16 + 1];
-    static bool raised[2] = {false, false};
+    static uint64_t raised[2] = {0, 0};  // per device: function attributes are per device
     std::lock_guard<std::mutex> lk(mu);
     const void* fn = zs ? (const void*)small_select_kernel<true> : (const void*)small_select_kernel<false>;
-    if (!raised[zs]) {
+    int dev = 0;
+    SAIR_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(raised[zs] & bit)) {
         SAIR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SMALL_SMEM_MAX));
         SAIR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        raised[zs] = true;
+        raised[zs] |= bit;
     }
     if (cs <= 8) return true;
     Known& k = known[zs][cs];
