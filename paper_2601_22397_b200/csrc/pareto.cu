@@ -1079,7 +1079,14 @@ __global__ void __launch_bounds__(256)
             if (exact) tp[threadIdx.x] = i < T ? perm[i] : 0xFFFFFFFFu;
             __syncthreads();
             const int lim = (int)min((size_t)BX_TILE, T - (size_t)I * BX_TILE);
-            if (!exact) {
+            // each warp's own 32 j (Morton-consecutive: a compact box) against
+            // the tile's box: a warp whose j all see it NONE skips the tile, one
+            // whose j all see it FULL adds its size -- warp-uniform branches
+            const int pcl = valid ? box_class<K>(tmin[I], tmax[I], rj, rj) : 0;
+            if (!exact && __all_sync(0xffffffffu, pcl == 0)) {
+            } else if (!exact && __all_sync(0xffffffffu, pcl == 1 || !valid)) {
+                if (valid) cnt += (uint32_t)lim;
+            } else if (!exact) {
                 uint32_t c2 = 0;
 #pragma unroll 8
                 for (int t = 0; t < lim; ++t) {
