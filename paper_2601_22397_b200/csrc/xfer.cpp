@@ -35,7 +35,9 @@ void copy_h2d_staged(void* dst, const void* src, size_t bytes, cudaStream_t st) 
     std::lock_guard<std::mutex> lk(g_xmu);
     if (!g_ring) {
         g_nt = ring_threads();
-        SAIR_CUDA(cudaMallocHost(reinterpret_cast<void**>(&g_ring), (size_t)g_nt * 2 * XCHUNK));
+        // portable: pinned for every device of the process (sharded callers)
+        SAIR_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g_ring), (size_t)g_nt * 2 * XCHUNK,
+                                cudaHostAllocPortable));
     }
     int dev = 0;
     SAIR_CUDA(cudaGetDevice(&dev));
