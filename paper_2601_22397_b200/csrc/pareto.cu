@@ -944,7 +944,7 @@ __global__ void __launch_bounds__(256)
 // staged in shared memory for the pairwise test `all(r_i <= r_j) && r_i != r_j`
 // plus the duplicate rule (an equal vector with a smaller original index makes
 // j a non-member: pareto.cpp:43-54 keeps the first of equal points).
-constexpr int BX_TILE = 256, BX_SUP = 32, BX_LCAP = 256 * BX_SUP;
+constexpr int BX_TILE = 256, BX_SUP = 32, BX_SUB = 64, BX_LCAP = 256 * BX_SUP;
 
 template <int K>
 __global__ void morton_key_kernel(const uint32_t* __restrict__ ranks, size_t T, int shift,
@@ -1014,6 +1014,7 @@ __device__ __forceinline__ int box_class(uint4 amin, uint4 amax, uint4 jmin, uin
 template <int K>
 __global__ void __launch_bounds__(256)
     dominance_box_kernel(const uint4* __restrict__ rv, const uint32_t* __restrict__ perm, size_t T,
+                         const uint4* __restrict__ bmin64, const uint4* __restrict__ bmax64,
                          const uint4* __restrict__ tmin, const uint4* __restrict__ tmax,
                          const uint4* __restrict__ smin, const uint4* __restrict__ smax,
                          uint32_t ntiles, uint32_t nsup, uint32_t tile_begin, int members_only,
@@ -1087,17 +1088,29 @@ __global__ void __launch_bounds__(256)
             } else if (!exact && __all_sync(0xffffffffu, pcl == 1 || !valid)) {
                 if (valid) cnt += (uint32_t)lim;
             } else if (!exact) {
+                // the same warp-uniform test per 64-tuple quarter of the tile
                 uint32_t c2 = 0;
+#pragma unroll 1
+                for (int q0 = 0; q0 < lim; q0 += BX_SUB) {
+                    const size_t sb = (size_t)I * (BX_TILE / BX_SUB) + (size_t)(q0 / BX_SUB);
+                    const int qn = min(BX_SUB, lim - q0);
+                    const int qc = valid ? box_class<K>(bmin64[sb], bmax64[sb], rj, rj) : 0;
+                    if (__all_sync(0xffffffffu, qc == 0)) continue;
+                    if (__all_sync(0xffffffffu, qc == 1 || !valid)) {
+                        c2 += (uint32_t)qn;
+                        continue;
+                    }
 #pragma unroll 8
-                for (int t = 0; t < lim; ++t) {
-                    const uint4 v = ti[t];
-                    bool le = v.x <= rj.x;
-                    if (K > 1) le &= v.y <= rj.y;
-                    if (K > 2) le &= v.z <= rj.z;
-                    if (K > 3) le &= v.w <= rj.w;
-                    c2 += le ? 1u : 0u;
+                    for (int t = q0; t < q0 + qn; ++t) {
+                        const uint4 v = ti[t];
+                        bool le = v.x <= rj.x;
+                        if (K > 1) le &= v.y <= rj.y;
+                        if (K > 2) le &= v.z <= rj.z;
+                        if (K > 3) le &= v.w <= rj.w;
+                        c2 += le ? 1u : 0u;
+                    }
                 }
-                cnt += c2;
+                if (valid) cnt += c2;
             } else {
                 if (stats && threadIdx.x == 0) atomicAdd(&stats[1], 1ull);
 #pragma unroll 4
@@ -1910,13 +1923,14 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
         if (K == 3) pack4_kernel<3><<<gr, 256, 0, st>>>(ranks, perm, T, rv);
         else pack4_kernel<4><<<gr, 256, 0, st>>>(ranks, perm, T, rv);
         const size_t ntiles = (T + BX_TILE - 1) / BX_TILE, nsup = (ntiles + BX_SUP - 1) / BX_SUP;
-        const size_t n32 = (T + 31) / 32;
+        const size_t n64 = (T + BX_SUB - 1) / BX_SUB;
         DBuf b_box;
-        uint4* bx = static_cast<uint4*>(b_box.get((n32 + ntiles + nsup) * 32 + 256));
-        uint4 *b32n = bx, *b32x = bx + n32;
-        uint4 *tmn = bx + 2 * n32, *tmx = tmn + ntiles, *smn = tmx + ntiles, *smx = smn + nsup;
-        box_kernel<<<(int)((n32 + 255) / 256), 256, 0, st>>>(rv, nullptr, T, 32, n32, b32n, b32x);
-        box_kernel<<<(int)((ntiles + 255) / 256), 256, 0, st>>>(b32n, b32x, n32, BX_TILE / 32,
+        uint4* bx = static_cast<uint4*>(b_box.get((n64 + ntiles + nsup) * 32 + 256));
+        uint4 *b64n = bx, *b64x = bx + n64;
+        uint4 *tmn = bx + 2 * n64, *tmx = tmn + ntiles, *smn = tmx + ntiles, *smx = smn + nsup;
+        box_kernel<<<(int)((n64 + 255) / 256), 256, 0, st>>>(rv, nullptr, T, BX_SUB, n64, b64n,
+                                                            b64x);
+        box_kernel<<<(int)((ntiles + 255) / 256), 256, 0, st>>>(b64n, b64x, n64, BX_TILE / BX_SUB,
                                                                ntiles, tmn, tmx);
         box_kernel<<<(int)((nsup + 255) / 256), 256, 0, st>>>(tmn, tmx, ntiles, BX_SUP, nsup, smn,
                                                              smx);
@@ -1938,11 +1952,11 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
         if (t_hi > t_lo) {
             if (K == 3)
                 dominance_box_kernel<3><<<(int)(t_hi - t_lo), 256, 0, st>>>(
-                    rv, perm, T, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
+                    rv, perm, T, b64n, b64x, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
                     (uint32_t)t_lo, members_only, dcnt, dmem, dst);
             else
                 dominance_box_kernel<4><<<(int)(t_hi - t_lo), 256, 0, st>>>(
-                    rv, perm, T, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
+                    rv, perm, T, b64n, b64x, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
                     (uint32_t)t_lo, members_only, dcnt, dmem, dst);
         }
         SAIR_LAUNCH("dominance_box_kernel");
