@@ -631,7 +631,7 @@ union PfTemp {
 // shared: scan/sort temp | c by arrival [PF_B] | inclusive prefix-min by rank [PF_B] | keep [PF_B]
 constexpr size_t PF_SMEM = sizeof(PfTemp) + PF_B * 16 + PF_B + 64;
 
-__global__ void __launch_bounds__(PF_THREADS)
+__global__ void __launch_bounds__(PF_THREADS, 2)  // two CTAs per SM (88 KB shared each)
     prefilter_kernel(const double2* __restrict__ pts, size_t T, double* __restrict__ rl,
                      double* __restrict__ rc, uint32_t* __restrict__ cnt,
                      unsigned int* __restrict__ nan_seen) {
