@@ -5,8 +5,9 @@ tuples/s; % HBM roofline"; configs[3]: 16M experiences, 4096 queries/batch,
 k=32).
 
 A step = one select() of a Q=4096 query batch (k = m = 32, lambda_div = 0, the
-fused veto scan off) over the whole device-resident store: 32 wide tensor-core
-passes of 128 queries (select_wide.cu).  Also measured in the same run:
+fused veto scan off) over the whole device-resident store: 16 wide tensor-core
+passes of 256 queries over the store's bf16 page copy (select_wide.cu), each
+after a TF32 sample pass for its start thresholds.  Also measured in the same run:
 "hbm_target" -- Q=8 queries per step, the single HBM-bound pass of the north
 star's >= 70% HBM target (select_mma.cu); "config2" -- configs[1], 1M x 64
 with 256-query batches; "pareto" -- configs[2], 4M 2-objective tuples
