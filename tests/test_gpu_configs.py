@@ -225,6 +225,20 @@ def test_config2_k7b_box_pruned_equals_pairwise(tmp_path):
         assert np.array_equal(mo, m), (K, dist)
 
 
+@pytest.mark.parametrize("K,dist", [(3, "uniform"), (4, "grid")])
+def test_k7b_parts_combine_by_a_sum(orc, K, dist):
+    """K7b split into parts (sair_dominance_counts_part: an equal share of the
+    j-tiles each, the multi-GPU split): the parts' counts sum to the whole and
+    their memberships OR to it; the whole equals the oracle."""
+    t = synth.tuples(4100 + K, 50000, K, dist)
+    cnt, mem = sair.dominance_counts(t)
+    ocnt, omem = orc.dominance_counts_mt(t, nthreads=THREADS)
+    assert np.array_equal(cnt, ocnt) and np.array_equal(mem, omem)
+    parts = [sair.dominance_counts(t, part=p, nparts=3) for p in range(3)]
+    assert np.array_equal(sum(p[0].astype(np.int64) for p in parts), cnt.astype(np.int64))
+    assert np.array_equal(parts[0][1] | parts[1][1] | parts[2][1], mem)
+
+
 def test_config2_windowed_scoring_of_every_tuple(orc):
     """K8 on a frontier beyond shared memory (anti-correlated 4M tuples, F ~
     17.6k): the bucketed windowed path (T >= 64k) scores every tuple exactly
