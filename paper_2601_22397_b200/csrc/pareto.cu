@@ -445,7 +445,28 @@ __global__ void __launch_bounds__(512) score_window_kernel(FrontierView f, const
 
 __global__ void point_query_kernel(FrontierView f, double pl, double pc, int op,
                                    double* __restrict__ out) {
-    if (threadIdx.x || blockIdx.x) return;
+    if (blockIdx.x) return;
+    if (op == Q_HV) {
+        // pareto.cpp:56-65: the slab terms in parallel (coalesced loads), their
+        // sum in the reference's order -- every lane runs the same chain over
+        // the terms shuffled in 32 at a time (one thread re-loading the
+        // frontier from global memory term by term took 2 ms at F = 17.7k)
+        const int lane = threadIdx.x & 31;
+        double hv = 0.0;
+        for (size_t i0 = 0; i0 < f.F; i0 += 32) {
+            const size_t i = i0 + lane;
+            double term = 0.0;
+            if (i < f.F) {
+                const double nl = i + 1 < f.F ? f.l[i + 1] : 1.0;
+                term = dmul(dsub(nl, f.l[i]), dsub(1.0, f.c[i]));
+            }
+            const int cnt = (int)min((size_t)32, f.F - i0);
+            for (int j = 0; j < cnt; ++j) hv = dadd(hv, __shfl_sync(0xffffffffu, term, j));
+        }
+        if (threadIdx.x == 0) out[0] = hv;
+        return;
+    }
+    if (threadIdx.x) return;
     switch (op) {
         case Q_DOMINATED: out[0] = f_dominated(f, pl, pc) ? 1.0 : 0.0; break;
         case Q_CONTRIB:
@@ -454,15 +475,6 @@ __global__ void point_query_kernel(FrontierView f, double pl, double pc, int op,
             break;
         case Q_DISTANCE: out[0] = f.F ? f_distance(f, pl, pc) : -1.0; break;
         case Q_REWARD: out[0] = f_reward(f, pl, pc, nullptr); break;
-        case Q_HV: {
-            double hv = 0.0;  // pareto.cpp:56-65
-            for (size_t i = 0; i < f.F; ++i) {
-                double nl = i + 1 < f.F ? f.l[i + 1] : 1.0;
-                hv = dadd(hv, dmul(dsub(nl, f.l[i]), dsub(1.0, f.c[i])));
-            }
-            out[0] = hv;
-            break;
-        }
     }
 }
 
@@ -1670,8 +1682,10 @@ size_t frontier_insert_batch(sair_frontier_s* f, const double* pts, size_t T) {
     // the tuples land first (l / c at F .. F+T), the sort arrays behind them
     // (sized for the worst case: every tuple survives the pre-filter)
     const size_t N = f->F + T, lc_bytes = ((N + 31) & ~(size_t)31) * 8 + N * 8;
-    char* base = static_cast<char*>(
-        f->b_in.get(((lc_bytes + 255) & ~(size_t)255) + N * (8 * 4 + 4 * 5) + 4096));
+    // 1/16 headroom: the next batch of the same size into the grown frontier
+    // must not reallocate (a free + malloc of ~300 MB per 4M batch)
+    const size_t need = ((lc_bytes + 255) & ~(size_t)255) + N * (8 * 4 + 4 * 5) + 4096;
+    char* base = static_cast<char*>(f->b_in.get(need > f->b_in.bytes ? need + need / 16 : need));
     double* l = reinterpret_cast<double*>(base);
     double* c = l + ((N + 31) & ~(size_t)31);
     const size_t n = f->F + stage_batch(f, pts, T, l + f->F, c + f->F);
