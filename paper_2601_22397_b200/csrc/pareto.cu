@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(256)
 // staged in shared memory for the pairwise test `all(r_i <= r_j) && r_i != r_j`
 // plus the duplicate rule (an equal vector with a smaller original index makes
 // j a non-member: pareto.cpp:43-54 keeps the first of equal points).
-constexpr int BX_TILE = 256, BX_SUP = 32, BX_SUB = 64, BX_LCAP = 256 * BX_SUP;
+constexpr int BX_TILE = 256, BX_SUP = 32, BX_SUB = 64, BX_JT = 128, BX_LCAP = BX_JT * BX_SUP;
 
 template <int K>
 __global__ void morton_key_kernel(const uint32_t* __restrict__ ranks, size_t T, int shift,
@@ -1024,7 +1024,7 @@ __device__ __forceinline__ int box_class(uint4 amin, uint4 amax, uint4 jmin, uin
 }
 
 template <int K>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(BX_JT)
     dominance_box_kernel(const uint4* __restrict__ rv, const uint32_t* __restrict__ perm, size_t T,
                          const uint4* __restrict__ bmin64, const uint4* __restrict__ bmax64,
                          const uint4* __restrict__ tmin, const uint4* __restrict__ tmax,
@@ -1036,12 +1036,19 @@ __global__ void __launch_bounds__(256)
     __shared__ uint32_t tp[BX_TILE];
     __shared__ uint32_t list[BX_LCAP];
     __shared__ uint32_t nlist, full_add;
+    // one CTA per BX_JT = 128 j (two 64-tuple boxes: a tighter box than the
+    // 256-tuple i-tiles' -- fewer PARTIAL tiles per j)
     const uint32_t J = tile_begin + blockIdx.x;
-    const size_t j = (size_t)J * BX_TILE + threadIdx.x;
+    const size_t j = (size_t)J * BX_JT + threadIdx.x;
     const bool valid = j < T;
     const uint4 rj = valid ? rv[j] : make_uint4(0u, 0u, 0u, 0u);
     const uint32_t pj = valid ? perm[j] : 0xFFFFFFFFu;
-    const uint4 jmin = tmin[J], jmax = tmax[J];
+    const size_t n64 = (T + BX_SUB - 1) / BX_SUB, jb = (size_t)J * (BX_JT / BX_SUB);
+    uint4 jmin = bmin64[jb], jmax = bmax64[jb];
+    if (jb + 1 < n64) {
+        jmin = umin4(jmin, bmin64[jb + 1]);
+        jmax = umax4(jmax, bmax64[jb + 1]);
+    }
     if (threadIdx.x == 0) {
         nlist = 0;
         full_add = 0;
@@ -1087,9 +1094,11 @@ __global__ void __launch_bounds__(256)
         for (uint32_t e = 0; e < nl; ++e) {
             const uint32_t I = list[e] & 0x7FFFFFFFu;
             const bool exact = (list[e] >> 31) != 0;
-            const size_t i = (size_t)I * BX_TILE + threadIdx.x;
-            ti[threadIdx.x] = i < T ? rv[i] : make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
-            if (exact) tp[threadIdx.x] = i < T ? perm[i] : 0xFFFFFFFFu;
+            for (int k = threadIdx.x; k < BX_TILE; k += blockDim.x) {
+                const size_t i = (size_t)I * BX_TILE + k;
+                ti[k] = i < T ? rv[i] : make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
+                if (exact) tp[k] = i < T ? perm[i] : 0xFFFFFFFFu;
+            }
             __syncthreads();
             const int lim = (int)min((size_t)BX_TILE, T - (size_t)I * BX_TILE);
             // each warp's own 32 j (Morton-consecutive: a compact box) against
@@ -1949,9 +1958,11 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
         box_kernel<<<(int)((nsup + 255) / 256), 256, 0, st>>>(tmn, tmx, ntiles, BX_SUP, nsup, smn,
                                                              smx);
         SAIR_LAUNCH("morton tiles");
-        // part p of n: an equal share of the j-tiles (the work per tile is
-        // about uniform); tuples outside the part get count 0 / member 0
-        const size_t t_lo = ntiles * (size_t)part / nparts, t_hi = ntiles * (size_t)(part + 1) / nparts;
+        // part p of n: an equal share of the j-tiles (BX_JT tuples each; the
+        // work per tile is about uniform); tuples outside the part get count 0
+        // / member 0
+        const size_t njt = (T + BX_JT - 1) / BX_JT;
+        const size_t t_lo = njt * (size_t)part / nparts, t_hi = njt * (size_t)(part + 1) / nparts;
         if (nparts > 1) {
             SAIR_CUDA(cudaMemsetAsync(dcnt, 0, T * 4, st));
             SAIR_CUDA(cudaMemsetAsync(dmem, 0, T, st));
@@ -1965,11 +1976,11 @@ void dominance_counts(const double* tuples, size_t T, int K, int device, uint32_
         }
         if (t_hi > t_lo) {
             if (K == 3)
-                dominance_box_kernel<3><<<(int)(t_hi - t_lo), 256, 0, st>>>(
+                dominance_box_kernel<3><<<(int)(t_hi - t_lo), BX_JT, 0, st>>>(
                     rv, perm, T, b64n, b64x, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
                     (uint32_t)t_lo, members_only, dcnt, dmem, dst);
             else
-                dominance_box_kernel<4><<<(int)(t_hi - t_lo), 256, 0, st>>>(
+                dominance_box_kernel<4><<<(int)(t_hi - t_lo), BX_JT, 0, st>>>(
                     rv, perm, T, b64n, b64x, tmn, tmx, smn, smx, (uint32_t)ntiles, (uint32_t)nsup,
                     (uint32_t)t_lo, members_only, dcnt, dmem, dst);
         }
